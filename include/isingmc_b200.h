@@ -1,0 +1,220 @@
+/* C ABI of the B200 batched sweep engine: the drop-in boundary for the hot path of
+ * isingmc (arXiv 1004.0024) — batched Metropolis sweeps over many independent sparse Ising
+ * chains under parallel tempering, executed by hand-written sm_100a CUDA kernels.
+ *
+ * Conventions are those of the reference's C interface (reference:
+ * proj/include/isingmc.h:1-38, proj/src/capi.cpp:21-65): every entry point returns an
+ * ising_status; on failure ising_b200_last_error() describes the problem for the calling
+ * thread (thread-local); handles are opaque and freed by their matching _free; input
+ * arrays are borrowed for the duration of the call; output arrays are caller-owned HOST
+ * memory; C++ exceptions never cross the boundary.  There is NO CPU fallback: without a
+ * usable CUDA device every batch entry point fails with ISING_ERR_INTERNAL.
+ *
+ * Each declaration cites the reference interface it replaces or extends.  "ref:" paths are
+ * relative to /root/reference/proj.
+ */
+#ifndef ISINGMC_B200_H
+#define ISINGMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ISING_B200_API __attribute__((visibility("default")))
+#else
+#define ISING_B200_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef ISINGMC_H /* same values as ref: include/isingmc.h:15-35 when both headers are used */
+typedef enum ising_status {
+    ISING_OK = 0,
+    ISING_ERR_ARGUMENT = 1,
+    ISING_ERR_PARSE = 2,
+    ISING_ERR_IO = 3,
+    ISING_ERR_INTERNAL = 4
+} ising_status;
+
+typedef enum ising_exp_kind {
+    ISING_EXP_ENGINE_DEFAULT = 0, /* fast (the default of every non-`reference` engine) */
+    ISING_EXP_EXACT = 1,
+    ISING_EXP_FAST = 2,
+    ISING_EXP_ACCURATE = 3
+} ising_exp_kind;
+#endif
+
+/* ref: ising_last_error, include/isingmc.h:38 / src/capi.cpp:33,145 */
+ISING_B200_API const char* ising_b200_last_error(void);
+
+/* Number of visible CUDA devices (0 if none / driver missing). Never fails. */
+ISING_B200_API int ising_b200_device_count(void);
+
+/* ---------------------------------------------------------------- models ---- */
+
+/* Immutable, shareable graph + fields (ref: SpinModel, include/isingmc/model.hpp:52-60). */
+typedef struct ising_b200_model ising_b200_model;
+
+/* From the flattened adjacency the reference engines use (ref: FlatEdges,
+ * include/isingmc/sweep.hpp:67-72; flatten(), src/sweep_state.cpp:84-106): spin i owns
+ * half-edges offsets[i]..offsets[i+1], the last tau_counts[i] of them tau edges.
+ * tau_counts may be NULL (all zero).  layers = 0 for a generic model, otherwise the model
+ * is declared layered (layers * per_layer == n_spins, ref: LayeredMeta model.hpp:44-50).
+ * Runs the structural checks of validate_model (ref: src/model.cpp:246-330). */
+ISING_B200_API ising_status ising_b200_model_from_csr(uint32_t n_spins, const float* h, const uint32_t* offsets,
+                                       const uint32_t* targets, const float* couplings,
+                                       const uint8_t* tau_counts, uint32_t layers,
+                                       uint32_t per_layer, ising_b200_model** out);
+
+/* ref: build_layered_model(LayerSpec, n_layers, j_tau), src/model.cpp:52-104: n_layers
+ * copies of a `positions`-site layer (undirected space edges p[e]-q[e] with coupling j[e]),
+ * spin (l,pos) -> l*positions+pos, tau edges of coupling j_tau to the next then the previous
+ * layer in the last two slots.  Same rejections (n_layers < 4, bad/duplicate/self edges). */
+ISING_B200_API ising_status ising_b200_model_build_layered(uint32_t positions, const float* h, uint32_t n_edges,
+                                            const uint32_t* p, const uint32_t* q, const float* j,
+                                            uint32_t n_layers, float j_tau,
+                                            ising_b200_model** out);
+
+ISING_B200_API void ising_b200_model_free(ising_b200_model* model); /* ref: ising_model_free */
+ISING_B200_API uint32_t ising_b200_model_spins(const ising_b200_model* model); /* ref: ising_model_spins */
+ISING_B200_API uint64_t ising_b200_model_half_edges(const ising_b200_model* model);
+/* ref: ising_model_layers, include/isingmc.h:53 — returns 1 and fills for layered models. */
+ISING_B200_API int ising_b200_model_layers(const ising_b200_model* model, uint32_t* layers, uint32_t* per_layer);
+/* Copies the CSR view out (arrays sized by _spins / _half_edges). */
+ISING_B200_API ising_status ising_b200_model_export_csr(const ising_b200_model* model, float* h, uint32_t* offsets,
+                                         uint32_t* targets, float* couplings, uint8_t* tau_counts);
+/* ref: ising_model_cost, include/isingmc.h:55 -> total_cost, src/model.cpp:108-126 (host, f64). */
+ISING_B200_API ising_status ising_b200_model_cost(const ising_b200_model* model, const int8_t* spins, uint32_t n,
+                                   double* cost);
+
+/* ---------------------------------------------------------------- batches ---- */
+
+/* Which sweep kernel family a batch uses. AUTO picks LAYERED when every model qualifies. */
+typedef enum ising_b200_kernel {
+    ISING_KERNEL_AUTO = 0,
+    ISING_KERNEL_GENERIC = 1, /* any graph: state in HBM, replica-interleaved [spin][32 chains] */
+    ISING_KERNEL_LAYERED = 2  /* identical-layer models: one layer of fields on chip per chain */
+} ising_b200_kernel;
+
+/* The batch counterpart of EngineConfig + the per-chain SweepParams
+ * (ref: include/isingmc/sweep.hpp:25-29,55-63).  Chains are grouped in ladders of n_betas;
+ * chain c = ladder * n_betas + k starts in beta slot k (beta = betas[k]).  n_betas = 1 gives
+ * plain independent replicas. */
+typedef struct ising_batch_params {
+    uint32_t n_ladders;
+    uint32_t n_betas;
+    const float* betas;         /* n_betas, each finite and >= 0 (ref: sweep_state.cpp:148-150) */
+    const uint32_t* seeds;      /* n_ladders*n_betas sweep-stream seeds, or NULL: base_seed +
+                                   (first_ladder*n_betas + c), the reference's lane-seed rule
+                                   (ref: sweep.hpp:59, rng.cpp:144-148) */
+    const uint32_t* swap_seeds; /* n_ladders, or NULL: swap_base_seed + first_ladder + l */
+    uint32_t base_seed;
+    uint32_t swap_base_seed;
+    uint64_t first_ladder;      /* global index of this shard's ladder 0 (multi-GPU sharding) */
+    float tau_scale;            /* ref: SweepParams::tau_scale, must be finite */
+    int exp_kind;               /* ising_exp_kind */
+    int device;                 /* CUDA device ordinal */
+    int kernel;                 /* ising_b200_kernel */
+    const int8_t* initial_spins; /* NULL: initial_spins(n, seed) per chain (ref:
+                                    sweep_state.cpp:211-223); else [chains][n_spins] of +/-1
+                                    (ref: init_state(model,cfg,initial), sweep_state.cpp:225-234) */
+} ising_batch_params;
+
+typedef struct ising_batch ising_batch;
+
+/* ref: init_state(model, cfg) for every chain (src/sweep_state.cpp:160-234): uploads the
+ * models, then ON THE DEVICE seeds each chain's MT19937, draws its initial spins, sums the
+ * effective fields in the reference's order and the initial energy.  models[model_of_ladder[l]]
+ * is ladder l's graph; model_of_ladder may be NULL when n_models == 1 (shared graph) or
+ * n_models == n_ladders (ladder l uses models[l]).  All models must have equal n_spins. */
+ISING_B200_API ising_status ising_batch_create(const ising_b200_model* const* models, uint32_t n_models,
+                                const uint32_t* model_of_ladder, const ising_batch_params* params,
+                                ising_batch** out);
+ISING_B200_API void ising_batch_free(ising_batch* batch);
+
+/* ref: run_sweeps(state, model, n), src/sweep_state.cpp:272-291, for every chain; after each
+ * swap_interval-th sweep (counted since creation) one tempering swap round runs.
+ * swap_interval = 0: never swap.  Asynchronous on the batch's stream; reads synchronise. */
+ISING_B200_API ising_status ising_batch_run(ising_batch* batch, uint64_t sweeps, uint32_t swap_interval);
+/* One swap round now (new: the reference has no tempering). */
+ISING_B200_API ising_status ising_batch_swap(ising_batch* batch);
+ISING_B200_API ising_status ising_batch_sync(ising_batch* batch);
+
+/* --- readout: all outputs are host buffers, chains in global order --- */
+/* ref: SweepState::spins (sweep.hpp:92) as +/-1 int8, [n_chains][n_spins], original order. */
+ISING_B200_API ising_status ising_batch_read_spins(ising_batch* batch, uint64_t first_chain, uint64_t n_chains,
+                                    int8_t* out);
+/* ref: SweepState::h_eff_space / h_eff_tau (sweep.hpp:93-94) of one chain. */
+ISING_B200_API ising_status ising_batch_read_fields(ising_batch* batch, uint64_t chain, float* h_space,
+                                     float* h_tau);
+/* ref: total_cost(model, state.spins) per chain (capi.cpp:119), f64, reference summation order. */
+ISING_B200_API ising_status ising_batch_read_energies(ising_batch* batch, double* out);
+/* Running energy used by the swap rule (initial cost + sum of flip energies). */
+ISING_B200_API ising_status ising_batch_read_running_energies(ising_batch* batch, double* out);
+/* ref: FlipStats::flips / attempts (sweep.hpp:38-44). Either pointer may be NULL. */
+ISING_B200_API ising_status ising_batch_read_stats(ising_batch* batch, uint64_t* flips, uint64_t* attempts);
+/* ref: state_checksum (sweep_state.cpp:325-336): FNV-1a over the sign sequence. */
+ISING_B200_API ising_status ising_batch_checksums(ising_batch* batch, uint64_t* out);
+/* ref: field_coherence_ulp (sweep_state.cpp:346-354) per chain. */
+ISING_B200_API ising_status ising_batch_field_coherence(ising_batch* batch, uint64_t* out);
+/* Current beta slot of each chain; per ladder and slot pair k,(k+1) the accept / attempt
+ * counts ([n_ladders][n_betas], last column unused). Either swap pointer may be NULL. */
+ISING_B200_API ising_status ising_batch_read_slots(ising_batch* batch, uint32_t* slot_of_chain);
+ISING_B200_API ising_status ising_batch_read_swap_stats(ising_batch* batch, uint64_t* accepts, uint64_t* attempts);
+
+/* Packs per-chain {energy f64, running energy f64, flips u64, checksum u64} (32 B per chain)
+ * into a DEVICE buffer (e.g. a torch CUDA tensor) so a multi-GPU caller can gather results
+ * with one NCCL all-gather and no host round trip.  device_out: n_chains * 32 bytes. */
+ISING_B200_API ising_status ising_batch_pack_results(ising_batch* batch, void* device_out);
+
+/* --- introspection / measurement --- */
+typedef struct ising_batch_info {
+    uint64_t n_chains;
+    uint32_t n_spins;
+    uint32_t n_tiles;        /* warps' worth of chains (32 per tile) */
+    int kernel;              /* ising_b200_kernel actually used */
+    uint64_t sweeps_done;
+    uint64_t device_bytes;   /* HBM held by this batch */
+    uint64_t sweep_launches; /* sweep kernel launches so far */
+    uint64_t swap_launches;
+    uint64_t other_launches; /* init / readout kernels */
+    double sweep_ms;         /* CUDA-event time summed over sweep launches (needs timing on) */
+    double swap_ms;
+    double last_run_ms;      /* CUDA-event time of the last ising_batch_run call, whole call */
+} ising_batch_info;
+/* timing = 1 brackets every sweep/swap launch with CUDA events on the batch's stream. */
+ISING_B200_API ising_status ising_batch_set_timing(ising_batch* batch, int timing);
+ISING_B200_API ising_status ising_batch_get_info(ising_batch* batch, ising_batch_info* out); /* synchronises */
+/* The batch's cudaStream_t, for callers that want to record their own events on it. */
+ISING_B200_API void* ising_batch_stream(ising_batch* batch);
+
+/* ---------------------------------------------------------------- one-shot ---- */
+/* Single-chain counterpart of ising_run (ref: include/isingmc.h:74-106, capi.cpp:96-139,
+ * 221-228) with the basic engine's semantics: same fields as ising_run_params /
+ * ising_run_report minus the CPU-tier knobs (engine, workers, wait statistics). */
+typedef struct ising_b200_run_params {
+    uint64_t sweeps;
+    float beta;
+    float tau_scale;
+    int exp_kind;
+    uint32_t seed;
+    int device;
+} ising_b200_run_params;
+
+typedef struct ising_b200_run_report {
+    double final_cost;
+    double flip_rate;
+    uint64_t flips;
+    uint64_t attempts;
+    uint64_t checksum;
+} ising_b200_run_report;
+
+ISING_B200_API ising_status ising_b200_run(const ising_b200_model* model, const ising_b200_run_params* params,
+                            ising_b200_run_report* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISINGMC_B200_H */

@@ -1,0 +1,351 @@
+/* TEST INFRASTRUCTURE ONLY — see ising_oracle.h.  Plain C restatement of the reference's
+ * scalar Metropolis sweep and its helpers; compile with
+ *   gcc -O2 -ffp-contract=off -fno-math-errno -fPIC -shared -pthread
+ * (contraction must stay off: the reference forbids FMA, src/CMakeLists.txt:23-29).
+ */
+#include "ising_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ MT19937 */
+
+void orc_mt_seed(orc_mt* g, uint32_t seed) { /* rng.cpp:37-44 */
+    g->w[0] = seed;
+    for (uint32_t i = 1; i < 624; ++i) {
+        uint32_t p = g->w[i - 1];
+        g->w[i] = 1812433253u * (p ^ (p >> 30)) + i;
+    }
+    g->cursor = 624;
+}
+
+static void mt_regenerate(orc_mt* g) { /* rng.cpp:22-25, 89-96 (plain loop) */
+    uint32_t* w = g->w;
+    for (uint32_t i = 0; i < 624; ++i) {
+        uint32_t y = (w[i] & 0x80000000u) | (w[(i + 1) % 624] & 0x7fffffffu);
+        uint32_t v = w[(i + 397) % 624] ^ (y >> 1);
+        if (y & 1u) v ^= 0x9908b0dfu;
+        w[i] = v;
+    }
+    g->cursor = 0;
+}
+
+uint32_t orc_mt_next(orc_mt* g) { /* rng.cpp:27-33, 99-102 */
+    if (g->cursor == 624) mt_regenerate(g);
+    uint32_t y = g->w[g->cursor++];
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9d2c5680u;
+    y ^= (y << 15) & 0xefc60000u;
+    y ^= y >> 18;
+    return y;
+}
+
+void orc_mt_fill(uint32_t seed, uint32_t* out, size_t count) {
+    orc_mt g;
+    orc_mt_seed(&g, seed);
+    for (size_t i = 0; i < count; ++i) out[i] = orc_mt_next(&g);
+}
+
+/* x / 2^32 truncated toward zero: keep the top 24 significant bits (rng.hpp:87-92). */
+float orc_u32_to_unit(uint32_t x) {
+    if (x == 0) return 0.0f;
+    int width = 32 - __builtin_clz(x);
+    if (width > 24) x &= ~((1u << (width - 24)) - 1u);
+    return (float)x * 0x1p-32f;
+}
+
+/* ------------------------------------------------------------------ exponentials */
+
+static const float kTwoLnSq2 = 0.9609060278364028f;   /* fastexp.hpp:15 */
+static const float kLog2eP23 = 12102203.161561485f;   /* fastexp.hpp:16 */
+static const float kLog2eP25 = 48408812.64624594f;    /* fastexp.hpp:17 */
+static const float kAccCutoff = -21.834136187592387f; /* fastexp.hpp:18 */
+static const float kImageLo = -1056964608.0f;         /* fastexp.hpp:22 */
+static const float kImageHi = 1073741760.0f;          /* fastexp.hpp:23 */
+
+static float image_to_float(float t) { /* fastexp.hpp:29-31 */
+    if (t < kImageLo) t = kImageLo; /* std::max(t, lo): x is never NaN on this path */
+    if (t > kImageHi) t = kImageHi;
+    int32_t i = (int32_t)lrintf(t) + 0x3F800000;
+    float f;
+    memcpy(&f, &i, sizeof f);
+    return f * kTwoLnSq2;
+}
+
+float orc_exp_fast(float x) { return image_to_float(x * kLog2eP23); }
+
+float orc_exp_accurate(float x) { /* fastexp.hpp:37-51 */
+    if (x >= 0.0f) return 1.0f;
+    if (x < kAccCutoff) return 0.0f;
+    return sqrtf(sqrtf(image_to_float(x * kLog2eP25)));
+}
+
+float orc_exp_exact(float x) { return (float)exp((double)x); } /* sweep_kernels.hpp:22 */
+
+float orc_exp_kind(int kind, float x) {
+    switch (kind) {
+        case ORC_EXP_EXACT: return orc_exp_exact(x);
+        case ORC_EXP_FAST: return orc_exp_fast(x);
+        default: return orc_exp_accurate(x);
+    }
+}
+
+/* ------------------------------------------------------------------ state helpers */
+
+void orc_initial_spins(uint32_t n, uint32_t seed, int8_t* out) {
+    orc_mt g;
+    orc_mt_seed(&g, seed ^ ORC_INIT_SPIN_SEED_MIX);
+    for (uint32_t i = 0; i < n; ++i) out[i] = (orc_mt_next(&g) >> 31) ? -1 : 1;
+}
+
+void orc_recompute_fields(const orc_model* m, const float* spins, float* hs, float* ht) {
+    for (uint32_t i = 0; i < m->n_spins; ++i) {
+        uint32_t end = m->offsets[i + 1], mid = end - m->tau_counts[i];
+        float a = m->h[i];
+        for (uint32_t e = m->offsets[i]; e < mid; ++e) a += m->couplings[e] * spins[m->targets[e]];
+        float b = 0.0f;
+        for (uint32_t e = mid; e < end; ++e) b += m->couplings[e] * spins[m->targets[e]];
+        hs[i] = a;
+        ht[i] = b;
+    }
+}
+
+double orc_total_cost(const orc_model* m, const float* spins) {
+    double cost = 0.0;
+    for (uint32_t i = 0; i < m->n_spins; ++i) {
+        cost -= (double)m->h[i] * (double)spins[i];
+        for (uint32_t e = m->offsets[i]; e < m->offsets[i + 1]; ++e) {
+            uint32_t t = m->targets[e];
+            if (t > i) cost -= (double)m->couplings[e] * (double)spins[i] * (double)spins[t];
+        }
+    }
+    return cost;
+}
+
+uint64_t orc_checksum(const float* spins, uint32_t n) {
+    uint64_t h = 1469598103934665603ull;
+    for (uint32_t i = 0; i < n; ++i) {
+        h ^= (uint64_t)(spins[i] > 0.0f ? 1 : 0);
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+static int64_t ulp_key(float v) {
+    int32_t b;
+    memcpy(&b, &v, sizeof b);
+    return b < 0 ? (int64_t)0x80000000ll - b : (int64_t)b;
+}
+
+uint64_t orc_field_coherence_ulp(const orc_model* m, const float* spins, const float* hs,
+                                 const float* ht) {
+    float* a = (float*)malloc(sizeof(float) * m->n_spins * 2);
+    float* b = a + m->n_spins;
+    orc_recompute_fields(m, spins, a, b);
+    uint64_t worst = 0;
+    for (uint32_t i = 0; i < m->n_spins; ++i) {
+        int64_t d1 = ulp_key(hs[i]) - ulp_key(a[i]);
+        int64_t d2 = ulp_key(ht[i]) - ulp_key(b[i]);
+        if (d1 < 0) d1 = -d1;
+        if (d2 < 0) d2 = -d2;
+        if ((uint64_t)d1 > worst) worst = (uint64_t)d1;
+        if ((uint64_t)d2 > worst) worst = (uint64_t)d2;
+    }
+    free(a);
+    return worst;
+}
+
+/* ------------------------------------------------------------------ chains */
+
+orc_chain* orc_chain_create(const orc_model* m, uint32_t seed, float beta, float tau_scale,
+                            int exp_kind, const int8_t* initial) {
+    orc_chain* c = (orc_chain*)calloc(1, sizeof *c);
+    if (!c) return NULL;
+    c->n = m->n_spins;
+    c->beta = beta;
+    c->tau_scale = tau_scale;
+    c->exp_kind = exp_kind;
+    c->spins = (float*)malloc(sizeof(float) * 3 * (size_t)(c->n ? c->n : 1));
+    if (!c->spins) {
+        free(c);
+        return NULL;
+    }
+    c->hs = c->spins + c->n;
+    c->ht = c->hs + c->n;
+    if (initial) {
+        for (uint32_t i = 0; i < c->n; ++i) c->spins[i] = (float)initial[i];
+    } else {
+        int8_t* tmp = (int8_t*)malloc(c->n ? c->n : 1);
+        orc_initial_spins(c->n, seed, tmp);
+        for (uint32_t i = 0; i < c->n; ++i) c->spins[i] = (float)tmp[i];
+        free(tmp);
+    }
+    orc_recompute_fields(m, c->spins, c->hs, c->ht);
+    orc_mt_seed(&c->rng, seed);
+    c->e_run = orc_total_cost(m, c->spins);
+    return c;
+}
+
+void orc_chain_free(orc_chain* c) {
+    if (!c) return;
+    free(c->spins);
+    free(c);
+}
+
+/* One uniform per spin in index order, accept iff u < p with NO min(1, .) clamp
+ * (sweep_basic.cpp:27-50).  The reference pulls uniforms from 624-wide batches; the
+ * stream is the same as one next_u32 per attempt. */
+void orc_chain_sweep(orc_chain* c, const orc_model* m, uint64_t sweeps) {
+    const float beta = c->beta, gamma = c->tau_scale;
+    for (uint64_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t i = 0; i < c->n; ++i) {
+            const float u = orc_u32_to_unit(orc_mt_next(&c->rng));
+            const float s = c->spins[i];
+            const float hs = c->hs[i], ht = c->ht[i];
+            const float x = -beta * (2.0f * s * (hs + gamma * ht)); /* sweep_kernels.hpp:14-16 */
+            const float p = orc_exp_kind(c->exp_kind, x);
+            if (u < p) {
+                const float two_s = 2.0f * s;
+                const uint32_t end = m->offsets[i + 1], mid = end - m->tau_counts[i];
+                for (uint32_t e = m->offsets[i]; e < mid; ++e)
+                    c->hs[m->targets[e]] -= two_s * m->couplings[e];
+                for (uint32_t e = mid; e < end; ++e)
+                    c->ht[m->targets[e]] -= two_s * m->couplings[e];
+                c->spins[i] = -s;
+                ++c->flips;
+                c->e_run += (double)(two_s * (hs + ht)); /* new: see orc_pt_run */
+            }
+        }
+        c->attempts += c->n;
+    }
+}
+
+/* ------------------------------------------------------------------ tempering driver */
+
+typedef struct pt_job {
+    const orc_model* const* models;
+    uint32_t n_ladders, n_betas;
+    const float* betas;
+    const uint32_t* seeds;
+    const uint32_t* swap_seeds;
+    float tau_scale;
+    int exp_kind;
+    uint64_t sweeps;
+    uint32_t swap_interval;
+    const int8_t* initial;
+    orc_pt_result* out;
+    uint32_t next_ladder; /* shared work counter */
+    pthread_mutex_t lock;
+    int failed;
+} pt_job;
+
+static int run_ladder(pt_job* job, uint32_t l) {
+    const uint32_t nb = job->n_betas;
+    const orc_model* m = job->models[l];
+    const uint32_t n = m->n_spins;
+    orc_chain** ch = (orc_chain**)calloc(nb, sizeof *ch);
+    uint32_t* at_slot = (uint32_t*)malloc(sizeof(uint32_t) * nb); /* chain holding slot k */
+    uint32_t* slot_of = (uint32_t*)malloc(sizeof(uint32_t) * nb); /* slot of chain j */
+    if (!ch || !at_slot || !slot_of) return -1;
+    for (uint32_t k = 0; k < nb; ++k) {
+        size_t c = (size_t)l * nb + k;
+        ch[k] = orc_chain_create(m, job->seeds[c], job->betas[k], job->tau_scale, job->exp_kind,
+                                 job->initial ? job->initial + c * n : NULL);
+        if (!ch[k]) return -1;
+        at_slot[k] = slot_of[k] = k;
+    }
+    orc_mt swap_rng;
+    orc_mt_seed(&swap_rng, job->swap_seeds[l] ^ ORC_SWAP_SEED_MIX);
+    orc_pt_result* out = job->out;
+    uint64_t round = 0;
+    for (uint64_t sw = 1; sw <= job->sweeps; ++sw) {
+        for (uint32_t j = 0; j < nb; ++j) orc_chain_sweep(ch[j], m, 1);
+        if (job->swap_interval == 0 || nb < 2 || sw % job->swap_interval != 0) continue;
+        for (uint32_t k = (uint32_t)(round & 1u); k + 1 < nb; k += 2) {
+            const uint32_t a = at_slot[k], b = at_slot[k + 1];
+            const float u = orc_u32_to_unit(orc_mt_next(&swap_rng));
+            const double arg =
+                ((double)job->betas[k] - (double)job->betas[k + 1]) * (ch[a]->e_run - ch[b]->e_run);
+            const float p = orc_exp_kind(job->exp_kind, (float)arg);
+            if (out && out->swap_att) ++out->swap_att[(size_t)l * nb + k];
+            if (u < p) {
+                at_slot[k] = b;
+                at_slot[k + 1] = a;
+                slot_of[a] = k + 1;
+                slot_of[b] = k;
+                ch[a]->beta = job->betas[k + 1];
+                ch[b]->beta = job->betas[k];
+                if (out && out->swap_acc) ++out->swap_acc[(size_t)l * nb + k];
+            }
+        }
+        ++round;
+    }
+    for (uint32_t j = 0; j < nb; ++j) {
+        size_t c = (size_t)l * nb + j;
+        if (out) {
+            if (out->spins)
+                for (uint32_t i = 0; i < n; ++i) out->spins[c * n + i] = ch[j]->spins[i] > 0 ? 1 : -1;
+            if (out->flips) out->flips[c] = ch[j]->flips;
+            if (out->e_run) out->e_run[c] = ch[j]->e_run;
+            if (out->energy) out->energy[c] = orc_total_cost(m, ch[j]->spins);
+            if (out->slot) out->slot[c] = slot_of[j];
+        }
+        orc_chain_free(ch[j]);
+    }
+    free(ch);
+    free(at_slot);
+    free(slot_of);
+    return 0;
+}
+
+static void* pt_worker(void* arg) {
+    pt_job* job = (pt_job*)arg;
+    for (;;) {
+        pthread_mutex_lock(&job->lock);
+        uint32_t l = job->next_ladder++;
+        pthread_mutex_unlock(&job->lock);
+        if (l >= job->n_ladders) break;
+        if (run_ladder(job, l) != 0) job->failed = 1;
+    }
+    return NULL;
+}
+
+int orc_pt_run(const orc_model* const* models, uint32_t n_ladders, uint32_t n_betas,
+               const float* betas, const uint32_t* seeds, const uint32_t* swap_seeds,
+               float tau_scale, int exp_kind, uint64_t sweeps, uint32_t swap_interval,
+               uint32_t threads, const int8_t* initial, orc_pt_result* out) {
+    if (!models || !betas || !seeds || n_betas == 0) return -1;
+    if (n_betas > 1 && swap_interval > 0 && !swap_seeds) return -1;
+    uint32_t* zero_seeds = NULL;
+    if (!swap_seeds) {
+        zero_seeds = (uint32_t*)calloc(n_ladders ? n_ladders : 1, sizeof(uint32_t));
+        swap_seeds = zero_seeds;
+    }
+    pt_job job;
+    memset(&job, 0, sizeof job);
+    job.models = models;
+    job.n_ladders = n_ladders;
+    job.n_betas = n_betas;
+    job.betas = betas;
+    job.seeds = seeds;
+    job.swap_seeds = swap_seeds;
+    job.tau_scale = tau_scale;
+    job.exp_kind = exp_kind;
+    job.sweeps = sweeps;
+    job.swap_interval = swap_interval;
+    job.initial = initial;
+    job.out = out;
+    pthread_mutex_init(&job.lock, NULL);
+    if (threads < 1) threads = 1;
+    if (threads > n_ladders) threads = n_ladders ? n_ladders : 1;
+    pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+    for (uint32_t t = 1; t < threads; ++t) pthread_create(&tid[t], NULL, pt_worker, &job);
+    pt_worker(&job);
+    for (uint32_t t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+    free(tid);
+    free(zero_seeds);
+    pthread_mutex_destroy(&job.lock);
+    return job.failed ? -1 : 0;
+}

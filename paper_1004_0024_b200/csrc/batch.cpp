@@ -1,0 +1,413 @@
+#include "batch.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace isingb200 {
+
+void cuda_check(cudaError_t status, const char* what) {
+    if (status != cudaSuccess) {
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(status));
+    }
+}
+
+DeviceBuffer::~DeviceBuffer() {
+    if (ptr_ != nullptr) cudaFree(ptr_);
+}
+
+void DeviceBuffer::allocate(size_t bytes, size_t& tally) {
+    if (ptr_ != nullptr) {
+        cudaFree(ptr_);
+        ptr_ = nullptr;
+    }
+    bytes_ = bytes;
+    if (bytes == 0) return;
+    cuda_check(cudaMalloc(&ptr_, bytes), "cudaMalloc");
+    tally += bytes;
+}
+
+namespace {
+
+template <typename T>
+void upload(DeviceBuffer& buf, const std::vector<T>& host, size_t& tally, cudaStream_t stream) {
+    buf.allocate(host.size() * sizeof(T), tally);
+    if (!host.empty()) {
+        cuda_check(cudaMemcpyAsync(buf.as<void>(), host.data(), host.size() * sizeof(T),
+                                   cudaMemcpyHostToDevice, stream),
+                   "upload");
+    }
+}
+
+}  // namespace
+
+void Batch::bind_device() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
+
+Batch::Batch(const std::vector<const HostModel*>& models,
+             const std::vector<uint32_t>& model_of_ladder, const BatchConfig& cfg,
+             const int8_t* initial_spins) {
+    // ---- argument checks (ref: check_engine_model, sweep_state.cpp:108-158)
+    if (models.empty()) throw Error("init_state: no model given");
+    if (cfg.n_ladders == 0 || cfg.n_betas == 0) throw Error("init_state: batch needs at least one chain");
+    if (cfg.betas.size() != cfg.n_betas) throw Error("init_state: betas count mismatch");
+    for (float beta : cfg.betas) {
+        if (!(beta >= 0.0f) || !std::isfinite(beta)) throw Error("init_state: beta must be finite and >= 0");
+    }
+    if (!std::isfinite(cfg.tau_scale)) throw Error("init_state: tau_scale must be finite");
+    if (cfg.exp_kind < 1 || cfg.exp_kind > 3) throw Error("invalid exp_kind value " + std::to_string(cfg.exp_kind));
+    const uint64_t chains64 = uint64_t(cfg.n_ladders) * cfg.n_betas;
+    if (chains64 > 0x7fffffffull) throw Error("init_state: too many chains for one batch");
+    if (cfg.seeds.size() != chains64 || cfg.swap_seeds.size() != cfg.n_ladders) {
+        throw Error("init_state: seed count mismatch");
+    }
+    if (model_of_ladder.size() != cfg.n_ladders) throw Error("init_state: model_of_ladder count mismatch");
+    const uint32_t n = models[0]->n_spins;
+    bool any_tau = false;
+    for (const HostModel* m : models) {
+        if (m == nullptr) throw Error("null argument");
+        if (m->n_spins != n) throw Error("init_state: all models of a batch must have the same spin count");
+        any_tau = any_tau || m->has_tau;
+    }
+    for (uint32_t idx : model_of_ladder) {
+        if (idx >= models.size()) throw Error("init_state: model_of_ladder entry out of range");
+    }
+    if (cfg.kernel < 0 || cfg.kernel > 2) throw Error("invalid kernel value " + std::to_string(cfg.kernel));
+    if (cfg.kernel == int(KernelFamily::layered)) {
+        throw Error("init_state: the layered kernel is not available for this batch");
+    }
+    family_ = KernelFamily::generic;
+
+    // ---- device
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        throw CudaError("no CUDA device available (this engine has no CPU fallback)");
+    }
+    if (cfg.device < 0 || cfg.device >= count) throw Error("invalid device ordinal " + std::to_string(cfg.device));
+    device_ = cfg.device;
+    bind_device();
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreate(&run_start_), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&run_stop_), "cudaEventCreate");
+
+    // ---- tiles: runs of consecutive ladders sharing a model, cut every 32 chains
+    std::vector<uint32_t> tile_first, tile_count, tile_model, chain_loc(chains64);
+    {
+        uint32_t l = 0;
+        while (l < cfg.n_ladders) {
+            uint32_t r = l;
+            while (r < cfg.n_ladders && model_of_ladder[r] == model_of_ladder[l]) ++r;
+            const uint32_t first = l * cfg.n_betas, last = r * cfg.n_betas;
+            for (uint32_t c = first; c < last; c += 32) {
+                const uint32_t cnt = std::min<uint32_t>(32, last - c);
+                for (uint32_t k = 0; k < cnt; ++k) chain_loc[c + k] = uint32_t(tile_first.size()) * 32 + k;
+                tile_first.push_back(c);
+                tile_count.push_back(cnt);
+                tile_model.push_back(model_of_ladder[l]);
+            }
+            l = r;
+        }
+    }
+
+    // ---- models
+    std::vector<DevModel> dev_models;
+    const auto keep = [&](auto const& host_vec) {
+        model_storage_.push_back(std::make_unique<DeviceBuffer>());
+        upload(*model_storage_.back(), host_vec, device_bytes_, stream_);
+        return model_storage_.back().get();
+    };
+    for (const HostModel* m : models) {
+        DevModel d{};
+        d.n_spins = m->n_spins;
+        d.has_tau = m->has_tau ? 1u : 0u;
+        d.h = keep(m->h)->as<float>();
+        d.offsets = keep(m->offsets)->as<uint32_t>();
+        d.targets = keep(m->targets)->as<uint32_t>();
+        d.couplings = keep(m->couplings)->as<float>();
+        d.tau_counts = keep(m->tau_counts)->as<uint8_t>();
+        dev_models.push_back(d);
+    }
+    upload(models_, dev_models, device_bytes_, stream_);
+
+    // ---- batch description
+    dev_.n_spins = n;
+    dev_.n_tiles = uint32_t(tile_first.size());
+    dev_.n_chains = uint32_t(chains64);
+    dev_.n_ladders = cfg.n_ladders;
+    dev_.n_betas = cfg.n_betas;
+    dev_.tau_scale = cfg.tau_scale;
+    dev_.exp_kind = cfg.exp_kind;
+    upload(tile_first_, tile_first, device_bytes_, stream_);
+    upload(tile_count_, tile_count, device_bytes_, stream_);
+    upload(tile_model_, tile_model, device_bytes_, stream_);
+    upload(chain_loc_, chain_loc, device_bytes_, stream_);
+    upload(seeds_, cfg.seeds, device_bytes_, stream_);
+    upload(betas_, cfg.betas, device_bytes_, stream_);
+    upload(swap_seeds_, cfg.swap_seeds, device_bytes_, stream_);
+    dev_.models = models_.as<DevModel>();
+    dev_.tile_first = tile_first_.as<uint32_t>();
+    dev_.tile_count = tile_count_.as<uint32_t>();
+    dev_.tile_model = tile_model_.as<uint32_t>();
+    dev_.chain_loc = chain_loc_.as<uint32_t>();
+    dev_.seeds = seeds_.as<uint32_t>();
+    dev_.betas = betas_.as<float>();
+    dev_.swap_seeds = swap_seeds_.as<uint32_t>();
+
+    const size_t tiles = dev_.n_tiles, chains = dev_.n_chains, ladders = dev_.n_ladders;
+    const size_t field_elems = std::max<size_t>(1, tiles * n * 32);
+    slot_of_chain_.allocate(chains * sizeof(uint32_t), device_bytes_);
+    chain_at_slot_.allocate(chains * sizeof(uint32_t), device_bytes_);
+    hs_.allocate(field_elems * sizeof(float), device_bytes_);
+    if (any_tau) ht_.allocate(field_elems * sizeof(float), device_bytes_);
+    spin_bits_.allocate(std::max<size_t>(1, tiles * n) * sizeof(uint32_t), device_bytes_);
+    mt_.allocate(tiles * kMtWords * 32 * sizeof(uint32_t), device_bytes_);
+    mt_pos_.allocate(tiles * sizeof(uint32_t), device_bytes_);
+    e_run_.allocate(chains * sizeof(double), device_bytes_);
+    flips_.allocate(chains * sizeof(unsigned long long), device_bytes_);
+    swap_mt_.allocate(ladders * kMtWords * sizeof(uint32_t), device_bytes_);
+    swap_pos_.allocate(ladders * sizeof(uint32_t), device_bytes_);
+    swap_acc_.allocate(chains * sizeof(unsigned long long), device_bytes_);
+    swap_att_.allocate(chains * sizeof(unsigned long long), device_bytes_);
+    dev_.slot_of_chain = slot_of_chain_.as<uint32_t>();
+    dev_.chain_at_slot = chain_at_slot_.as<uint32_t>();
+    dev_.hs = hs_.as<float>();
+    dev_.ht = any_tau ? ht_.as<float>() : nullptr;
+    dev_.spin_bits = spin_bits_.as<uint32_t>();
+    dev_.mt = mt_.as<uint32_t>();
+    dev_.mt_pos = mt_pos_.as<uint32_t>();
+    dev_.e_run = e_run_.as<double>();
+    dev_.flips = flips_.as<unsigned long long>();
+    dev_.swap_mt = swap_mt_.as<uint32_t>();
+    dev_.swap_pos = swap_pos_.as<uint32_t>();
+    dev_.swap_acc = swap_acc_.as<unsigned long long>();
+    dev_.swap_att = swap_att_.as<unsigned long long>();
+
+    // ---- initial state, on the device
+    DeviceBuffer initial_dev;
+    size_t ignored = 0;
+    if (initial_spins != nullptr) {
+        const size_t total = chains * n;
+        for (size_t k = 0; k < total; ++k) {
+            if (initial_spins[k] != 1 && initial_spins[k] != -1) throw Error("init_state: spins must be +/-1");
+        }
+        initial_dev.allocate(std::max<size_t>(1, total), ignored);
+        cuda_check(cudaMemcpyAsync(initial_dev.as<void>(), initial_spins, total, cudaMemcpyHostToDevice,
+                                   stream_),
+                   "upload initial spins");
+    }
+    cuda_check(launch_init(dev_, initial_spins ? initial_dev.as<int8_t>() : nullptr, stream_), "init kernel");
+    other_launches += 2;
+    cuda_check(cudaStreamSynchronize(stream_), "init");
+}
+
+Batch::~Batch() {
+    cudaSetDevice(device_);
+    if (stream_ != nullptr) cudaStreamSynchronize(stream_);
+    for (TimedLaunch& t : pending_) {
+        cudaEventDestroy(t.start);
+        cudaEventDestroy(t.stop);
+    }
+    if (run_start_ != nullptr) cudaEventDestroy(run_start_);
+    if (run_stop_ != nullptr) cudaEventDestroy(run_stop_);
+    if (stream_ != nullptr) cudaStreamDestroy(stream_);
+}
+
+void Batch::begin_timed(bool is_swap) {
+    if (!timing_) return;
+    TimedLaunch t{};
+    t.is_swap = is_swap;
+    cuda_check(cudaEventCreate(&t.start), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&t.stop), "cudaEventCreate");
+    cuda_check(cudaEventRecord(t.start, stream_), "cudaEventRecord");
+    pending_.push_back(t);
+}
+
+void Batch::end_timed() {
+    if (!timing_) return;
+    cuda_check(cudaEventRecord(pending_.back().stop, stream_), "cudaEventRecord");
+}
+
+void Batch::drain_timings() {
+    for (TimedLaunch& t : pending_) {
+        float ms = 0.0f;
+        cuda_check(cudaEventSynchronize(t.stop), "cudaEventSynchronize");
+        cuda_check(cudaEventElapsedTime(&ms, t.start, t.stop), "cudaEventElapsedTime");
+        (t.is_swap ? swap_ms_ : sweep_ms_) += double(ms);
+        cudaEventDestroy(t.start);
+        cudaEventDestroy(t.stop);
+    }
+    pending_.clear();
+}
+
+void Batch::launch_sweeps(uint32_t sweeps) {
+    if (sweeps == 0) return;
+    begin_timed(false);
+    cuda_check(launch_sweep_generic(dev_, sweeps, stream_), "sweep kernel");
+    end_timed();
+    ++sweep_launches;
+    sweeps_done_ += sweeps;
+}
+
+void Batch::launch_swap_round() {
+    begin_timed(true);
+    cuda_check(launch_swap(dev_, swap_rounds_, stream_), "swap kernel");
+    end_timed();
+    ++swap_launches;
+    ++swap_rounds_;
+}
+
+void Batch::run(uint64_t sweeps, uint32_t swap_interval) {
+    bind_device();
+    cuda_check(cudaEventRecord(run_start_, stream_), "cudaEventRecord");
+    const bool swapping = swap_interval != 0 && dev_.n_betas > 1;
+    uint64_t left = sweeps;
+    while (left > 0) {
+        uint64_t step = left;
+        if (swapping) step = std::min<uint64_t>(left, swap_interval - sweeps_done_ % swap_interval);
+        step = std::min<uint64_t>(step, 1u << 20);
+        launch_sweeps(uint32_t(step));
+        left -= step;
+        if (swapping && sweeps_done_ % swap_interval == 0) launch_swap_round();
+    }
+    cuda_check(cudaEventRecord(run_stop_, stream_), "cudaEventRecord");
+    run_timed_ = true;
+}
+
+void Batch::swap_round() {
+    bind_device();
+    if (dev_.n_betas > 1) launch_swap_round();
+}
+
+void Batch::sync() {
+    bind_device();
+    cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+    drain_timings();
+}
+
+double Batch::sweep_ms() {
+    sync();
+    return sweep_ms_;
+}
+double Batch::swap_ms() {
+    sync();
+    return swap_ms_;
+}
+double Batch::last_run_ms() {
+    sync();
+    if (!run_timed_) return 0.0;
+    float ms = 0.0f;
+    cuda_check(cudaEventElapsedTime(&ms, run_start_, run_stop_), "cudaEventElapsedTime");
+    return double(ms);
+}
+
+// ---- readout -------------------------------------------------------------------------
+
+namespace {
+template <typename T>
+void download(T* host, const void* dev, size_t count, cudaStream_t stream) {
+    if (count == 0) return;
+    cuda_check(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, stream), "download");
+    cuda_check(cudaStreamSynchronize(stream), "download");
+}
+}  // namespace
+
+void Batch::read_spins(uint64_t first_chain, uint64_t n_chains, int8_t* out) {
+    bind_device();
+    if (first_chain > dev_.n_chains || n_chains > dev_.n_chains - first_chain) {
+        throw Error("read_spins: chain range out of bounds");
+    }
+    if (n_chains != 0 && out == nullptr) throw Error("null argument");
+    // stage through a bounded scratch buffer so that huge batches do not double their footprint
+    const size_t n = dev_.n_spins;
+    const uint64_t per_pass = std::max<uint64_t>(1, (256ull << 20) / std::max<size_t>(1, n));
+    size_t ignored = 0;
+    for (uint64_t done = 0; done < n_chains; done += per_pass) {
+        const uint64_t cnt = std::min<uint64_t>(per_pass, n_chains - done);
+        if (scratch_.bytes() < cnt * n) scratch_.allocate(cnt * n, ignored);
+        cuda_check(launch_unpack_spins(dev_, uint32_t(first_chain + done), uint32_t(cnt),
+                                       scratch_.as<int8_t>(), stream_),
+                   "unpack kernel");
+        ++other_launches;
+        download(out + done * n, scratch_.as<void>(), cnt * n, stream_);
+    }
+}
+
+void Batch::read_fields(uint64_t chain, float* hs, float* ht) {
+    bind_device();
+    if (chain >= dev_.n_chains) throw Error("read_fields: chain out of range");
+    if (hs == nullptr || ht == nullptr) throw Error("null argument");
+    const size_t n = dev_.n_spins;
+    size_t ignored = 0;
+    if (scratch_.bytes() < 2 * n * sizeof(float)) scratch_.allocate(2 * n * sizeof(float), ignored);
+    float* d = scratch_.as<float>();
+    cuda_check(launch_gather_fields(dev_, uint32_t(chain), d, d + n, stream_), "gather kernel");
+    ++other_launches;
+    download(hs, d, n, stream_);
+    download(ht, d + n, n, stream_);
+}
+
+void Batch::read_energies(double* out) {
+    bind_device();
+    if (out == nullptr) throw Error("null argument");
+    size_t ignored = 0;
+    if (scratch_.bytes() < dev_.n_chains * sizeof(double)) scratch_.allocate(dev_.n_chains * sizeof(double), ignored);
+    cuda_check(launch_energies(dev_, scratch_.as<double>(), stream_), "energy kernel");
+    ++other_launches;
+    download(out, scratch_.as<void>(), dev_.n_chains, stream_);
+}
+
+void Batch::read_running_energies(double* out) {
+    bind_device();
+    if (out == nullptr) throw Error("null argument");
+    download(out, dev_.e_run, dev_.n_chains, stream_);
+}
+
+void Batch::read_stats(uint64_t* flips, uint64_t* attempts) {
+    bind_device();
+    if (flips != nullptr) download(flips, dev_.flips, dev_.n_chains, stream_);
+    else sync();
+    if (attempts != nullptr) {
+        for (uint32_t c = 0; c < dev_.n_chains; ++c) attempts[c] = sweeps_done_ * dev_.n_spins;
+    }
+}
+
+void Batch::read_checksums(uint64_t* out) {
+    bind_device();
+    if (out == nullptr) throw Error("null argument");
+    size_t ignored = 0;
+    if (scratch_.bytes() < dev_.n_chains * sizeof(uint64_t)) scratch_.allocate(dev_.n_chains * sizeof(uint64_t), ignored);
+    cuda_check(launch_checksums(dev_, scratch_.as<unsigned long long>(), stream_), "checksum kernel");
+    ++other_launches;
+    download(out, scratch_.as<void>(), dev_.n_chains, stream_);
+}
+
+void Batch::read_coherence(uint64_t* out) {
+    bind_device();
+    if (out == nullptr) throw Error("null argument");
+    size_t ignored = 0;
+    if (scratch_.bytes() < dev_.n_chains * sizeof(uint64_t)) scratch_.allocate(dev_.n_chains * sizeof(uint64_t), ignored);
+    cuda_check(launch_coherence(dev_, scratch_.as<unsigned long long>(), stream_), "coherence kernel");
+    ++other_launches;
+    download(out, scratch_.as<void>(), dev_.n_chains, stream_);
+}
+
+void Batch::read_slots(uint32_t* out) {
+    bind_device();
+    if (out == nullptr) throw Error("null argument");
+    download(out, dev_.slot_of_chain, dev_.n_chains, stream_);
+}
+
+void Batch::read_swap_stats(uint64_t* acc, uint64_t* att) {
+    bind_device();
+    if (acc != nullptr) download(acc, dev_.swap_acc, dev_.n_chains, stream_);
+    if (att != nullptr) download(att, dev_.swap_att, dev_.n_chains, stream_);
+}
+
+void Batch::pack_results(void* device_out) {
+    bind_device();
+    if (device_out == nullptr) throw Error("null argument");
+    cuda_check(launch_pack_results(dev_, device_out, stream_), "pack kernel");
+    ++other_launches;
+    cuda_check(cudaStreamSynchronize(stream_), "pack");
+}
+
+}  // namespace isingb200

@@ -1,0 +1,76 @@
+// Device-side description of a batch and the kernel launchers.  Layout (HBM):
+//
+//   chains are packed in TILES of 32 — one tile per warp, lane = chain ("replica").  A tile
+//   never mixes models, so every graph access of a warp is warp-uniform.
+//     hs, ht      f32 [tile][spin][32]     replica-interleaved effective fields
+//     spin_bits   u32 [tile][spin]         bit `lane` set <=> that chain's spin is -1
+//     mt          u32 [tile][624][32]      replica-interleaved MT19937 state (the reference's
+//                                          InterlacedMt layout words[w*K+k], rng.hpp:51-53, K=32)
+//     mt_pos      u32 [tile]               next state word to regenerate (all lanes in lockstep)
+//   per chain:  slot (beta index), running energy f64, flips u64
+//   per ladder: chain_at_slot[n_betas], swap MT state [624][n_ladders], accept/attempt counts
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace isingb200 {
+
+constexpr uint32_t kMtWords = 624;  // MT19937 state words per chain (ref: rng.hpp:11)
+
+struct DevModel {
+    uint32_t n_spins;
+    uint32_t has_tau;
+    const float* h;
+    const uint32_t* offsets;
+    const uint32_t* targets;
+    const float* couplings;
+    const uint8_t* tau_counts;
+};
+
+struct DevBatch {
+    uint32_t n_spins;
+    uint32_t n_tiles;
+    uint32_t n_chains;
+    uint32_t n_ladders;
+    uint32_t n_betas;
+    float tau_scale;
+    int exp_kind;
+    const DevModel* models;
+    const uint32_t* tile_first;  // first chain of the tile
+    const uint32_t* tile_count;  // active lanes
+    const uint32_t* tile_model;
+    const uint32_t* chain_loc;   // chain -> tile*32 + lane
+    const uint32_t* seeds;       // per chain
+    const float* betas;          // n_betas
+    uint32_t* slot_of_chain;
+    uint32_t* chain_at_slot;     // [ladder][n_betas] -> global chain id
+    float* hs;
+    float* ht;                   // nullptr when no model has tau edges
+    uint32_t* spin_bits;
+    uint32_t* mt;
+    uint32_t* mt_pos;
+    double* e_run;
+    unsigned long long* flips;
+    // tempering
+    const uint32_t* swap_seeds;  // per ladder
+    uint32_t* swap_mt;           // [624][n_ladders]
+    uint32_t* swap_pos;          // per ladder
+    unsigned long long* swap_acc;  // [ladder][n_betas]
+    unsigned long long* swap_att;
+};
+
+// All launchers enqueue on `stream` and return the launch error (cudaGetLastError).
+cudaError_t launch_init(const DevBatch& b, const int8_t* initial_spins_dev, cudaStream_t stream);
+cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_t stream);
+cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
+cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);
+cudaError_t launch_checksums(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);
+cudaError_t launch_coherence(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);
+cudaError_t launch_unpack_spins(const DevBatch& b, uint32_t first_chain, uint32_t n_chains,
+                                int8_t* out_dev, cudaStream_t stream);
+cudaError_t launch_gather_fields(const DevBatch& b, uint32_t chain, float* hs_dev, float* ht_dev,
+                                 cudaStream_t stream);
+cudaError_t launch_pack_results(const DevBatch& b, void* out_dev, cudaStream_t stream);
+
+}  // namespace isingb200

@@ -1,0 +1,463 @@
+// Generic-graph kernels: state lives in HBM in the replica-interleaved layout described in
+// device_batch.hpp, one warp per tile of 32 chains, lane = chain.  Every chain follows the
+// reference's scalar engine exactly (ref: proj/src/sweep_basic.cpp:12-56): spins in index
+// order, one MT19937 draw per attempt, accept iff u < exp_kind(x) with no clamp, neighbour
+// fields decremented by (2s)*J in adjacency order.
+#include "device_batch.hpp"
+#include "device_math.cuh"
+
+namespace isingb200 {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kThreads = kWarpsPerBlock * 32;
+constexpr int kChunk = 8;  // attempts whose random draws are generated together
+
+// ---------------------------------------------------------------------------------------
+// One chain's MT19937 inside a replica-interleaved block: word i lives at w[i * stride].
+// The state is regenerated in place one word per draw (the classic loop of
+// ref: rng.cpp:89-96, unrolled in time): draw j of a block rewrites word j from the old words
+// j, j+1 and word j+397 (already new once j >= 227), which is exactly what a whole-block twist
+// followed by reading word j produces.
+struct MtLane {
+    uint32_t* w;
+    uint32_t stride;
+    uint32_t pos;  // next word to regenerate, 0..623
+    uint32_t cur;  // old value of word `pos`
+
+    __device__ __forceinline__ void open(uint32_t* base, uint32_t stride_, uint32_t pos_) {
+        w = base;
+        stride = stride_;
+        pos = pos_;
+        cur = w[size_t(pos) * stride];
+    }
+
+    __device__ __forceinline__ uint32_t next_raw() {
+        const uint32_t jn = pos + 1 == kMtN ? 0u : pos + 1;
+        const uint32_t jf = pos >= kMtN - kMtM ? pos - (kMtN - kMtM) : pos + kMtM;
+        const uint32_t nxt = w[size_t(jn) * stride];
+        const uint32_t far = w[size_t(jf) * stride];
+        const uint32_t v = mt_recurrence(cur, nxt, far);
+        w[size_t(pos) * stride] = v;
+        cur = nxt;
+        pos = jn;
+        return mt_temper(v);
+    }
+
+    // `count` (<= kChunk) draws with every load issued before the first store: none of the
+    // words read here is rewritten inside the chunk (the far word is 227 draws old or newer
+    // by a whole block), so the loads overlap instead of serialising on L2 latency.
+    __device__ __forceinline__ void next_chunk(uint32_t count, float (&u)[kChunk]) {
+        uint32_t nxt[kChunk], far[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            if (uint32_t(k) < count) {
+                uint32_t jn = pos + k + 1;
+                jn = jn >= kMtN ? jn - kMtN : jn;
+                uint32_t jf = pos + k + kMtM;
+                jf = jf >= kMtN ? jf - kMtN : jf;
+                nxt[k] = w[size_t(jn) * stride];
+                far[k] = w[size_t(jf) * stride];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            if (uint32_t(k) < count) {
+                const uint32_t v = mt_recurrence(cur, nxt[k], far[k]);
+                uint32_t j = pos + k;
+                j = j >= kMtN ? j - kMtN : j;
+                w[size_t(j) * stride] = v;
+                cur = nxt[k];
+                u[k] = u32_to_unit(mt_temper(v));
+            }
+        }
+        pos += count;
+        pos = pos >= kMtN ? pos - kMtN : pos;
+    }
+};
+
+// ref: Mt19937::reseed, rng.cpp:37-44
+__device__ void mt_seed_lane(uint32_t* w, uint32_t stride, uint32_t seed) {
+    uint32_t prev = seed;
+    w[0] = prev;
+    for (uint32_t i = 1; i < kMtN; ++i) {
+        prev = 1812433253u * (prev ^ (prev >> 30)) + i;
+        w[size_t(i) * stride] = prev;
+    }
+}
+
+struct TileView {
+    uint32_t tile, lane, chain;
+    bool active;
+    DevModel model;
+    float* hs;
+    float* ht;
+    uint32_t* words;
+    uint32_t* mt;
+};
+
+__device__ __forceinline__ bool open_tile(const DevBatch& b, TileView& t) {
+    t.tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (t.tile >= b.n_tiles) return false;
+    t.lane = threadIdx.x & 31u;
+    t.active = t.lane < b.tile_count[t.tile];
+    t.chain = b.tile_first[t.tile] + t.lane;
+    t.model = b.models[b.tile_model[t.tile]];
+    const size_t base = size_t(t.tile) * b.n_spins;
+    t.hs = b.hs + base * 32 + t.lane;
+    t.ht = b.ht ? b.ht + base * 32 + t.lane : nullptr;
+    t.words = b.spin_bits + base;
+    t.mt = b.mt + size_t(t.tile) * kMtN * 32 + t.lane;
+    return true;
+}
+
+__device__ __forceinline__ float spin_of(uint32_t word, uint32_t lane) {
+    return (word >> lane) & 1u ? -1.0f : 1.0f;
+}
+
+// ref: recompute_fields, sweep_state.cpp:236-255 — f32 sums in adjacency order, h_i first.
+__device__ __forceinline__ void fields_of_spin(const DevModel& m, const uint32_t* words,
+                                               uint32_t lane, uint32_t i, float& hs, float& ht) {
+    const uint32_t end = m.offsets[i + 1], mid = end - m.tau_counts[i];
+    float a = m.h[i];
+    for (uint32_t e = m.offsets[i]; e < mid; ++e) {
+        a = __fadd_rn(a, __fmul_rn(m.couplings[e], spin_of(words[m.targets[e]], lane)));
+    }
+    float c = 0.0f;
+    for (uint32_t e = mid; e < end; ++e) {
+        c = __fadd_rn(c, __fmul_rn(m.couplings[e], spin_of(words[m.targets[e]], lane)));
+    }
+    hs = a;
+    ht = c;
+}
+
+// ref: total_cost, model.cpp:108-126 — f64, index order, each undirected edge once (t > i).
+__device__ double chain_cost(const DevModel& m, const uint32_t* words, uint32_t lane) {
+    double cost = 0.0;
+    for (uint32_t i = 0; i < m.n_spins; ++i) {
+        const double si = double(spin_of(words[i], lane));
+        cost = __dsub_rn(cost, __dmul_rn(double(m.h[i]), si));
+        for (uint32_t e = m.offsets[i]; e < m.offsets[i + 1]; ++e) {
+            const uint32_t t = m.targets[e];
+            if (t > i) {
+                const double st = double(spin_of(words[t], lane));
+                cost = __dsub_rn(cost, __dmul_rn(__dmul_rn(double(m.couplings[e]), si), st));
+            }
+        }
+    }
+    return cost;
+}
+
+// ref: state_checksum, sweep_state.cpp:325-336
+__device__ unsigned long long chain_checksum(const uint32_t* words, uint32_t n, uint32_t lane) {
+    unsigned long long h = 1469598103934665603ull;
+    for (uint32_t i = 0; i < n; ++i) {
+        h ^= (unsigned long long)(((words[i] >> lane) & 1u) ^ 1u);  // 1 for s > 0
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+// ---------------------------------------------------------------------------------------
+// init_state for every chain of a tile (ref: sweep_state.cpp:160-234).
+__global__ void __launch_bounds__(kThreads) init_kernel(DevBatch b, const int8_t* initial) {
+    TileView t;
+    if (!open_tile(b, t)) return;
+    const uint32_t n = b.n_spins;
+    const uint32_t seed = t.active ? b.seeds[t.chain] : 0u;
+
+    if (initial == nullptr) {
+        // initial_spins(): a generator kept apart from the sweep stream, bit 31 -> -1
+        mt_seed_lane(t.mt, 32, seed ^ kInitSpinSeedMix);
+        MtLane g;
+        g.open(t.mt, 32, 0);
+        for (uint32_t i = 0; i < n; ++i) {
+            const bool neg = t.active && (g.next_raw() >> 31);
+            const uint32_t word = __ballot_sync(0xffffffffu, neg);
+            if (t.lane == 0) t.words[i] = word;
+        }
+    } else {
+        const int8_t* mine = initial + size_t(t.chain) * n;
+        for (uint32_t i = 0; i < n; ++i) {
+            const bool neg = t.active && mine[i] < 0;
+            const uint32_t word = __ballot_sync(0xffffffffu, neg);
+            if (t.lane == 0) t.words[i] = word;
+        }
+    }
+    __syncwarp();
+    mt_seed_lane(t.mt, 32, seed);
+    if (t.lane == 0) b.mt_pos[t.tile] = 0;
+
+    for (uint32_t i = 0; i < n; ++i) {
+        float a, c;
+        fields_of_spin(t.model, t.words, t.lane, i, a, c);
+        t.hs[size_t(i) * 32] = a;
+        if (t.ht) t.ht[size_t(i) * 32] = c;
+    }
+    if (t.active) {
+        b.e_run[t.chain] = chain_cost(t.model, t.words, t.lane);
+        b.flips[t.chain] = 0ull;
+    }
+}
+
+// Swap generators: one thread per ladder.
+__global__ void init_swap_kernel(DevBatch b) {
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= b.n_ladders) return;
+    mt_seed_lane(b.swap_mt + l, b.n_ladders, b.swap_seeds[l] ^ kSwapSeedMix);
+    b.swap_pos[l] = 0;
+    for (uint32_t k = 0; k < b.n_betas; ++k) {
+        b.chain_at_slot[size_t(l) * b.n_betas + k] = l * b.n_betas + k;
+        b.slot_of_chain[size_t(l) * b.n_betas + k] = k;
+        b.swap_acc[size_t(l) * b.n_betas + k] = 0ull;
+        b.swap_att[size_t(l) * b.n_betas + k] = 0ull;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// The sweep.  TAU selects models with tau edges (two field arrays); generic models keep
+// h_eff_tau == +0 forever, and hs + gamma*(+0) only differs from hs in the sign of a zero,
+// which no exp_kind can see, so the tau array is neither stored nor read for them.
+template <int EXP, bool TAU>
+__global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uint32_t sweeps) {
+    TileView t;
+    if (!open_tile(b, t)) return;
+    const uint32_t n = b.n_spins;
+    const DevModel& m = t.model;
+    const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
+    const float gamma = b.tau_scale;
+    double e_run = t.active ? b.e_run[t.chain] : 0.0;
+    unsigned long long flips = 0;
+
+    MtLane g;
+    g.open(t.mt, 32, b.mt_pos[t.tile]);
+
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk) {
+            const uint32_t count = min(uint32_t(kChunk), n - i0);
+            float u[kChunk];
+            uint32_t word[kChunk];
+            g.next_chunk(count, u);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (uint32_t(k) < count) word[k] = t.words[i0 + k];
+            }
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (uint32_t(k) >= count) break;
+                const uint32_t i = i0 + k;
+                const float two_s = (word[k] >> t.lane) & 1u ? -2.0f : 2.0f;
+                const float hsi = t.hs[size_t(i) * 32];
+                float hti = 0.0f;
+                float x;
+                if constexpr (TAU) {
+                    hti = t.ht[size_t(i) * 32];
+                    x = flip_exponent(neg_beta, gamma, two_s, hsi, hti);
+                } else {
+                    x = __fmul_rn(neg_beta, __fmul_rn(two_s, hsi));
+                }
+                const float p = exp_kind<EXP>(x);
+                const bool accept = t.active && (u[k] < p);
+                const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+                if (ballot != 0u) {
+                    const uint32_t end = m.offsets[i + 1];
+                    const uint32_t mid = TAU ? end - m.tau_counts[i] : end;
+                    for (uint32_t e = m.offsets[i]; e < mid; ++e) {
+                        const size_t at = size_t(m.targets[e]) * 32;
+                        const float d = __fmul_rn(two_s, m.couplings[e]);
+                        if (accept) t.hs[at] = __fsub_rn(t.hs[at], d);
+                    }
+                    if constexpr (TAU) {
+                        for (uint32_t e = mid; e < end; ++e) {
+                            const size_t at = size_t(m.targets[e]) * 32;
+                            const float d = __fmul_rn(two_s, m.couplings[e]);
+                            if (accept) t.ht[at] = __fsub_rn(t.ht[at], d);
+                        }
+                    }
+                    if (accept) {
+                        ++flips;
+                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(hsi, hti))));
+                    }
+                    if (t.lane == 0) t.words[i] = word[k] ^ ballot;
+                }
+            }
+        }
+        __syncwarp();  // lane 0's spin-word stores become visible to the whole warp
+    }
+
+    if (t.lane == 0) b.mt_pos[t.tile] = g.pos;
+    if (t.active) {
+        b.e_run[t.chain] = e_run;
+        b.flips[t.chain] += flips;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Tempering swap round (new semantics, oracle/ising_oracle.h): pairs of
+// slots (k,k+1), k = round&1, +2, ...; one draw per pair from the ladder's own generator;
+// accept iff u < exp_kind(float((beta_k - beta_k1) * (E_a - E_b))); the chains exchange slots.
+__global__ void swap_kernel(DevBatch b, unsigned long long round) {
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= b.n_ladders) return;
+    const uint32_t nb = b.n_betas;
+    MtLane g;
+    g.open(b.swap_mt + l, b.n_ladders, b.swap_pos[l]);
+    uint32_t* at_slot = b.chain_at_slot + size_t(l) * nb;
+    for (uint32_t k = uint32_t(round & 1ull); k + 1 < nb; k += 2) {
+        const uint32_t ca = at_slot[k], cb = at_slot[k + 1];
+        const float u = u32_to_unit(g.next_raw());
+        const double db = __dsub_rn(double(b.betas[k]), double(b.betas[k + 1]));
+        const double de = __dsub_rn(b.e_run[ca], b.e_run[cb]);
+        const float p = exp_kind_dyn(b.exp_kind, __double2float_rn(__dmul_rn(db, de)));
+        ++b.swap_att[size_t(l) * nb + k];
+        if (u < p) {
+            at_slot[k] = cb;
+            at_slot[k + 1] = ca;
+            b.slot_of_chain[ca] = k + 1;
+            b.slot_of_chain[cb] = k;
+            ++b.swap_acc[size_t(l) * nb + k];
+        }
+    }
+    b.swap_pos[l] = g.pos;
+}
+
+// ---------------------------------------------------------------------------------------
+// Readout.
+__global__ void __launch_bounds__(kThreads) energies_kernel(DevBatch b, double* out) {
+    TileView t;
+    if (!open_tile(b, t) || !t.active) return;
+    out[t.chain] = chain_cost(t.model, t.words, t.lane);
+}
+
+__global__ void __launch_bounds__(kThreads) checksums_kernel(DevBatch b, unsigned long long* out) {
+    TileView t;
+    if (!open_tile(b, t) || !t.active) return;
+    out[t.chain] = chain_checksum(t.words, b.n_spins, t.lane);
+}
+
+// ref: field_coherence_ulp / ulp_distance, sweep_state.cpp:338-354
+__device__ __forceinline__ long long ulp_key(float v) {
+    const int bits = __float_as_int(v);
+    return bits < 0 ? 0x80000000ll - (long long)bits : (long long)bits;
+}
+
+__global__ void __launch_bounds__(kThreads) coherence_kernel(DevBatch b, unsigned long long* out) {
+    TileView t;
+    if (!open_tile(b, t) || !t.active) return;
+    unsigned long long worst = 0;
+    for (uint32_t i = 0; i < b.n_spins; ++i) {
+        float a, c;
+        fields_of_spin(t.model, t.words, t.lane, i, a, c);
+        const long long d1 = llabs(ulp_key(t.hs[size_t(i) * 32]) - ulp_key(a));
+        const long long d2 = t.ht ? llabs(ulp_key(t.ht[size_t(i) * 32]) - ulp_key(c)) : 0ll;
+        worst = max(worst, (unsigned long long)max(d1, d2));
+    }
+    out[t.chain] = worst;
+}
+
+__global__ void unpack_spins_kernel(DevBatch b, uint32_t first_chain, uint32_t n_chains,
+                                    int8_t* out) {
+    const size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t total = size_t(n_chains) * b.n_spins;
+    if (idx >= total) return;
+    const uint32_t c = first_chain + uint32_t(idx / b.n_spins);
+    const uint32_t i = uint32_t(idx % b.n_spins);
+    const uint32_t loc = b.chain_loc[c];
+    const uint32_t word = b.spin_bits[size_t(loc >> 5) * b.n_spins + i];
+    out[idx] = (word >> (loc & 31u)) & 1u ? int8_t(-1) : int8_t(1);
+}
+
+__global__ void gather_fields_kernel(DevBatch b, uint32_t chain, float* hs, float* ht) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.n_spins) return;
+    const uint32_t loc = b.chain_loc[chain];
+    const size_t at = (size_t(loc >> 5) * b.n_spins + i) * 32 + (loc & 31u);
+    hs[i] = b.hs[at];
+    ht[i] = b.ht ? b.ht[at] : 0.0f;
+}
+
+struct ResultRecord {  // 32 bytes per chain, see ising_batch_pack_results
+    double energy;
+    double e_run;
+    unsigned long long flips;
+    unsigned long long checksum;
+};
+
+__global__ void __launch_bounds__(kThreads) pack_results_kernel(DevBatch b, ResultRecord* out) {
+    TileView t;
+    if (!open_tile(b, t) || !t.active) return;
+    ResultRecord r;
+    r.energy = chain_cost(t.model, t.words, t.lane);
+    r.e_run = b.e_run[t.chain];
+    r.flips = b.flips[t.chain];
+    r.checksum = chain_checksum(t.words, b.n_spins, t.lane);
+    out[t.chain] = r;
+}
+
+inline dim3 tile_grid(const DevBatch& b) { return dim3((b.n_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock); }
+
+template <int EXP>
+void launch_sweep_exp(const DevBatch& b, uint32_t sweeps, cudaStream_t s) {
+    if (b.ht) sweep_generic_kernel<EXP, true><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+    else sweep_generic_kernel<EXP, false><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+}
+
+}  // namespace
+
+cudaError_t launch_init(const DevBatch& b, const int8_t* initial, cudaStream_t s) {
+    init_kernel<<<tile_grid(b), kThreads, 0, s>>>(b, initial);
+    init_swap_kernel<<<(b.n_ladders + 127) / 128, 128, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_t s) {
+    switch (b.exp_kind) {
+        case kExpExact: launch_sweep_exp<kExpExact>(b, sweeps, s); break;
+        case kExpFast: launch_sweep_exp<kExpFast>(b, sweeps, s); break;
+        default: launch_sweep_exp<kExpAccurate>(b, sweeps, s); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t s) {
+    swap_kernel<<<(b.n_ladders + 127) / 128, 128, 0, s>>>(b, round);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energies(const DevBatch& b, double* out, cudaStream_t s) {
+    energies_kernel<<<tile_grid(b), kThreads, 0, s>>>(b, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_checksums(const DevBatch& b, unsigned long long* out, cudaStream_t s) {
+    checksums_kernel<<<tile_grid(b), kThreads, 0, s>>>(b, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coherence(const DevBatch& b, unsigned long long* out, cudaStream_t s) {
+    coherence_kernel<<<tile_grid(b), kThreads, 0, s>>>(b, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_spins(const DevBatch& b, uint32_t first_chain, uint32_t n_chains,
+                                int8_t* out, cudaStream_t s) {
+    const size_t total = size_t(n_chains) * b.n_spins;
+    if (total == 0) return cudaSuccess;
+    unpack_spins_kernel<<<unsigned((total + 255) / 256), 256, 0, s>>>(b, first_chain, n_chains, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_fields(const DevBatch& b, uint32_t chain, float* hs, float* ht,
+                                 cudaStream_t s) {
+    if (b.n_spins == 0) return cudaSuccess;
+    gather_fields_kernel<<<(b.n_spins + 255) / 256, 256, 0, s>>>(b, chain, hs, ht);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_results(const DevBatch& b, void* out, cudaStream_t s) {
+    pack_results_kernel<<<tile_grid(b), kThreads, 0, s>>>(b, static_cast<ResultRecord*>(out));
+    return cudaGetLastError();
+}
+
+}  // namespace isingb200
