@@ -1,0 +1,254 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs:
+spins, accept counts, beta slots and running energies bit-exact, energies within 1e-5 relative
+(BASELINE.json north_star).  Shapes follow BASELINE.json's five configurations at sizes the
+oracle finishes in seconds."""
+import numpy as np
+import pytest
+
+import paper_1004_0024_b200 as ib
+from paper_1004_0024_b200 import _lib
+from helpers import assert_batch_matches, bits, csr_from_npz, ins, oracle_batch, product_model
+
+pytestmark = pytest.mark.gpu
+
+REL_ENERGY = 1e-5  # north_star tolerance for energies
+KERNELS = [ib.KERNEL_GENERIC]
+
+
+def run_both(port, csrs, n_ladders, betas, sweeps, swap_interval, *, seed0=ins.CHAIN_SEED_BASE, tau_scale=1.0,
+             exp_kind=2, model_of_ladder=None, initial=None, kernel=ib.KERNEL_AUTO, chunks=None):
+    betas = np.atleast_1d(np.asarray(betas, np.float32))
+    chains = n_ladders * betas.size
+    seeds = (seed0 + np.arange(chains)).astype(np.uint32)
+    swap_seeds = (ins.SWAP_SEED_BASE + np.arange(n_ladders)).astype(np.uint32)
+    want = oracle_batch(port, csrs, n_ladders, betas, seeds, swap_seeds, sweeps, swap_interval, tau_scale,
+                        exp_kind, model_of_ladder, initial)
+    models = [product_model(c) for c in csrs]
+    state = ib.init_state(models, betas, n_ladders, seeds=seeds, swap_seeds=swap_seeds,
+                          params=ib.SweepParams(tau_scale, exp_kind), model_of_ladder=model_of_ladder,
+                          initial_spins=initial, kernel=kernel)
+    for part in (chunks or [sweeps]):
+        state.run(part, swap_interval)
+    return state, want
+
+
+@pytest.mark.parametrize("name", ["cubic4_pm1", "cubic6_gauss_h", "mixed6", "layered_24x8", "layered_16x4_gamma"])
+def test_reference_golden_trajectories(lib, golden, name):
+    """Outputs of the reference itself (tests/golden/make_golden.py), no oracle in the loop."""
+    g = golden(f"traj_{name}")
+    csr = csr_from_npz(g)
+    model = product_model(csr)
+    beta, gamma, sweeps = float(g["beta"]), float(g["tau_scale"]), int(g["sweeps"])
+    for kind in (1, 2, 3):
+        seeds = [int(s) for k, s in g["runs"] if k == kind]
+        with ib.init_state(model, [beta], len(seeds), seeds=seeds, params=ib.SweepParams(gamma, kind)) as st:
+            for c, seed in enumerate(seeds):
+                tag = f"k{kind}_s{seed}"
+                np.testing.assert_array_equal(st.spins(c, 1)[0], g[f"{tag}_spins0"])
+                hs, ht = st.fields(c)
+                np.testing.assert_array_equal(bits(hs), bits(g[f"{tag}_hs0"]))
+                np.testing.assert_array_equal(bits(ht), bits(g[f"{tag}_ht0"]))
+            st.run(sweeps // 2)
+            for c, seed in enumerate(seeds):
+                np.testing.assert_array_equal(st.spins(c, 1)[0], g[f"k{kind}_s{seed}_spins_mid"])
+            st.run(sweeps - sweeps // 2)
+            flips, attempts = st.stats()
+            energies, sums, coh = st.energies(), st.checksums(), st.field_coherence_ulp()
+            for c, seed in enumerate(seeds):
+                tag = f"k{kind}_s{seed}"
+                np.testing.assert_array_equal(st.spins(c, 1)[0], g[f"{tag}_spins"])
+                hs, ht = st.fields(c)
+                np.testing.assert_array_equal(bits(hs), bits(g[f"{tag}_hs"]))
+                np.testing.assert_array_equal(bits(ht), bits(g[f"{tag}_ht"]))
+                assert flips[c] == g[f"{tag}_flips"] and attempts[c] == g[f"{tag}_attempts"]
+                assert energies[c] == pytest.approx(float(g[f"{tag}_cost"]), rel=REL_ENERGY)
+                assert energies[c] == float(g[f"{tag}_cost"])  # same f64 summation order: exact
+                assert sums[c] == g[f"{tag}_checksum"]
+                assert coh[c] == g[f"{tag}_coherence"]
+
+
+def test_two_spin_hand_trace_and_frozen_chain(lib, golden):
+    # ref: tests/test_sweep.cpp:122-145
+    two = ib.SpinModel.from_csr(2, [0, 0], [0, 1, 2], [1, 0], [1.0, 1.0])
+    with ib.init_state(two, [0.0], 1, seeds=[1], params=ib.SweepParams(1.0, ib.ExpKind.exact),
+                       initial_spins=[[1, -1]]) as st:
+        hs, ht = st.fields(0)
+        assert hs.tolist() == [-1.0, 1.0] and ht.tolist() == [0.0, 0.0]
+        st.run(1)
+        assert st.spins()[0].tolist() == [-1, 1]
+        st.run(1)
+        assert st.spins()[0].tolist() == [1, -1]
+        flips, attempts = st.stats()
+        assert flips[0] == 4 and attempts[0] == 4
+        np.testing.assert_array_equal(st.spins()[0], golden("traj_two_spin")["spins"])
+    one = ib.SpinModel.from_csr(1, [1.0], [0, 0], [], [])
+    for kind in (1, 2, 3):
+        with ib.init_state(one, [200.0], 1, seeds=[1], params=ib.SweepParams(1.0, kind), initial_spins=[[1]]) as st:
+            st.run(100)
+            assert st.stats()[0][0] == 0 and st.spins()[0].tolist() == [1]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c1_single_chain_cubic(lib, port, kernel):
+    """BASELINE config 1: 16^3 periodic lattice, J = +/-1, h = 0, one replica at beta = 1."""
+    csr = ins.cubic_pm1(16, ins.INSTANCE_SEED, 0.0)
+    state, want = run_both(port, [csr], 1, [1.0], 1000, 0, kernel=kernel)
+    e = assert_batch_matches(state, want, REL_ENERGY)
+    assert 0.05 < want["flips"][0] / (1000 * 4096) < 0.15
+    assert state.checksums()[0] == ib.state_checksum(want["spins"][0])
+    assert abs(state.running_energies()[0] - e[0]) == 0.0  # +/-1 couplings, h = 0: every dE is exact
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("exp_kind", [1, 2, 3])
+def test_c2_many_replicas_gaussian_fields(lib, port, kernel, exp_kind):
+    """BASELINE config 2 shape: same lattice, h ~ N(0, 0.5^2), replicas seeded base + id; a chain
+    count that leaves a ragged last tile."""
+    csr = ins.cubic_pm1(16, ins.INSTANCE_SEED, 0.5)
+    state, want = run_both(port, [csr], 70, [1.0], 60, 0, exp_kind=exp_kind, kernel=kernel)
+    assert_batch_matches(state, want, REL_ENERGY)
+    assert state.info()["n_tiles"] == 3
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c3_tempering_mixed_degree_distinct_graphs(lib, port, kernel):
+    """BASELINE config 3 shape: lattice + 0-2 extra edges per spin, Gaussian J and h, a geometric
+    ladder with a swap attempt every sweep, every system its own graph."""
+    csrs = [ins.cubic_mixed_degree(8, ins.INSTANCE_SEED + k) for k in range(5)]
+    betas = ins.geometric_betas(0.1, 3.0, 32)
+    state, want = run_both(port, csrs, 5, betas, 120, 1, kernel=kernel)
+    assert_batch_matches(state, want, REL_ENERGY)
+    assert want["swap_acc"].sum() > 100 and (want["swap_att"][:, :31].sum(1) == 120 * 31 // 2).all()
+    assert (np.sort(want["slot"].reshape(5, 32), 1) == np.arange(32)).all()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("swap_interval", [1, 10])
+def test_c4_layered_tempering(lib, port, kernel, swap_interval):
+    """BASELINE config 4/5 shape: identical layers, J = +/-1, J_perp = 1.5 ring along tau, Gaussian h."""
+    csrs = [ins.build_layered_csr(*ins.layered_spec(32, ins.INSTANCE_SEED + k), 8, 1.5) for k in range(3)]
+    betas = ins.geometric_betas(0.2, 5.0, 16)
+    state, want = run_both(port, csrs, 3, betas, 90, swap_interval, kernel=kernel)
+    assert_batch_matches(state, want, REL_ENERGY)
+    assert want["swap_acc"].sum() > 0
+    # tau fields only ever take the values {-2J, 0, +2J} (the basis of the on-chip tau elision)
+    _, ht = state.fields(7)
+    assert set(np.unique(ht)).issubset({-3.0, 0.0, 3.0})
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_shared_graph_many_ladders_tau_scale(lib, port, kernel):
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 77), 6, 0.75)
+    betas = ins.geometric_betas(0.3, 2.0, 6)
+    state, want = run_both(port, [csr], 11, betas, 50, 2, tau_scale=0.5, exp_kind=3, kernel=kernel)
+    assert_batch_matches(state, want, REL_ENERGY)
+
+
+def test_split_runs_equal_one_run(lib, port):
+    """run(a); run(b) == run(a + b): the swap cadence counts sweeps since creation."""
+    csr = ins.cubic_mixed_degree(6, 9)
+    betas = ins.geometric_betas(0.2, 2.0, 4)
+    state, want = run_both(port, [csr], 6, betas, 35, 3, chunks=[1, 4, 7, 0, 23])
+    assert_batch_matches(state, want, REL_ENERGY)
+
+
+def test_explicit_swap_round_matches_interval(lib, port):
+    csr = ins.cubic_mixed_degree(6, 9)
+    betas = ins.geometric_betas(0.2, 2.0, 5)
+    seeds = np.arange(40, 50, dtype=np.uint32)
+    want = oracle_batch(port, [csr], 2, betas, seeds, [5, 6], 12, 4)
+    with ib.init_state(product_model(csr), betas, 2, seeds=seeds, swap_seeds=[5, 6]) as st:
+        for _ in range(3):
+            st.run(4, 0)
+            st.swap()
+        assert_batch_matches(st, want, REL_ENERGY)
+
+
+def test_results_do_not_depend_on_batch_composition(lib, port):
+    """The reference's worker-count invariance (ref: tests/test_bench.cpp:153-166) as the
+    multi-GPU property: a ladder's bits are the same alone, in a big batch, or in a shard
+    addressed through first_ladder."""
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 3), 4, 1.5)
+    model = product_model(csr)
+    betas = ins.geometric_betas(0.2, 3.0, 8)
+    with ib.init_state(model, betas, 9, base_seed=100, swap_base_seed=900) as full:
+        full.run(40, 5)
+        all_spins, all_sums, all_slots = full.spins(), full.checksums(), full.slots()
+    for first, count in ((0, 4), (4, 5), (8, 1)):
+        with ib.init_state(model, betas, count, base_seed=100, swap_base_seed=900, first_ladder=first) as part:
+            part.run(40, 5)
+            np.testing.assert_array_equal(part.spins(), all_spins[first * 8:(first + count) * 8])
+            np.testing.assert_array_equal(part.checksums(), all_sums[first * 8:(first + count) * 8])
+            np.testing.assert_array_equal(part.slots(), all_slots[first * 8:(first + count) * 8])
+
+
+def test_edge_cases(lib, port):
+    # one spin, no edges; 33 chains (ragged second tile); zero sweeps; isolated spins in a graph
+    one = dict(n_spins=1, h=np.array([0.3], np.float32), offsets=[0, 0], targets=[], couplings=[])
+    state, want = run_both(port, [one], 33, [0.7], 500, 0)
+    assert_batch_matches(state, want)
+    state, want = run_both(port, [one], 1, [0.7], 0, 0)
+    assert_batch_matches(state, want)
+    iso = dict(n_spins=5, h=np.array([0.1, -0.2, 0, 1, -1], np.float32), offsets=[0, 1, 1, 2, 2, 2],
+               targets=[2, 0], couplings=[0.5, 0.5])
+    state, want = run_both(port, [iso], 2, [0.2, 1.5], 300, 1)
+    assert_batch_matches(state, want)
+    # beta = 0 with the exact exponential: every attempt is accepted
+    with ib.init_state(product_model(iso), [0.0], 1, params=ib.SweepParams(1.0, 1)) as st:
+        st.run(11)
+        assert st.stats()[0][0] == 55
+
+
+def test_one_shot_run_report(lib, port):
+    """ref: ising_run, include/isingmc.h:74-106 / tests/test_capi.cpp:129-148."""
+    csr = ins.cubic_pm1(6, 11, 0.5)
+    rep = ib.run_single(product_model(csr), 200, 0.9, 321, exp_kind=ib.ExpKind.default)
+    model = port.model(csr)
+    chain = port.chain(model, 321, 0.9, 1.0, 2)
+    chain.sweep(200)
+    assert rep["flips"] == chain.flips and rep["attempts"] == 200 * 216
+    assert rep["checksum"] == port.checksum(chain.spins)
+    assert rep["final_cost"] == port.total_cost(model, chain.spins)
+    assert rep["flip_rate"] == chain.flips / (200 * 216)
+
+
+def test_argument_errors(lib):
+    # ref: check_engine_model, src/sweep_state.cpp:148-157; capi status mapping capi.cpp:37-59
+    model = product_model(ins.cubic_pm1(3, 1, 0.0))
+    other = product_model(ins.cubic_pm1(4, 1, 0.0))
+    cases = [
+        (dict(betas=[-1.0]), "beta must be finite"),
+        (dict(betas=[float("nan")]), "beta must be finite"),
+        (dict(betas=[1.0], params=ib.SweepParams(float("inf"), 2)), "tau_scale must be finite"),
+        (dict(betas=[1.0], params=ib.SweepParams(1.0, 9)), "invalid exp_kind"),
+        (dict(betas=[1.0], device=99), "invalid device"),
+        (dict(betas=[1.0], n_ladders=0), "at least one chain"),
+        (dict(betas=[1.0], initial_spins=[[0] * 27]), "spins must be +/-1"),
+    ]
+    for kwargs, text in cases:
+        kwargs.setdefault("n_ladders", 1)
+        with pytest.raises(ib.IsingError) as err:
+            ib.init_state(model, **kwargs)
+        assert err.value.status == _lib.ISING_ERR_ARGUMENT and text in str(err.value), str(err.value)
+    with pytest.raises(ib.IsingError) as err:
+        ib.init_state([model, other], [1.0], 2)
+    assert "same spin count" in str(err.value)
+    with ib.init_state(model, [1.0], 2) as st:
+        with pytest.raises(ib.IsingError):
+            st.spins(1, 5)
+        with pytest.raises(ib.IsingError):
+            st.fields(2)
+
+
+def test_pack_results_matches_host_readouts(lib):
+    import torch
+    csr = ins.cubic_mixed_degree(6, 9)
+    with ib.init_state(product_model(csr), ins.geometric_betas(0.2, 2.0, 4), 5) as st:
+        st.run(30, 2)
+        buf = torch.zeros(st.n_chains * 4, dtype=torch.int64, device="cuda")
+        st.pack_results(buf.data_ptr())
+        rec = buf.cpu().numpy().reshape(-1, 4)
+        np.testing.assert_array_equal(rec[:, 0].view(np.float64), st.energies())
+        np.testing.assert_array_equal(rec[:, 1].view(np.float64), st.running_energies())
+        np.testing.assert_array_equal(rec[:, 2].view(np.uint64), st.stats()[0])
+        np.testing.assert_array_equal(rec[:, 3].view(np.uint64), st.checksums())
