@@ -270,10 +270,13 @@ class Reference:
         lib.ref_chain_coherence.argtypes = [C.c_void_p, C.c_void_p]
         lib.ref_flip_probability.restype = C.c_float
         lib.ref_flip_probability.argtypes = [C.c_void_p, C.c_uint32]
-        lib.ref_run_ladders.restype = C.c_double
-        lib.ref_run_ladders.argtypes = [C.POINTER(C.c_void_p), C.c_uint32, C.c_uint32, f32p, u32p, u32p,
-                                        C.c_float, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32,
-                                        u64p, f64p]
+        lib.ref_ladders_create.restype = C.c_void_p
+        lib.ref_ladders_create.argtypes = [C.POINTER(C.c_void_p), C.c_uint32, C.c_uint32, f32p, u32p, u32p,
+                                           C.c_float, C.c_int, C.c_int]
+        lib.ref_ladders_free.argtypes = [C.c_void_p]
+        lib.ref_ladders_run.restype = C.c_double
+        lib.ref_ladders_run.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32]
+        lib.ref_ladders_read.argtypes = [C.c_void_p, u64p, f64p]
         self.lib = lib
 
     def error(self) -> str:
@@ -325,20 +328,37 @@ class Reference:
     def chain(self, model, seed, beta, tau_scale=1.0, exp_kind=EXP_FAST, initial=None, engine=1):
         return RefChain(self, model, seed, beta, tau_scale, exp_kind, initial, engine)
 
-    def run_ladders(self, models, n_ladders, betas, seeds, swap_seeds, sweeps, swap_interval, tau_scale=1.0,
-                    exp_kind=EXP_FAST, threads=1, engine=1) -> dict:
-        """Timed multi-threaded CPU run (the reference arm of bench.py)."""
+    def ladders(self, models, n_ladders, betas, seeds, swap_seeds, tau_scale=1.0, exp_kind=EXP_FAST, engine=1):
+        """Persistent set of ladders for timed multi-threaded CPU runs (bench.py's reference arm)."""
+        return RefLadders(self, models, n_ladders, betas, seeds, swap_seeds, tau_scale, exp_kind, engine)
+
+
+class RefLadders:
+    def __init__(self, ref, models, n_ladders, betas, seeds, swap_seeds, tau_scale, exp_kind, engine):
+        self.ref, self.models = ref, models
         betas = np.ascontiguousarray(betas, np.float32)
-        nb = betas.size
+        self.n_chains = n_ladders * betas.size
         seeds = np.ascontiguousarray(seeds, np.uint32)
         swap = None if swap_seeds is None else np.ascontiguousarray(swap_seeds, np.uint32)
-        flips = np.zeros(n_ladders * nb, np.uint64)
-        energy = np.zeros(n_ladders * nb, np.float64)
         handles = (C.c_void_p * n_ladders)(*[m.handle for m in models])
-        secs = self.lib.ref_run_ladders(handles, n_ladders, nb, _p(betas, C.c_float), _p(seeds, C.c_uint32),
-                                        _p(swap, C.c_uint32), tau_scale, exp_kind, engine, sweeps,
-                                        swap_interval, threads, _p(flips, C.c_uint64), _p(energy, C.c_double))
-        return dict(seconds=secs, flips=flips, energy=energy)
+        self.handle = ref.lib.ref_ladders_create(handles, n_ladders, betas.size, _p(betas, C.c_float),
+                                                 _p(seeds, C.c_uint32), _p(swap, C.c_uint32), tau_scale,
+                                                 exp_kind, engine)
+        if not self.handle:
+            raise ValueError(ref.error())
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            self.ref.lib.ref_ladders_free(self.handle)
+            self.handle = None
+
+    def run(self, sweeps, swap_interval, threads) -> float:
+        return self.ref.lib.ref_ladders_run(self.handle, sweeps, swap_interval, threads)
+
+    def read(self):
+        flips, energy = np.zeros(self.n_chains, np.uint64), np.zeros(self.n_chains, np.float64)
+        self.ref.lib.ref_ladders_read(self.handle, _p(flips, C.c_uint64), _p(energy, C.c_double))
+        return flips, energy
 
 
 class RefModel:

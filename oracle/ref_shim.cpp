@@ -3,6 +3,7 @@
 // oracle/_ref/libisingref.so).  Nothing here restates an algorithm: every call forwards to
 // the reference's own C++ API (include/isingmc/{rng,fastexp,model,sweep}.hpp).  Used to pin
 // oracle/ising_oracle.c, to generate tests/golden/, and as the "reference" CPU baseline.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -179,60 +180,90 @@ float ref_flip_probability(const void* s, uint32_t spin) {
 // reference has no tempering and exposes no per-flip hook, so the swap step here uses
 // total_cost() energies at the swap point (same pair schedule and draw as the oracle's
 // definition); it is <2% of the CPU time and is timing scaffolding, not a parity path.
-// Returns seconds spent in the sweep(+swap) loop; state setup is outside the clock.
-double ref_run_ladders(const void* const* models, uint32_t n_ladders, uint32_t n_betas,
-                       const float* betas, const uint32_t* seeds, const uint32_t* swap_seeds,
-                       float tau_scale, int exp_kind, int engine, uint64_t sweeps,
-                       uint32_t swap_interval, uint32_t threads, uint64_t* flips_out,
-                       double* energy_out) {
+struct RefLadders {
     struct Ladder {
+        const SpinModel* model;
         std::vector<SweepState> chains;
         std::vector<uint32_t> at_slot;
+        Mt19937 swap_rng{0};
+        uint64_t round = 0;
     };
-    std::vector<Ladder> ladders(n_ladders);
-    for (uint32_t l = 0; l < n_ladders; ++l) {
-        const auto& model = *static_cast<const SpinModel*>(models[l]);
-        for (uint32_t k = 0; k < n_betas; ++k) {
-            EngineConfig cfg;
-            cfg.engine = engine_of(engine);
-            cfg.params = {betas[k], tau_scale, exp_of(exp_kind)};
-            cfg.seed = seeds[size_t(l) * n_betas + k];
-            ladders[l].chains.push_back(init_state(model, cfg));
-            ladders[l].at_slot.push_back(k);
+    std::vector<Ladder> ladders;
+    std::vector<float> betas;
+    int exp_kind = 2;
+    uint64_t sweeps_done = 0;
+};
+
+void* ref_ladders_create(const void* const* models, uint32_t n_ladders, uint32_t n_betas,
+                         const float* betas, const uint32_t* seeds, const uint32_t* swap_seeds,
+                         float tau_scale, int exp_kind, int engine) {
+    try {
+        auto* set = new RefLadders;
+        set->betas.assign(betas, betas + n_betas);
+        set->exp_kind = exp_kind;
+        set->ladders.resize(n_ladders);
+        for (uint32_t l = 0; l < n_ladders; ++l) {
+            auto& lad = set->ladders[l];
+            lad.model = static_cast<const SpinModel*>(models[l]);
+            lad.swap_rng.reseed((swap_seeds ? swap_seeds[l] : 0u) ^ 0x85EBCA6Bu);
+            for (uint32_t k = 0; k < n_betas; ++k) {
+                EngineConfig cfg;
+                cfg.engine = engine_of(engine);
+                cfg.params = {betas[k], tau_scale, exp_of(exp_kind)};
+                cfg.seed = seeds[size_t(l) * n_betas + k];
+                lad.chains.push_back(init_state(*lad.model, cfg));
+                lad.at_slot.push_back(k);
+            }
         }
+        return set;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
     }
+}
+
+void ref_ladders_free(void* p) { delete static_cast<RefLadders*>(p); }
+
+// Runs `sweeps` more sweeps of every chain (swap round after every swap_interval-th sweep,
+// counted since creation) on `threads` workers; returns the seconds spent.
+double ref_ladders_run(void* p, uint64_t sweeps, uint32_t swap_interval, uint32_t threads) {
+    auto& set = *static_cast<RefLadders*>(p);
+    const uint32_t nb = uint32_t(set.betas.size());
+    const uint64_t base = set.sweeps_done;
     std::atomic<uint32_t> next{0};
     const auto work = [&]() {
         for (;;) {
             const uint32_t l = next.fetch_add(1);
-            if (l >= n_ladders) return;
-            const auto& model = *static_cast<const SpinModel*>(models[l]);
-            Ladder& lad = ladders[l];
-            Mt19937 swap_rng((swap_seeds ? swap_seeds[l] : 0u) ^ 0x85EBCA6Bu);
-            uint64_t round = 0;
-            if (swap_interval == 0 || n_betas < 2) {
+            if (l >= set.ladders.size()) return;
+            auto& lad = set.ladders[l];
+            const SpinModel& model = *lad.model;
+            if (swap_interval == 0 || nb < 2) {
                 for (auto& c : lad.chains) run_sweeps(c, model, sweeps);
                 continue;
             }
-            for (uint64_t sw = 1; sw <= sweeps; ++sw) {
-                for (auto& c : lad.chains) run_sweeps(c, model, 1);
-                if (sw % swap_interval != 0) continue;
-                for (uint32_t k = uint32_t(round & 1u); k + 1 < n_betas; k += 2) {
+            uint64_t left = sweeps, done = base;
+            while (left > 0) {
+                const uint64_t step = std::min<uint64_t>(left, swap_interval - done % swap_interval);
+                for (auto& c : lad.chains) run_sweeps(c, model, step);
+                left -= step;
+                done += step;
+                if (done % swap_interval != 0) continue;
+                for (uint32_t k = uint32_t(lad.round & 1u); k + 1 < nb; k += 2) {
                     const uint32_t a = lad.at_slot[k], b = lad.at_slot[k + 1];
-                    const float u = u32_to_unit(swap_rng.next_u32());
+                    const float u = u32_to_unit(lad.swap_rng.next_u32());
                     const double ea = total_cost(model, std::span<const float>(lad.chains[a].spins));
                     const double eb = total_cost(model, std::span<const float>(lad.chains[b].spins));
-                    const float x = float((double(betas[k]) - double(betas[k + 1])) * (ea - eb));
-                    const float p = exp_kind == 2 ? exp_fast(x)
-                                    : exp_kind == 3 ? exp_accurate(x)
-                                                    : float(std::exp(double(x)));
-                    if (u < p) {
+                    const float x = float((double(set.betas[k]) - double(set.betas[k + 1])) * (ea - eb));
+                    const float pr = set.exp_kind == 2   ? exp_fast(x)
+                                     : set.exp_kind == 3 ? exp_accurate(x)
+                                                         : float(std::exp(double(x)));
+                    if (u < pr) {
                         std::swap(lad.at_slot[k], lad.at_slot[k + 1]);
-                        lad.chains[a].params.beta = betas[k + 1];
-                        lad.chains[b].params.beta = betas[k];
+                        lad.chains[a].params.beta = set.betas[k + 1];
+                        lad.chains[b].params.beta = set.betas[k];
                     }
                 }
-                ++round;
+                ++lad.round;
             }
         }
     };
@@ -241,18 +272,20 @@ double ref_run_ladders(const void* const* models, uint32_t n_ladders, uint32_t n
     for (uint32_t t = 1; t < threads; ++t) pool.emplace_back(work);
     work();
     for (auto& t : pool) t.join();
-    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    for (uint32_t l = 0; l < n_ladders; ++l) {
-        const auto& model = *static_cast<const SpinModel*>(models[l]);
-        for (uint32_t k = 0; k < n_betas; ++k) {
-            const SweepState& c = ladders[l].chains[k];
-            if (flips_out) flips_out[size_t(l) * n_betas + k] = c.stats.flips;
-            if (energy_out) {
-                energy_out[size_t(l) * n_betas + k] = total_cost(model, std::span<const float>(c.spins));
-            }
+    set.sweeps_done += sweeps;
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void ref_ladders_read(const void* p, uint64_t* flips_out, double* energy_out) {
+    const auto& set = *static_cast<const RefLadders*>(p);
+    size_t c = 0;
+    for (const auto& lad : set.ladders) {
+        for (const SweepState& s : lad.chains) {
+            if (flips_out) flips_out[c] = s.stats.flips;
+            if (energy_out) energy_out[c] = total_cost(*lad.model, std::span<const float>(s.spins));
+            ++c;
         }
     }
-    return secs;
 }
 
 }  // extern "C"
