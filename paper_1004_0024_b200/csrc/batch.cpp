@@ -72,10 +72,24 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         if (idx >= models.size()) throw Error("init_state: model_of_ladder entry out of range");
     }
     if (cfg.kernel < 0 || cfg.kernel > 2) throw Error("invalid kernel value " + std::to_string(cfg.kernel));
-    if (cfg.kernel == int(KernelFamily::layered)) {
-        throw Error("init_state: the layered kernel is not available for this batch");
+    // The layered family needs every model to qualify (HostModel::layered_uniform) and one layer
+    // to fit the on-chip window: <= 512 positions (TMEM columns) and the graph within shared memory.
+    uint32_t max_per_layer = 0, max_layer_edges = 0;
+    bool layered_ok = true;
+    for (const HostModel* m : models) {
+        layered_ok = layered_ok && m->layered_uniform;
+        max_per_layer = std::max(max_per_layer, m->per_layer);
+        max_layer_edges = std::max<uint32_t>(max_layer_edges, uint32_t(m->layer_targets.size()));
     }
-    family_ = KernelFamily::generic;
+    const size_t layered_smem = layered_ok ? layered_smem_bytes(max_per_layer, max_layer_edges) : 0;
+    layered_ok = layered_ok && layered_smem != 0;
+    if (cfg.kernel == int(KernelFamily::layered) && !layered_ok) {
+        throw Error("init_state: the layered kernel needs identical-layer models with equal tau couplings "
+                    "and at most 512 positions per layer");
+    }
+    family_ = (cfg.kernel != int(KernelFamily::generic) && layered_ok) ? KernelFamily::layered
+                                                                        : KernelFamily::generic;
+    if (family_ == KernelFamily::layered) any_tau = false;  // the tau field is rebuilt, never stored
 
     // ---- device
     int count = 0;
@@ -127,6 +141,41 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         dev_models.push_back(d);
     }
     upload(models_, dev_models, device_bytes_, stream_);
+
+    if (family_ == KernelFamily::layered) {
+        cudaDeviceProp prop{};
+        cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+        if (prop.major != 10) throw CudaError("the layered kernel needs an sm_100 device (tcgen05 tensor memory)");
+        sm_count_ = prop.multiProcessorCount;
+        std::vector<DevLayerGraph> graphs;
+        for (const HostModel* m : models) {
+            std::vector<uint16_t> targets16(m->layer_targets.begin(), m->layer_targets.end());
+            std::vector<float> j2(m->layer_couplings.size()), tau2(m->per_layer), tau2g(m->per_layer);
+            for (size_t e = 0; e < j2.size(); ++e) j2[e] = 2.0f * m->layer_couplings[e];
+            for (uint32_t p = 0; p < m->per_layer; ++p) {
+                tau2[p] = 2.0f * m->layer_tau[p];
+                tau2g[p] = cfg.tau_scale * tau2[p];  // f32 product, as gamma * h_tau in the reference
+            }
+            DevLayerGraph g{};
+            g.per_layer = m->per_layer;
+            g.layers = m->layers;
+            g.n_edges = uint32_t(j2.size());
+            g.offsets = keep(m->layer_offsets)->as<uint32_t>();
+            g.targets = keep(targets16)->as<uint16_t>();
+            g.j2 = keep(j2)->as<float>();
+            g.tau2 = keep(tau2)->as<float>();
+            g.tau2g = keep(tau2g)->as<float>();
+            graphs.push_back(g);
+            cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");  // temporaries die here
+        }
+        upload(layer_graphs_, graphs, device_bytes_, stream_);
+        cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");
+        dev_.layer_graphs = layer_graphs_.as<DevLayerGraph>();
+        dev_.max_layer_edges = max_layer_edges;
+        dev_.max_per_layer = max_per_layer;
+        dev_.layered_smem = uint32_t(layered_smem);
+        cuda_check(prepare_layered_kernels(layered_smem), "cudaFuncSetAttribute");
+    }
 
     // ---- batch description
     dev_.n_spins = n;
@@ -241,7 +290,11 @@ void Batch::drain_timings() {
 void Batch::launch_sweeps(uint32_t sweeps) {
     if (sweeps == 0) return;
     begin_timed(false);
-    cuda_check(launch_sweep_generic(dev_, sweeps, stream_), "sweep kernel");
+    if (family_ == KernelFamily::layered) {
+        cuda_check(launch_sweep_layered(dev_, sweeps, sm_count_, stream_), "layered sweep kernel");
+    } else {
+        cuda_check(launch_sweep_generic(dev_, sweeps, stream_), "sweep kernel");
+    }
     end_timed();
     ++sweep_launches;
     sweeps_done_ += sweeps;

@@ -117,7 +117,9 @@ class Batch {
     DeviceBuffer models_, tile_first_, tile_count_, tile_model_, chain_loc_, seeds_, betas_;
     DeviceBuffer slot_of_chain_, chain_at_slot_, hs_, ht_, spin_bits_, mt_, mt_pos_, e_run_, flips_;
     DeviceBuffer swap_seeds_, swap_mt_, swap_pos_, swap_acc_, swap_att_;
+    DeviceBuffer layer_graphs_;
     DeviceBuffer scratch_;  // readout staging
+    int sm_count_ = 0;
 
     // timing
     bool timing_ = false;

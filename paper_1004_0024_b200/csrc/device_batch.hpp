@@ -28,7 +28,26 @@ struct DevModel {
     const uint8_t* tau_counts;
 };
 
+// One layer of an identical-layer model, as the layered kernel keeps it in shared memory.
+// Edge e of position p (layer_offsets[p] <= e < layer_offsets[p+1]) goes to position
+// targets[e] of the same layer with doubled coupling j2[e] = 2*J (exact); tau2[p] = 2*J_tau(p)
+// and tau2g[p] = fl(tau_scale * tau2[p]) are the two non-zero magnitudes of the tau field.
+struct DevLayerGraph {
+    uint32_t per_layer;
+    uint32_t layers;
+    uint32_t n_edges;
+    const uint32_t* offsets;  // per_layer + 1
+    const uint16_t* targets;  // n_edges
+    const float* j2;          // n_edges
+    const float* tau2;        // per_layer
+    const float* tau2g;       // per_layer
+};
+
 struct DevBatch {
+    const DevLayerGraph* layer_graphs;  // per model; nullptr unless the layered family is used
+    uint32_t max_layer_edges;           // largest n_edges over the batch's models
+    uint32_t layered_smem;              // dynamic shared memory of one layered-kernel CTA
+    uint32_t max_per_layer;             // largest per_layer over the batch's models
     uint32_t n_spins;
     uint32_t n_tiles;
     uint32_t n_chains;
@@ -63,6 +82,11 @@ struct DevBatch {
 // All launchers enqueue on `stream` and return the launch error (cudaGetLastError).
 cudaError_t launch_init(const DevBatch& b, const int8_t* initial_spins_dev, cudaStream_t stream);
 cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_t stream);
+// Layered family: needs b.layer_graphs; `sm_count` persistent CTAs of 4 sweep warps.
+cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_count, cudaStream_t stream);
+// Bytes of dynamic shared memory one CTA of the layered kernel needs (0: does not fit).
+size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_layer_edges);
+cudaError_t prepare_layered_kernels(size_t smem_bytes);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);
 cudaError_t launch_checksums(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);

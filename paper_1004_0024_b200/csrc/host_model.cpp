@@ -101,7 +101,13 @@ void analyse_layers(HostModel& m) {
     for (uint32_t pos = 0; pos < P; ++pos) {
         m.layer_offsets[pos] = uint32_t(m.layer_targets.size());
         for (uint32_t e = m.offsets[pos]; e + 2 < m.offsets[pos + 1]; ++e) {
-            m.layer_targets.push_back(m.targets[e] % P);
+            const uint32_t t = m.targets[e] % P;
+            // the kernel batches a flip's neighbour updates, so a repeated target must not occur
+            for (uint32_t k = m.layer_offsets[pos]; k < m.layer_targets.size(); ++k) {
+                if (m.layer_targets[k] == t) return;
+            }
+            if (!std::isfinite(2.0f * m.couplings[e])) return;
+            m.layer_targets.push_back(t);
             m.layer_couplings.push_back(m.couplings[e]);
         }
     }

@@ -5,6 +5,7 @@
 // fields decremented by (2s)*J in adjacency order.
 #include "device_batch.hpp"
 #include "device_math.cuh"
+#include "device_mt.cuh"
 
 namespace isingb200 {
 
@@ -12,80 +13,6 @@ namespace {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
-constexpr int kChunk = 8;  // attempts whose random draws are generated together
-
-// ---------------------------------------------------------------------------------------
-// One chain's MT19937 inside a replica-interleaved block: word i lives at w[i * stride].
-// The state is regenerated in place one word per draw (the classic loop of
-// ref: rng.cpp:89-96, unrolled in time): draw j of a block rewrites word j from the old words
-// j, j+1 and word j+397 (already new once j >= 227), which is exactly what a whole-block twist
-// followed by reading word j produces.
-struct MtLane {
-    uint32_t* w;
-    uint32_t stride;
-    uint32_t pos;  // next word to regenerate, 0..623
-    uint32_t cur;  // old value of word `pos`
-
-    __device__ __forceinline__ void open(uint32_t* base, uint32_t stride_, uint32_t pos_) {
-        w = base;
-        stride = stride_;
-        pos = pos_;
-        cur = w[size_t(pos) * stride];
-    }
-
-    __device__ __forceinline__ uint32_t next_raw() {
-        const uint32_t jn = pos + 1 == kMtN ? 0u : pos + 1;
-        const uint32_t jf = pos >= kMtN - kMtM ? pos - (kMtN - kMtM) : pos + kMtM;
-        const uint32_t nxt = w[size_t(jn) * stride];
-        const uint32_t far = w[size_t(jf) * stride];
-        const uint32_t v = mt_recurrence(cur, nxt, far);
-        w[size_t(pos) * stride] = v;
-        cur = nxt;
-        pos = jn;
-        return mt_temper(v);
-    }
-
-    // `count` (<= kChunk) draws with every load issued before the first store: none of the
-    // words read here is rewritten inside the chunk (the far word is 227 draws old or newer
-    // by a whole block), so the loads overlap instead of serialising on L2 latency.
-    __device__ __forceinline__ void next_chunk(uint32_t count, float (&u)[kChunk]) {
-        uint32_t nxt[kChunk], far[kChunk];
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-            if (uint32_t(k) < count) {
-                uint32_t jn = pos + k + 1;
-                jn = jn >= kMtN ? jn - kMtN : jn;
-                uint32_t jf = pos + k + kMtM;
-                jf = jf >= kMtN ? jf - kMtN : jf;
-                nxt[k] = w[size_t(jn) * stride];
-                far[k] = w[size_t(jf) * stride];
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-            if (uint32_t(k) < count) {
-                const uint32_t v = mt_recurrence(cur, nxt[k], far[k]);
-                uint32_t j = pos + k;
-                j = j >= kMtN ? j - kMtN : j;
-                w[size_t(j) * stride] = v;
-                cur = nxt[k];
-                u[k] = u32_to_unit(mt_temper(v));
-            }
-        }
-        pos += count;
-        pos = pos >= kMtN ? pos - kMtN : pos;
-    }
-};
-
-// ref: Mt19937::reseed, rng.cpp:37-44
-__device__ void mt_seed_lane(uint32_t* w, uint32_t stride, uint32_t seed) {
-    uint32_t prev = seed;
-    w[0] = prev;
-    for (uint32_t i = 1; i < kMtN; ++i) {
-        prev = 1812433253u * (prev ^ (prev >> 30)) + i;
-        w[size_t(i) * stride] = prev;
-    }
-}
 
 struct TileView {
     uint32_t tile, lane, chain;
@@ -374,7 +301,15 @@ __global__ void gather_fields_kernel(DevBatch b, uint32_t chain, float* hs, floa
     const uint32_t loc = b.chain_loc[chain];
     const size_t at = (size_t(loc >> 5) * b.n_spins + i) * 32 + (loc & 31u);
     hs[i] = b.hs[at];
-    ht[i] = b.ht ? b.ht[at] : 0.0f;
+    if (b.ht) {
+        ht[i] = b.ht[at];
+    } else {
+        // not stored (generic graphs: identically zero; layered family: rebuilt exactly from spins)
+        float a, c;
+        fields_of_spin(b.models[b.tile_model[loc >> 5]], b.spin_bits + size_t(loc >> 5) * b.n_spins, loc & 31u,
+                       i, a, c);
+        ht[i] = c;
+    }
 }
 
 struct ResultRecord {  // 32 bytes per chain, see ising_batch_pack_results

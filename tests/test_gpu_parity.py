@@ -12,7 +12,8 @@ from helpers import assert_batch_matches, bits, csr_from_npz, ins, oracle_batch,
 pytestmark = pytest.mark.gpu
 
 REL_ENERGY = 1e-5  # north_star tolerance for energies
-KERNELS = [ib.KERNEL_GENERIC]
+KERNELS = [ib.KERNEL_GENERIC]                       # any graph
+LAYERED_KERNELS = [ib.KERNEL_GENERIC, ib.KERNEL_LAYERED]  # identical-layer models: both families
 
 
 def run_both(port, csrs, n_ladders, betas, sweeps, swap_interval, *, seed0=ins.CHAIN_SEED_BASE, tau_scale=1.0,
@@ -39,9 +40,12 @@ def test_reference_golden_trajectories(lib, golden, name):
     csr = csr_from_npz(g)
     model = product_model(csr)
     beta, gamma, sweeps = float(g["beta"]), float(g["tau_scale"]), int(g["sweeps"])
-    for kind in (1, 2, 3):
+    families = LAYERED_KERNELS if name.startswith("layered") else KERNELS
+    for kind, family in [(k, f) for k in (1, 2, 3) for f in families]:
         seeds = [int(s) for k, s in g["runs"] if k == kind]
-        with ib.init_state(model, [beta], len(seeds), seeds=seeds, params=ib.SweepParams(gamma, kind)) as st:
+        with ib.init_state(model, [beta], len(seeds), seeds=seeds, params=ib.SweepParams(gamma, kind),
+                           kernel=family) as st:
+            assert st.info()["kernel"] == family
             for c, seed in enumerate(seeds):
                 tag = f"k{kind}_s{seed}"
                 np.testing.assert_array_equal(st.spins(c, 1)[0], g[f"{tag}_spins0"])
@@ -59,7 +63,7 @@ def test_reference_golden_trajectories(lib, golden, name):
                 np.testing.assert_array_equal(st.spins(c, 1)[0], g[f"{tag}_spins"])
                 hs, ht = st.fields(c)
                 np.testing.assert_array_equal(bits(hs), bits(g[f"{tag}_hs"]))
-                np.testing.assert_array_equal(bits(ht), bits(g[f"{tag}_ht"]))
+                np.testing.assert_array_equal(bits(ht), bits(g[f"{tag}_ht"]))  # rebuilt, not stored, when layered
                 assert flips[c] == g[f"{tag}_flips"] and attempts[c] == g[f"{tag}_attempts"]
                 assert energies[c] == pytest.approx(float(g[f"{tag}_cost"]), rel=REL_ENERGY)
                 assert energies[c] == float(g[f"{tag}_cost"])  # same f64 summation order: exact
@@ -122,7 +126,7 @@ def test_c3_tempering_mixed_degree_distinct_graphs(lib, port, kernel):
     assert (np.sort(want["slot"].reshape(5, 32), 1) == np.arange(32)).all()
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", LAYERED_KERNELS)
 @pytest.mark.parametrize("swap_interval", [1, 10])
 def test_c4_layered_tempering(lib, port, kernel, swap_interval):
     """BASELINE config 4/5 shape: identical layers, J = +/-1, J_perp = 1.5 ring along tau, Gaussian h."""
@@ -136,7 +140,7 @@ def test_c4_layered_tempering(lib, port, kernel, swap_interval):
     assert set(np.unique(ht)).issubset({-3.0, 0.0, 3.0})
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", LAYERED_KERNELS)
 def test_shared_graph_many_ladders_tau_scale(lib, port, kernel):
     csr = ins.build_layered_csr(*ins.layered_spec(16, 77), 6, 0.75)
     betas = ins.geometric_betas(0.3, 2.0, 6)
@@ -164,18 +168,20 @@ def test_explicit_swap_round_matches_interval(lib, port):
         assert_batch_matches(st, want, REL_ENERGY)
 
 
-def test_results_do_not_depend_on_batch_composition(lib, port):
+@pytest.mark.parametrize("kernel", LAYERED_KERNELS)
+def test_results_do_not_depend_on_batch_composition(lib, port, kernel):
     """The reference's worker-count invariance (ref: tests/test_bench.cpp:153-166) as the
     multi-GPU property: a ladder's bits are the same alone, in a big batch, or in a shard
     addressed through first_ladder."""
     csr = ins.build_layered_csr(*ins.layered_spec(16, 3), 4, 1.5)
     model = product_model(csr)
     betas = ins.geometric_betas(0.2, 3.0, 8)
-    with ib.init_state(model, betas, 9, base_seed=100, swap_base_seed=900) as full:
+    with ib.init_state(model, betas, 9, base_seed=100, swap_base_seed=900, kernel=kernel) as full:
         full.run(40, 5)
         all_spins, all_sums, all_slots = full.spins(), full.checksums(), full.slots()
     for first, count in ((0, 4), (4, 5), (8, 1)):
-        with ib.init_state(model, betas, count, base_seed=100, swap_base_seed=900, first_ladder=first) as part:
+        with ib.init_state(model, betas, count, base_seed=100, swap_base_seed=900, first_ladder=first,
+                           kernel=kernel) as part:
             part.run(40, 5)
             np.testing.assert_array_equal(part.spins(), all_spins[first * 8:(first + count) * 8])
             np.testing.assert_array_equal(part.checksums(), all_sums[first * 8:(first + count) * 8])
@@ -252,3 +258,41 @@ def test_pack_results_matches_host_readouts(lib):
         np.testing.assert_array_equal(rec[:, 1].view(np.float64), st.running_energies())
         np.testing.assert_array_equal(rec[:, 2].view(np.uint64), st.stats()[0])
         np.testing.assert_array_equal(rec[:, 3].view(np.uint64), st.checksums())
+
+
+def test_layered_family_selection_and_rejection(lib):
+    """AUTO picks the on-chip family exactly when every model qualifies; asking for it otherwise
+    is an argument error (no silent fallback)."""
+    layered = product_model(ins.build_layered_csr(*ins.layered_spec(16, 3), 4, 1.5))
+    generic = product_model(ins.cubic_pm1(4, 1, 0.0))  # 64 spins like the layered one
+    with ib.init_state(layered, [1.0], 2) as st:
+        assert st.info()["kernel"] == ib.KERNEL_LAYERED
+    with ib.init_state(generic, [1.0], 2) as st:
+        assert st.info()["kernel"] == ib.KERNEL_GENERIC
+    with ib.init_state([layered, generic], [1.0], 2) as st:
+        assert st.info()["kernel"] == ib.KERNEL_GENERIC
+    with pytest.raises(ib.IsingError) as err:
+        ib.init_state(generic, [1.0], 2, kernel=ib.KERNEL_LAYERED)
+    assert err.value.status == _lib.ISING_ERR_ARGUMENT and "layered kernel needs" in str(err.value)
+    # unequal tau couplings per spin: still a valid layered model, but the tau field must be stored
+    csr = ins.build_layered_csr(*ins.layered_spec(8, 5), 4, 1.5)
+    csr["couplings"] = csr["couplings"].copy()
+    P, n = 8, 32
+    for i in range(n):  # scale the (up, down) pair of layer boundary 0|1 consistently
+        l, p = divmod(i, P)
+        end = csr["offsets"][i + 1]
+        if l == 0:
+            csr["couplings"][end - 2] = 0.5  # up edge of layer 0
+        if l == 1:
+            csr["couplings"][end - 1] = 0.5  # down edge of layer 1
+    with ib.init_state(product_model(csr), [1.0], 1) as st:
+        assert st.info()["kernel"] == ib.KERNEL_GENERIC
+
+
+def test_layered_many_tiles_and_sweeps(lib, port):
+    """More tiles than one CTA round holds warps for, ragged last tile, several launches."""
+    csr = ins.build_layered_csr(*ins.layered_spec(40, 8), 5, 1.5)
+    betas = ins.geometric_betas(0.3, 3.0, 3)
+    state, want = run_both(port, [csr], 45, betas, 24, 4, kernel=ib.KERNEL_LAYERED, chunks=[3, 9, 12])
+    assert state.info()["kernel"] == ib.KERNEL_LAYERED and state.info()["n_tiles"] == 5
+    assert_batch_matches(state, want, REL_ENERGY)
