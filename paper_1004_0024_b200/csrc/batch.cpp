@@ -316,6 +316,8 @@ void Batch::run(uint64_t sweeps, uint32_t swap_interval) {
     while (left > 0) {
         uint64_t step = left;
         if (swapping) step = std::min<uint64_t>(left, swap_interval - sweeps_done_ % swap_interval);
+        // the kernels count a launch's flips in 32 bits: keep sweeps * n_spins below 2^32
+        step = std::min<uint64_t>(step, std::max<uint64_t>(1, 0xFFFFFFFFull / std::max<uint32_t>(1, dev_.n_spins)));
         step = std::min<uint64_t>(step, 1u << 20);
         launch_sweeps(uint32_t(step));
         left -= step;

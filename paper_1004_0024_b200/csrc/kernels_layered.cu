@@ -1,8 +1,11 @@
 // Layered-model sweep kernel: the performance path for identical-layer ("QMC-style") models.
 //
-// One persistent CTA per SM, four sweep warps per CTA, one warp per tile of 32 chains
-// (lane = chain).  What makes it fast is that a chain's working set for one layer lives ON CHIP:
+// One persistent CTA per SM; four SWEEP warps and four RNG warps per CTA.  Sweep warp w and RNG
+// warp 4+w share a tile of 32 chains (lane = chain) and — because warp_id % 4 picks the SM
+// sub-partition — the same scheduler, so the generator's integer work fills the issue slots the
+// sweep's dependent floating-point chain leaves empty.
 //
+// A chain's working set for one layer lives ON CHIP:
 //   * Tensor Memory holds the space fields of the layer being swept: column p of the warp's own
 //     32-lane TMEM quarter is h_eff_space[(layer, p)] of its 32 chains (512 columns x 128 lanes x
 //     4 B = the whole 256 KB TMEM of an SM for 4 warps x 512 positions).  Every neighbour
@@ -13,10 +16,12 @@
 //     generic layout streams, and both tau read-modify-writes of every flip.
 //   * Spins are one bit per chain: a 32-bit word per (tile, spin) holds the 32 lanes' signs.
 //     Three layers of words (previous, current, next) sit in shared memory per warp.
-//   * One layer's graph (CSR of in-layer targets with doubled couplings) sits in shared memory.
+//   * One layer's graph ({column, 2J} per half-edge) sits in shared memory.
+//   * The RNG warp regenerates the chains' MT19937 states (replica-interleaved in HBM/L2) and
+//     hands uniforms over through a shared-memory ring guarded by mbarriers.
 //
-// HBM traffic per sweep is therefore one read and one write of the f32 space fields plus the bit
-// words: 8.25 B per attempt, streamed layer by layer with full 128-byte lines per warp access.
+// HBM traffic per sweep is one read and one write of the f32 space fields plus the bit words
+// (8.25 B per attempt) and the MT19937 state words (12 B per attempt while they miss L2).
 // The trajectory is the reference's (ref: proj/src/sweep_basic.cpp:12-56) bit for bit.
 #include "device_batch.hpp"
 #include "device_math.cuh"
@@ -27,8 +32,11 @@ namespace isingb200 {
 namespace {
 
 constexpr int kSweepWarps = 4;          // one TMEM lane quarter each
-constexpr int kLayeredThreads = kSweepWarps * 32;
+constexpr int kLayeredThreads = 2 * kSweepWarps * 32;
 constexpr uint32_t kTmemColumns = 512;  // the whole TMEM: one CTA per SM
+constexpr uint32_t kStageDraws = 64;    // uniforms per ring stage (per lane)
+constexpr uint32_t kStages = 2;
+constexpr uint32_t kGenBatch = 16;      // draws whose state loads are in flight together
 
 // ---- Tensor Memory access (sm_100a tcgen05).  All of these are warp-collective.
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t columns) {
@@ -69,205 +77,328 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
                  : "memory");
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// ---- mbarrier (shared::cta) helpers for the uniform ring
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (done == 0u);
 }
 
-// ---- shared-memory carve-up (per CTA): [tmem base][per-warp region x 4]
-struct WarpSmem {
-    uint32_t* offsets;   // P + 1
-    float* j2;           // max_edges
-    float* tau2;         // P
-    float* tau2g;        // P
-    uint32_t* words;     // 3 * P : ring of spin-bit layers
-    uint16_t* targets;   // max_edges
+// ---- shared-memory carve-up (per CTA): [tmem base | barriers][per-pair region x 4]
+struct PairSmem {
+    uint32_t* offsets;  // P + 1
+    uint2* edges;       // max_edges : {TMEM column, bits of 2J}
+    float2* tau;        // P : {gamma*2J_tau, 2J_tau}
+    uint2* agree_sign;  // P : per layer, {~(up ^ dn), up} spin words
+    uint32_t* words;    // 3 * P : ring of spin-bit layers
+    float* ring;        // kStages * kStageDraws * 32 uniforms
 };
 
-__host__ __device__ inline size_t warp_region_bytes(uint32_t P, uint32_t max_edges) {
-    size_t words = size_t(P + 1) + max_edges + 2 * size_t(P) + 3 * size_t(P);
-    size_t bytes = words * 4 + ((size_t(max_edges) * 2 + 15) / 16) * 16;
-    return (bytes + 15) / 16 * 16;
+constexpr size_t kHeaderBytes = 256;  // tmem slot + 4 pairs x (full[kStages] + empty[kStages]) barriers
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
+
+__host__ __device__ inline size_t pair_region_bytes(uint32_t P, uint32_t max_edges) {
+    return align16(size_t(P + 1) * 4) + align16(size_t(max_edges) * 8) + align16(size_t(P) * 8) +
+           align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(kStages) * kStageDraws * 32 * 4;
 }
 
-__device__ __forceinline__ WarpSmem carve(unsigned char* base, uint32_t P, uint32_t max_edges) {
-    WarpSmem s;
-    uint32_t* w = reinterpret_cast<uint32_t*>(base);
-    s.offsets = w;
-    w += P + 1;
-    s.j2 = reinterpret_cast<float*>(w);
-    w += max_edges;
-    s.tau2 = reinterpret_cast<float*>(w);
-    w += P;
-    s.tau2g = reinterpret_cast<float*>(w);
-    w += P;
-    s.words = w;
-    w += 3 * P;
-    s.targets = reinterpret_cast<uint16_t*>(w);
+__device__ __forceinline__ PairSmem carve(unsigned char* base, uint32_t P, uint32_t max_edges) {
+    PairSmem s;
+    s.offsets = reinterpret_cast<uint32_t*>(base);
+    base += align16(size_t(P + 1) * 4);
+    s.edges = reinterpret_cast<uint2*>(base);
+    base += align16(size_t(max_edges) * 8);
+    s.tau = reinterpret_cast<float2*>(base);
+    base += align16(size_t(P) * 8);
+    s.agree_sign = reinterpret_cast<uint2*>(base);
+    base += align16(size_t(P) * 8);
+    s.words = reinterpret_cast<uint32_t*>(base);
+    base += align16(size_t(P) * 12);
+    s.ring = reinterpret_cast<float*>(base);
     return s;
 }
 
-// Copies one layer of spin-bit words between HBM and the warp's ring (each lane its own slice).
-__device__ __forceinline__ void words_load(uint32_t* dst, const uint32_t* src, uint32_t P, uint32_t lane) {
+__device__ __forceinline__ void words_copy(uint32_t* dst, const uint32_t* src, uint32_t P, uint32_t lane) {
     for (uint32_t k = lane; k < P; k += 32) dst[k] = src[k];
 }
-__device__ __forceinline__ void words_store(uint32_t* dst, const uint32_t* src, uint32_t P, uint32_t lane) {
-    for (uint32_t k = lane; k < P; k += 32) dst[k] = src[k];
+
+// ---------------------------------------------------------------------------------------
+// RNG warp: regenerates `take` words of every lane's MT19937 state in place and writes the
+// tempered, truncated uniforms to out[k*32].  The state is walked in runs that do not cross
+// the recurrence's wrap points (word 227: the far operand wraps; word 623: the next operand
+// wraps), so inside a run all three operands advance by one row (ref: rng.cpp:89-96).
+__device__ __forceinline__ void mt_generate(uint32_t* w, uint32_t& pos, uint32_t& cur, uint32_t take,
+                                            float* out) {
+    uint32_t done = 0;
+    while (done < take) {
+        const uint32_t seg_end = pos < kMtN - kMtM ? kMtN - kMtM : (pos < kMtN - 1 ? kMtN - 1 : kMtN);
+        const uint32_t cnt = min(take - done, seg_end - pos);
+        uint32_t* wp = w + size_t(pos) * 32;
+        const uint32_t* fp = w + size_t(pos < kMtN - kMtM ? pos + kMtM : pos - (kMtN - kMtM)) * 32;
+        const uint32_t* np = pos == kMtN - 1 ? w : wp + 32;
+        uint32_t k = 0;
+        for (; k + kGenBatch <= cnt; k += kGenBatch) {
+            uint32_t nxt[kGenBatch], far[kGenBatch];
+#pragma unroll
+            for (int i = 0; i < int(kGenBatch); ++i) {
+                nxt[i] = np[size_t(k + i) * 32];
+                far[i] = fp[size_t(k + i) * 32];
+            }
+#pragma unroll
+            for (int i = 0; i < int(kGenBatch); ++i) {
+                const uint32_t v = mt_recurrence(cur, nxt[i], far[i]);
+                wp[size_t(k + i) * 32] = v;
+                cur = nxt[i];
+                out[size_t(k + i) * 32] = u32_to_unit(mt_temper(v));
+            }
+        }
+        for (; k < cnt; ++k) {
+            const uint32_t nx = np[size_t(k) * 32];
+            const uint32_t v = mt_recurrence(cur, nx, fp[size_t(k) * 32]);
+            wp[size_t(k) * 32] = v;
+            cur = nx;
+            out[size_t(k) * 32] = u32_to_unit(mt_temper(v));
+        }
+        pos += cnt;
+        pos = pos == kMtN ? 0u : pos;
+        done += cnt;
+        out += size_t(cnt) * 32;
+    }
+}
+
+struct RingCursor {
+    uint32_t stage = 0;
+    uint32_t parity = 0;
+    __device__ __forceinline__ void advance() {
+        if (++stage == kStages) {
+            stage = 0;
+            parity ^= 1u;
+        }
+    }
+};
+
+__device__ void rng_warp(const DevBatch& b, uint32_t sweeps, uint32_t pair, uint32_t lane, const PairSmem& s,
+                         uint64_t* full, uint64_t* empty, RingCursor& cursor, uint32_t tile) {
+    uint32_t* w = b.mt + size_t(tile) * kMtN * 32 + lane;
+    uint32_t pos = b.mt_pos[tile];
+    uint32_t cur = w[size_t(pos) * 32];
+    uint64_t remaining = uint64_t(sweeps) * b.n_spins;
+    while (remaining != 0) {
+        const uint32_t take = remaining < kStageDraws ? uint32_t(remaining) : kStageDraws;
+        mbar_wait(&empty[cursor.stage], cursor.parity ^ 1u);
+        mt_generate(w, pos, cur, take, s.ring + size_t(cursor.stage) * kStageDraws * 32 + lane);
+        mbar_arrive(&full[cursor.stage]);
+        cursor.advance();
+        remaining -= take;
+    }
+    if (lane == 0) b.mt_pos[tile] = pos;
+    (void)pair;
+}
+
+// ---------------------------------------------------------------------------------------
+template <int EXP>
+__device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s, uint64_t* full,
+                           uint64_t* empty, RingCursor& cursor, uint32_t tile, uint32_t tm,
+                           const DevLayerGraph& g) {
+    const uint32_t P = g.per_layer, L = g.layers, n = b.n_spins;
+    const bool active = lane < b.tile_count[tile];
+    const uint32_t chain = b.tile_first[tile] + lane;
+    // -2*beta: x = -beta*((2s)*v) == (-2*beta*s)*v exactly (doubling is exact, one rounding each way)
+    const uint32_t nb2 = __float_as_uint(active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
+    double e_run = active ? b.e_run[chain] : 0.0;
+    uint32_t flips = 0;
+    float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
+    uint32_t* words_g = b.spin_bits + size_t(tile) * n;
+    const uint32_t sh = 31u - lane;  // shift that brings this lane's bit to the sign position
+
+    uint32_t slot_dn = 2, slot_cur = 0, slot_up = 1;
+    words_copy(s.words + slot_dn * P, words_g + size_t(L - 1) * P, P, lane);
+    words_copy(s.words + slot_cur * P, words_g, P, lane);
+    words_copy(s.words + slot_up * P, words_g + size_t(1) * P, P, lane);
+    __syncwarp();
+
+    uint32_t ui = 0;        // draws consumed from the current ring stage
+    bool have_stage = false;
+    const float* ring = s.ring + lane;
+
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t l = 0; l < L; ++l) {
+            float* hs_l = hs_g + size_t(l) * P * 32;
+            const float* hs_next = hs_g + size_t(l + 1 == L ? 0 : l + 1) * P * 32 - lane;
+            // ---- feed: this layer's fields HBM -> TMEM
+            for (uint32_t p0 = 0; p0 < P; p0 += 32) {
+                float v[4][8];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t p = p0 + q * 8 + k;
+                        v[q][k] = p < P ? hs_l[size_t(p) * 32] : 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (p0 + q * 8 < P) tmem_st8(tm + p0 + q * 8, v[q]);
+                }
+            }
+            uint32_t* w_cur = s.words + slot_cur * P;
+            {   // the tau field of this whole layer is fixed while it is swept: previous layer already
+                // visited, next layer not yet.  agree = neighbours equal, sign = their common spin bit.
+                const uint32_t* w_up = s.words + slot_up * P;
+                const uint32_t* w_dn = s.words + slot_dn * P;
+                for (uint32_t k = lane; k < P; k += 32) s.agree_sign[k] = make_uint2(~(w_up[k] ^ w_dn[k]), w_up[k]);
+            }
+            __syncwarp();
+            tmem_wait_st();
+
+            for (uint32_t p = 0; p < P; ++p) {
+                if (!have_stage) {
+                    mbar_wait(&full[cursor.stage], cursor.parity);
+                    have_stage = true;
+                }
+                const float u = ring[(size_t(cursor.stage) * kStageDraws + ui) * 32];
+                const float h = tmem_ld(tm + p);
+                const uint2 as = s.agree_sign[p];
+                const float2 tau = s.tau[p];
+                const uint32_t word = w_cur[p];
+                if ((p & 31u) == 0 && p + lane < P) prefetch_l2(hs_next + size_t(p + lane) * 32);
+                const uint32_t sgn_s = (word << sh) & 0x80000000u;       // sign bit set <=> s = -1
+                const uint32_t sgn_up = (as.y << sh) & 0x80000000u;
+                const uint32_t agree = uint32_t(int32_t(as.x << sh) >> 31);  // all ones when s_up == s_dn
+                // tau field J*(s_up + s_dn) in {+2J, +0, -2J}, scaled by gamma for the exponent
+                const float htg = __uint_as_float((__float_as_uint(tau.x) ^ sgn_up) & agree);
+                tmem_wait_ld();
+                const float v = __fadd_rn(h, htg);
+                const float x = __fmul_rn(__uint_as_float(nb2 ^ sgn_s), v);
+                const float pr = exp_kind<EXP>(x);
+                const bool accept = active && (u < pr);
+                const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+                if (ballot != 0u) {
+                    const uint32_t neg_d = sgn_s ^ 0x80000000u;  // sign of -(2s): h -= (2s)*J == h + (-(2s)J)
+                    const uint32_t e1 = s.offsets[p + 1];
+                    for (uint32_t e = s.offsets[p]; e < e1; ++e) {
+                        const uint2 ed = s.edges[e];
+                        const float old = tmem_ld(tm + ed.x);
+                        const float nd = __uint_as_float(ed.y ^ neg_d);
+                        tmem_wait_ld();
+                        tmem_st(tm + ed.x, accept ? __fadd_rn(old, nd) : old);
+                    }
+                    if (accept) {
+                        ++flips;
+                        const float ht = __uint_as_float((__float_as_uint(tau.y) ^ sgn_up) & agree);
+                        const float two_s = __uint_as_float(0x40000000u ^ sgn_s);
+                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(h, ht))));
+                    }
+                    if (lane == 0) w_cur[p] = word ^ ballot;
+                    tmem_wait_st();
+                }
+                if (++ui == kStageDraws) {
+                    mbar_arrive(&empty[cursor.stage]);
+                    cursor.advance();
+                    ui = 0;
+                    have_stage = false;
+                }
+            }
+
+            // ---- retire: TMEM -> HBM, and rotate the spin-bit ring
+            for (uint32_t p0 = 0; p0 < P; p0 += 8) {
+                float v[8];
+                tmem_ld8(tm + p0, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (p0 + k < P) hs_l[size_t(p0 + k) * 32] = v[k];
+                }
+            }
+            __syncwarp();
+            words_copy(words_g + size_t(l) * P, w_cur, P, lane);
+            // layer l-1's slot is free now: it receives layer l+2 (the `up` of the next layer)
+            words_copy(s.words + slot_dn * P, words_g + size_t((l + 2) % L) * P, P, lane);
+            __syncwarp();
+            const uint32_t freed = slot_dn;
+            slot_dn = slot_cur;
+            slot_cur = slot_up;
+            slot_up = freed;
+        }
+    }
+    if (ui != 0) {  // hand a partly used last stage back
+        mbar_arrive(&empty[cursor.stage]);
+        cursor.advance();
+    }
+    if (active) {
+        b.e_run[chain] = e_run;
+        b.flips[chain] += flips;
+    }
+    __syncwarp();
 }
 
 template <int EXP>
 __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBatch b, uint32_t sweeps) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 16);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t n = b.n_spins;
+    const uint32_t pair = warp & 3u;
+    const bool is_rng = warp >= kSweepWarps;
+    uint64_t* full = bars + pair * 2 * kStages;
+    uint64_t* empty = full + kStages;
 
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
+    if (threadIdx.x < kSweepWarps * 2 * kStages) mbar_init(&bars[threadIdx.x], 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_base = *tmem_slot;
-    // this warp's lane quarter: bits 31..16 of a TMEM address are the lane, 15..0 the column
-    const uint32_t tm = tmem_base + ((warp * 32u) << 16);
+    // this pair's lane quarter: bits 31..16 of a TMEM address are the lane, 15..0 the column
+    const uint32_t tm = tmem_base + ((pair * 32u) << 16);
+    const PairSmem s = carve(smem_raw + kHeaderBytes + size_t(pair) * pair_region_bytes(b.max_per_layer, b.max_layer_edges),
+                             b.max_per_layer, b.max_layer_edges);
+    RingCursor cursor;
 
-    // tiles are dealt round-robin: CTA c, warp w, round r -> tile c + grid*(w + 4r)
-    for (uint32_t tile = blockIdx.x + gridDim.x * warp; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
-        const DevLayerGraph g = b.layer_graphs[b.tile_model[tile]];
-        const uint32_t P = g.per_layer, L = g.layers;
-        const WarpSmem s =
-            carve(smem_raw + 16 + size_t(warp) * warp_region_bytes(b.max_per_layer, b.max_layer_edges), P,
-                  b.max_layer_edges);
-        // ---- graph of one layer into shared memory
-        for (uint32_t k = lane; k <= P; k += 32) s.offsets[k] = g.offsets[k];
-        for (uint32_t k = lane; k < g.n_edges; k += 32) {
-            s.j2[k] = g.j2[k];
-            s.targets[k] = g.targets[k];
-        }
-        for (uint32_t k = lane; k < P; k += 32) {
-            s.tau2[k] = g.tau2[k];
-            s.tau2g[k] = g.tau2g[k];
-        }
-
-        const bool active = lane < b.tile_count[tile];
-        const uint32_t chain = b.tile_first[tile] + lane;
-        const float neg_beta = active ? -b.betas[b.slot_of_chain[chain]] : 0.0f;
-        double e_run = active ? b.e_run[chain] : 0.0;
-        unsigned long long flips = 0;
-        float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
-        uint32_t* words_g = b.spin_bits + size_t(tile) * n;
-        MtLane rng;
-        rng.open(b.mt + size_t(tile) * kMtN * 32 + lane, 32, b.mt_pos[tile]);
-
-        // ring of three word layers (previous, current, next); slots rotate as the sweep advances
-        uint32_t slot_dn = 2, slot_cur = 0, slot_up = 1;
-        words_load(s.words + slot_dn * P, words_g + size_t(L - 1) * P, P, lane);
-        words_load(s.words + slot_cur * P, words_g, P, lane);
-        words_load(s.words + slot_up * P, words_g + size_t(1) * P, P, lane);
-        __syncwarp();
-
-        for (uint32_t sw = 0; sw < sweeps; ++sw) {
-            for (uint32_t l = 0; l < L; ++l) {
-                float* hs_l = hs_g + size_t(l) * P * 32;
-                const float* hs_next = hs_g + size_t(l + 1 == L ? 0 : l + 1) * P * 32;
-                // ---- feed: this layer's fields HBM -> TMEM, 8 columns per step
-                for (uint32_t p0 = 0; p0 < P; p0 += 32) {
-                    float v[4][8];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const uint32_t p = p0 + q * 8 + k;
-                            v[q][k] = p < P ? hs_l[size_t(p) * 32] : 0.0f;
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (p0 + q * 8 < P) tmem_st8(tm + p0 + q * 8, v[q]);
-                    }
-                }
-                tmem_wait_st();
-
-                uint32_t* w_cur = s.words + slot_cur * P;
-                const uint32_t* w_up = s.words + slot_up * P;
-                const uint32_t* w_dn = s.words + slot_dn * P;
-
-                for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
-                    const uint32_t count = min(uint32_t(kChunk), P - p0);
-                    float u[kChunk];
-                    rng.next_chunk(count, u);
-                    // pull the same positions of the next layer towards L2 while this one computes
-                    if (lane < count) prefetch_l2(hs_next + size_t(p0 + lane) * 32 - lane);
-#pragma unroll
-                    for (int k = 0; k < kChunk; ++k) {
-                        if (uint32_t(k) >= count) break;
-                        const uint32_t p = p0 + k;
-                        const uint32_t word = w_cur[p];
-                        const uint32_t sbit = (word >> lane) & 1u;
-                        const uint32_t ub = (w_up[p] >> lane) & 1u, db = (w_dn[p] >> lane) & 1u;
-                        const float h = tmem_ld(tm + p);
-                        // tau field J*(s_up + s_dn): +/-2J when the neighbours agree, +0 otherwise
-                        const float t2g = s.tau2g[p], t2 = s.tau2[p];
-                        const float htg = ub == db ? (ub ? -t2g : t2g) : 0.0f;
-                        const float ht = ub == db ? (ub ? -t2 : t2) : 0.0f;
-                        const float two_s = sbit ? -2.0f : 2.0f;
-                        tmem_wait_ld();
-                        const float x = __fmul_rn(neg_beta, __fmul_rn(two_s, __fadd_rn(h, htg)));
-                        const float pr = exp_kind<EXP>(x);
-                        const bool accept = active && (u[k] < pr);
-                        const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
-                        if (ballot != 0u) {
-                            const uint32_t e1 = s.offsets[p + 1];
-                            for (uint32_t e = s.offsets[p]; e < e1; ++e) {
-                                const uint32_t col = tm + s.targets[e];
-                                const float j2 = s.j2[e];
-                                const float old = tmem_ld(col);
-                                const float d = sbit ? -j2 : j2;  // (2s)*J, exact
-                                tmem_wait_ld();
-                                tmem_st(col, accept ? __fsub_rn(old, d) : old);
-                            }
-                            if (accept) {
-                                ++flips;
-                                e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(h, ht))));
-                            }
-                            if (lane == 0) w_cur[p] = word ^ ballot;
-                            tmem_wait_st();
-                        }
-                    }
-                }
-
-                // ---- retire: TMEM -> HBM, and rotate the spin-bit ring
-                for (uint32_t p0 = 0; p0 < P; p0 += 8) {
-                    float v[8];
-                    tmem_ld8(tm + p0, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        if (p0 + k < P) hs_l[size_t(p0 + k) * 32] = v[k];
-                    }
-                }
-                __syncwarp();
-                words_store(words_g + size_t(l) * P, w_cur, P, lane);
-                // layer l-1's slot is free now: it receives layer l+2 (the `up` of the next layer)
-                const uint32_t l2 = (l + 2) % L;
-                __syncwarp();
-                words_load(s.words + slot_dn * P, words_g + size_t(l2) * P, P, lane);
-                __syncwarp();
-                const uint32_t freed = slot_dn;
-                slot_dn = slot_cur;
-                slot_cur = slot_up;
-                slot_up = freed;
+    // tiles are dealt round-robin: CTA c, pair w, round r -> tile c + grid*(w + 4r)
+    for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
+        if (is_rng) {
+            rng_warp(b, sweeps, pair, lane, s, full, empty, cursor, tile);
+        } else {
+            const DevLayerGraph g = b.layer_graphs[b.tile_model[tile]];
+            // ---- graph of one layer into shared memory
+            for (uint32_t k = lane; k <= g.per_layer; k += 32) s.offsets[k] = g.offsets[k];
+            for (uint32_t k = lane; k < g.n_edges; k += 32) {
+                s.edges[k] = make_uint2(uint32_t(g.targets[k]), __float_as_uint(g.j2[k]));
             }
+            for (uint32_t k = lane; k < g.per_layer; k += 32) s.tau[k] = make_float2(g.tau2g[k], g.tau2[k]);
+            __syncwarp();
+            sweep_warp<EXP>(b, sweeps, lane, s, full, empty, cursor, tile, tm, g);
         }
-
-        if (lane == 0) b.mt_pos[tile] = rng.pos;
-        if (active) {
-            b.e_run[chain] = e_run;
-            b.flips[chain] += flips;
-        }
-        __syncwarp();
     }
 
-    tmem_wait_ld();
-    tmem_wait_st();
+    if (!is_rng) {
+        tmem_wait_ld();
+        tmem_wait_st();
+    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem_base, kTmemColumns);
@@ -277,7 +408,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
 
 size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_layer_edges) {
     if (per_layer == 0 || per_layer > kTmemColumns) return 0;
-    const size_t bytes = 16 + kSweepWarps * warp_region_bytes(per_layer, max_layer_edges);
+    const size_t bytes = kHeaderBytes + kSweepWarps * pair_region_bytes(per_layer, max_layer_edges);
     return bytes <= 227 * 1024 ? bytes : 0;
 }
 
@@ -293,9 +424,8 @@ cudaError_t prepare_layered_kernels(size_t smem_bytes) {
 }
 
 cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_count, cudaStream_t stream) {
-    // all models of a batch share n_spins but may differ in per_layer; size for the largest region
     const size_t smem = size_t(b.layered_smem);
-    const uint32_t ctas = uint32_t(sm_count) < (b.n_tiles + 0u) ? uint32_t(sm_count) : b.n_tiles;
+    const uint32_t ctas = uint32_t(sm_count) < b.n_tiles ? uint32_t(sm_count) : b.n_tiles;
     const dim3 grid(ctas ? ctas : 1);
     switch (b.exp_kind) {
         case kExpExact: sweep_layered_kernel<kExpExact><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps); break;
