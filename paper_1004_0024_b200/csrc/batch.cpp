@@ -74,18 +74,30 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     if (cfg.kernel < 0 || cfg.kernel > 2) throw Error("invalid kernel value " + std::to_string(cfg.kernel));
     // The layered family needs every model to qualify (HostModel::layered_uniform) and one layer
     // to fit the on-chip window: <= 512 positions (TMEM columns) and the graph within shared memory.
-    uint32_t max_per_layer = 0, max_layer_edges = 0;
+    uint32_t max_per_layer = 0, max_far_edges = 0;
     bool layered_ok = true;
+    const auto is_band = [](uint32_t p, uint32_t t) { return (t > p ? t - p : p - t) <= 2; };
     for (const HostModel* m : models) {
-        layered_ok = layered_ok && m->layered_uniform;
+        layered_ok = layered_ok && m->layered_uniform && m->per_layer % 8 == 0;
         max_per_layer = std::max(max_per_layer, m->per_layer);
-        max_layer_edges = std::max<uint32_t>(max_layer_edges, uint32_t(m->layer_targets.size()));
+        if (!m->layered_uniform) continue;
+        uint32_t far = 0;
+        for (uint32_t p = 0; p < m->per_layer; ++p) {
+            uint32_t far_here = 0;
+            for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
+                far_here += is_band(p, m->layer_targets[e]) ? 0u : 1u;
+            }
+            layered_ok = layered_ok && far_here < 256;
+            far += far_here;
+        }
+        max_far_edges = std::max(max_far_edges, far);
     }
-    const size_t layered_smem = layered_ok ? layered_smem_bytes(max_per_layer, max_layer_edges) : 0;
+    const bool graph_shared = models.size() == 1;
+    const size_t layered_smem = layered_ok ? layered_smem_bytes(max_per_layer, max_far_edges, graph_shared) : 0;
     layered_ok = layered_ok && layered_smem != 0;
     if (cfg.kernel == int(KernelFamily::layered) && !layered_ok) {
         throw Error("init_state: the layered kernel needs identical-layer models with equal tau couplings "
-                    "and at most 512 positions per layer");
+                    "and a multiple of 8, at most 512, positions per layer");
     }
     family_ = (cfg.kernel != int(KernelFamily::generic) && layered_ok) ? KernelFamily::layered
                                                                         : KernelFamily::generic;
@@ -148,31 +160,54 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         if (prop.major != 10) throw CudaError("the layered kernel needs an sm_100 device (tcgen05 tensor memory)");
         sm_count_ = prop.multiProcessorCount;
         std::vector<DevLayerGraph> graphs;
+        const auto bits = [](float v) {
+            uint32_t b;
+            std::memcpy(&b, &v, sizeof b);
+            return b;
+        };
         for (const HostModel* m : models) {
-            std::vector<uint16_t> targets16(m->layer_targets.begin(), m->layer_targets.end());
-            std::vector<float> j2(m->layer_couplings.size()), tau2(m->per_layer), tau2g(m->per_layer);
-            for (size_t e = 0; e < j2.size(); ++e) j2[e] = 2.0f * m->layer_couplings[e];
-            for (uint32_t p = 0; p < m->per_layer; ++p) {
-                tau2[p] = 2.0f * m->layer_tau[p];
-                tau2g[p] = cfg.tau_scale * tau2[p];  // f32 product, as gamma * h_tau in the reference
+            const uint32_t P = m->per_layer;
+            std::vector<uint4> pos(P), band_j2(P), band_mask(P);
+            std::vector<uint2> far;
+            for (uint32_t p = 0; p < P; ++p) {
+                uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
+                const uint32_t far_begin = uint32_t(far.size());
+                for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
+                    const uint32_t t = m->layer_targets[e];
+                    const float doubled = 2.0f * m->layer_couplings[e];  // exact
+                    if (is_band(p, t)) {
+                        const int off = int(t) - int(p);             // -2, -1, +1, +2
+                        const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
+                        j2[slot] = bits(doubled);
+                        mask[slot] = 0;
+                    } else {
+                        far.push_back(make_uint2(t, bits(doubled)));
+                    }
+                }
+                const float tau2 = 2.0f * m->layer_tau[p];
+                const float tau2g = cfg.tau_scale * tau2;  // f32 product, as gamma * h_tau in the reference
+                pos[p] = make_uint4(bits(tau2g), bits(tau2), far_begin | (uint32_t(far.size()) - far_begin) << 24, 0);
+                band_j2[p] = make_uint4(j2[0], j2[1], j2[2], j2[3]);
+                band_mask[p] = make_uint4(mask[0], mask[1], mask[2], mask[3]);
             }
             DevLayerGraph g{};
-            g.per_layer = m->per_layer;
+            g.per_layer = P;
             g.layers = m->layers;
-            g.n_edges = uint32_t(j2.size());
-            g.offsets = keep(m->layer_offsets)->as<uint32_t>();
-            g.targets = keep(targets16)->as<uint16_t>();
-            g.j2 = keep(j2)->as<float>();
-            g.tau2 = keep(tau2)->as<float>();
-            g.tau2g = keep(tau2g)->as<float>();
+            g.n_far = uint32_t(far.size());
+            if (far.empty()) far.push_back(make_uint2(0, 0));
+            g.pos = keep(pos)->as<uint4>();
+            g.band_j2 = keep(band_j2)->as<uint4>();
+            g.band_mask = keep(band_mask)->as<uint4>();
+            g.far = keep(far)->as<uint2>();
             graphs.push_back(g);
             cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");  // temporaries die here
         }
         upload(layer_graphs_, graphs, device_bytes_, stream_);
         cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");
         dev_.layer_graphs = layer_graphs_.as<DevLayerGraph>();
-        dev_.max_layer_edges = max_layer_edges;
+        dev_.max_far_edges = max_far_edges;
         dev_.max_per_layer = max_per_layer;
+        dev_.graph_shared = graph_shared ? 1u : 0u;
         dev_.layered_smem = uint32_t(layered_smem);
         cuda_check(prepare_layered_kernels(layered_smem), "cudaFuncSetAttribute");
     }

@@ -32,22 +32,30 @@ struct DevModel {
 // Edge e of position p (layer_offsets[p] <= e < layer_offsets[p+1]) goes to position
 // targets[e] of the same layer with doubled coupling j2[e] = 2*J (exact); tau2[p] = 2*J_tau(p)
 // and tau2g[p] = fl(tau_scale * tau2[p]) are the two non-zero magnitudes of the tau field.
+//
+// The in-layer edges of position p are split by distance: the BAND slots are the (up to four)
+// neighbours at p-2, p-1, p+1, p+2, which the kernel keeps in a register window; everything else
+// is a FAR edge, updated in Tensor Memory.
 struct DevLayerGraph {
     uint32_t per_layer;
     uint32_t layers;
-    uint32_t n_edges;
-    const uint32_t* offsets;  // per_layer + 1
-    const uint16_t* targets;  // n_edges
-    const float* j2;          // n_edges
-    const float* tau2;        // per_layer
-    const float* tau2g;       // per_layer
+    uint32_t n_far;
+    // per position: {bits of tau2g, bits of tau2, far_begin | far_count << 24, 0}
+    const uint4* pos;
+    // per position: bits of 2J for the slots -2, -1, +1, +2 (0 when the slot is empty) ...
+    const uint4* band_j2;
+    // ... and 0x80000000 for an empty slot, 0 otherwise: (j2 ^ sign) | mask is then -0.0, the
+    // additive identity for every float bit pattern, so an empty slot costs no predicate.
+    const uint4* band_mask;
+    const uint2* far;  // {position, bits of 2J}
 };
 
 struct DevBatch {
     const DevLayerGraph* layer_graphs;  // per model; nullptr unless the layered family is used
-    uint32_t max_layer_edges;           // largest n_edges over the batch's models
+    uint32_t max_far_edges;             // largest n_far over the batch's models
     uint32_t layered_smem;              // dynamic shared memory of one layered-kernel CTA
     uint32_t max_per_layer;             // largest per_layer over the batch's models
+    uint32_t graph_shared;              // 1: all tiles use model 0, one shared-memory copy per CTA
     uint32_t n_spins;
     uint32_t n_tiles;
     uint32_t n_chains;
@@ -85,7 +93,7 @@ cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_
 // Layered family: needs b.layer_graphs; `sm_count` persistent CTAs of 4 sweep warps.
 cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_count, cudaStream_t stream);
 // Bytes of dynamic shared memory one CTA of the layered kernel needs (0: does not fit).
-size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_layer_edges);
+size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared);
 cudaError_t prepare_layered_kernels(size_t smem_bytes);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);

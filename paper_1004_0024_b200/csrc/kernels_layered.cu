@@ -8,17 +8,23 @@
 // A chain's working set for one layer lives ON CHIP:
 //   * Tensor Memory holds the space fields of the layer being swept: column p of the warp's own
 //     32-lane TMEM quarter is h_eff_space[(layer, p)] of its 32 chains (512 columns x 128 lanes x
-//     4 B = the whole 256 KB TMEM of an SM for 4 warps x 512 positions).  Every neighbour
-//     update of a flip is a tcgen05.ld / tcgen05.st on a warp-uniform column — no HBM traffic.
+//     4 B = the whole 256 KB TMEM of an SM for 4 warps x 512 positions).
+//   * A five-entry REGISTER WINDOW slides over the columns p-2..p+2 of the position being
+//     attempted.  Updates of the near ("band") neighbours are predicated register adds, so the
+//     loop-carried dependency from one attempt to the next is a single FADD; only the far
+//     neighbours of a flip are read-modify-written in Tensor Memory (tcgen05.ld / tcgen05.st).
 //   * The tau field is NOT stored.  For these models it only takes the values {2J, +0, -2J}
 //     and every incremental update of it is exact (HostModel::layered_uniform), so it is rebuilt
 //     from two spin bits of the adjacent layers.  That removes 8 of the 17 bytes per attempt the
 //     generic layout streams, and both tau read-modify-writes of every flip.
 //   * Spins are one bit per chain: a 32-bit word per (tile, spin) holds the 32 lanes' signs.
 //     Three layers of words (previous, current, next) sit in shared memory per warp.
-//   * One layer's graph ({column, 2J} per half-edge) sits in shared memory.
+//   * One layer's graph (band couplings + far-edge list per position) sits in shared memory.
 //   * The RNG warp regenerates the chains' MT19937 states (replica-interleaved in HBM/L2) and
 //     hands uniforms over through a shared-memory ring guarded by mbarriers.
+//
+// The attempt itself is branch-free (flips are predicated, empty band slots add -0.0), so the
+// compiler can overlap the side work of attempt p with the decision chain of attempt p+1.
 //
 // HBM traffic per sweep is one read and one write of the f32 space fields plus the bit words
 // (8.25 B per attempt) and the MT19937 state words (12 B per attempt while they miss L2).
@@ -37,6 +43,7 @@ constexpr uint32_t kTmemColumns = 512;  // the whole TMEM: one CTA per SM
 constexpr uint32_t kStageDraws = 64;    // uniforms per ring stage (per lane)
 constexpr uint32_t kStages = 2;
 constexpr uint32_t kGenBatch = 16;      // draws whose state loads are in flight together
+constexpr uint32_t kUnroll = 8;         // attempts per unrolled chunk == register-window ring size
 
 // ---- Tensor Memory access (sm_100a tcgen05).  All of these are warp-collective.
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t columns) {
@@ -89,6 +96,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait suspends the warp in hardware (up to the hint) instead of spinning on the issue port.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done;
@@ -96,20 +104,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         asm volatile(
             "{\n"
             ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
             "selp.u32 %0, 1, 0, p;\n"
             "}\n"
             : "=r"(done)
-            : "r"(addr), "r"(parity)
+            : "r"(addr), "r"(parity), "r"(100000u)
             : "memory");
     } while (done == 0u);
 }
 
-// ---- shared-memory carve-up (per CTA): [tmem base | barriers][per-pair region x 4]
+// ---- shared-memory carve-up (per CTA): [header][graph x (1 | 4)][per-pair dynamic region x 4]
+struct GraphSmem {
+    uint4* pos;        // P
+    uint4* band_j2;    // P
+    uint4* band_mask;  // P
+    uint2* far;        // max_far
+};
 struct PairSmem {
-    uint32_t* offsets;  // P + 1
-    uint2* edges;       // max_edges : {TMEM column, bits of 2J}
-    float2* tau;        // P : {gamma*2J_tau, 2J_tau}
     uint2* agree_sign;  // P : per layer, {~(up ^ dn), up} spin words
     uint32_t* words;    // 3 * P : ring of spin-bit layers
     float* ring;        // kStages * kStageDraws * 32 uniforms
@@ -118,26 +129,39 @@ struct PairSmem {
 constexpr size_t kHeaderBytes = 256;  // tmem slot + 4 pairs x (full[kStages] + empty[kStages]) barriers
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
-
-__host__ __device__ inline size_t pair_region_bytes(uint32_t P, uint32_t max_edges) {
-    return align16(size_t(P + 1) * 4) + align16(size_t(max_edges) * 8) + align16(size_t(P) * 8) +
-           align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(kStages) * kStageDraws * 32 * 4;
+__host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
+    return size_t(P) * 48 + align16(size_t(max_far ? max_far : 1) * 8);
+}
+__host__ __device__ inline size_t pair_bytes(uint32_t P) {
+    return align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(kStages) * kStageDraws * 32 * 4;
 }
 
-__device__ __forceinline__ PairSmem carve(unsigned char* base, uint32_t P, uint32_t max_edges) {
+__device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P) {
+    GraphSmem g;
+    g.pos = reinterpret_cast<uint4*>(base);
+    g.band_j2 = g.pos + P;
+    g.band_mask = g.band_j2 + P;
+    g.far = reinterpret_cast<uint2*>(g.band_mask + P);
+    return g;
+}
+__device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P) {
     PairSmem s;
-    s.offsets = reinterpret_cast<uint32_t*>(base);
-    base += align16(size_t(P + 1) * 4);
-    s.edges = reinterpret_cast<uint2*>(base);
-    base += align16(size_t(max_edges) * 8);
-    s.tau = reinterpret_cast<float2*>(base);
-    base += align16(size_t(P) * 8);
     s.agree_sign = reinterpret_cast<uint2*>(base);
     base += align16(size_t(P) * 8);
     s.words = reinterpret_cast<uint32_t*>(base);
     base += align16(size_t(P) * 12);
     s.ring = reinterpret_cast<float*>(base);
     return s;
+}
+
+__device__ __forceinline__ void load_graph(const GraphSmem& dst, const DevLayerGraph& g, uint32_t tid,
+                                           uint32_t nthreads) {
+    for (uint32_t k = tid; k < g.per_layer; k += nthreads) {
+        dst.pos[k] = g.pos[k];
+        dst.band_j2[k] = g.band_j2[k];
+        dst.band_mask[k] = g.band_mask[k];
+    }
+    for (uint32_t k = tid; k < g.n_far; k += nthreads) dst.far[k] = g.far[k];
 }
 
 __device__ __forceinline__ void words_copy(uint32_t* dst, const uint32_t* src, uint32_t P, uint32_t lane) {
@@ -199,8 +223,8 @@ struct RingCursor {
     }
 };
 
-__device__ void rng_warp(const DevBatch& b, uint32_t sweeps, uint32_t pair, uint32_t lane, const PairSmem& s,
-                         uint64_t* full, uint64_t* empty, RingCursor& cursor, uint32_t tile) {
+__device__ void rng_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s, uint64_t* full,
+                         uint64_t* empty, RingCursor& cursor, uint32_t tile) {
     uint32_t* w = b.mt + size_t(tile) * kMtN * 32 + lane;
     uint32_t pos = b.mt_pos[tile];
     uint32_t cur = w[size_t(pos) * 32];
@@ -214,24 +238,99 @@ __device__ void rng_warp(const DevBatch& b, uint32_t sweeps, uint32_t pair, uint
         remaining -= take;
     }
     if (lane == 0) b.mt_pos[tile] = pos;
-    (void)pair;
 }
 
 // ---------------------------------------------------------------------------------------
+// Per-lane state of a sweep warp that lives across attempts.
+struct LaneState {
+    uint32_t nb2;      // bits of -2*beta
+    uint32_t sh;       // 31 - lane: shift that brings this lane's bit to the sign position
+    uint32_t flips;
+    double e_run;
+    bool active;
+};
+
+// One Metropolis attempt at position p = p0 + K of the current layer (K is the compile-time
+// index inside the unrolled chunk; the register window r[] is indexed by position & 7).
+template <int EXP, int K>
+__device__ __forceinline__ void attempt(float (&r)[kUnroll], LaneState& st, uint32_t p0, uint32_t P, uint32_t tm,
+                                        const GraphSmem& g, const PairSmem& s, uint32_t* w_cur, const float* u_ptr,
+                                        uint32_t lane) {
+    const uint32_t p = p0 + K;
+    const uint4 rec = g.pos[p];
+    const uint4 bj = g.band_j2[p];
+    const uint4 bm = g.band_mask[p];
+    const uint2 as = s.agree_sign[p];
+    const uint32_t word = w_cur[p];
+    const float u = u_ptr[K * 32];
+
+    const uint32_t sgn_s = (word << st.sh) & 0x80000000u;            // sign bit set <=> s = -1
+    const uint32_t sgn_up = (as.y << st.sh) & 0x80000000u;
+    const uint32_t agree = uint32_t(int32_t(as.x << st.sh) >> 31);  // all ones when s_up == s_dn
+    // tau field J*(s_up + s_dn) in {+2J, +0, -2J}; rec.x carries it already scaled by gamma
+    const float htg = __uint_as_float((rec.x ^ sgn_up) & agree);
+    const float h = r[K];
+    // x = -beta*((2s)*(h + gamma*ht)) == (-2*beta*s)*(h + gamma*ht): doubling is exact, so both
+    // forms round once and to the same value (ref: sweep_kernels.hpp:14-16)
+    const float x = __fmul_rn(__uint_as_float(st.nb2 ^ sgn_s), __fadd_rn(h, htg));
+    const float pr = exp_kind<EXP>(x);
+    const bool accept = st.active && (u < pr);
+
+    // ---- band neighbours: h -= (2s)*J  ==  h + (-(2s)*J); an empty slot adds -0.0 (identity)
+    const uint32_t neg_d = sgn_s ^ 0x80000000u;
+    tmem_wait_ld();  // the entry for p+2 was requested right after the previous attempt
+    if (accept) {
+        r[(K + 6) & 7] = __fadd_rn(r[(K + 6) & 7], __uint_as_float((bj.x ^ neg_d) | bm.x));
+        r[(K + 7) & 7] = __fadd_rn(r[(K + 7) & 7], __uint_as_float((bj.y ^ neg_d) | bm.y));
+        r[(K + 1) & 7] = __fadd_rn(r[(K + 1) & 7], __uint_as_float((bj.z ^ neg_d) | bm.z));
+        r[(K + 2) & 7] = __fadd_rn(r[(K + 2) & 7], __uint_as_float((bj.w ^ neg_d) | bm.w));
+        ++st.flips;
+        const float ht = __uint_as_float((rec.y ^ sgn_up) & agree);
+        const float two_s = __uint_as_float(0x40000000u ^ sgn_s);
+        st.e_run = __dadd_rn(st.e_run, double(__fmul_rn(two_s, __fadd_rn(h, ht))));
+    }
+    const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+    if (lane == 0) w_cur[p] = word ^ ballot;
+
+    // ---- retire column p-2: no later attempt of this layer can reach it through the band
+    if (K >= 2 || p0 != 0) tmem_st(tm + p - 2, r[(K + 6) & 7]);
+
+    // ---- far neighbours: read-modify-write in Tensor Memory
+    const uint32_t far_count = rec.z >> 24;
+    if (far_count != 0u && ballot != 0u) {
+        tmem_wait_st();
+        const uint32_t far_begin = rec.z & 0xffffffu;
+        for (uint32_t e = far_begin; e < far_begin + far_count; ++e) {
+            const uint2 ed = g.far[e];
+            const float old = tmem_ld(tm + ed.x);
+            const float nd = __uint_as_float(ed.y ^ neg_d);
+            tmem_wait_ld();
+            tmem_st(tm + ed.x, accept ? __fadd_rn(old, nd) : old);
+        }
+        tmem_wait_st();
+    }
+}
+
+// Feeds the window entry for position p+3 after attempt p (it is first needed by attempt p+1).
+template <int K>
+__device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t p0, uint32_t P, uint32_t tm) {
+    if (K <= 4 || p0 + kUnroll < P) r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
+}
+
 template <int EXP>
-__device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s, uint64_t* full,
-                           uint64_t* empty, RingCursor& cursor, uint32_t tile, uint32_t tm,
-                           const DevLayerGraph& g) {
-    const uint32_t P = g.per_layer, L = g.layers, n = b.n_spins;
-    const bool active = lane < b.tile_count[tile];
+__device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
+                           const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor, uint32_t tile,
+                           uint32_t tm, uint32_t P, uint32_t L) {
+    const uint32_t n = b.n_spins;
     const uint32_t chain = b.tile_first[tile] + lane;
-    // -2*beta: x = -beta*((2s)*v) == (-2*beta*s)*v exactly (doubling is exact, one rounding each way)
-    const uint32_t nb2 = __float_as_uint(active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
-    double e_run = active ? b.e_run[chain] : 0.0;
-    uint32_t flips = 0;
+    LaneState st;
+    st.active = lane < b.tile_count[tile];
+    st.nb2 = __float_as_uint(st.active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
+    st.sh = 31u - lane;
+    st.flips = 0;
+    st.e_run = st.active ? b.e_run[chain] : 0.0;
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
     uint32_t* words_g = b.spin_bits + size_t(tile) * n;
-    const uint32_t sh = 31u - lane;  // shift that brings this lane's bit to the sign position
 
     uint32_t slot_dn = 2, slot_cur = 0, slot_up = 1;
     words_copy(s.words + slot_dn * P, words_g + size_t(L - 1) * P, P, lane);
@@ -239,29 +338,30 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
     words_copy(s.words + slot_up * P, words_g + size_t(1) * P, P, lane);
     __syncwarp();
 
-    uint32_t ui = 0;        // draws consumed from the current ring stage
-    bool have_stage = false;
+    uint32_t ui = 0;  // draws consumed from the current ring stage (a multiple of kUnroll)
     const float* ring = s.ring + lane;
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
             float* hs_l = hs_g + size_t(l) * P * 32;
             const float* hs_next = hs_g + size_t(l + 1 == L ? 0 : l + 1) * P * 32 - lane;
-            // ---- feed: this layer's fields HBM -> TMEM
-            for (uint32_t p0 = 0; p0 < P; p0 += 32) {
+            // ---- feed: this layer's fields HBM -> TMEM (P is a multiple of 8)
+            uint32_t p0 = 0;
+            for (; p0 + 32 <= P; p0 += 32) {
                 float v[4][8];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t p = p0 + q * 8 + k;
-                        v[q][k] = p < P ? hs_l[size_t(p) * 32] : 0.0f;
-                    }
+                    for (int k = 0; k < 8; ++k) v[q][k] = hs_l[size_t(p0 + q * 8 + k) * 32];
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (p0 + q * 8 < P) tmem_st8(tm + p0 + q * 8, v[q]);
-                }
+                for (int q = 0; q < 4; ++q) tmem_st8(tm + p0 + q * 8, v[q]);
+            }
+            for (; p0 < P; p0 += 8) {
+                float v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = hs_l[size_t(p0 + k) * 32];
+                tmem_st8(tm + p0, v);
             }
             uint32_t* w_cur = s.words + slot_cur * P;
             {   // the tau field of this whole layer is fixed while it is swept: previous layer already
@@ -273,64 +373,54 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             __syncwarp();
             tmem_wait_st();
 
-            for (uint32_t p = 0; p < P; ++p) {
-                if (!have_stage) {
-                    mbar_wait(&full[cursor.stage], cursor.parity);
-                    have_stage = true;
-                }
-                const float u = ring[(size_t(cursor.stage) * kStageDraws + ui) * 32];
-                const float h = tmem_ld(tm + p);
-                const uint2 as = s.agree_sign[p];
-                const float2 tau = s.tau[p];
-                const uint32_t word = w_cur[p];
-                if ((p & 31u) == 0 && p + lane < P) prefetch_l2(hs_next + size_t(p + lane) * 32);
-                const uint32_t sgn_s = (word << sh) & 0x80000000u;       // sign bit set <=> s = -1
-                const uint32_t sgn_up = (as.y << sh) & 0x80000000u;
-                const uint32_t agree = uint32_t(int32_t(as.x << sh) >> 31);  // all ones when s_up == s_dn
-                // tau field J*(s_up + s_dn) in {+2J, +0, -2J}, scaled by gamma for the exponent
-                const float htg = __uint_as_float((__float_as_uint(tau.x) ^ sgn_up) & agree);
-                tmem_wait_ld();
-                const float v = __fadd_rn(h, htg);
-                const float x = __fmul_rn(__uint_as_float(nb2 ^ sgn_s), v);
-                const float pr = exp_kind<EXP>(x);
-                const bool accept = active && (u < pr);
-                const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
-                if (ballot != 0u) {
-                    const uint32_t neg_d = sgn_s ^ 0x80000000u;  // sign of -(2s): h -= (2s)*J == h + (-(2s)J)
-                    const uint32_t e1 = s.offsets[p + 1];
-                    for (uint32_t e = s.offsets[p]; e < e1; ++e) {
-                        const uint2 ed = s.edges[e];
-                        const float old = tmem_ld(tm + ed.x);
-                        const float nd = __uint_as_float(ed.y ^ neg_d);
-                        tmem_wait_ld();
-                        tmem_st(tm + ed.x, accept ? __fadd_rn(old, nd) : old);
-                    }
-                    if (accept) {
-                        ++flips;
-                        const float ht = __uint_as_float((__float_as_uint(tau.y) ^ sgn_up) & agree);
-                        const float two_s = __uint_as_float(0x40000000u ^ sgn_s);
-                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(h, ht))));
-                    }
-                    if (lane == 0) w_cur[p] = word ^ ballot;
-                    tmem_wait_st();
-                }
-                if (++ui == kStageDraws) {
+            // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
+            float r[kUnroll];
+#pragma unroll
+            for (int k = 0; k < int(kUnroll); ++k) r[k] = 0.0f;
+            r[0] = tmem_ld(tm + 0);
+            r[1] = tmem_ld(tm + 1);
+            r[2] = tmem_ld(tm + 2);
+            tmem_wait_ld();
+
+            for (p0 = 0; p0 < P; p0 += kUnroll) {
+                if (ui == 0) mbar_wait(&full[cursor.stage], cursor.parity);
+                const float* u_ptr = ring + (size_t(cursor.stage) * kStageDraws + ui) * 32;
+                if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
+                attempt<EXP, 0>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<0>(r, p0, P, tm);
+                attempt<EXP, 1>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<1>(r, p0, P, tm);
+                attempt<EXP, 2>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<2>(r, p0, P, tm);
+                attempt<EXP, 3>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<3>(r, p0, P, tm);
+                attempt<EXP, 4>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<4>(r, p0, P, tm);
+                attempt<EXP, 5>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<5>(r, p0, P, tm);
+                attempt<EXP, 6>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<6>(r, p0, P, tm);
+                attempt<EXP, 7>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                feed<7>(r, p0, P, tm);
+                ui += kUnroll;
+                if (ui == kStageDraws) {
                     mbar_arrive(&empty[cursor.stage]);
                     cursor.advance();
                     ui = 0;
-                    have_stage = false;
                 }
             }
+            // the last two columns leave the window
+            tmem_st(tm + P - 2, r[6]);
+            tmem_st(tm + P - 1, r[7]);
+            tmem_wait_st();
 
             // ---- retire: TMEM -> HBM, and rotate the spin-bit ring
-            for (uint32_t p0 = 0; p0 < P; p0 += 8) {
+            for (p0 = 0; p0 < P; p0 += 8) {
                 float v[8];
                 tmem_ld8(tm + p0, v);
                 tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (p0 + k < P) hs_l[size_t(p0 + k) * 32] = v[k];
-                }
+                for (int k = 0; k < 8; ++k) hs_l[size_t(p0 + k) * 32] = v[k];
             }
             __syncwarp();
             words_copy(words_g + size_t(l) * P, w_cur, P, lane);
@@ -347,9 +437,9 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
         mbar_arrive(&empty[cursor.stage]);
         cursor.advance();
     }
-    if (active) {
-        b.e_run[chain] = e_run;
-        b.flips[chain] += flips;
+    if (st.active) {
+        b.e_run[chain] = st.e_run;
+        b.flips[chain] += st.flips;
     }
     __syncwarp();
 }
@@ -365,8 +455,17 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     uint64_t* full = bars + pair * 2 * kStages;
     uint64_t* empty = full + kStages;
 
+    const uint32_t maxP = b.max_per_layer;
+    const size_t gbytes = graph_bytes(maxP, b.max_far_edges);
+    unsigned char* graph_base = smem_raw + kHeaderBytes + (b.graph_shared ? 0 : size_t(pair) * gbytes);
+    unsigned char* pair_base =
+        smem_raw + kHeaderBytes + (b.graph_shared ? 1 : kSweepWarps) * gbytes + size_t(pair) * pair_bytes(maxP);
+    const GraphSmem gs = carve_graph(graph_base, maxP);
+    const PairSmem s = carve_pair(pair_base, maxP);
+
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
     if (threadIdx.x < kSweepWarps * 2 * kStages) mbar_init(&bars[threadIdx.x], 32);
+    if (b.graph_shared) load_graph(gs, b.layer_graphs[0], threadIdx.x, kLayeredThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -374,24 +473,19 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     const uint32_t tmem_base = *tmem_slot;
     // this pair's lane quarter: bits 31..16 of a TMEM address are the lane, 15..0 the column
     const uint32_t tm = tmem_base + ((pair * 32u) << 16);
-    const PairSmem s = carve(smem_raw + kHeaderBytes + size_t(pair) * pair_region_bytes(b.max_per_layer, b.max_layer_edges),
-                             b.max_per_layer, b.max_layer_edges);
     RingCursor cursor;
 
     // tiles are dealt round-robin: CTA c, pair w, round r -> tile c + grid*(w + 4r)
     for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
         if (is_rng) {
-            rng_warp(b, sweeps, pair, lane, s, full, empty, cursor, tile);
+            rng_warp(b, sweeps, lane, s, full, empty, cursor, tile);
         } else {
             const DevLayerGraph g = b.layer_graphs[b.tile_model[tile]];
-            // ---- graph of one layer into shared memory
-            for (uint32_t k = lane; k <= g.per_layer; k += 32) s.offsets[k] = g.offsets[k];
-            for (uint32_t k = lane; k < g.n_edges; k += 32) {
-                s.edges[k] = make_uint2(uint32_t(g.targets[k]), __float_as_uint(g.j2[k]));
+            if (!b.graph_shared) {
+                load_graph(gs, g, lane, 32);
+                __syncwarp();
             }
-            for (uint32_t k = lane; k < g.per_layer; k += 32) s.tau[k] = make_float2(g.tau2g[k], g.tau2[k]);
-            __syncwarp();
-            sweep_warp<EXP>(b, sweeps, lane, s, full, empty, cursor, tile, tm, g);
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, empty, cursor, tile, tm, g.per_layer, g.layers);
         }
     }
 
@@ -406,9 +500,10 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
 
 }  // namespace
 
-size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_layer_edges) {
-    if (per_layer == 0 || per_layer > kTmemColumns) return 0;
-    const size_t bytes = kHeaderBytes + kSweepWarps * pair_region_bytes(per_layer, max_layer_edges);
+size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared) {
+    if (per_layer == 0 || per_layer > kTmemColumns || per_layer % kUnroll != 0) return 0;
+    const size_t bytes = kHeaderBytes + (graph_shared ? 1 : kSweepWarps) * graph_bytes(per_layer, max_far_edges) +
+                         kSweepWarps * pair_bytes(per_layer);
     return bytes <= 227 * 1024 ? bytes : 0;
 }
 
