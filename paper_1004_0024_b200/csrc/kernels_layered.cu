@@ -57,15 +57,17 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t columns) {
 }
 __device__ __forceinline__ float tmem_ld(uint32_t taddr) {
     uint32_t v;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
     return __uint_as_float(v);
 }
 __device__ __forceinline__ void tmem_st(uint32_t taddr, float v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v))
-                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v)));
 }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// No "memory" clobbers on the Tensor Memory traffic of the inner loop: volatile asm statements keep
+// their order among themselves, and ordinary shared/global accesses are free to move across them
+// (TMEM is a separate address space), which lets the compiler hoist the next attempt's loads.
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
@@ -97,7 +99,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // try_wait suspends the warp in hardware (up to the hint) instead of spinning on the issue port.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t backoff_ns = 0) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done;
     do {
@@ -110,6 +112,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "=r"(done)
             : "r"(addr), "r"(parity), "r"(100000u)
             : "memory");
+        if (done == 0u) __nanosleep(backoff_ns);
     } while (done == 0u);
 }
 
@@ -231,7 +234,7 @@ __device__ void rng_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, cons
     uint64_t remaining = uint64_t(sweeps) * b.n_spins;
     while (remaining != 0) {
         const uint32_t take = remaining < kStageDraws ? uint32_t(remaining) : kStageDraws;
-        mbar_wait(&empty[cursor.stage], cursor.parity ^ 1u);
+        mbar_wait(&empty[cursor.stage], cursor.parity ^ 1u, 1000);
         mt_generate(w, pos, cur, take, s.ring + size_t(cursor.stage) * kStageDraws * 32 + lane);
         mbar_arrive(&full[cursor.stage]);
         cursor.advance();
@@ -250,62 +253,94 @@ struct LaneState {
     bool active;
 };
 
+// Everything an attempt needs that does not depend on earlier flips of the same chunk; loaded one
+// attempt ahead so the shared-memory latency hides behind the previous decision chain.
+struct Prep {
+    uint4 rec, bj, bm;
+    uint2 as;
+    uint32_t word;
+    float u;
+};
+struct ChunkPtrs {  // all pre-offset to the chunk's first position
+    const uint4* pos;
+    const uint4* band_j2;
+    const uint4* band_mask;
+    const uint2* agree_sign;
+    uint32_t* words;
+    const float* u;
+};
+template <int K>
+__device__ __forceinline__ Prep load_prep(const ChunkPtrs& c) {
+    Prep q;
+    q.rec = c.pos[K];
+    q.bj = c.band_j2[K];
+    q.bm = c.band_mask[K];
+    q.as = c.agree_sign[K];
+    q.word = c.words[K];
+    q.u = c.u[K * 32];
+    return q;
+}
+
 // One Metropolis attempt at position p = p0 + K of the current layer (K is the compile-time
 // index inside the unrolled chunk; the register window r[] is indexed by position & 7).
 template <int EXP, int K>
-__device__ __forceinline__ void attempt(float (&r)[kUnroll], LaneState& st, uint32_t p0, uint32_t P, uint32_t tm,
-                                        const GraphSmem& g, const PairSmem& s, uint32_t* w_cur, const float* u_ptr,
-                                        uint32_t lane) {
+__device__ __forceinline__ void attempt(float (&r)[kUnroll], LaneState& st, const Prep& q, uint32_t p0, uint32_t tm,
+                                        const uint2* far, uint32_t* w_chunk, uint32_t lane) {
     const uint32_t p = p0 + K;
-    const uint4 rec = g.pos[p];
-    const uint4 bj = g.band_j2[p];
-    const uint4 bm = g.band_mask[p];
-    const uint2 as = s.agree_sign[p];
-    const uint32_t word = w_cur[p];
-    const float u = u_ptr[K * 32];
-
-    const uint32_t sgn_s = (word << st.sh) & 0x80000000u;            // sign bit set <=> s = -1
-    const uint32_t sgn_up = (as.y << st.sh) & 0x80000000u;
-    const uint32_t agree = uint32_t(int32_t(as.x << st.sh) >> 31);  // all ones when s_up == s_dn
+    const uint32_t sgn_s = (q.word << st.sh) & 0x80000000u;            // sign bit set <=> s = -1
+    const uint32_t sgn_up = (q.as.y << st.sh) & 0x80000000u;
+    const uint32_t agree = uint32_t(int32_t(q.as.x << st.sh) >> 31);  // all ones when s_up == s_dn
     // tau field J*(s_up + s_dn) in {+2J, +0, -2J}; rec.x carries it already scaled by gamma
-    const float htg = __uint_as_float((rec.x ^ sgn_up) & agree);
+    const float htg = __uint_as_float((q.rec.x ^ sgn_up) & agree);
     const float h = r[K];
     // x = -beta*((2s)*(h + gamma*ht)) == (-2*beta*s)*(h + gamma*ht): doubling is exact, so both
     // forms round once and to the same value (ref: sweep_kernels.hpp:14-16)
     const float x = __fmul_rn(__uint_as_float(st.nb2 ^ sgn_s), __fadd_rn(h, htg));
     const float pr = exp_kind<EXP>(x);
-    const bool accept = st.active && (u < pr);
+    const bool accept = st.active && (q.u < pr);
 
     // ---- band neighbours: h -= (2s)*J  ==  h + (-(2s)*J); an empty slot adds -0.0 (identity)
     const uint32_t neg_d = sgn_s ^ 0x80000000u;
     tmem_wait_ld();  // the entry for p+2 was requested right after the previous attempt
     if (accept) {
-        r[(K + 6) & 7] = __fadd_rn(r[(K + 6) & 7], __uint_as_float((bj.x ^ neg_d) | bm.x));
-        r[(K + 7) & 7] = __fadd_rn(r[(K + 7) & 7], __uint_as_float((bj.y ^ neg_d) | bm.y));
-        r[(K + 1) & 7] = __fadd_rn(r[(K + 1) & 7], __uint_as_float((bj.z ^ neg_d) | bm.z));
-        r[(K + 2) & 7] = __fadd_rn(r[(K + 2) & 7], __uint_as_float((bj.w ^ neg_d) | bm.w));
+        r[(K + 6) & 7] = __fadd_rn(r[(K + 6) & 7], __uint_as_float((q.bj.x ^ neg_d) | q.bm.x));
+        r[(K + 7) & 7] = __fadd_rn(r[(K + 7) & 7], __uint_as_float((q.bj.y ^ neg_d) | q.bm.y));
+        r[(K + 1) & 7] = __fadd_rn(r[(K + 1) & 7], __uint_as_float((q.bj.z ^ neg_d) | q.bm.z));
+        r[(K + 2) & 7] = __fadd_rn(r[(K + 2) & 7], __uint_as_float((q.bj.w ^ neg_d) | q.bm.w));
         ++st.flips;
-        const float ht = __uint_as_float((rec.y ^ sgn_up) & agree);
+        const float ht = __uint_as_float((q.rec.y ^ sgn_up) & agree);
         const float two_s = __uint_as_float(0x40000000u ^ sgn_s);
         st.e_run = __dadd_rn(st.e_run, double(__fmul_rn(two_s, __fadd_rn(h, ht))));
     }
     const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
-    if (lane == 0) w_cur[p] = word ^ ballot;
+    if (lane == 0) w_chunk[K] = q.word ^ ballot;
 
     // ---- retire column p-2: no later attempt of this layer can reach it through the band
     if (K >= 2 || p0 != 0) tmem_st(tm + p - 2, r[(K + 6) & 7]);
 
-    // ---- far neighbours: read-modify-write in Tensor Memory
-    const uint32_t far_count = rec.z >> 24;
+    // ---- far neighbours: read-modify-write in Tensor Memory (the first two with their loads batched)
+    const uint32_t far_count = q.rec.z >> 24;
     if (far_count != 0u && ballot != 0u) {
+        const uint2* fe = far + (q.rec.z & 0xffffffu);
         tmem_wait_st();
-        const uint32_t far_begin = rec.z & 0xffffffu;
-        for (uint32_t e = far_begin; e < far_begin + far_count; ++e) {
-            const uint2 ed = g.far[e];
-            const float old = tmem_ld(tm + ed.x);
-            const float nd = __uint_as_float(ed.y ^ neg_d);
+        const uint2 e0 = fe[0];
+        const uint2 e1 = fe[far_count > 1u ? 1 : 0];
+        float v0 = tmem_ld(tm + e0.x);
+        float v1 = 0.0f;
+        if (far_count > 1u) v1 = tmem_ld(tm + e1.x);
+        tmem_wait_ld();
+        if (accept) {
+            v0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
+            v1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
+        }
+        tmem_st(tm + e0.x, v0);
+        if (far_count > 1u) tmem_st(tm + e1.x, v1);
+        for (uint32_t e = 2; e < far_count; ++e) {
+            const uint2 ed = fe[e];
+            float v = tmem_ld(tm + ed.x);
             tmem_wait_ld();
-            tmem_st(tm + ed.x, accept ? __fadd_rn(old, nd) : old);
+            if (accept) v = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
+            tmem_st(tm + ed.x, v);
         }
         tmem_wait_st();
     }
@@ -384,23 +419,37 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
 
             for (p0 = 0; p0 < P; p0 += kUnroll) {
                 if (ui == 0) mbar_wait(&full[cursor.stage], cursor.parity);
-                const float* u_ptr = ring + (size_t(cursor.stage) * kStageDraws + ui) * 32;
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
-                attempt<EXP, 0>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                ChunkPtrs c;
+                c.pos = g.pos + p0;
+                c.band_j2 = g.band_j2 + p0;
+                c.band_mask = g.band_mask + p0;
+                c.agree_sign = s.agree_sign + p0;
+                c.words = w_cur + p0;
+                c.u = ring + (size_t(cursor.stage) * kStageDraws + ui) * 32;
+                const Prep q0 = load_prep<0>(c);
+                const Prep q1 = load_prep<1>(c);
+                attempt<EXP, 0>(r, st, q0, p0, tm, g.far, c.words, lane);
                 feed<0>(r, p0, P, tm);
-                attempt<EXP, 1>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                const Prep q2 = load_prep<2>(c);
+                attempt<EXP, 1>(r, st, q1, p0, tm, g.far, c.words, lane);
                 feed<1>(r, p0, P, tm);
-                attempt<EXP, 2>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                const Prep q3 = load_prep<3>(c);
+                attempt<EXP, 2>(r, st, q2, p0, tm, g.far, c.words, lane);
                 feed<2>(r, p0, P, tm);
-                attempt<EXP, 3>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                const Prep q4 = load_prep<4>(c);
+                attempt<EXP, 3>(r, st, q3, p0, tm, g.far, c.words, lane);
                 feed<3>(r, p0, P, tm);
-                attempt<EXP, 4>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                const Prep q5 = load_prep<5>(c);
+                attempt<EXP, 4>(r, st, q4, p0, tm, g.far, c.words, lane);
                 feed<4>(r, p0, P, tm);
-                attempt<EXP, 5>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                const Prep q6 = load_prep<6>(c);
+                attempt<EXP, 5>(r, st, q5, p0, tm, g.far, c.words, lane);
                 feed<5>(r, p0, P, tm);
-                attempt<EXP, 6>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                const Prep q7 = load_prep<7>(c);
+                attempt<EXP, 6>(r, st, q6, p0, tm, g.far, c.words, lane);
                 feed<6>(r, p0, P, tm);
-                attempt<EXP, 7>(r, st, p0, P, tm, g, s, w_cur, u_ptr, lane);
+                attempt<EXP, 7>(r, st, q7, p0, tm, g.far, c.words, lane);
                 feed<7>(r, p0, P, tm);
                 ui += kUnroll;
                 if (ui == kStageDraws) {

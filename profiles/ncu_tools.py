@@ -21,6 +21,7 @@ def segments(path, warp_attempts, min_freq=0.01):
     agg = {s: sum(int(r[ix[s]] or 0) for r in data) for s in stalls}
     print("  ".join(f"{s[6:]} {100 * v / tot:.1f}%" for s, v in sorted(agg.items(), key=lambda x: -x[1])[:8]))
     seg, prev = [], None
+    merged = collections.OrderedDict()
 
     def flush():
         if not seg:
@@ -33,9 +34,12 @@ def segments(path, warp_attempts, min_freq=0.01):
         st = collections.Counter()
         for s in seg:
             st.update(s[4])
-        top = ", ".join(f"{k[6:]} {100 * v / tot:.1f}" for k, v in st.most_common(3) if v)
-        print(f"L{seg[0][0]:4d}-{seg[-1][0]:4d} n={n:4d} f={f:6.3f} inst/att={n * f:6.2f} smp={100 * smp / tot:5.1f}% [{top}] "
-              f"{dict(ops.most_common(5))}")
+        key = (n, tuple(sorted(ops.items())))
+        m = merged.setdefault(key, dict(first=seg[0][0], copies=0, inst=0.0, smp=0, st=collections.Counter(), ops=ops, n=n))
+        m["copies"] += 1
+        m["inst"] += n * f
+        m["smp"] += smp
+        m["st"].update(st)
 
     for n, r in enumerate(data):
         f = round(int(r[ix["Instructions Executed"]]) / warp_attempts, 3)
@@ -45,6 +49,10 @@ def segments(path, warp_attempts, min_freq=0.01):
         seg.append((n, f, int(r[ix["# Samples"]]), r[ix["Source"]], {s: int(r[ix[s]] or 0) for s in stalls}))
         prev = f
     flush()
+    for m in merged.values():
+        top = ", ".join(f"{k[6:]} {100 * v / tot:.1f}" for k, v in m["st"].most_common(3) if v)
+        print(f"L{m['first']:4d} n={m['n']:4d} x{m['copies']:2d} inst/att={m['inst']:6.2f} smp={100 * m['smp'] / tot:5.1f}% "
+              f"[{top}] {dict(m['ops'].most_common(6))}")
 
 
 def raw(path, keys):
