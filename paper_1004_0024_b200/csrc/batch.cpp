@@ -208,6 +208,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         dev_.max_far_edges = max_far_edges;
         dev_.max_per_layer = max_per_layer;
         dev_.graph_shared = graph_shared ? 1u : 0u;
+        dev_.layered_stages = layered_stage_count(max_per_layer, max_far_edges, graph_shared);
         dev_.layered_smem = uint32_t(layered_smem);
         cuda_check(prepare_layered_kernels(layered_smem), "cudaFuncSetAttribute");
     }

@@ -56,6 +56,7 @@ struct DevBatch {
     uint32_t layered_smem;              // dynamic shared memory of one layered-kernel CTA
     uint32_t max_per_layer;             // largest per_layer over the batch's models
     uint32_t graph_shared;              // 1: all tiles use model 0, one shared-memory copy per CTA
+    uint32_t layered_stages;            // depth of the helper/sweep stage ring (2, 4 or 8)
     uint32_t n_spins;
     uint32_t n_tiles;
     uint32_t n_chains;
@@ -94,6 +95,7 @@ cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_
 cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_count, cudaStream_t stream);
 // Bytes of dynamic shared memory one CTA of the layered kernel needs (0: does not fit).
 size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared);
+uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared);
 cudaError_t prepare_layered_kernels(size_t smem_bytes);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);

@@ -1,9 +1,23 @@
 // Layered-model sweep kernel: the performance path for identical-layer ("QMC-style") models.
 //
-// One persistent CTA per SM; four SWEEP warps and four RNG warps per CTA.  Sweep warp w and RNG
-// warp 4+w share a tile of 32 chains (lane = chain) and — because warp_id % 4 picks the SM
-// sub-partition — the same scheduler, so the generator's integer work fills the issue slots the
-// sweep's dependent floating-point chain leaves empty.
+// One persistent CTA per SM; four SWEEP warps and four HELPER warps per CTA.  Sweep warp w and
+// helper warp 4+w share a tile of 32 chains (lane = chain) and — because warp_id % 4 picks the SM
+// sub-partition — the same scheduler.  The sweep of a chain is strictly sequential (attempt p+1
+// needs the flips of attempt p), so the sweep warp is latency bound; everything that does not
+// sit on that loop-carried chain is moved to the helper, whose instructions fill the issue
+// slots the chain leaves empty:
+//
+//   helper warp, ahead of the sweep   MT19937 regeneration (replica-interleaved state in HBM/L2),
+//                                     tempering, u32 -> unit float, and per attempt the lane's
+//                                     sign constants and tau field ("prep record")
+//   sweep warp                        decision, band-neighbour updates, ballot, far-neighbour
+//                                     updates, Tensor Memory window traffic
+//   helper warp, behind the sweep     accept counts, running energy, spin-word updates
+//
+// The two meet in a shared-memory ring of 8-attempt stages guarded by mbarriers: the helper
+// fills a stage with prep records {u, -2*beta*s, gamma*h_tau, h_tau}; the sweep warp consumes it,
+// writes back the field it decided on and the accept ballot, and hands the stage back; the helper
+// post-processes it before refilling.
 //
 // A chain's working set for one layer lives ON CHIP:
 //   * Tensor Memory holds the space fields of the layer being swept: column p of the warp's own
@@ -18,13 +32,8 @@
 //     from two spin bits of the adjacent layers.  That removes 8 of the 17 bytes per attempt the
 //     generic layout streams, and both tau read-modify-writes of every flip.
 //   * Spins are one bit per chain: a 32-bit word per (tile, spin) holds the 32 lanes' signs.
-//     Three layers of words (previous, current, next) sit in shared memory per warp.
+//     Three layers of words (previous, current, next) sit in shared memory per pair.
 //   * One layer's graph (band couplings + far-edge list per position) sits in shared memory.
-//   * The RNG warp regenerates the chains' MT19937 states (replica-interleaved in HBM/L2) and
-//     hands uniforms over through a shared-memory ring guarded by mbarriers.
-//
-// The attempt itself is branch-free (flips are predicated, empty band slots add -0.0), so the
-// compiler can overlap the side work of attempt p with the decision chain of attempt p+1.
 //
 // HBM traffic per sweep is one read and one write of the f32 space fields plus the bit words
 // (8.25 B per attempt) and the MT19937 state words (12 B per attempt while they miss L2).
@@ -40,10 +49,8 @@ namespace {
 constexpr int kSweepWarps = 4;          // one TMEM lane quarter each
 constexpr int kLayeredThreads = 2 * kSweepWarps * 32;
 constexpr uint32_t kTmemColumns = 512;  // the whole TMEM: one CTA per SM
-constexpr uint32_t kStageDraws = 64;    // uniforms per ring stage (per lane)
-constexpr uint32_t kStages = 2;
-constexpr uint32_t kGenBatch = 16;      // draws whose state loads are in flight together
-constexpr uint32_t kUnroll = 8;         // attempts per unrolled chunk == register-window ring size
+constexpr uint32_t kUnroll = 8;         // attempts per ring stage == unrolled chunk == window ring size
+constexpr uint32_t kMaxStages = 8;
 
 // ---- Tensor Memory access (sm_100a tcgen05).  All of these are warp-collective.
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t columns) {
@@ -55,6 +62,9 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t colum
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t columns) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(columns) : "memory");
 }
+// No "memory" clobbers on the Tensor Memory traffic of the inner loop: volatile asm statements keep
+// their order among themselves, and ordinary shared/global accesses are free to move across them
+// (TMEM is a separate address space), which lets the compiler hoist the next attempt's loads.
 __device__ __forceinline__ float tmem_ld(uint32_t taddr) {
     uint32_t v;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
@@ -63,9 +73,6 @@ __device__ __forceinline__ float tmem_ld(uint32_t taddr) {
 __device__ __forceinline__ void tmem_st(uint32_t taddr, float v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v)));
 }
-// No "memory" clobbers on the Tensor Memory traffic of the inner loop: volatile asm statements keep
-// their order among themselves, and ordinary shared/global accesses are free to move across them
-// (TMEM is a separate address space), which lets the compiler hoist the next attempt's loads.
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
 
@@ -88,7 +95,7 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
 
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-// ---- mbarrier (shared::cta) helpers for the uniform ring
+// ---- mbarrier (shared::cta) helpers for the stage ring
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -98,27 +105,26 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// try_wait suspends the warp in hardware (up to the hint) instead of spinning on the issue port.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t backoff_ns = 0) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t backoff_ns) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done;
     do {
         asm volatile(
             "{\n"
             ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
             "selp.u32 %0, 1, 0, p;\n"
             "}\n"
             : "=r"(done)
-            : "r"(addr), "r"(parity), "r"(100000u)
+            : "r"(addr), "r"(parity)
             : "memory");
-        if (done == 0u) __nanosleep(backoff_ns);
+        if (done == 0u && backoff_ns != 0u) __nanosleep(backoff_ns);
     } while (done == 0u);
 }
 
 // ---- shared-memory carve-up (per CTA): [header][graph x (1 | 4)][per-pair dynamic region x 4]
 struct GraphSmem {
-    uint4* pos;        // P
+    uint4* pos;        // P : {gamma*2J_tau, 2J_tau, far_begin | far_count << 24, 0}
     uint4* band_j2;    // P
     uint4* band_mask;  // P
     uint2* far;        // max_far
@@ -126,17 +132,20 @@ struct GraphSmem {
 struct PairSmem {
     uint2* agree_sign;  // P : per layer, {~(up ^ dn), up} spin words
     uint32_t* words;    // 3 * P : ring of spin-bit layers
-    float* ring;        // kStages * kStageDraws * 32 uniforms
+    float4* recs;       // stages * 8 * 32 prep records {u | h, -2*beta*s, gamma*h_tau, h_tau}
+    uint32_t* ballots;  // stages * 8
 };
 
-constexpr size_t kHeaderBytes = 256;  // tmem slot + 4 pairs x (full[kStages] + empty[kStages]) barriers
+// header: tmem slot (16 B) + per pair full[8] + empty[8] barriers (128 B) x 4
+constexpr size_t kHeaderBytes = 16 + kSweepWarps * 2 * kMaxStages * 8;
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
     return size_t(P) * 48 + align16(size_t(max_far ? max_far : 1) * 8);
 }
-__host__ __device__ inline size_t pair_bytes(uint32_t P) {
-    return align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(kStages) * kStageDraws * 32 * 4;
+__host__ __device__ inline size_t pair_bytes(uint32_t P, uint32_t stages) {
+    return align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(stages) * kUnroll * 32 * 16 +
+           align16(size_t(stages) * kUnroll * 4);
 }
 
 __device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P) {
@@ -147,13 +156,15 @@ __device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P
     g.far = reinterpret_cast<uint2*>(g.band_mask + P);
     return g;
 }
-__device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P) {
+__device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P, uint32_t stages) {
     PairSmem s;
     s.agree_sign = reinterpret_cast<uint2*>(base);
     base += align16(size_t(P) * 8);
     s.words = reinterpret_cast<uint32_t*>(base);
     base += align16(size_t(P) * 12);
-    s.ring = reinterpret_cast<float*>(base);
+    s.recs = reinterpret_cast<float4*>(base);
+    base += size_t(stages) * kUnroll * 32 * 16;
+    s.ballots = reinterpret_cast<uint32_t*>(base);
     return s;
 }
 
@@ -171,157 +182,242 @@ __device__ __forceinline__ void words_copy(uint32_t* dst, const uint32_t* src, u
     for (uint32_t k = lane; k < P; k += 32) dst[k] = src[k];
 }
 
-// ---------------------------------------------------------------------------------------
-// RNG warp: regenerates `take` words of every lane's MT19937 state in place and writes the
-// tempered, truncated uniforms to out[k*32].  The state is walked in runs that do not cross
-// the recurrence's wrap points (word 227: the far operand wraps; word 623: the next operand
-// wraps), so inside a run all three operands advance by one row (ref: rng.cpp:89-96).
-__device__ __forceinline__ void mt_generate(uint32_t* w, uint32_t& pos, uint32_t& cur, uint32_t take,
-                                            float* out) {
-    uint32_t done = 0;
-    while (done < take) {
-        const uint32_t seg_end = pos < kMtN - kMtM ? kMtN - kMtM : (pos < kMtN - 1 ? kMtN - 1 : kMtN);
-        const uint32_t cnt = min(take - done, seg_end - pos);
-        uint32_t* wp = w + size_t(pos) * 32;
-        const uint32_t* fp = w + size_t(pos < kMtN - kMtM ? pos + kMtM : pos - (kMtN - kMtM)) * 32;
-        const uint32_t* np = pos == kMtN - 1 ? w : wp + 32;
-        uint32_t k = 0;
-        for (; k + kGenBatch <= cnt; k += kGenBatch) {
-            uint32_t nxt[kGenBatch], far[kGenBatch];
-#pragma unroll
-            for (int i = 0; i < int(kGenBatch); ++i) {
-                nxt[i] = np[size_t(k + i) * 32];
-                far[i] = fp[size_t(k + i) * 32];
-            }
-#pragma unroll
-            for (int i = 0; i < int(kGenBatch); ++i) {
-                const uint32_t v = mt_recurrence(cur, nxt[i], far[i]);
-                wp[size_t(k + i) * 32] = v;
-                cur = nxt[i];
-                out[size_t(k + i) * 32] = u32_to_unit(mt_temper(v));
-            }
-        }
-        for (; k < cnt; ++k) {
-            const uint32_t nx = np[size_t(k) * 32];
-            const uint32_t v = mt_recurrence(cur, nx, fp[size_t(k) * 32]);
-            wp[size_t(k) * 32] = v;
-            cur = nx;
-            out[size_t(k) * 32] = u32_to_unit(mt_temper(v));
-        }
-        pos += cnt;
-        pos = pos == kMtN ? 0u : pos;
-        done += cnt;
-        out += size_t(cnt) * 32;
-    }
-}
-
+// Position of a pair in its stage ring.  Both warps of a pair walk the same sequence of stages;
+// a stage's barrier phase parity is the number of times it has been waited on, kept as one bit
+// per stage.
 struct RingCursor {
     uint32_t stage = 0;
-    uint32_t parity = 0;
-    __device__ __forceinline__ void advance() {
-        if (++stage == kStages) {
-            stage = 0;
-            parity ^= 1u;
-        }
-    }
+    uint32_t parity_bits = 0;  // next parity to wait for, per stage
+    __device__ __forceinline__ uint32_t parity() const { return (parity_bits >> stage) & 1u; }
+    __device__ __forceinline__ void waited() { parity_bits ^= 1u << stage; }
+    __device__ __forceinline__ void advance(uint32_t stages) { stage = stage + 1 == stages ? 0u : stage + 1; }
 };
 
-__device__ void rng_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s, uint64_t* full,
-                         uint64_t* empty, RingCursor& cursor, uint32_t tile) {
-    uint32_t* w = b.mt + size_t(tile) * kMtN * 32 + lane;
-    uint32_t pos = b.mt_pos[tile];
-    uint32_t cur = w[size_t(pos) * 32];
-    uint64_t remaining = uint64_t(sweeps) * b.n_spins;
-    while (remaining != 0) {
-        const uint32_t take = remaining < kStageDraws ? uint32_t(remaining) : kStageDraws;
-        mbar_wait(&empty[cursor.stage], cursor.parity ^ 1u, 1000);
-        mt_generate(w, pos, cur, take, s.ring + size_t(cursor.stage) * kStageDraws * 32 + lane);
-        mbar_arrive(&full[cursor.stage]);
-        cursor.advance();
-        remaining -= take;
-    }
-    if (lane == 0) b.mt_pos[tile] = pos;
-}
-
-// ---------------------------------------------------------------------------------------
-// Per-lane state of a sweep warp that lives across attempts.
-struct LaneState {
-    uint32_t nb2;      // bits of -2*beta
-    uint32_t sh;       // 31 - lane: shift that brings this lane's bit to the sign position
-    uint32_t flips;
+// =======================================================================================
+// Helper warp
+// =======================================================================================
+struct HelperState {
+    uint32_t* mt;      // this lane's MT19937 state column
+    uint32_t pos, cur;
+    uint32_t nxt[kUnroll], far[kUnroll];  // operands of the next 8 draws, loaded one chunk ahead
+    uint32_t nb2, sh, flips;
     double e_run;
     bool active;
 };
 
-// Everything an attempt needs that does not depend on earlier flips of the same chunk; loaded one
-// attempt ahead so the shared-memory latency hides behind the previous decision chain.
-struct Prep {
-    uint4 rec, bj, bm;
-    uint2 as;
-    uint32_t word;
-    float u;
-};
-struct ChunkPtrs {  // all pre-offset to the chunk's first position
-    const uint4* pos;
-    const uint4* band_j2;
-    const uint4* band_mask;
-    const uint2* agree_sign;
-    uint32_t* words;
-    const float* u;
-};
-template <int K>
-__device__ __forceinline__ Prep load_prep(const ChunkPtrs& c) {
-    Prep q;
-    q.rec = c.pos[K];
-    q.bj = c.band_j2[K];
-    q.bm = c.band_mask[K];
-    q.as = c.agree_sign[K];
-    q.word = c.words[K];
-    q.u = c.u[K * 32];
-    return q;
+// Loads the recurrence operands of draws pos..pos+7 (ref: rng.cpp:22-25).  Fast path: the run does
+// not cross a wrap point (word 227: far operand wraps, 623: next operand wraps).
+__device__ __forceinline__ void mt_load_operands(HelperState& h) {
+    const uint32_t pos = h.pos;
+    const bool straight = pos + kUnroll <= kMtN - kMtM || (pos >= kMtN - kMtM && pos + kUnroll <= kMtN - 1);
+    if (straight) {
+        const uint32_t* np = h.mt + size_t(pos + 1) * 32;
+        const uint32_t* fp = h.mt + size_t(pos < kMtN - kMtM ? pos + kMtM : pos - (kMtN - kMtM)) * 32;
+#pragma unroll
+        for (int k = 0; k < int(kUnroll); ++k) {
+            h.nxt[k] = np[size_t(k) * 32];
+            h.far[k] = fp[size_t(k) * 32];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < int(kUnroll); ++k) {
+            uint32_t jn = pos + k + 1, jf = pos + k + kMtM;
+            jn = jn >= kMtN ? jn - kMtN : jn;
+            jf = jf >= kMtN ? jf - kMtN : jf;
+            h.nxt[k] = h.mt[size_t(jn) * 32];
+            h.far[k] = h.mt[size_t(jf) * 32];
+        }
+    }
 }
 
+// Regenerates words pos..pos+7 in place from the preloaded operands and returns the raw outputs.
+// None of the operands of a chunk is a word the chunk before it rewrote (the `next` words lie
+// ahead of it, the `far` words 227 draws behind or 397 ahead), so loading them a chunk early
+// reads exactly what the in-place loop of ref: rng.cpp:89-96 reads.
+__device__ __forceinline__ void mt_generate8(HelperState& h, uint32_t (&raw)[kUnroll]) {
+    const uint32_t pos = h.pos;
+#pragma unroll
+    for (int k = 0; k < int(kUnroll); ++k) {
+        uint32_t j = pos + k;
+        j = j >= kMtN ? j - kMtN : j;
+        const uint32_t nx = h.nxt[k];
+        const uint32_t v = mt_recurrence(h.cur, nx, h.far[k]);
+        h.mt[size_t(j) * 32] = v;
+        h.cur = nx;
+        raw[k] = mt_temper(v);
+    }
+    h.pos = pos + kUnroll >= kMtN ? pos + kUnroll - kMtN : pos + kUnroll;
+}
+
+// Accept counts, running energy and spin words of one consumed stage (ref: sweep_basic.cpp:47-48;
+// the energy bookkeeping is the tempering definition of oracle/ising_oracle.h).
+__device__ __forceinline__ void post_stage(HelperState& h, const float4* recs, const uint32_t* ballots,
+                                           uint32_t* words, uint32_t lane) {
+#pragma unroll
+    for (int k = 0; k < int(kUnroll); ++k) {
+        const uint32_t ballot = ballots[k];
+        const float4 rec = recs[k * 32];
+        if ((ballot >> lane) & 1u) {
+            ++h.flips;
+            // rec.y = -2*beta*s carries the opposite of the spin's sign: 2s = 2.0 with the sign of s
+            const float two_s = __uint_as_float(0x40000000u | (~__float_as_uint(rec.y) & 0x80000000u));
+            h.e_run = __dadd_rn(h.e_run, double(__fmul_rn(two_s, __fadd_rn(rec.x, rec.w))));
+        }
+        if (lane == 0 && ballot != 0u) words[k] ^= ballot;
+    }
+}
+
+__device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
+                            const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor,
+                            uint32_t stages, uint32_t tile, uint32_t P, uint32_t L) {
+    const uint32_t n = b.n_spins;
+    const uint32_t chain = b.tile_first[tile] + lane;
+    HelperState h;
+    h.active = lane < b.tile_count[tile];
+    h.nb2 = __float_as_uint(h.active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
+    h.sh = 31u - lane;
+    h.flips = 0;
+    h.e_run = h.active ? b.e_run[chain] : 0.0;
+    h.mt = b.mt + size_t(tile) * kMtN * 32 + lane;
+    h.pos = b.mt_pos[tile];
+    h.cur = h.mt[size_t(h.pos) * 32];
+    mt_load_operands(h);
+
+    uint32_t* words_g = b.spin_bits + size_t(tile) * n;
+    uint32_t slot_dn = 2, slot_cur = 0, slot_up = 1;
+    words_copy(s.words + slot_dn * P, words_g + size_t(L - 1) * P, P, lane);
+    words_copy(s.words + slot_cur * P, words_g, P, lane);
+    words_copy(s.words + slot_up * P, words_g + size_t(1) * P, P, lane);
+    __syncwarp();
+
+    // bit s set: stage s holds results of the sweep warp that still await post-processing
+    uint32_t unposted = 0;
+    uint32_t post_p0[kMaxStages];  // chunk start position of the content of every stage
+#pragma unroll
+    for (int k = 0; k < int(kMaxStages); ++k) post_p0[k] = 0;
+
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t l = 0; l < L; ++l) {
+            uint32_t* w_cur = s.words + slot_cur * P;
+            {   // the tau field of this whole layer is fixed while it is swept: previous layer already
+                // visited, next layer not yet.  agree = neighbours equal, sign = their common spin bit.
+                const uint32_t* w_up = s.words + slot_up * P;
+                const uint32_t* w_dn = s.words + slot_dn * P;
+                for (uint32_t k = lane; k < P; k += 32) s.agree_sign[k] = make_uint2(~(w_up[k] ^ w_dn[k]), w_up[k]);
+            }
+            __syncwarp();
+
+            for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
+                const uint32_t st = cursor.stage;
+                float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
+                if ((unposted >> st) & 1u) {  // recycle: wait for the sweep warp, then post-process
+                    mbar_wait(&empty[st], cursor.parity(), 200);
+                    cursor.waited();
+                    uint32_t pp = 0;
+#pragma unroll
+                    for (int k = 0; k < int(kMaxStages); ++k) pp = st == uint32_t(k) ? post_p0[k] : pp;
+                    post_stage(h, recs, s.ballots + st * kUnroll, w_cur + pp, lane);
+                }
+                uint32_t raw[kUnroll];
+                mt_generate8(h, raw);
+                mt_load_operands(h);  // operands of the next chunk: in flight while this one is prepared
+#pragma unroll
+                for (int k = 0; k < int(kUnroll); ++k) {
+                    const uint32_t p = p0 + k;
+                    const uint32_t word = w_cur[p];
+                    const uint2 as = s.agree_sign[p];
+                    const uint4 tau = g.pos[p];
+                    const uint32_t sgn_s = (word << h.sh) & 0x80000000u;  // sign bit set <=> s = -1
+                    const uint32_t sgn_up = (as.y << h.sh) & 0x80000000u;
+                    const uint32_t agree = uint32_t(int32_t(as.x << h.sh) >> 31);  // ones when s_up == s_dn
+                    float4 rec;
+                    rec.x = h.active ? u32_to_unit(raw[k]) : 2.0f;  // padding lanes never accept
+                    // x = -beta*((2s)*v) == (-2*beta*s)*v: doubling is exact, one rounding either way
+                    rec.y = __uint_as_float(h.nb2 ^ sgn_s);
+                    // tau field J*(s_up + s_dn) in {+2J, +0, -2J}: scaled by gamma, and raw
+                    rec.z = __uint_as_float((tau.x ^ sgn_up) & agree);
+                    rec.w = __uint_as_float((tau.y ^ sgn_up) & agree);
+                    recs[k * 32] = rec;
+                }
+#pragma unroll
+                for (int k = 0; k < int(kMaxStages); ++k) post_p0[k] = st == uint32_t(k) ? p0 : post_p0[k];
+                unposted |= 1u << st;
+                mbar_arrive(&full[st]);
+                cursor.advance(stages);
+            }
+
+            // ---- end of layer: collect every outstanding stage, then rotate the spin-bit ring
+            {
+                uint32_t st = cursor.stage;  // oldest stage first
+                for (uint32_t k = 0; k < stages; ++k) {
+                    if ((unposted >> st) & 1u) {
+                        mbar_wait(&empty[st], (cursor.parity_bits >> st) & 1u, 200);
+                        cursor.parity_bits ^= 1u << st;
+                        uint32_t pp = 0;
+#pragma unroll
+                        for (int q = 0; q < int(kMaxStages); ++q) pp = st == uint32_t(q) ? post_p0[q] : pp;
+                        post_stage(h, s.recs + size_t(st) * kUnroll * 32 + lane, s.ballots + st * kUnroll,
+                                   w_cur + pp, lane);
+                        unposted &= ~(1u << st);
+                    }
+                    st = st + 1 == stages ? 0u : st + 1;
+                }
+            }
+            __syncwarp();
+            words_copy(words_g + size_t(l) * P, w_cur, P, lane);
+            // layer l-1's slot is free now: it receives layer l+2 (the `up` of the next layer)
+            words_copy(s.words + slot_dn * P, words_g + size_t((l + 2) % L) * P, P, lane);
+            __syncwarp();
+            const uint32_t freed = slot_dn;
+            slot_dn = slot_cur;
+            slot_cur = slot_up;
+            slot_up = freed;
+        }
+    }
+    if (lane == 0) b.mt_pos[tile] = h.pos;
+    if (h.active) {
+        b.e_run[chain] = h.e_run;
+        b.flips[chain] += h.flips;
+    }
+    __syncwarp();
+}
+
+// =======================================================================================
+// Sweep warp
+// =======================================================================================
 // One Metropolis attempt at position p = p0 + K of the current layer (K is the compile-time
 // index inside the unrolled chunk; the register window r[] is indexed by position & 7).
 template <int EXP, int K>
-__device__ __forceinline__ void attempt(float (&r)[kUnroll], LaneState& st, const Prep& q, uint32_t p0, uint32_t tm,
-                                        const uint2* far, uint32_t* w_chunk, uint32_t lane) {
-    const uint32_t p = p0 + K;
-    const uint32_t sgn_s = (q.word << st.sh) & 0x80000000u;            // sign bit set <=> s = -1
-    const uint32_t sgn_up = (q.as.y << st.sh) & 0x80000000u;
-    const uint32_t agree = uint32_t(int32_t(q.as.x << st.sh) >> 31);  // all ones when s_up == s_dn
-    // tau field J*(s_up + s_dn) in {+2J, +0, -2J}; rec.x carries it already scaled by gamma
-    const float htg = __uint_as_float((q.rec.x ^ sgn_up) & agree);
+__device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, const uint4 bj, const uint4 bm,
+                                        uint32_t far_info, uint32_t p0, uint32_t tm, const uint2* far,
+                                        float* rec_x, uint32_t* ballots, uint32_t lane) {
     const float h = r[K];
-    // x = -beta*((2s)*(h + gamma*ht)) == (-2*beta*s)*(h + gamma*ht): doubling is exact, so both
-    // forms round once and to the same value (ref: sweep_kernels.hpp:14-16)
-    const float x = __fmul_rn(__uint_as_float(st.nb2 ^ sgn_s), __fadd_rn(h, htg));
+    const float x = __fmul_rn(rec.y, __fadd_rn(h, rec.z));  // ref: sweep_kernels.hpp:14-16
     const float pr = exp_kind<EXP>(x);
-    const bool accept = st.active && (q.u < pr);
+    const bool accept = rec.x < pr;  // no clamp: ref sweep_basic.cpp:36-37
 
     // ---- band neighbours: h -= (2s)*J  ==  h + (-(2s)*J); an empty slot adds -0.0 (identity)
-    const uint32_t neg_d = sgn_s ^ 0x80000000u;
+    const uint32_t neg_d = __float_as_uint(rec.y) & 0x80000000u;  // sign of -(2s), beta >= 0
     tmem_wait_ld();  // the entry for p+2 was requested right after the previous attempt
-    if (accept) {
-        r[(K + 6) & 7] = __fadd_rn(r[(K + 6) & 7], __uint_as_float((q.bj.x ^ neg_d) | q.bm.x));
-        r[(K + 7) & 7] = __fadd_rn(r[(K + 7) & 7], __uint_as_float((q.bj.y ^ neg_d) | q.bm.y));
-        r[(K + 1) & 7] = __fadd_rn(r[(K + 1) & 7], __uint_as_float((q.bj.z ^ neg_d) | q.bm.z));
-        r[(K + 2) & 7] = __fadd_rn(r[(K + 2) & 7], __uint_as_float((q.bj.w ^ neg_d) | q.bm.w));
-        ++st.flips;
-        const float ht = __uint_as_float((q.rec.y ^ sgn_up) & agree);
-        const float two_s = __uint_as_float(0x40000000u ^ sgn_s);
-        st.e_run = __dadd_rn(st.e_run, double(__fmul_rn(two_s, __fadd_rn(h, ht))));
-    }
+    const float a0 = __fadd_rn(r[(K + 6) & 7], __uint_as_float((bj.x ^ neg_d) | bm.x));
+    const float a1 = __fadd_rn(r[(K + 7) & 7], __uint_as_float((bj.y ^ neg_d) | bm.y));
+    const float a2 = __fadd_rn(r[(K + 1) & 7], __uint_as_float((bj.z ^ neg_d) | bm.z));
+    const float a3 = __fadd_rn(r[(K + 2) & 7], __uint_as_float((bj.w ^ neg_d) | bm.w));
+    r[(K + 6) & 7] = accept ? a0 : r[(K + 6) & 7];
+    r[(K + 7) & 7] = accept ? a1 : r[(K + 7) & 7];
+    r[(K + 1) & 7] = accept ? a2 : r[(K + 1) & 7];
+    r[(K + 2) & 7] = accept ? a3 : r[(K + 2) & 7];
     const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
-    if (lane == 0) w_chunk[K] = q.word ^ ballot;
+    rec_x[K * 128] = h;  // the helper needs the field this decision saw (energy bookkeeping)
+    if (lane == 0) ballots[K] = ballot;
 
     // ---- retire column p-2: no later attempt of this layer can reach it through the band
-    if (K >= 2 || p0 != 0) tmem_st(tm + p - 2, r[(K + 6) & 7]);
+    if (K >= 2 || p0 != 0) tmem_st(tm + p0 + K - 2, r[(K + 6) & 7]);
 
     // ---- far neighbours: read-modify-write in Tensor Memory (the first two with their loads batched)
-    const uint32_t far_count = q.rec.z >> 24;
+    const uint32_t far_count = far_info >> 24;
     if (far_count != 0u && ballot != 0u) {
-        const uint2* fe = far + (q.rec.z & 0xffffffu);
+        const uint2* fe = far + (far_info & 0xffffffu);
         tmem_wait_st();
         const uint2 e0 = fe[0];
         const uint2 e1 = fe[far_count > 1u ? 1 : 0];
@@ -329,18 +425,16 @@ __device__ __forceinline__ void attempt(float (&r)[kUnroll], LaneState& st, cons
         float v1 = 0.0f;
         if (far_count > 1u) v1 = tmem_ld(tm + e1.x);
         tmem_wait_ld();
-        if (accept) {
-            v0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
-            v1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
-        }
-        tmem_st(tm + e0.x, v0);
-        if (far_count > 1u) tmem_st(tm + e1.x, v1);
+        const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
+        const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
+        tmem_st(tm + e0.x, accept ? n0 : v0);
+        if (far_count > 1u) tmem_st(tm + e1.x, accept ? n1 : v1);
         for (uint32_t e = 2; e < far_count; ++e) {
             const uint2 ed = fe[e];
-            float v = tmem_ld(tm + ed.x);
+            const float v = tmem_ld(tm + ed.x);
             tmem_wait_ld();
-            if (accept) v = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
-            tmem_st(tm + ed.x, v);
+            const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
+            tmem_st(tm + ed.x, accept ? nv : v);
         }
         tmem_wait_st();
     }
@@ -352,29 +446,17 @@ __device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t p0, uint32_t 
     if (K <= 4 || p0 + kUnroll < P) r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
 }
 
+#define ISING_ATTEMPT(K)                                                                                   \
+    attempt<EXP, K>(r, rec##K, g.band_j2[p0 + K], g.band_mask[p0 + K], g.pos[p0 + K].z, p0, tm, g.far, rec_x, \
+                    ballots, lane);                                                                        \
+    feed<K>(r, p0, P, tm);
+
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor, uint32_t tile,
-                           uint32_t tm, uint32_t P, uint32_t L) {
+                           const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor,
+                           uint32_t stages, uint32_t tile, uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
-    const uint32_t chain = b.tile_first[tile] + lane;
-    LaneState st;
-    st.active = lane < b.tile_count[tile];
-    st.nb2 = __float_as_uint(st.active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
-    st.sh = 31u - lane;
-    st.flips = 0;
-    st.e_run = st.active ? b.e_run[chain] : 0.0;
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
-    uint32_t* words_g = b.spin_bits + size_t(tile) * n;
-
-    uint32_t slot_dn = 2, slot_cur = 0, slot_up = 1;
-    words_copy(s.words + slot_dn * P, words_g + size_t(L - 1) * P, P, lane);
-    words_copy(s.words + slot_cur * P, words_g, P, lane);
-    words_copy(s.words + slot_up * P, words_g + size_t(1) * P, P, lane);
-    __syncwarp();
-
-    uint32_t ui = 0;  // draws consumed from the current ring stage (a multiple of kUnroll)
-    const float* ring = s.ring + lane;
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
@@ -398,14 +480,6 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 for (int k = 0; k < 8; ++k) v[k] = hs_l[size_t(p0 + k) * 32];
                 tmem_st8(tm + p0, v);
             }
-            uint32_t* w_cur = s.words + slot_cur * P;
-            {   // the tau field of this whole layer is fixed while it is swept: previous layer already
-                // visited, next layer not yet.  agree = neighbours equal, sign = their common spin bit.
-                const uint32_t* w_up = s.words + slot_up * P;
-                const uint32_t* w_dn = s.words + slot_dn * P;
-                for (uint32_t k = lane; k < P; k += 32) s.agree_sign[k] = make_uint2(~(w_up[k] ^ w_dn[k]), w_up[k]);
-            }
-            __syncwarp();
             tmem_wait_st();
 
             // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
@@ -418,52 +492,32 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             tmem_wait_ld();
 
             for (p0 = 0; p0 < P; p0 += kUnroll) {
-                if (ui == 0) mbar_wait(&full[cursor.stage], cursor.parity);
+                const uint32_t st = cursor.stage;
+                mbar_wait(&full[st], cursor.parity(), 0);
+                cursor.waited();
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
-                ChunkPtrs c;
-                c.pos = g.pos + p0;
-                c.band_j2 = g.band_j2 + p0;
-                c.band_mask = g.band_mask + p0;
-                c.agree_sign = s.agree_sign + p0;
-                c.words = w_cur + p0;
-                c.u = ring + (size_t(cursor.stage) * kStageDraws + ui) * 32;
-                const Prep q0 = load_prep<0>(c);
-                const Prep q1 = load_prep<1>(c);
-                attempt<EXP, 0>(r, st, q0, p0, tm, g.far, c.words, lane);
-                feed<0>(r, p0, P, tm);
-                const Prep q2 = load_prep<2>(c);
-                attempt<EXP, 1>(r, st, q1, p0, tm, g.far, c.words, lane);
-                feed<1>(r, p0, P, tm);
-                const Prep q3 = load_prep<3>(c);
-                attempt<EXP, 2>(r, st, q2, p0, tm, g.far, c.words, lane);
-                feed<2>(r, p0, P, tm);
-                const Prep q4 = load_prep<4>(c);
-                attempt<EXP, 3>(r, st, q3, p0, tm, g.far, c.words, lane);
-                feed<3>(r, p0, P, tm);
-                const Prep q5 = load_prep<5>(c);
-                attempt<EXP, 4>(r, st, q4, p0, tm, g.far, c.words, lane);
-                feed<4>(r, p0, P, tm);
-                const Prep q6 = load_prep<6>(c);
-                attempt<EXP, 5>(r, st, q5, p0, tm, g.far, c.words, lane);
-                feed<5>(r, p0, P, tm);
-                const Prep q7 = load_prep<7>(c);
-                attempt<EXP, 6>(r, st, q6, p0, tm, g.far, c.words, lane);
-                feed<6>(r, p0, P, tm);
-                attempt<EXP, 7>(r, st, q7, p0, tm, g.far, c.words, lane);
-                feed<7>(r, p0, P, tm);
-                ui += kUnroll;
-                if (ui == kStageDraws) {
-                    mbar_arrive(&empty[cursor.stage]);
-                    cursor.advance();
-                    ui = 0;
-                }
+                const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
+                float* rec_x = reinterpret_cast<float*>(s.recs + size_t(st) * kUnroll * 32 + lane);
+                uint32_t* ballots = s.ballots + st * kUnroll;
+                const float4 rec0 = recs[0 * 32], rec1 = recs[1 * 32], rec2 = recs[2 * 32], rec3 = recs[3 * 32];
+                const float4 rec4 = recs[4 * 32], rec5 = recs[5 * 32], rec6 = recs[6 * 32], rec7 = recs[7 * 32];
+                ISING_ATTEMPT(0)
+                ISING_ATTEMPT(1)
+                ISING_ATTEMPT(2)
+                ISING_ATTEMPT(3)
+                ISING_ATTEMPT(4)
+                ISING_ATTEMPT(5)
+                ISING_ATTEMPT(6)
+                ISING_ATTEMPT(7)
+                mbar_arrive(&empty[st]);
+                cursor.advance(stages);
             }
             // the last two columns leave the window
             tmem_st(tm + P - 2, r[6]);
             tmem_st(tm + P - 1, r[7]);
             tmem_wait_st();
 
-            // ---- retire: TMEM -> HBM, and rotate the spin-bit ring
+            // ---- retire: TMEM -> HBM
             for (p0 = 0; p0 < P; p0 += 8) {
                 float v[8];
                 tmem_ld8(tm + p0, v);
@@ -471,27 +525,11 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
 #pragma unroll
                 for (int k = 0; k < 8; ++k) hs_l[size_t(p0 + k) * 32] = v[k];
             }
-            __syncwarp();
-            words_copy(words_g + size_t(l) * P, w_cur, P, lane);
-            // layer l-1's slot is free now: it receives layer l+2 (the `up` of the next layer)
-            words_copy(s.words + slot_dn * P, words_g + size_t((l + 2) % L) * P, P, lane);
-            __syncwarp();
-            const uint32_t freed = slot_dn;
-            slot_dn = slot_cur;
-            slot_cur = slot_up;
-            slot_up = freed;
         }
-    }
-    if (ui != 0) {  // hand a partly used last stage back
-        mbar_arrive(&empty[cursor.stage]);
-        cursor.advance();
-    }
-    if (st.active) {
-        b.e_run[chain] = st.e_run;
-        b.flips[chain] += st.flips;
     }
     __syncwarp();
 }
+#undef ISING_ATTEMPT
 
 template <int EXP>
 __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBatch b, uint32_t sweeps) {
@@ -500,20 +538,21 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 16);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t pair = warp & 3u;
-    const bool is_rng = warp >= kSweepWarps;
-    uint64_t* full = bars + pair * 2 * kStages;
-    uint64_t* empty = full + kStages;
+    const bool is_helper = warp >= kSweepWarps;
+    uint64_t* full = bars + pair * 2 * kMaxStages;
+    uint64_t* empty = full + kMaxStages;
 
     const uint32_t maxP = b.max_per_layer;
+    const uint32_t stages = b.layered_stages;
     const size_t gbytes = graph_bytes(maxP, b.max_far_edges);
     unsigned char* graph_base = smem_raw + kHeaderBytes + (b.graph_shared ? 0 : size_t(pair) * gbytes);
-    unsigned char* pair_base =
-        smem_raw + kHeaderBytes + (b.graph_shared ? 1 : kSweepWarps) * gbytes + size_t(pair) * pair_bytes(maxP);
+    unsigned char* pair_base = smem_raw + kHeaderBytes + (b.graph_shared ? 1 : kSweepWarps) * gbytes +
+                               size_t(pair) * pair_bytes(maxP, stages);
     const GraphSmem gs = carve_graph(graph_base, maxP);
-    const PairSmem s = carve_pair(pair_base, maxP);
+    const PairSmem s = carve_pair(pair_base, maxP, stages);
 
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
-    if (threadIdx.x < kSweepWarps * 2 * kStages) mbar_init(&bars[threadIdx.x], 32);
+    if (threadIdx.x < kSweepWarps * 2 * kMaxStages) mbar_init(&bars[threadIdx.x], 32);
     if (b.graph_shared) load_graph(gs, b.layer_graphs[0], threadIdx.x, kLayeredThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -526,19 +565,21 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
 
     // tiles are dealt round-robin: CTA c, pair w, round r -> tile c + grid*(w + 4r)
     for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
-        if (is_rng) {
-            rng_warp(b, sweeps, lane, s, full, empty, cursor, tile);
-        } else {
-            const DevLayerGraph g = b.layer_graphs[b.tile_model[tile]];
-            if (!b.graph_shared) {
-                load_graph(gs, g, lane, 32);
-                __syncwarp();
-            }
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, empty, cursor, tile, tm, g.per_layer, g.layers);
+        const DevLayerGraph g = b.layer_graphs[b.tile_model[tile]];
+        if (!b.graph_shared) {
+            // both warps of the pair use the pair's graph copy: the sweep warp loads it, the helper waits
+            if (!is_helper) load_graph(gs, g, lane, 32);
+            asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
         }
+        if (is_helper) {
+            helper_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
+        } else {
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, tm, g.per_layer, g.layers);
+        }
+        if (!b.graph_shared) asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
     }
 
-    if (!is_rng) {
+    if (!is_helper) {
         tmem_wait_ld();
         tmem_wait_st();
     }
@@ -549,11 +590,30 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
 
 }  // namespace
 
+// Ring depth: 8 stages when they fit, otherwise 4 (multi-model batches keep a graph copy per pair).
+static uint32_t pick_stages(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared, size_t* bytes_out) {
+    for (uint32_t stages : {8u, 4u, 2u}) {
+        const size_t bytes = kHeaderBytes + (graph_shared ? 1 : kSweepWarps) * graph_bytes(per_layer, max_far_edges) +
+                             kSweepWarps * pair_bytes(per_layer, stages);
+        if (bytes <= 227 * 1024) {
+            *bytes_out = bytes;
+            return stages;
+        }
+    }
+    *bytes_out = 0;
+    return 0;
+}
+
 size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared) {
     if (per_layer == 0 || per_layer > kTmemColumns || per_layer % kUnroll != 0) return 0;
-    const size_t bytes = kHeaderBytes + (graph_shared ? 1 : kSweepWarps) * graph_bytes(per_layer, max_far_edges) +
-                         kSweepWarps * pair_bytes(per_layer);
-    return bytes <= 227 * 1024 ? bytes : 0;
+    size_t bytes = 0;
+    pick_stages(per_layer, max_far_edges, graph_shared, &bytes);
+    return bytes;
+}
+
+uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared) {
+    size_t bytes = 0;
+    return pick_stages(per_layer, max_far_edges, graph_shared, &bytes);
 }
 
 cudaError_t prepare_layered_kernels(size_t smem_bytes) {
