@@ -47,7 +47,8 @@ namespace isingb200 {
 namespace {
 
 constexpr int kSweepWarps = 4;          // one TMEM lane quarter each
-constexpr int kLayeredThreads = 2 * kSweepWarps * 32;
+constexpr int kRolesPerPair = 3;        // sweep, producer, post
+constexpr int kLayeredThreads = kRolesPerPair * kSweepWarps * 32;
 constexpr uint32_t kTmemColumns = 512;  // the whole TMEM: one CTA per SM
 constexpr uint32_t kUnroll = 8;         // attempts per ring stage == unrolled chunk == window ring size
 constexpr uint32_t kMaxStages = 8;
@@ -134,10 +135,11 @@ struct PairSmem {
     uint32_t* words;    // 3 * P : ring of spin-bit layers
     float4* recs;       // stages * 8 * 32 prep records {u | h, -2*beta*s, gamma*h_tau, h_tau}
     uint32_t* ballots;  // stages * 8
+    uint32_t* stage_p0; // stages : chunk start position of the content of every stage
 };
 
-// header: tmem slot (16 B) + per pair full[8] + empty[8] barriers (128 B) x 4
-constexpr size_t kHeaderBytes = 16 + kSweepWarps * 2 * kMaxStages * 8;
+// header: tmem slot (16 B) + per pair full[8] + consumed[8] + empty[8] barriers (192 B) x 4
+constexpr size_t kHeaderBytes = 16 + kSweepWarps * 3 * kMaxStages * 8;
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
@@ -145,7 +147,7 @@ __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
 }
 __host__ __device__ inline size_t pair_bytes(uint32_t P, uint32_t stages) {
     return align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(stages) * kUnroll * 32 * 16 +
-           align16(size_t(stages) * kUnroll * 4);
+           align16(size_t(stages) * kUnroll * 4) + align16(size_t(stages) * 4);
 }
 
 __device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P) {
@@ -165,6 +167,8 @@ __device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P, 
     s.recs = reinterpret_cast<float4*>(base);
     base += size_t(stages) * kUnroll * 32 * 16;
     s.ballots = reinterpret_cast<uint32_t*>(base);
+    base += align16(size_t(stages) * kUnroll * 4);
+    s.stage_p0 = reinterpret_cast<uint32_t*>(base);
     return s;
 }
 
@@ -194,20 +198,19 @@ struct RingCursor {
 };
 
 // =======================================================================================
-// Helper warp
+// Producer warp (ahead of the sweep) and post warp (behind it)
 // =======================================================================================
-struct HelperState {
+struct ProducerState {
     uint32_t* mt;      // this lane's MT19937 state column
     uint32_t pos, cur;
     uint32_t nxt[kUnroll], far[kUnroll];  // operands of the next 8 draws, loaded one chunk ahead
-    uint32_t nb2, sh, flips;
-    double e_run;
+    uint32_t nb2, sh;
     bool active;
 };
 
 // Loads the recurrence operands of draws pos..pos+7 (ref: rng.cpp:22-25).  Fast path: the run does
 // not cross a wrap point (word 227: far operand wraps, 623: next operand wraps).
-__device__ __forceinline__ void mt_load_operands(HelperState& h) {
+__device__ __forceinline__ void mt_load_operands(ProducerState& h) {
     const uint32_t pos = h.pos;
     const bool straight = pos + kUnroll <= kMtN - kMtM || (pos >= kMtN - kMtM && pos + kUnroll <= kMtN - 1);
     if (straight) {
@@ -234,12 +237,13 @@ __device__ __forceinline__ void mt_load_operands(HelperState& h) {
 // None of the operands of a chunk is a word the chunk before it rewrote (the `next` words lie
 // ahead of it, the `far` words 227 draws behind or 397 ahead), so loading them a chunk early
 // reads exactly what the in-place loop of ref: rng.cpp:89-96 reads.
-__device__ __forceinline__ void mt_generate8(HelperState& h, uint32_t (&raw)[kUnroll]) {
+__device__ __forceinline__ void mt_generate8(ProducerState& h, uint32_t (&raw)[kUnroll]) {
     const uint32_t pos = h.pos;
+    const bool wraps = pos + kUnroll > kMtN;
 #pragma unroll
     for (int k = 0; k < int(kUnroll); ++k) {
         uint32_t j = pos + k;
-        j = j >= kMtN ? j - kMtN : j;
+        if (wraps) j = j >= kMtN ? j - kMtN : j;
         const uint32_t nx = h.nxt[k];
         const uint32_t v = mt_recurrence(h.cur, nx, h.far[k]);
         h.mt[size_t(j) * 32] = v;
@@ -249,35 +253,16 @@ __device__ __forceinline__ void mt_generate8(HelperState& h, uint32_t (&raw)[kUn
     h.pos = pos + kUnroll >= kMtN ? pos + kUnroll - kMtN : pos + kUnroll;
 }
 
-// Accept counts, running energy and spin words of one consumed stage (ref: sweep_basic.cpp:47-48;
-// the energy bookkeeping is the tempering definition of oracle/ising_oracle.h).
-__device__ __forceinline__ void post_stage(HelperState& h, const float4* recs, const uint32_t* ballots,
-                                           uint32_t* words, uint32_t lane) {
-#pragma unroll
-    for (int k = 0; k < int(kUnroll); ++k) {
-        const uint32_t ballot = ballots[k];
-        const float4 rec = recs[k * 32];
-        if ((ballot >> lane) & 1u) {
-            ++h.flips;
-            // rec.y = -2*beta*s carries the opposite of the spin's sign: 2s = 2.0 with the sign of s
-            const float two_s = __uint_as_float(0x40000000u | (~__float_as_uint(rec.y) & 0x80000000u));
-            h.e_run = __dadd_rn(h.e_run, double(__fmul_rn(two_s, __fadd_rn(rec.x, rec.w))));
-        }
-        if (lane == 0 && ballot != 0u) words[k] ^= ballot;
-    }
-}
-
-__device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                            const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor,
-                            uint32_t stages, uint32_t tile, uint32_t P, uint32_t L) {
+// Producer: MT19937, uniforms and the prep records of every attempt; owns the spin-word ring.
+__device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
+                              const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor,
+                              uint32_t stages, uint32_t tile, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
     const uint32_t chain = b.tile_first[tile] + lane;
-    HelperState h;
+    ProducerState h;
     h.active = lane < b.tile_count[tile];
     h.nb2 = __float_as_uint(h.active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
     h.sh = 31u - lane;
-    h.flips = 0;
-    h.e_run = h.active ? b.e_run[chain] : 0.0;
     h.mt = b.mt + size_t(tile) * kMtN * 32 + lane;
     h.pos = b.mt_pos[tile];
     h.cur = h.mt[size_t(h.pos) * 32];
@@ -290,15 +275,11 @@ __device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, c
     words_copy(s.words + slot_up * P, words_g + size_t(1) * P, P, lane);
     __syncwarp();
 
-    // bit s set: stage s holds results of the sweep warp that still await post-processing
-    uint32_t unposted = 0;
-    uint32_t post_p0[kMaxStages];  // chunk start position of the content of every stage
-#pragma unroll
-    for (int k = 0; k < int(kMaxStages); ++k) post_p0[k] = 0;
+    uint32_t in_flight = 0;  // bit s set: stage s was filled and its `empty` has not been waited for yet
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
-            uint32_t* w_cur = s.words + slot_cur * P;
+            const uint32_t* w_cur = s.words + slot_cur * P;
             {   // the tau field of this whole layer is fixed while it is swept: previous layer already
                 // visited, next layer not yet.  agree = neighbours equal, sign = their common spin bit.
                 const uint32_t* w_up = s.words + slot_up * P;
@@ -310,13 +291,9 @@ __device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, c
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
                 float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
-                if ((unposted >> st) & 1u) {  // recycle: wait for the sweep warp, then post-process
-                    mbar_wait(&empty[st], cursor.parity(), 200);
+                if ((in_flight >> st) & 1u) {  // recycle: the post warp must be done with it
+                    mbar_wait(&empty[st], cursor.parity(), 100);
                     cursor.waited();
-                    uint32_t pp = 0;
-#pragma unroll
-                    for (int k = 0; k < int(kMaxStages); ++k) pp = st == uint32_t(k) ? post_p0[k] : pp;
-                    post_stage(h, recs, s.ballots + st * kUnroll, w_cur + pp, lane);
                 }
                 uint32_t raw[kUnroll];
                 mt_generate8(h, raw);
@@ -326,7 +303,7 @@ __device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, c
                     const uint32_t p = p0 + k;
                     const uint32_t word = w_cur[p];
                     const uint2 as = s.agree_sign[p];
-                    const uint4 tau = g.pos[p];
+                    const uint2 tau = *reinterpret_cast<const uint2*>(g.pos + p);
                     const uint32_t sgn_s = (word << h.sh) & 0x80000000u;  // sign bit set <=> s = -1
                     const uint32_t sgn_up = (as.y << h.sh) & 0x80000000u;
                     const uint32_t agree = uint32_t(int32_t(as.x << h.sh) >> 31);  // ones when s_up == s_dn
@@ -339,26 +316,20 @@ __device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, c
                     rec.w = __uint_as_float((tau.y ^ sgn_up) & agree);
                     recs[k * 32] = rec;
                 }
-#pragma unroll
-                for (int k = 0; k < int(kMaxStages); ++k) post_p0[k] = st == uint32_t(k) ? p0 : post_p0[k];
-                unposted |= 1u << st;
+                in_flight |= 1u << st;
                 mbar_arrive(&full[st]);
                 cursor.advance(stages);
             }
 
-            // ---- end of layer: collect every outstanding stage, then rotate the spin-bit ring
+            // ---- end of layer: every stage must have been post-processed (the spin words of this
+            // layer are final) before the ring rotates and the next layer's tau words are formed
             {
                 uint32_t st = cursor.stage;  // oldest stage first
                 for (uint32_t k = 0; k < stages; ++k) {
-                    if ((unposted >> st) & 1u) {
-                        mbar_wait(&empty[st], (cursor.parity_bits >> st) & 1u, 200);
+                    if ((in_flight >> st) & 1u) {
+                        mbar_wait(&empty[st], (cursor.parity_bits >> st) & 1u, 100);
                         cursor.parity_bits ^= 1u << st;
-                        uint32_t pp = 0;
-#pragma unroll
-                        for (int q = 0; q < int(kMaxStages); ++q) pp = st == uint32_t(q) ? post_p0[q] : pp;
-                        post_stage(h, s.recs + size_t(st) * kUnroll * 32 + lane, s.ballots + st * kUnroll,
-                                   w_cur + pp, lane);
-                        unposted &= ~(1u << st);
+                        in_flight &= ~(1u << st);
                     }
                     st = st + 1 == stages ? 0u : st + 1;
                 }
@@ -375,9 +346,50 @@ __device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, c
         }
     }
     if (lane == 0) b.mt_pos[tile] = h.pos;
-    if (h.active) {
-        b.e_run[chain] = h.e_run;
-        b.flips[chain] += h.flips;
+    __syncwarp();
+}
+
+// Post: accept counts, running energy and spin words of every consumed stage (ref:
+// sweep_basic.cpp:47-48; the energy bookkeeping is the tempering definition of
+// oracle/ising_oracle.h).
+__device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s,
+                          uint64_t* consumed, uint64_t* empty, RingCursor& cursor, uint32_t stages,
+                          uint32_t tile, uint32_t P, uint32_t L) {
+    const uint32_t chain = b.tile_first[tile] + lane;
+    const bool active = lane < b.tile_count[tile];
+    double e_run = active ? b.e_run[chain] : 0.0;
+    uint32_t flips = 0;
+    uint32_t slot_cur = 0;  // follows the producer's ring rotation: layer l lives in slot l % 3 of the visit order
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t l = 0; l < L; ++l) {
+            uint32_t* w_cur = s.words + slot_cur * P;
+            for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
+                const uint32_t st = cursor.stage;
+                mbar_wait(&consumed[st], cursor.parity(), 100);
+                cursor.waited();
+                const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
+                const uint32_t* ballots = s.ballots + st * kUnroll;
+#pragma unroll
+                for (int k = 0; k < int(kUnroll); ++k) {
+                    const uint32_t ballot = ballots[k];
+                    const float4 rec = recs[k * 32];
+                    // rec.y = -2*beta*s carries the opposite of the spin's sign: 2s = 2.0 with the sign of s
+                    const float two_s = __uint_as_float(0x40000000u | (~__float_as_uint(rec.y) & 0x80000000u));
+                    const double de = double(__fmul_rn(two_s, __fadd_rn(rec.x, rec.w)));
+                    const bool mine = (ballot >> lane) & 1u;
+                    flips += mine ? 1u : 0u;
+                    e_run = mine ? __dadd_rn(e_run, de) : e_run;
+                    if (lane == 0 && ballot != 0u) w_cur[p0 + k] ^= ballot;
+                }
+                mbar_arrive(&empty[st]);
+                cursor.advance(stages);
+            }
+            slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
+        }
+    }
+    if (active) {
+        b.e_run[chain] = e_run;
+        b.flips[chain] += flips;
     }
     __syncwarp();
 }
@@ -385,6 +397,32 @@ __device__ void helper_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, c
 // =======================================================================================
 // Sweep warp
 // =======================================================================================
+// Far neighbours of a flipped spin: h[t] -= (2s)*J as a Tensor Memory read-modify-write on column t
+// (the first two with their loads batched).  All 32 lanes move data; only accepting lanes change it.
+__device__ __noinline__ void far_update(uint32_t tm, const uint2* fe, uint32_t far_count, uint32_t neg_d,
+                                        bool accept) {
+    tmem_wait_st();  // a column retired by an earlier attempt may be a target
+    const uint2 e0 = fe[0];
+    const uint2 e1 = fe[far_count > 1u ? 1 : 0];
+    const float v0 = tmem_ld(tm + e0.x);
+    float v1 = 0.0f;
+    if (far_count > 1u) v1 = tmem_ld(tm + e1.x);
+    tmem_wait_ld();
+    const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
+    const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
+    tmem_st(tm + e0.x, accept ? n0 : v0);
+    if (far_count > 1u) tmem_st(tm + e1.x, accept ? n1 : v1);
+#pragma unroll 1
+    for (uint32_t e = 2; e < far_count; ++e) {
+        const uint2 ed = fe[e];
+        const float v = tmem_ld(tm + ed.x);
+        tmem_wait_ld();
+        const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
+        tmem_st(tm + ed.x, accept ? nv : v);
+    }
+    tmem_wait_st();  // a target may be the next column to enter the window
+}
+
 // One Metropolis attempt at position p = p0 + K of the current layer (K is the compile-time
 // index inside the unrolled chunk; the register window r[] is indexed by position & 7).
 template <int EXP, int K>
@@ -414,30 +452,8 @@ __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, c
     // ---- retire column p-2: no later attempt of this layer can reach it through the band
     if (K >= 2 || p0 != 0) tmem_st(tm + p0 + K - 2, r[(K + 6) & 7]);
 
-    // ---- far neighbours: read-modify-write in Tensor Memory (the first two with their loads batched)
-    const uint32_t far_count = far_info >> 24;
-    if (far_count != 0u && ballot != 0u) {
-        const uint2* fe = far + (far_info & 0xffffffu);
-        tmem_wait_st();
-        const uint2 e0 = fe[0];
-        const uint2 e1 = fe[far_count > 1u ? 1 : 0];
-        float v0 = tmem_ld(tm + e0.x);
-        float v1 = 0.0f;
-        if (far_count > 1u) v1 = tmem_ld(tm + e1.x);
-        tmem_wait_ld();
-        const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
-        const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
-        tmem_st(tm + e0.x, accept ? n0 : v0);
-        if (far_count > 1u) tmem_st(tm + e1.x, accept ? n1 : v1);
-        for (uint32_t e = 2; e < far_count; ++e) {
-            const uint2 ed = fe[e];
-            const float v = tmem_ld(tm + ed.x);
-            tmem_wait_ld();
-            const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
-            tmem_st(tm + ed.x, accept ? nv : v);
-        }
-        tmem_wait_st();
-    }
+    // ---- far neighbours: read-modify-write in Tensor Memory, out of line to keep this loop small
+    if ((far_info >> 24) != 0u && ballot != 0u) far_update(tm, far + (far_info & 0xffffffu), far_info >> 24, neg_d, accept);
 }
 
 // Feeds the window entry for position p+3 after attempt p (it is first needed by attempt p+1).
@@ -453,7 +469,7 @@ __device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t p0, uint32_t 
 
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint64_t* empty, RingCursor& cursor,
+                           const PairSmem& s, uint64_t* full, uint64_t* consumed, RingCursor& cursor,
                            uint32_t stages, uint32_t tile, uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
@@ -509,7 +525,7 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 ISING_ATTEMPT(5)
                 ISING_ATTEMPT(6)
                 ISING_ATTEMPT(7)
-                mbar_arrive(&empty[st]);
+                mbar_arrive(&consumed[st]);
                 cursor.advance(stages);
             }
             // the last two columns leave the window
@@ -538,9 +554,10 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 16);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t pair = warp & 3u;
-    const bool is_helper = warp >= kSweepWarps;
-    uint64_t* full = bars + pair * 2 * kMaxStages;
-    uint64_t* empty = full + kMaxStages;
+    const uint32_t role = warp >> 2;  // 0 sweep, 1 producer, 2 post — all three on scheduler `pair`
+    uint64_t* full = bars + pair * 3 * kMaxStages;   // producer -> sweep
+    uint64_t* consumed = full + kMaxStages;          // sweep -> post
+    uint64_t* empty = consumed + kMaxStages;         // post -> producer
 
     const uint32_t maxP = b.max_per_layer;
     const uint32_t stages = b.layered_stages;
@@ -552,7 +569,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     const PairSmem s = carve_pair(pair_base, maxP, stages);
 
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
-    if (threadIdx.x < kSweepWarps * 2 * kMaxStages) mbar_init(&bars[threadIdx.x], 32);
+    if (threadIdx.x < kSweepWarps * 3 * kMaxStages) mbar_init(&bars[threadIdx.x], 32);
     if (b.graph_shared) load_graph(gs, b.layer_graphs[0], threadIdx.x, kLayeredThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -567,19 +584,21 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
         const DevLayerGraph g = b.layer_graphs[b.tile_model[tile]];
         if (!b.graph_shared) {
-            // both warps of the pair use the pair's graph copy: the sweep warp loads it, the helper waits
-            if (!is_helper) load_graph(gs, g, lane, 32);
-            asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+            // the three warps of the pair use the pair's graph copy: the sweep warp loads it
+            if (role == 0) load_graph(gs, g, lane, 32);
+            asm volatile("bar.sync %0, 96;" ::"r"(pair + 1) : "memory");
         }
-        if (is_helper) {
-            helper_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
+        if (role == 1) {
+            producer_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
+        } else if (role == 2) {
+            post_warp(b, sweeps, lane, s, consumed, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else {
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, tm, g.per_layer, g.layers);
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, consumed, cursor, stages, tile, tm, g.per_layer, g.layers);
         }
-        if (!b.graph_shared) asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+        if (!b.graph_shared) asm volatile("bar.sync %0, 96;" ::"r"(pair + 1) : "memory");
     }
 
-    if (!is_helper) {
+    if (role == 0) {
         tmem_wait_ld();
         tmem_wait_st();
     }
