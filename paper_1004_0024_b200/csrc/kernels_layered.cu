@@ -478,17 +478,34 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
         for (uint32_t l = 0; l < L; ++l) {
             float* hs_l = hs_g + size_t(l) * P * 32;
             const float* hs_next = hs_g + size_t(l + 1 == L ? 0 : l + 1) * P * 32 - lane;
-            // ---- feed: this layer's fields HBM -> TMEM (P is a multiple of 8)
+            // ---- feed: this layer's fields HBM -> TMEM (P is a multiple of 8).  Two batches of 32
+            // columns in flight: the next batch's loads are issued before this batch is stored.
             uint32_t p0 = 0;
-            for (; p0 + 32 <= P; p0 += 32) {
+            if (P >= 32) {
                 float v[4][8];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) v[q][k] = hs_l[size_t(p0 + q * 8 + k) * 32];
+                    for (int k = 0; k < 8; ++k) v[q][k] = hs_l[size_t(q * 8 + k) * 32];
+                }
+                for (; p0 + 64 <= P; p0 += 32) {
+                    float nv[4][8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) nv[q][k] = hs_l[size_t(p0 + 32 + q * 8 + k) * 32];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) tmem_st8(tm + p0 + q * 8, v[q]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) v[q][k] = nv[q][k];
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) tmem_st8(tm + p0 + q * 8, v[q]);
+                p0 += 32;
             }
             for (; p0 < P; p0 += 8) {
                 float v[8];
