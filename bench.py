@@ -294,10 +294,10 @@ def main():
             er = st.running_energies()     # D2H per step: energies used by the swap rule
             d2h += fl.nbytes + er.nbytes
         if world > 1:  # one NCCL all-gather of the packed per-chain results, no host round trip
-            rec = torch.empty(chains * 4, dtype=torch.int64, device="cuda")
+            from paper_1004_0024_b200 import sharding
+            rec = torch.empty((chains, sharding.RECORD_WORDS), dtype=torch.int64, device="cuda")
             st.pack_results(rec.data_ptr())
-            allrec = torch.empty(world * chains * 4, dtype=torch.int64, device="cuda")
-            dist.all_gather_into_tensor(allrec, rec)
+            allrec = sharding.all_gather_records(rec, [chains] * world)
             host = allrec.cpu() if rank == 0 else None
             d2h_final = world * chains * 32 if rank == 0 else 0
         else:

@@ -1,0 +1,127 @@
+"""BASELINE.json's full-size configurations on the GPU, checked through size-independent
+properties (the oracle cannot finish them): agreement of the two kernel families, the running
+energy against the recomputed energy, determinism (a checksum of checksums), shard invariance,
+and bit parity with the oracle on a subsample of ladders inside the full batch."""
+import numpy as np
+import pytest
+
+import paper_1004_0024_b200 as ib
+from paper_1004_0024_b200 import sharding, workloads
+from helpers import ins, oracle_batch, product_model
+
+pytestmark = pytest.mark.gpu
+
+
+def fold(values) -> int:
+    """Order-sensitive checksum of checksums (FNV-1a over the 64-bit words)."""
+    h = 1469598103934665603
+    for v in np.asarray(values, np.uint64).tolist():
+        h = ((h ^ v) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+@pytest.fixture(scope="module")
+def c5():
+    wl = workloads.get("c5")
+    return wl, wl.make_csrs()[0]
+
+
+def test_c5_full_batch_properties_and_subsample_parity(lib, port, c5):
+    """16,384 chains x 32,768 spins (config 5), 20 sweeps with a swap round every 10."""
+    wl, csr = c5
+    model = product_model(csr)
+    sweeps = 20
+    with ib.init_state(model, wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as st:
+        info = st.info()
+        assert info["kernel"] == ib.KERNEL_LAYERED and info["n_chains"] == 16384 and info["n_tiles"] == 512
+        e0 = st.energies()
+        np.testing.assert_array_equal(st.running_energies(), e0)  # initial running energy == total_cost
+        st.run(sweeps, wl.swap_interval)
+        energies, e_run = st.energies(), st.running_energies()
+        flips, attempts = st.stats()
+        sums, slots = st.checksums(), st.slots()
+        coherence = st.field_coherence_ulp()
+        sample = st.spins(16 * 1000, 32)  # ladders 1000 and 1001, deep inside the batch
+    assert (attempts == sweeps * 32768).all()
+    # energies within 1e-5 relative of the f32-accumulated running energy (north_star tolerance)
+    np.testing.assert_allclose(e_run, energies, rtol=1e-5)
+    assert (energies < e0).mean() > 0.9  # cold and warm chains relax from the random start
+    rate = flips.reshape(-1, 16).mean(0) / attempts[0]
+    assert rate[0] > 0.3 and rate[-1] < 0.1  # hot end flips often, cold end rarely (slots barely move in 2 rounds)
+    assert (np.sort(slots.reshape(-1, 16), 1) == np.arange(16)).all()
+    assert coherence.max() <= 4096  # incremental fields stay a few ULP of a recompute away (near-zero fields inflate ULPs)
+    # bit parity of a subsample against the oracle: seeds are functions of the global chain id
+    seeds = sharding.chain_seeds(ins.CHAIN_SEED_BASE, 1000, 2, 16)
+    swap_seeds = sharding.ladder_seeds(ins.SWAP_SEED_BASE, 1000, 2)
+    want = oracle_batch(port, [csr], 2, wl.betas, seeds, swap_seeds, sweeps, wl.swap_interval)
+    np.testing.assert_array_equal(sample, want["spins"])
+    np.testing.assert_array_equal(flips[16000:16032], want["flips"])
+    np.testing.assert_array_equal(e_run[16000:16032].view(np.uint64), want["e_run"].view(np.uint64))
+    np.testing.assert_array_equal(slots[16000:16032], want["slot"])
+    # determinism: a second run gives the same checksum of checksums
+    with ib.init_state(model, wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as again:
+        again.run(sweeps, wl.swap_interval)
+        assert fold(again.checksums()) == fold(sums)
+
+
+def test_c5_shards_reproduce_the_full_batch(lib, c5):
+    """Weak-scaling property: a shard addressed by first_ladder carries the same bits as the
+    corresponding slice of a larger batch (what makes 1/2/4/8-GPU results identical)."""
+    wl, csr = c5
+    model = product_model(csr)
+    with ib.init_state(model, wl.betas, 192, base_seed=5, swap_base_seed=6) as whole:
+        whole.run(10, 5)
+        sums, slots = whole.checksums(), whole.slots()
+    for rank in range(3):
+        first, count = sharding.shard_ladders(192, rank, 3)
+        with ib.init_state(model, wl.betas, count, base_seed=5, swap_base_seed=6, first_ladder=first) as part:
+            part.run(10, 5)
+            np.testing.assert_array_equal(part.checksums(), sums[first * 16:(first + count) * 16])
+            np.testing.assert_array_equal(part.slots(), slots[first * 16:(first + count) * 16])
+
+
+def test_c4_kernel_families_agree_on_distinct_instances(lib):
+    """Config 4 shape (32 betas, one instance per ladder, swap every sweep): the on-chip layered
+    kernel and the generic HBM kernel must produce identical chains."""
+    wl = workloads.get("c4")
+    csrs = [ins.build_layered_csr(*ins.layered_spec(512, ins.INSTANCE_SEED + k, 0.5, 6), 64, 1.5) for k in range(3)]
+    models = [product_model(c) for c in csrs]
+    out = {}
+    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC):
+        with ib.init_state(models, wl.betas, 3, base_seed=11, swap_base_seed=12, kernel=family) as st:
+            assert st.info()["kernel"] == family
+            st.run(6, 1)
+            out[family] = (st.checksums(), st.stats()[0], st.slots(), st.running_energies(), st.energies())
+    for a, b in zip(out[ib.KERNEL_LAYERED], out[ib.KERNEL_GENERIC]):
+        np.testing.assert_array_equal(a, b)
+    assert out[ib.KERNEL_LAYERED][1].sum() > 0
+
+
+def test_c3_full_width_ladder_subsample(lib, port):
+    """Config 3 shape at full ladder width (32 betas, swap every sweep) on a few distinct graphs."""
+    wl = workloads.get("c3")
+    csrs = [ins.cubic_mixed_degree(16, ins.INSTANCE_SEED + k) for k in range(2)]
+    seeds = sharding.chain_seeds(ins.CHAIN_SEED_BASE, 0, 2, 32)
+    swap_seeds = sharding.ladder_seeds(ins.SWAP_SEED_BASE, 0, 2)
+    want = oracle_batch(port, csrs, 2, wl.betas, seeds, swap_seeds, 60, 1)
+    with ib.init_state([product_model(c) for c in csrs], wl.betas, 2, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as st:
+        st.run(60, 1)
+        np.testing.assert_array_equal(st.spins(), want["spins"])
+        np.testing.assert_array_equal(st.stats()[0], want["flips"])
+        np.testing.assert_array_equal(st.slots(), want["slot"])
+        np.testing.assert_allclose(st.energies(), want["energy"], rtol=1e-5)
+
+
+def test_layer_width_not_multiple_of_8_uses_generic_family(lib, port):
+    csr = ins.build_layered_csr(*ins.layered_spec(12, 9), 5, 1.5)
+    seeds = np.arange(10, 14, dtype=np.uint32)
+    want = oracle_batch(port, [csr], 1, [0.3, 0.6, 1.2, 2.4], seeds, [3], 40, 2)
+    with ib.init_state(product_model(csr), [0.3, 0.6, 1.2, 2.4], 1, seeds=seeds, swap_seeds=[3]) as st:
+        assert st.info()["kernel"] == ib.KERNEL_GENERIC
+        st.run(40, 2)
+        np.testing.assert_array_equal(st.spins(), want["spins"])
+    with pytest.raises(ib.IsingError):
+        ib.init_state(product_model(csr), [1.0], 1, kernel=ib.KERNEL_LAYERED)
