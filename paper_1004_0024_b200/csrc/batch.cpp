@@ -282,6 +282,28 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     cuda_check(launch_init(dev_, initial_spins ? initial_dev.as<int8_t>() : nullptr, stream_), "init kernel");
     other_launches += 2;
     cuda_check(cudaStreamSynchronize(stream_), "init");
+
+    // The MT19937 states (2,496 B per chain) are re-read and re-written every 624 attempts while
+    // 8 B per attempt of field data stream past them.  Ask for them to persist in L2 so they stop
+    // costing HBM traffic; this is a hint, so failure (older driver, MIG, ...) is not an error.
+    {
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, device_) == cudaSuccess && prop.persistingL2CacheMaxSize > 0 &&
+            prop.accessPolicyMaxWindowSize > 0) {
+            const size_t want = std::min<size_t>(mt_.bytes(), size_t(prop.persistingL2CacheMaxSize));
+            const size_t window = std::min<size_t>(mt_.bytes(), size_t(prop.accessPolicyMaxWindowSize));
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess && window > 0) {
+                cudaStreamAttrValue attr{};
+                attr.accessPolicyWindow.base_ptr = mt_.as<void>();
+                attr.accessPolicyWindow.num_bytes = window;
+                attr.accessPolicyWindow.hitRatio = float(std::min(1.0, double(want) / double(window)));
+                attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr);
+            }
+        }
+        cudaGetLastError();  // a refused hint must not poison later error checks
+    }
 }
 
 Batch::~Batch() {

@@ -486,14 +486,14 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) v[q][k] = hs_l[size_t(q * 8 + k) * 32];
+                    for (int k = 0; k < 8; ++k) v[q][k] = __ldcs(hs_l + size_t(q * 8 + k) * 32);
                 }
                 for (; p0 + 64 <= P; p0 += 32) {
                     float nv[4][8];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) nv[q][k] = hs_l[size_t(p0 + 32 + q * 8 + k) * 32];
+                        for (int k = 0; k < 8; ++k) nv[q][k] = __ldcs(hs_l + size_t(p0 + 32 + q * 8 + k) * 32);
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) tmem_st8(tm + p0 + q * 8, v[q]);
@@ -510,7 +510,7 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             for (; p0 < P; p0 += 8) {
                 float v[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = hs_l[size_t(p0 + k) * 32];
+                for (int k = 0; k < 8; ++k) v[k] = __ldcs(hs_l + size_t(p0 + k) * 32);
                 tmem_st8(tm + p0, v);
             }
             tmem_wait_st();
@@ -556,7 +556,7 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 tmem_ld8(tm + p0, v);
                 tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 8; ++k) hs_l[size_t(p0 + k) * 32] = v[k];
+                for (int k = 0; k < 8; ++k) __stcs(hs_l + size_t(p0 + k) * 32, v[k]);
             }
         }
     }
