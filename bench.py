@@ -269,7 +269,9 @@ def main():
     prof = ROOT / "profiles" / "sweep_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(f"{wl.name}:{after['kernel']}")
+            entry = json.loads(prof.read_text()).get(f"{wl.name}:{after['kernel']}")
+            # per launch, like `achieved`: the profiled bytes per attempt x the attempts of one launch here
+            traffic = entry["dram_bytes_per_attempt"] * attempts_per_step * args.steps / max(1, sweep_launches)
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
