@@ -171,7 +171,11 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             std::vector<uint2> far;
             for (uint32_t p = 0; p < P; ++p) {
                 uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
-                const uint32_t far_begin = uint32_t(far.size());
+                // far edges are split by direction: FORWARD targets (t > p) have not entered the
+                // register window yet and are updated by the sweep warp itself; BACKWARD targets
+                // (t < p) have already left it and are updated by the post warp, later
+                std::vector<uint2> backward;
+                const uint32_t fwd_begin = uint32_t(far.size());
                 for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
                     const uint32_t t = m->layer_targets[e];
                     const float doubled = 2.0f * m->layer_couplings[e];  // exact
@@ -180,13 +184,19 @@ Batch::Batch(const std::vector<const HostModel*>& models,
                         const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
                         j2[slot] = bits(doubled);
                         mask[slot] = 0;
-                    } else {
+                    } else if (t > p) {
                         far.push_back(make_uint2(t, bits(doubled)));
+                    } else {
+                        backward.push_back(make_uint2(t, bits(doubled)));
                     }
                 }
+                const uint32_t fwd_count = uint32_t(far.size()) - fwd_begin;
+                const uint32_t bwd_begin = uint32_t(far.size());
+                far.insert(far.end(), backward.begin(), backward.end());
                 const float tau2 = 2.0f * m->layer_tau[p];
                 const float tau2g = cfg.tau_scale * tau2;  // f32 product, as gamma * h_tau in the reference
-                pos[p] = make_uint4(bits(tau2g), bits(tau2), far_begin | (uint32_t(far.size()) - far_begin) << 24, 0);
+                pos[p] = make_uint4(bits(tau2g), bits(tau2), fwd_begin | fwd_count << 24,
+                                    bwd_begin | uint32_t(backward.size()) << 24);
                 band_j2[p] = make_uint4(j2[0], j2[1], j2[2], j2[3]);
                 band_mask[p] = make_uint4(mask[0], mask[1], mask[2], mask[3]);
             }

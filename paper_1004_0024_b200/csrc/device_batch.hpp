@@ -40,7 +40,8 @@ struct DevLayerGraph {
     uint32_t per_layer;
     uint32_t layers;
     uint32_t n_far;
-    // per position: {bits of tau2g, bits of tau2, far_begin | far_count << 24, 0}
+    // per position: {bits of tau2g, bits of tau2, forward far edges begin | count << 24,
+    //                backward far edges begin | count << 24}  (indices into `far`)
     const uint4* pos;
     // per position: bits of 2J for the slots -2, -1, +1, +2 (0 when the slot is empty) ...
     const uint4* band_j2;

@@ -139,7 +139,8 @@ struct PairSmem {
 };
 
 // header: tmem slot (16 B) + per pair full[8] + consumed[8] + empty[8] barriers (192 B) x 4
-constexpr size_t kHeaderBytes = 16 + kSweepWarps * 3 * kMaxStages * 8;
+constexpr size_t kRingBarriers = kSweepWarps * 3 * kMaxStages;
+constexpr size_t kHeaderBytes = 16 + (kRingBarriers + kSweepWarps) * 8;  // + one layer_done barrier per pair
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
@@ -352,9 +353,16 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
 // Post: accept counts, running energy and spin words of every consumed stage (ref:
 // sweep_basic.cpp:47-48; the energy bookkeeping is the tempering definition of
 // oracle/ising_oracle.h).
-__device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s,
-                          uint64_t* consumed, uint64_t* empty, RingCursor& cursor, uint32_t stages,
-                          uint32_t tile, uint32_t P, uint32_t L) {
+// It also applies the BACKWARD far-neighbour updates of every flip: their target columns left the
+// sweep warp's register window before the flipping attempt ran and are not read again by it until
+// the layer is retired, so this warp (same TMEM lane quarter) can update them off the critical
+// path.  Per column the order of updates stays the sequential one: a column's forward updates
+// (sweep warp) all come from attempts before it, its backward updates (here, in attempt order)
+// from attempts after it.
+__device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
+                          const PairSmem& s, uint64_t* consumed, uint64_t* empty, uint64_t* layer_done,
+                          RingCursor& cursor, uint32_t stages, uint32_t tile, uint32_t tm, uint32_t P,
+                          uint32_t L) {
     const uint32_t chain = b.tile_first[tile] + lane;
     const bool active = lane < b.tile_count[tile];
     double e_run = active ? b.e_run[chain] : 0.0;
@@ -367,8 +375,10 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                 const uint32_t st = cursor.stage;
                 mbar_wait(&consumed[st], cursor.parity(), 100);
                 cursor.waited();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
+                bool stored = false;
 #pragma unroll
                 for (int k = 0; k < int(kUnroll); ++k) {
                     const uint32_t ballot = ballots[k];
@@ -380,10 +390,28 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                     flips += mine ? 1u : 0u;
                     e_run = mine ? __dadd_rn(e_run, de) : e_run;
                     if (lane == 0 && ballot != 0u) w_cur[p0 + k] ^= ballot;
+                    const uint32_t back = g.pos[p0 + k].w;
+                    if ((back >> 24) != 0u && ballot != 0u) {
+                        const uint32_t neg_d = __float_as_uint(rec.y) & 0x80000000u;
+                        const uint2* fe = g.far + (back & 0xffffffu);
+#pragma unroll 1
+                        for (uint32_t e = 0; e < (back >> 24); ++e) {
+                            const uint2 ed = fe[e];
+                            if (stored) tmem_wait_st();  // an earlier update of this stage may hit the same column
+                            const float v = tmem_ld(tm + ed.x);
+                            tmem_wait_ld();
+                            const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
+                            tmem_st(tm + ed.x, mine ? nv : v);
+                            stored = true;
+                        }
+                    }
                 }
+                if (stored) tmem_wait_st();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);
             }
+            mbar_arrive(layer_done);  // every backward update of this layer has landed
             slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
         }
     }
@@ -469,8 +497,9 @@ __device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t p0, uint32_t 
 
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint64_t* consumed, RingCursor& cursor,
-                           uint32_t stages, uint32_t tile, uint32_t tm, uint32_t P, uint32_t L) {
+                           const PairSmem& s, uint64_t* full, uint64_t* consumed, uint64_t* layer_done,
+                           uint32_t& layer_parity, RingCursor& cursor, uint32_t stages, uint32_t tile,
+                           uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
 
@@ -542,6 +571,9 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 ISING_ATTEMPT(5)
                 ISING_ATTEMPT(6)
                 ISING_ATTEMPT(7)
+                // the post warp may now update columns this chunk retired: they must have landed
+                tmem_wait_st();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&consumed[st]);
                 cursor.advance(stages);
             }
@@ -549,6 +581,10 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             tmem_st(tm + P - 2, r[6]);
             tmem_st(tm + P - 1, r[7]);
             tmem_wait_st();
+            // the post warp's backward updates of this layer must be in before the layer is read out
+            mbar_wait(layer_done, layer_parity, 0);
+            layer_parity ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
             // ---- retire: TMEM -> HBM
             for (p0 = 0; p0 < P; p0 += 8) {
@@ -575,6 +611,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     uint64_t* full = bars + pair * 3 * kMaxStages;   // producer -> sweep
     uint64_t* consumed = full + kMaxStages;          // sweep -> post
     uint64_t* empty = consumed + kMaxStages;         // post -> producer
+    uint64_t* layer_done = bars + kRingBarriers + pair;  // post -> sweep, once per layer
 
     const uint32_t maxP = b.max_per_layer;
     const uint32_t stages = b.layered_stages;
@@ -586,7 +623,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     const PairSmem s = carve_pair(pair_base, maxP, stages);
 
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
-    if (threadIdx.x < kSweepWarps * 3 * kMaxStages) mbar_init(&bars[threadIdx.x], 32);
+    if (threadIdx.x < kRingBarriers + kSweepWarps) mbar_init(&bars[threadIdx.x], 32);
     if (b.graph_shared) load_graph(gs, b.layer_graphs[0], threadIdx.x, kLayeredThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -596,6 +633,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     // this pair's lane quarter: bits 31..16 of a TMEM address are the lane, 15..0 the column
     const uint32_t tm = tmem_base + ((pair * 32u) << 16);
     RingCursor cursor;
+    uint32_t layer_parity = 0;
 
     // tiles are dealt round-robin: CTA c, pair w, round r -> tile c + grid*(w + 4r)
     for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
@@ -608,14 +646,16 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         if (role == 1) {
             producer_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else if (role == 2) {
-            post_warp(b, sweeps, lane, s, consumed, empty, cursor, stages, tile, g.per_layer, g.layers);
+            post_warp(b, sweeps, lane, gs, s, consumed, empty, layer_done, cursor, stages, tile, tm, g.per_layer,
+                      g.layers);
         } else {
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, consumed, cursor, stages, tile, tm, g.per_layer, g.layers);
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, consumed, layer_done, layer_parity, cursor, stages, tile,
+                            tm, g.per_layer, g.layers);
         }
         if (!b.graph_shared) asm volatile("bar.sync %0, 96;" ::"r"(pair + 1) : "memory");
     }
 
-    if (role == 0) {
+    if (role != 1) {  // the two roles that touch Tensor Memory
         tmem_wait_ld();
         tmem_wait_st();
     }
