@@ -169,13 +169,24 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             const uint32_t P = m->per_layer;
             std::vector<uint4> pos(P), band_j2(P), band_mask(P);
             std::vector<uint2> far;
+            // Far edges are split by who applies them.  The POST warp, which trails the sweep warp by
+            // whole 8-attempt chunks, takes every target the sweep warp is not going to read soon:
+            // backward targets (already out of its register window) and forward targets that enter the
+            // window at least two chunks after the flipping attempt's chunk.  The sweep warp keeps the
+            // near forward targets.  need[a] = how many chunks of the layer the post warp must have
+            // finished before column a+3 may enter the window after attempt a.
+            const auto delegated = [](uint32_t p, uint32_t t) { return t < p || (t - 3) / 8 >= p / 8 + 2; };
+            std::vector<uint32_t> need(P, 0);
+            for (uint32_t p = 0; p < P; ++p) {
+                for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
+                    const uint32_t t = m->layer_targets[e];
+                    if (!is_band(p, t) && t > p && delegated(p, t)) need[t - 3] = std::max(need[t - 3], p / 8 + 1);
+                }
+            }
             for (uint32_t p = 0; p < P; ++p) {
                 uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
-                // far edges are split by direction: FORWARD targets (t > p) have not entered the
-                // register window yet and are updated by the sweep warp itself; BACKWARD targets
-                // (t < p) have already left it and are updated by the post warp, later
-                std::vector<uint2> backward;
-                const uint32_t fwd_begin = uint32_t(far.size());
+                std::vector<uint2> for_post;
+                const uint32_t near_begin = uint32_t(far.size());
                 for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
                     const uint32_t t = m->layer_targets[e];
                     const float doubled = 2.0f * m->layer_couplings[e];  // exact
@@ -184,19 +195,19 @@ Batch::Batch(const std::vector<const HostModel*>& models,
                         const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
                         j2[slot] = bits(doubled);
                         mask[slot] = 0;
-                    } else if (t > p) {
-                        far.push_back(make_uint2(t, bits(doubled)));
+                    } else if (delegated(p, t)) {
+                        for_post.push_back(make_uint2(t, bits(doubled)));
                     } else {
-                        backward.push_back(make_uint2(t, bits(doubled)));
+                        far.push_back(make_uint2(t, bits(doubled)));
                     }
                 }
-                const uint32_t fwd_count = uint32_t(far.size()) - fwd_begin;
-                const uint32_t bwd_begin = uint32_t(far.size());
-                far.insert(far.end(), backward.begin(), backward.end());
+                const uint32_t near_count = uint32_t(far.size()) - near_begin;
+                const uint32_t post_begin = uint32_t(far.size());
+                far.insert(far.end(), for_post.begin(), for_post.end());
                 const float tau2 = 2.0f * m->layer_tau[p];
                 const float tau2g = cfg.tau_scale * tau2;  // f32 product, as gamma * h_tau in the reference
-                pos[p] = make_uint4(bits(tau2g), bits(tau2), fwd_begin | fwd_count << 24,
-                                    bwd_begin | uint32_t(backward.size()) << 24);
+                pos[p] = make_uint4(bits(tau2g), bits(tau2), near_begin | near_count << 16 | need[p] << 20,
+                                    post_begin | uint32_t(for_post.size()) << 24);
                 band_j2[p] = make_uint4(j2[0], j2[1], j2[2], j2[3]);
                 band_mask[p] = make_uint4(mask[0], mask[1], mask[2], mask[3]);
             }

@@ -47,7 +47,7 @@ namespace isingb200 {
 namespace {
 
 constexpr int kSweepWarps = 4;          // one TMEM lane quarter each
-constexpr int kRolesPerPair = 3;        // sweep, producer, post
+constexpr int kRolesPerPair = 4;        // sweep, producer, post, far
 constexpr int kLayeredThreads = kRolesPerPair * kSweepWarps * 32;
 constexpr uint32_t kTmemColumns = 512;  // the whole TMEM: one CTA per SM
 constexpr uint32_t kUnroll = 8;         // attempts per ring stage == unrolled chunk == window ring size
@@ -140,7 +140,7 @@ struct PairSmem {
 
 // header: tmem slot (16 B) + per pair full[8] + consumed[8] + empty[8] barriers (192 B) x 4
 constexpr size_t kRingBarriers = kSweepWarps * 3 * kMaxStages;
-constexpr size_t kHeaderBytes = 16 + (kRingBarriers + kSweepWarps) * 8;  // + one layer_done barrier per pair
+constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one post-progress counter per pair
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
@@ -353,16 +353,9 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
 // Post: accept counts, running energy and spin words of every consumed stage (ref:
 // sweep_basic.cpp:47-48; the energy bookkeeping is the tempering definition of
 // oracle/ising_oracle.h).
-// It also applies the BACKWARD far-neighbour updates of every flip: their target columns left the
-// sweep warp's register window before the flipping attempt ran and are not read again by it until
-// the layer is retired, so this warp (same TMEM lane quarter) can update them off the critical
-// path.  Per column the order of updates stays the sequential one: a column's forward updates
-// (sweep warp) all come from attempts before it, its backward updates (here, in attempt order)
-// from attempts after it.
-__device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                          const PairSmem& s, uint64_t* consumed, uint64_t* empty, uint64_t* layer_done,
-                          RingCursor& cursor, uint32_t stages, uint32_t tile, uint32_t tm, uint32_t P,
-                          uint32_t L) {
+__device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s,
+                          uint64_t* consumed, uint64_t* empty, RingCursor& cursor, uint32_t stages,
+                          uint32_t tile, uint32_t P, uint32_t L) {
     const uint32_t chain = b.tile_first[tile] + lane;
     const bool active = lane < b.tile_count[tile];
     double e_run = active ? b.e_run[chain] : 0.0;
@@ -375,10 +368,8 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                 const uint32_t st = cursor.stage;
                 mbar_wait(&consumed[st], cursor.parity(), 100);
                 cursor.waited();
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
-                bool stored = false;
 #pragma unroll
                 for (int k = 0; k < int(kUnroll); ++k) {
                     const uint32_t ballot = ballots[k];
@@ -390,34 +381,84 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                     flips += mine ? 1u : 0u;
                     e_run = mine ? __dadd_rn(e_run, de) : e_run;
                     if (lane == 0 && ballot != 0u) w_cur[p0 + k] ^= ballot;
-                    const uint32_t back = g.pos[p0 + k].w;
-                    if ((back >> 24) != 0u && ballot != 0u) {
-                        const uint32_t neg_d = __float_as_uint(rec.y) & 0x80000000u;
-                        const uint2* fe = g.far + (back & 0xffffffu);
-#pragma unroll 1
-                        for (uint32_t e = 0; e < (back >> 24); ++e) {
-                            const uint2 ed = fe[e];
-                            if (stored) tmem_wait_st();  // an earlier update of this stage may hit the same column
-                            const float v = tmem_ld(tm + ed.x);
-                            tmem_wait_ld();
-                            const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
-                            tmem_st(tm + ed.x, mine ? nv : v);
-                            stored = true;
-                        }
-                    }
                 }
-                if (stored) tmem_wait_st();
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);
             }
-            mbar_arrive(layer_done);  // every backward update of this layer has landed
             slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
         }
     }
     if (active) {
         b.e_run[chain] = e_run;
         b.flips[chain] += flips;
+    }
+    __syncwarp();
+}
+
+// Far: applies the far-neighbour updates the sweep warp does not need soon — every BACKWARD target
+// (its column left the register window before the flipping attempt ran) and every FORWARD target
+// that enters the window at least two chunks later.  It trails the sweep warp by whole chunks,
+// shares its TMEM lane quarter, and publishes how many chunks it has finished; the sweep warp
+// waits on that count before it reads a column this warp may still owe an update.  Per column the
+// updates stay in attempt order: this warp walks attempts in order, and the sweep warp touches a
+// column (near forward update, window entry) only after the chunks that could still target it here.
+__device__ void far_warp(uint32_t sweeps, uint32_t lane, const GraphSmem& g, const PairSmem& s,
+                         uint64_t* consumed, uint64_t* empty, uint32_t* far_done, uint32_t& chunks_done,
+                         RingCursor& cursor, uint32_t stages, uint32_t tm, uint32_t P, uint32_t L) {
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t l = 0; l < L; ++l) {
+            for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
+                const uint32_t st = cursor.stage;
+                mbar_wait(&consumed[st], cursor.parity(), 32);
+                cursor.waited();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const float* rec_y = reinterpret_cast<const float*>(s.recs + size_t(st) * kUnroll * 32 + lane) + 1;
+                const uint32_t* ballots = s.ballots + st * kUnroll;
+                bool stored = false;
+#pragma unroll 1
+                for (uint32_t k = 0; k < kUnroll; ++k) {
+                    const uint32_t ballot = ballots[k];
+                    const uint32_t info = g.pos[p0 + k].w;
+                    const uint32_t count = info >> 24;
+                    if (count == 0u || ballot == 0u) continue;
+                    const bool mine = (ballot >> lane) & 1u;
+                    const uint32_t neg_d = __float_as_uint(rec_y[k * 128]) & 0x80000000u;
+                    const uint2* fe = g.far + (info & 0xffffffu);
+                    if (stored) tmem_wait_st();  // an earlier attempt of this stage may have hit the same column
+                    // the targets of one attempt are distinct: load them together (first two), then store
+                    const uint2 e0 = fe[0];
+                    const uint2 e1 = fe[count > 1u ? 1 : 0];
+                    const float v0 = tmem_ld(tm + e0.x);
+                    float v1 = 0.0f;
+                    if (count > 1u) v1 = tmem_ld(tm + e1.x);
+                    tmem_wait_ld();
+                    const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
+                    const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
+                    tmem_st(tm + e0.x, mine ? n0 : v0);
+                    if (count > 1u) tmem_st(tm + e1.x, mine ? n1 : v1);
+#pragma unroll 1
+                    for (uint32_t e = 2; e < count; ++e) {
+                        const uint2 ed = fe[e];
+                        const float v = tmem_ld(tm + ed.x);
+                        tmem_wait_ld();
+                        const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
+                        tmem_st(tm + ed.x, mine ? nv : v);
+                    }
+                    stored = true;
+                }
+                if (stored) tmem_wait_st();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&empty[st]);
+                cursor.advance(stages);
+                // publish progress: the sweep warp orders its own reads of the updated columns on it
+                ++chunks_done;
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(far_done)), "r"(chunks_done)
+                                 : "memory");
+                }
+            }
+        }
     }
     __syncwarp();
 }
@@ -451,12 +492,33 @@ __device__ __noinline__ void far_update(uint32_t tm, const uint2* fe, uint32_t f
     tmem_wait_st();  // a target may be the next column to enter the window
 }
 
+// Progress of the post warp as seen by the sweep warp.  Chunks are counted over the whole kernel
+// (both warps walk the same sequence), `cached` is the last value read.
+struct PostSync {
+    uint32_t addr;        // shared-memory address of the pair's counter
+    uint32_t cached;
+    uint32_t layer_base;  // chunks finished before this layer began
+};
+// Blocks until the post warp has finished `need_abs` chunks; then its Tensor Memory updates of
+// those chunks are ordered before whatever this warp does next.
+__device__ __forceinline__ void wait_post(PostSync& ps, uint32_t need_abs) {
+    if (int32_t(need_abs - ps.cached) > 0) {
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(ps.addr) : "memory");
+        } while (int32_t(need_abs - v) > 0);
+        ps.cached = v;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+}
+
 // One Metropolis attempt at position p = p0 + K of the current layer (K is the compile-time
 // index inside the unrolled chunk; the register window r[] is indexed by position & 7).
 template <int EXP, int K>
 __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, const uint4 bj, const uint4 bm,
-                                        uint32_t far_info, uint32_t p0, uint32_t tm, const uint2* far,
-                                        float* rec_x, uint32_t* ballots, uint32_t lane) {
+                                        uint32_t far_info, PostSync& ps, uint32_t chunks_before, uint32_t p0,
+                                        uint32_t tm, const uint2* far, float* rec_x, uint32_t* ballots,
+                                        uint32_t lane) {
     const float h = r[K];
     const float x = __fmul_rn(rec.y, __fadd_rn(h, rec.z));  // ref: sweep_kernels.hpp:14-16
     const float pr = exp_kind<EXP>(x);
@@ -481,24 +543,39 @@ __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, c
     if (K >= 2 || p0 != 0) tmem_st(tm + p0 + K - 2, r[(K + 6) & 7]);
 
     // ---- far neighbours: read-modify-write in Tensor Memory, out of line to keep this loop small
-    if ((far_info >> 24) != 0u && ballot != 0u) far_update(tm, far + (far_info & 0xffffffu), far_info >> 24, neg_d, accept);
+    // (near forward targets only: everything else is the post warp's; a near target may also have
+    // updates pending there, all from earlier chunks, which must land first)
+    const uint32_t near_count = (far_info >> 16) & 15u;
+    if (near_count != 0u && ballot != 0u) {
+        wait_post(ps, chunks_before);
+        far_update(tm, far + (far_info & 0xffffu), near_count, neg_d, accept);
+    }
 }
 
 // Feeds the window entry for position p+3 after attempt p (it is first needed by attempt p+1).
+// The post warp may still owe that column updates from attempts at least two chunks back:
+// far_info carries how many chunks of this layer it must have finished.
 template <int K>
-__device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t p0, uint32_t P, uint32_t tm) {
-    if (K <= 4 || p0 + kUnroll < P) r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
+__device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t far_info, PostSync& ps, uint32_t p0, uint32_t P,
+                                     uint32_t tm) {
+    if (K <= 4 || p0 + kUnroll < P) {
+        wait_post(ps, ps.layer_base + ((far_info >> 20) & 0x7fu));
+        r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
+    }
 }
 
 #define ISING_ATTEMPT(K)                                                                                   \
-    attempt<EXP, K>(r, rec##K, g.band_j2[p0 + K], g.band_mask[p0 + K], g.pos[p0 + K].z, p0, tm, g.far, rec_x, \
-                    ballots, lane);                                                                        \
-    feed<K>(r, p0, P, tm);
+    {                                                                                                      \
+        const uint32_t far_info = g.pos[p0 + K].z;                                                         \
+        attempt<EXP, K>(r, rec##K, g.band_j2[p0 + K], g.band_mask[p0 + K], far_info, ps, chunk_seq, p0, tm,  \
+                        g.far, rec_x, ballots, lane);                                                      \
+        feed<K>(r, far_info, ps, p0, P, tm);                                                               \
+    }
 
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint64_t* consumed, uint64_t* layer_done,
-                           uint32_t& layer_parity, RingCursor& cursor, uint32_t stages, uint32_t tile,
+                           const PairSmem& s, uint64_t* full, uint64_t* consumed, PostSync& ps,
+                           uint32_t& chunk_seq, RingCursor& cursor, uint32_t stages, uint32_t tile,
                            uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
@@ -553,6 +630,7 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             r[2] = tmem_ld(tm + 2);
             tmem_wait_ld();
 
+            ps.layer_base = chunk_seq;
             for (p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
                 mbar_wait(&full[st], cursor.parity(), 0);
@@ -576,15 +654,14 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&consumed[st]);
                 cursor.advance(stages);
+                ++chunk_seq;
             }
             // the last two columns leave the window
             tmem_st(tm + P - 2, r[6]);
             tmem_st(tm + P - 1, r[7]);
             tmem_wait_st();
             // the post warp's backward updates of this layer must be in before the layer is read out
-            mbar_wait(layer_done, layer_parity, 0);
-            layer_parity ^= 1u;
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            wait_post(ps, chunk_seq);
 
             // ---- retire: TMEM -> HBM
             for (p0 = 0; p0 < P; p0 += 8) {
@@ -607,11 +684,11 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 16);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t pair = warp & 3u;
-    const uint32_t role = warp >> 2;  // 0 sweep, 1 producer, 2 post — all three on scheduler `pair`
+    const uint32_t role = warp >> 2;  // 0 sweep, 1 producer, 2 post, 3 far — all four on scheduler `pair`
     uint64_t* full = bars + pair * 3 * kMaxStages;   // producer -> sweep
     uint64_t* consumed = full + kMaxStages;          // sweep -> post
     uint64_t* empty = consumed + kMaxStages;         // post -> producer
-    uint64_t* layer_done = bars + kRingBarriers + pair;  // post -> sweep, once per layer
+    uint32_t* post_done = reinterpret_cast<uint32_t*>(bars + kRingBarriers) + pair;  // post -> sweep progress
 
     const uint32_t maxP = b.max_per_layer;
     const uint32_t stages = b.layered_stages;
@@ -623,7 +700,9 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     const PairSmem s = carve_pair(pair_base, maxP, stages);
 
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
-    if (threadIdx.x < kRingBarriers + kSweepWarps) mbar_init(&bars[threadIdx.x], 32);
+    // `empty` collects both trailing roles (post and far): 64 arrivals; the others 32
+    if (threadIdx.x < kRingBarriers) mbar_init(&bars[threadIdx.x], (threadIdx.x % (3 * kMaxStages)) >= 2 * kMaxStages ? 64 : 32);
+    if (threadIdx.x < kSweepWarps) reinterpret_cast<uint32_t*>(bars + kRingBarriers)[threadIdx.x] = 0u;
     if (b.graph_shared) load_graph(gs, b.layer_graphs[0], threadIdx.x, kLayeredThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -633,7 +712,8 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     // this pair's lane quarter: bits 31..16 of a TMEM address are the lane, 15..0 the column
     const uint32_t tm = tmem_base + ((pair * 32u) << 16);
     RingCursor cursor;
-    uint32_t layer_parity = 0;
+    uint32_t chunk_seq = 0;  // chunks this role has finished, over the whole kernel
+    PostSync ps{smem_u32(post_done), 0u, 0u};
 
     // tiles are dealt round-robin: CTA c, pair w, round r -> tile c + grid*(w + 4r)
     for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
@@ -641,21 +721,23 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         if (!b.graph_shared) {
             // the three warps of the pair use the pair's graph copy: the sweep warp loads it
             if (role == 0) load_graph(gs, g, lane, 32);
-            asm volatile("bar.sync %0, 96;" ::"r"(pair + 1) : "memory");
+            asm volatile("bar.sync %0, 128;" ::"r"(pair + 1) : "memory");
         }
         if (role == 1) {
             producer_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else if (role == 2) {
-            post_warp(b, sweeps, lane, gs, s, consumed, empty, layer_done, cursor, stages, tile, tm, g.per_layer,
-                      g.layers);
+            post_warp(b, sweeps, lane, s, consumed, empty, cursor, stages, tile, g.per_layer, g.layers);
+        } else if (role == 3) {
+            far_warp(sweeps, lane, gs, s, consumed, empty, post_done, chunk_seq, cursor, stages, tm, g.per_layer,
+                     g.layers);
         } else {
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, consumed, layer_done, layer_parity, cursor, stages, tile,
-                            tm, g.per_layer, g.layers);
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, consumed, ps, chunk_seq, cursor, stages, tile, tm,
+                            g.per_layer, g.layers);
         }
-        if (!b.graph_shared) asm volatile("bar.sync %0, 96;" ::"r"(pair + 1) : "memory");
+        if (!b.graph_shared) asm volatile("bar.sync %0, 128;" ::"r"(pair + 1) : "memory");
     }
 
-    if (role != 1) {  // the two roles that touch Tensor Memory
+    if (role == 0 || role == 3) {  // the two roles that touch Tensor Memory
         tmem_wait_ld();
         tmem_wait_st();
     }
