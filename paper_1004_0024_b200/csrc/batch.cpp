@@ -183,6 +183,12 @@ Batch::Batch(const std::vector<const HostModel*>& models,
                     if (!is_band(p, t) && t > p && delegated(p, t)) need[t - 3] = std::max(need[t - 3], p / 8 + 1);
                 }
             }
+            // the sweep warp checks once per chunk: the chunk's first position carries the maximum
+            for (uint32_t p0 = 0; p0 < P; p0 += 8) {
+                uint32_t most = 0;
+                for (uint32_t k = 0; k < 8; ++k) most = std::max(most, need[p0 + k]);
+                for (uint32_t k = 0; k < 8; ++k) need[p0 + k] = k == 0 ? most : 0;
+            }
             for (uint32_t p = 0; p < P; ++p) {
                 uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
                 std::vector<uint2> for_post;

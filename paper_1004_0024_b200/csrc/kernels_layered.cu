@@ -558,10 +558,8 @@ __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, c
 template <int K>
 __device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t far_info, PostSync& ps, uint32_t p0, uint32_t P,
                                      uint32_t tm) {
-    if (K <= 4 || p0 + kUnroll < P) {
-        wait_post(ps, ps.layer_base + ((far_info >> 20) & 0x7fu));
-        r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
-    }
+    // (checked once per chunk, before its first attempt: see sweep_warp)
+    if (K <= 4 || p0 + kUnroll < P) r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
 }
 
 #define ISING_ATTEMPT(K)                                                                                   \
@@ -635,6 +633,10 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 const uint32_t st = cursor.stage;
                 mbar_wait(&full[st], cursor.parity(), 0);
                 cursor.waited();
+                // columns entering the window during this chunk may be owed updates by the far warp
+                // from attempts at least two chunks back: the chunk's first position carries how many
+                // chunks of this layer it must have finished
+                wait_post(ps, ps.layer_base + ((g.pos[p0].z >> 20) & 0x7fu));
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 float* rec_x = reinterpret_cast<float*>(s.recs + size_t(st) * kUnroll * 32 + lane);
