@@ -293,7 +293,7 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
                 const uint32_t st = cursor.stage;
                 float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 if ((in_flight >> st) & 1u) {  // recycle: the post warp must be done with it
-                    mbar_wait(&empty[st], cursor.parity(), 100);
+                    mbar_wait(&empty[st], cursor.parity(), 400);
                     cursor.waited();
                 }
                 uint32_t raw[kUnroll];
@@ -366,7 +366,7 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
             uint32_t* w_cur = s.words + slot_cur * P;
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
-                mbar_wait(&consumed[st], cursor.parity(), 100);
+                mbar_wait(&consumed[st], cursor.parity(), 800);
                 cursor.waited();
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
@@ -409,7 +409,7 @@ __device__ void far_warp(uint32_t sweeps, uint32_t lane, const GraphSmem& g, con
         for (uint32_t l = 0; l < L; ++l) {
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
-                mbar_wait(&consumed[st], cursor.parity(), 32);
+                mbar_wait(&consumed[st], cursor.parity(), 200);
                 cursor.waited();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const float* rec_y = reinterpret_cast<const float*>(s.recs + size_t(st) * kUnroll * 32 + lane) + 1;
