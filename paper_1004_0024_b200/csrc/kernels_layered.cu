@@ -123,6 +123,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32
     } while (done == 0u);
 }
 
+// Hardware-blocking rendezvous of a tile's sweep, post and far warps (named barrier, 96 threads):
+// the sweep warp calls it when it has finished a chunk, the trailing two when they are ready to
+// start that chunk, so they sleep in the barrier instead of polling, and the sweep warp can never
+// be more than one chunk ahead of them.
+__device__ __forceinline__ void chunk_barrier(uint32_t id) {
+    asm volatile("bar.sync %0, 96;" ::"r"(id) : "memory");
+}
+
 // ---- shared-memory carve-up (per CTA): [header][graph x (1 | 4)][per-pair dynamic region x 4]
 struct GraphSmem {
     uint4* pos;        // P : {gamma*2J_tau, 2J_tau, far_begin | far_count << 24, 0}
@@ -354,7 +362,7 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
 // sweep_basic.cpp:47-48; the energy bookkeeping is the tempering definition of
 // oracle/ising_oracle.h).
 __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s,
-                          uint64_t* consumed, uint64_t* empty, RingCursor& cursor, uint32_t stages,
+                          uint32_t bar_id, uint64_t* empty, RingCursor& cursor, uint32_t stages,
                           uint32_t tile, uint32_t P, uint32_t L) {
     const uint32_t chain = b.tile_first[tile] + lane;
     const bool active = lane < b.tile_count[tile];
@@ -366,8 +374,7 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
             uint32_t* w_cur = s.words + slot_cur * P;
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
-                mbar_wait(&consumed[st], cursor.parity(), 800);
-                cursor.waited();
+                chunk_barrier(bar_id);  // the sweep warp has finished this chunk
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
 #pragma unroll
@@ -385,6 +392,7 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);
             }
+            chunk_barrier(bar_id);  // layer rendezvous (the sweep warp waits for the far warp here)
             slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
         }
     }
@@ -403,14 +411,13 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
 // updates stay in attempt order: this warp walks attempts in order, and the sweep warp touches a
 // column (near forward update, window entry) only after the chunks that could still target it here.
 __device__ void far_warp(uint32_t sweeps, uint32_t lane, const GraphSmem& g, const PairSmem& s,
-                         uint64_t* consumed, uint64_t* empty, uint32_t* far_done, uint32_t& chunks_done,
+                         uint32_t bar_id, uint64_t* empty, uint32_t* far_done, uint32_t& chunks_done,
                          RingCursor& cursor, uint32_t stages, uint32_t tm, uint32_t P, uint32_t L) {
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
-                mbar_wait(&consumed[st], cursor.parity(), 200);
-                cursor.waited();
+                chunk_barrier(bar_id);  // the sweep warp has finished this chunk
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const float* rec_y = reinterpret_cast<const float*>(s.recs + size_t(st) * kUnroll * 32 + lane) + 1;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
@@ -458,6 +465,7 @@ __device__ void far_warp(uint32_t sweeps, uint32_t lane, const GraphSmem& g, con
                                  : "memory");
                 }
             }
+            chunk_barrier(bar_id);  // layer rendezvous: every update of this layer has landed
         }
     }
     __syncwarp();
@@ -572,7 +580,7 @@ __device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t far_info, Pos
 
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint64_t* consumed, PostSync& ps,
+                           const PairSmem& s, uint64_t* full, uint32_t bar_id, PostSync& ps,
                            uint32_t& chunk_seq, RingCursor& cursor, uint32_t stages, uint32_t tile,
                            uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
@@ -633,10 +641,9 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 const uint32_t st = cursor.stage;
                 mbar_wait(&full[st], cursor.parity(), 0);
                 cursor.waited();
-                // columns entering the window during this chunk may be owed updates by the far warp
-                // from attempts at least two chunks back: the chunk's first position carries how many
-                // chunks of this layer it must have finished
-                wait_post(ps, ps.layer_base + ((g.pos[p0].z >> 20) & 0x7fu));
+                // columns entering the window during this chunk may be owed updates by the far warp from
+                // attempts at least two chunks back: the chunk rendezvous below guarantees it has
+                // finished those (it cannot be more than one chunk behind)
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 float* rec_x = reinterpret_cast<float*>(s.recs + size_t(st) * kUnroll * 32 + lane);
@@ -654,7 +661,8 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 // the post warp may now update columns this chunk retired: they must have landed
                 tmem_wait_st();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&consumed[st]);
+                chunk_barrier(bar_id);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 cursor.advance(stages);
                 ++chunk_seq;
             }
@@ -663,7 +671,8 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             tmem_st(tm + P - 1, r[7]);
             tmem_wait_st();
             // the post warp's backward updates of this layer must be in before the layer is read out
-            wait_post(ps, chunk_seq);
+            chunk_barrier(bar_id);  // layer rendezvous
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
             // ---- retire: TMEM -> HBM
             for (p0 = 0; p0 < P; p0 += 8) {
@@ -688,8 +697,8 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     const uint32_t pair = warp & 3u;
     const uint32_t role = warp >> 2;  // 0 sweep, 1 producer, 2 post, 3 far — all four on scheduler `pair`
     uint64_t* full = bars + pair * 3 * kMaxStages;   // producer -> sweep
-    uint64_t* consumed = full + kMaxStages;          // sweep -> post
-    uint64_t* empty = consumed + kMaxStages;         // post -> producer
+    uint64_t* empty = full + 2 * kMaxStages;         // post + far -> producer
+    const uint32_t bar_id = 5 + pair;                // named barrier of the tile's sweep/post/far rendezvous
     uint32_t* post_done = reinterpret_cast<uint32_t*>(bars + kRingBarriers) + pair;  // post -> sweep progress
 
     const uint32_t maxP = b.max_per_layer;
@@ -728,12 +737,12 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         if (role == 1) {
             producer_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else if (role == 2) {
-            post_warp(b, sweeps, lane, s, consumed, empty, cursor, stages, tile, g.per_layer, g.layers);
+            post_warp(b, sweeps, lane, s, bar_id, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else if (role == 3) {
-            far_warp(sweeps, lane, gs, s, consumed, empty, post_done, chunk_seq, cursor, stages, tm, g.per_layer,
+            far_warp(sweeps, lane, gs, s, bar_id, empty, post_done, chunk_seq, cursor, stages, tm, g.per_layer,
                      g.layers);
         } else {
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, consumed, ps, chunk_seq, cursor, stages, tile, tm,
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, bar_id, ps, chunk_seq, cursor, stages, tile, tm,
                             g.per_layer, g.layers);
         }
         if (!b.graph_shared) asm volatile("bar.sync %0, 128;" ::"r"(pair + 1) : "memory");
