@@ -358,12 +358,65 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
     __syncwarp();
 }
 
+// Layer change, shared by the tile's sweep, post and far warps (part 0, 1, 2 of 3): each retires
+// its third of the finished layer's columns TMEM -> HBM and feeds the same columns with the next
+// layer HBM -> TMEM (full 128-byte lines, streaming hints), so the sweep warp pays a third of the
+// transfer.  A warp only reuses columns it has read out itself, so no rendezvous is needed between
+// the two halves; the caller closes the transition with one (chunk_barrier) before the sweep resumes.
+__device__ __forceinline__ void layer_transition(uint32_t part, uint32_t tm, float* hs_old, const float* hs_new,
+                                                 uint32_t P) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (hs_old != nullptr) {
+        for (uint32_t p0 = part * 8; p0 < P; p0 += 24) {
+            float v[8];
+            tmem_ld8(tm + p0, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) __stcs(hs_old + size_t(p0 + k) * 32, v[k]);
+        }
+    }
+    if (hs_new != nullptr) {
+        // this warp's 8-column groups sit 24 columns apart; four of them (32 loads) are requested
+        // before the previous four are stored, so two batches are always in flight
+        uint32_t p0 = part * 8;
+        float v[4][8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[q][k] = p0 + q * 24 < P ? __ldcs(hs_new + size_t(p0 + q * 24 + k) * 32) : 0.0f;
+        }
+        for (; p0 < P; p0 += 96) {
+            float nv[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    nv[q][k] = p0 + 96 + q * 24 < P ? __ldcs(hs_new + size_t(p0 + 96 + q * 24 + k) * 32) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (p0 + q * 24 < P) tmem_st8(tm + p0 + q * 24, v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[q][k] = nv[q][k];
+            }
+        }
+    }
+    tmem_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
 // Post: accept counts, running energy and spin words of every consumed stage (ref:
 // sweep_basic.cpp:47-48; the energy bookkeeping is the tempering definition of
 // oracle/ising_oracle.h).
 __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s,
                           uint32_t bar_id, uint64_t* empty, RingCursor& cursor, uint32_t stages,
-                          uint32_t tile, uint32_t P, uint32_t L) {
+                          uint32_t tile, uint32_t tm, uint32_t P, uint32_t L) {
+    float* hs_g = b.hs + size_t(tile) * b.n_spins * 32 + lane;
+    float* hs_prev = nullptr;
     const uint32_t chain = b.tile_first[tile] + lane;
     const bool active = lane < b.tile_count[tile];
     double e_run = active ? b.e_run[chain] : 0.0;
@@ -372,6 +425,9 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
             uint32_t* w_cur = s.words + slot_cur * P;
+            layer_transition(1, tm, hs_prev, hs_g + size_t(l) * P * 32, P);
+            chunk_barrier(bar_id);
+            hs_prev = hs_g + size_t(l) * P * 32;
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
                 chunk_barrier(bar_id);  // the sweep warp has finished this chunk
@@ -396,6 +452,8 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
             slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
         }
     }
+    layer_transition(1, tm, hs_prev, nullptr, P);
+    chunk_barrier(bar_id);
     if (active) {
         b.e_run[chain] = e_run;
         b.flips[chain] += flips;
@@ -410,11 +468,15 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
 // waits on that count before it reads a column this warp may still owe an update.  Per column the
 // updates stay in attempt order: this warp walks attempts in order, and the sweep warp touches a
 // column (near forward update, window entry) only after the chunks that could still target it here.
-__device__ void far_warp(uint32_t sweeps, uint32_t lane, const GraphSmem& g, const PairSmem& s,
+__device__ void far_warp(float* hs_g, uint32_t sweeps, uint32_t lane, const GraphSmem& g, const PairSmem& s,
                          uint32_t bar_id, uint64_t* empty, uint32_t* far_done, uint32_t& chunks_done,
                          RingCursor& cursor, uint32_t stages, uint32_t tm, uint32_t P, uint32_t L) {
+    float* hs_prev = nullptr;
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
+            layer_transition(2, tm, hs_prev, hs_g + size_t(l) * P * 32, P);
+            chunk_barrier(bar_id);
+            hs_prev = hs_g + size_t(l) * P * 32;
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
                 chunk_barrier(bar_id);  // the sweep warp has finished this chunk
@@ -468,6 +530,8 @@ __device__ void far_warp(uint32_t sweeps, uint32_t lane, const GraphSmem& g, con
             chunk_barrier(bar_id);  // layer rendezvous: every update of this layer has landed
         }
     }
+    layer_transition(2, tm, hs_prev, nullptr, P);
+    chunk_barrier(bar_id);
     __syncwarp();
 }
 
@@ -585,47 +649,19 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                            uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
+    float* hs_prev = nullptr;
+    uint32_t p0 = 0;
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
             float* hs_l = hs_g + size_t(l) * P * 32;
             const float* hs_next = hs_g + size_t(l + 1 == L ? 0 : l + 1) * P * 32 - lane;
-            // ---- feed: this layer's fields HBM -> TMEM (P is a multiple of 8).  Two batches of 32
-            // columns in flight: the next batch's loads are issued before this batch is stored.
-            uint32_t p0 = 0;
-            if (P >= 32) {
-                float v[4][8];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) v[q][k] = __ldcs(hs_l + size_t(q * 8 + k) * 32);
-                }
-                for (; p0 + 64 <= P; p0 += 32) {
-                    float nv[4][8];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) nv[q][k] = __ldcs(hs_l + size_t(p0 + 32 + q * 8 + k) * 32);
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) tmem_st8(tm + p0 + q * 8, v[q]);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) v[q][k] = nv[q][k];
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) tmem_st8(tm + p0 + q * 8, v[q]);
-                p0 += 32;
-            }
-            for (; p0 < P; p0 += 8) {
-                float v[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = __ldcs(hs_l + size_t(p0 + k) * 32);
-                tmem_st8(tm + p0, v);
-            }
-            tmem_wait_st();
+            // ---- layer change: retire the previous layer, feed this one (a third each with the
+            // post and far warps), then rendezvous
+            layer_transition(0, tm, hs_prev, hs_l, P);
+            chunk_barrier(bar_id);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            hs_prev = hs_l;
 
             // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
             float r[kUnroll];
@@ -670,20 +706,14 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             tmem_st(tm + P - 2, r[6]);
             tmem_st(tm + P - 1, r[7]);
             tmem_wait_st();
-            // the post warp's backward updates of this layer must be in before the layer is read out
-            chunk_barrier(bar_id);  // layer rendezvous
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-            // ---- retire: TMEM -> HBM
-            for (p0 = 0; p0 < P; p0 += 8) {
-                float v[8];
-                tmem_ld8(tm + p0, v);
-                tmem_wait_ld();
-#pragma unroll
-                for (int k = 0; k < 8; ++k) __stcs(hs_l + size_t(p0 + k) * 32, v[k]);
-            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            // layer rendezvous: the far warp's updates of this layer are in, and the three warps may
+            // now read the layer out together
+            chunk_barrier(bar_id);
         }
     }
+    layer_transition(0, tm, hs_prev, nullptr, P);
+    chunk_barrier(bar_id);
     __syncwarp();
 }
 #undef ISING_ATTEMPT
@@ -737,9 +767,10 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         if (role == 1) {
             producer_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else if (role == 2) {
-            post_warp(b, sweeps, lane, s, bar_id, empty, cursor, stages, tile, g.per_layer, g.layers);
+            post_warp(b, sweeps, lane, s, bar_id, empty, cursor, stages, tile, tm, g.per_layer, g.layers);
         } else if (role == 3) {
-            far_warp(sweeps, lane, gs, s, bar_id, empty, post_done, chunk_seq, cursor, stages, tm, g.per_layer,
+            far_warp(b.hs + size_t(tile) * b.n_spins * 32 + lane, sweeps, lane, gs, s, bar_id, empty, post_done, chunk_seq,
+                     cursor, stages, tm, g.per_layer,
                      g.layers);
         } else {
             sweep_warp<EXP>(b, sweeps, lane, gs, s, full, bar_id, ps, chunk_seq, cursor, stages, tile, tm,
@@ -748,7 +779,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         if (!b.graph_shared) asm volatile("bar.sync %0, 128;" ::"r"(pair + 1) : "memory");
     }
 
-    if (role == 0 || role == 3) {  // the two roles that touch Tensor Memory
+    if (role != 1) {  // the roles that touch Tensor Memory
         tmem_wait_ld();
         tmem_wait_st();
     }
