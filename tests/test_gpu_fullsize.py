@@ -125,3 +125,27 @@ def test_layer_width_not_multiple_of_8_uses_generic_family(lib, port):
         np.testing.assert_array_equal(st.spins(), want["spins"])
     with pytest.raises(ib.IsingError):
         ib.init_state(product_model(csr), [1.0], 1, kernel=ib.KERNEL_LAYERED)
+
+
+def test_more_tiles_than_warp_slots_each_pair_sweeps_several_tiles(lib, port):
+    """700 tiles on 148 x 4 tile slots: every (sweep, producer, post, far) warp group walks more
+    than one tile in a launch, across several launches.  Both families must agree everywhere and a
+    subsample must match the oracle."""
+    csr = ins.build_layered_csr(*ins.layered_spec(24, 17), 4, 1.5)
+    model = product_model(csr)
+    betas = ins.geometric_betas(0.3, 2.5, 4)
+    ladders = 700 * 8  # 22,400 chains = 700 tiles
+    out = {}
+    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC):
+        with ib.init_state(model, betas, ladders, base_seed=31, swap_base_seed=32, kernel=family) as st:
+            assert st.info()["n_tiles"] == 700 and st.info()["kernel"] == family
+            st.run(7, 3)
+            st.run(5, 3)
+            out[family] = (st.checksums(), st.stats()[0], st.slots(), st.running_energies())
+            if family == ib.KERNEL_LAYERED:
+                sample = st.spins(4 * 5000, 8)  # ladders 5000, 5001: tile 625, in the second round of its pair
+    for a, b in zip(out[ib.KERNEL_LAYERED], out[ib.KERNEL_GENERIC]):
+        np.testing.assert_array_equal(a, b)
+    want = oracle_batch(port, [csr], 2, betas, sharding.chain_seeds(31, 5000, 2, 4),
+                        sharding.ladder_seeds(32, 5000, 2), 12, 3)
+    np.testing.assert_array_equal(sample, want["spins"])
