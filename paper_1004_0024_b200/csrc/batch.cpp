@@ -87,7 +87,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
                 far_here += is_band(p, m->layer_targets[e]) ? 0u : 1u;
             }
-            layered_ok = layered_ok && far_here < 256;
+            layered_ok = layered_ok && far_here < 16;  // 4-bit edge counts in DevLayerGraph::pos
             far += far_here;
         }
         max_far_edges = std::max(max_far_edges, far);
@@ -167,31 +167,19 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         };
         for (const HostModel* m : models) {
             const uint32_t P = m->per_layer;
-            std::vector<uint4> pos(P), band_j2(P), band_mask(P);
+            std::vector<uint4> pos(P), band_pm(2 * size_t(P));
             std::vector<uint2> far;
-            // Far edges are split by who applies them.  The POST warp, which trails the sweep warp by
+            // Far edges are split by who applies them.  The FAR warp, which trails the sweep warp by
             // whole 8-attempt chunks, takes every target the sweep warp is not going to read soon:
             // backward targets (already out of its register window) and forward targets that enter the
             // window at least two chunks after the flipping attempt's chunk.  The sweep warp keeps the
-            // near forward targets.  need[a] = how many chunks of the layer the post warp must have
-            // finished before column a+3 may enter the window after attempt a.
+            // near forward targets; a chunk without any (and not the first or last of the layer) runs
+            // its lean loop, which moves the window in and out of Tensor Memory eight columns at a time.
             const auto delegated = [](uint32_t p, uint32_t t) { return t < p || (t - 3) / 8 >= p / 8 + 2; };
-            std::vector<uint32_t> need(P, 0);
-            for (uint32_t p = 0; p < P; ++p) {
-                for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
-                    const uint32_t t = m->layer_targets[e];
-                    if (!is_band(p, t) && t > p && delegated(p, t)) need[t - 3] = std::max(need[t - 3], p / 8 + 1);
-                }
-            }
-            // the sweep warp checks once per chunk: the chunk's first position carries the maximum
-            for (uint32_t p0 = 0; p0 < P; p0 += 8) {
-                uint32_t most = 0;
-                for (uint32_t k = 0; k < 8; ++k) most = std::max(most, need[p0 + k]);
-                for (uint32_t k = 0; k < 8; ++k) need[p0 + k] = k == 0 ? most : 0;
-            }
+            std::vector<uint32_t> near_counts(P, 0);
             for (uint32_t p = 0; p < P; ++p) {
                 uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
-                std::vector<uint2> for_post;
+                std::vector<uint2> for_far_warp;
                 const uint32_t near_begin = uint32_t(far.size());
                 for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
                     const uint32_t t = m->layer_targets[e];
@@ -202,20 +190,33 @@ Batch::Batch(const std::vector<const HostModel*>& models,
                         j2[slot] = bits(doubled);
                         mask[slot] = 0;
                     } else if (delegated(p, t)) {
-                        for_post.push_back(make_uint2(t, bits(doubled)));
+                        for_far_warp.push_back(make_uint2(t, bits(doubled)));
                     } else {
                         far.push_back(make_uint2(t, bits(doubled)));
                     }
                 }
                 const uint32_t near_count = uint32_t(far.size()) - near_begin;
-                const uint32_t post_begin = uint32_t(far.size());
-                far.insert(far.end(), for_post.begin(), for_post.end());
+                near_counts[p] = near_count;
+                const uint32_t far_begin = uint32_t(far.size());
+                far.insert(far.end(), for_far_warp.begin(), for_far_warp.end());
                 const float tau2 = 2.0f * m->layer_tau[p];
                 const float tau2g = cfg.tau_scale * tau2;  // f32 product, as gamma * h_tau in the reference
-                pos[p] = make_uint4(bits(tau2g), bits(tau2), near_begin | near_count << 16 | need[p] << 20,
-                                    post_begin | uint32_t(for_post.size()) << 24);
-                band_j2[p] = make_uint4(j2[0], j2[1], j2[2], j2[3]);
-                band_mask[p] = make_uint4(mask[0], mask[1], mask[2], mask[3]);
+                pos[p] = make_uint4(bits(tau2g), bits(tau2), near_begin | near_count << 16,
+                                    far_begin | uint32_t(for_far_warp.size()) << 24);
+                // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign of
+                // -s; an empty slot adds -0.0.  Entry 2p is for s = -1 (sign bit of -2*beta*s clear),
+                // entry 2p+1 for s = +1.
+                for (uint32_t neg = 0; neg < 2; ++neg) {
+                    const uint32_t flip = neg ? 0x80000000u : 0u;
+                    band_pm[2 * size_t(p) + neg] = make_uint4((j2[0] ^ flip) | mask[0], (j2[1] ^ flip) | mask[1],
+                                                             (j2[2] ^ flip) | mask[2], (j2[3] ^ flip) | mask[3]);
+                }
+            }
+            // bit 20 of the chunk's first position: the chunk needs the careful (per-attempt) loop
+            for (uint32_t p0 = 0; p0 < P; p0 += 8) {
+                bool careful = p0 == 0 || p0 + 8 >= P;
+                for (uint32_t k = 0; k < 8; ++k) careful = careful || near_counts[p0 + k] != 0;
+                if (careful) pos[p0].z |= 1u << 20;
             }
             DevLayerGraph g{};
             g.per_layer = P;
@@ -223,8 +224,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             g.n_far = uint32_t(far.size());
             if (far.empty()) far.push_back(make_uint2(0, 0));
             g.pos = keep(pos)->as<uint4>();
-            g.band_j2 = keep(band_j2)->as<uint4>();
-            g.band_mask = keep(band_mask)->as<uint4>();
+            g.band_pm = keep(band_pm)->as<uint4>();
             g.far = keep(far)->as<uint2>();
             graphs.push_back(g);
             cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");  // temporaries die here

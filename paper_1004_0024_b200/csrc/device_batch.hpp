@@ -40,14 +40,14 @@ struct DevLayerGraph {
     uint32_t per_layer;
     uint32_t layers;
     uint32_t n_far;
-    // per position: {bits of tau2g, bits of tau2, forward far edges begin | count << 24,
-    //                backward far edges begin | count << 24}  (indices into `far`)
+    // per position: {bits of tau2g, bits of tau2,
+    //                near forward far edges: begin | count << 16 | careful-chunk flag << 20,
+    //                far-warp edges: begin | count << 24}  (indices into `far`)
     const uint4* pos;
-    // per position: bits of 2J for the slots -2, -1, +1, +2 (0 when the slot is empty) ...
-    const uint4* band_j2;
-    // ... and 0x80000000 for an empty slot, 0 otherwise: (j2 ^ sign) | mask is then -0.0, the
-    // additive identity for every float bit pattern, so an empty slot costs no predicate.
-    const uint4* band_mask;
+    // per position two entries (2p: flipped spin was -1, 2p+1: it was +1): what the flip adds to the
+    // fields at p-2, p-1, p+1, p+2, i.e. -(2s)*J as bits; an empty slot holds -0.0, the additive
+    // identity for every float bit pattern, so it costs no predicate.
+    const uint4* band_pm;
     const uint2* far;  // {position, bits of 2J}
 };
 

@@ -86,6 +86,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
 }
+// wait::ld tied to the registers of a tmem_ld8, so that no use of them can be scheduled before it
+__device__ __forceinline__ void tmem_wait_ld8(float (&v)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]));
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                  "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
@@ -99,6 +104,15 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 // ---- mbarrier (shared::cta) helpers for the stage ring
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    // not volatile: only used on the layer graph, which is constant while a tile is swept
+    asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -133,10 +147,9 @@ __device__ __forceinline__ void chunk_barrier(uint32_t id) {
 
 // ---- shared-memory carve-up (per CTA): [header][graph x (1 | 4)][per-pair dynamic region x 4]
 struct GraphSmem {
-    uint4* pos;        // P : {gamma*2J_tau, 2J_tau, far_begin | far_count << 24, 0}
-    uint4* band_j2;    // P
-    uint4* band_mask;  // P
-    uint2* far;        // max_far
+    uint4* pos;      // P : DevLayerGraph::pos
+    uint4* band_pm;  // 2P : DevLayerGraph::band_pm (32-byte aligned: the entry pair of a position)
+    uint2* far;      // max_far
 };
 struct PairSmem {
     uint2* agree_sign;  // P : per layer, {~(up ^ dn), up} spin words
@@ -152,7 +165,7 @@ constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one post-prog
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
-    return size_t(P) * 48 + align16(size_t(max_far ? max_far : 1) * 8);
+    return (size_t(P) * 48 + size_t(max_far ? max_far : 1) * 8 + 31) / 32 * 32;  // keeps band_pm pairs 32-byte aligned
 }
 __host__ __device__ inline size_t pair_bytes(uint32_t P, uint32_t stages) {
     return align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(stages) * kUnroll * 32 * 16 +
@@ -162,9 +175,8 @@ __host__ __device__ inline size_t pair_bytes(uint32_t P, uint32_t stages) {
 __device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P) {
     GraphSmem g;
     g.pos = reinterpret_cast<uint4*>(base);
-    g.band_j2 = g.pos + P;
-    g.band_mask = g.band_j2 + P;
-    g.far = reinterpret_cast<uint2*>(g.band_mask + P);
+    g.band_pm = g.pos + P;
+    g.far = reinterpret_cast<uint2*>(g.band_pm + 2 * size_t(P));
     return g;
 }
 __device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P, uint32_t stages) {
@@ -185,8 +197,8 @@ __device__ __forceinline__ void load_graph(const GraphSmem& dst, const DevLayerG
                                            uint32_t nthreads) {
     for (uint32_t k = tid; k < g.per_layer; k += nthreads) {
         dst.pos[k] = g.pos[k];
-        dst.band_j2[k] = g.band_j2[k];
-        dst.band_mask[k] = g.band_mask[k];
+        dst.band_pm[2 * k] = g.band_pm[2 * k];
+        dst.band_pm[2 * k + 1] = g.band_pm[2 * k + 1];
     }
     for (uint32_t k = tid; k < g.n_far; k += nthreads) dst.far[k] = g.far[k];
 }
@@ -584,63 +596,86 @@ __device__ __forceinline__ void wait_post(PostSync& ps, uint32_t need_abs) {
     }
 }
 
-// One Metropolis attempt at position p = p0 + K of the current layer (K is the compile-time
-// index inside the unrolled chunk; the register window r[] is indexed by position & 7).
-template <int EXP, int K>
-__device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, const uint4 bj, const uint4 bm,
-                                        uint32_t far_info, PostSync& ps, uint32_t chunks_before, uint32_t p0,
-                                        uint32_t tm, const uint2* far, float* rec_x, uint32_t* ballots,
-                                        uint32_t lane) {
-    const float h = r[K];
-    const float x = __fmul_rn(rec.y, __fadd_rn(h, rec.z));  // ref: sweep_kernels.hpp:14-16
-    const float pr = exp_kind<EXP>(x);
-    const bool accept = rec.x < pr;  // no clamp: ref sweep_basic.cpp:36-37
+// The Metropolis decision of one attempt (ref: sweep_kernels.hpp:14-16, sweep_basic.cpp:36-37: no clamp).
+template <int EXP>
+__device__ __forceinline__ bool decide(float h, const float4 rec) {
+    const float x = __fmul_rn(rec.y, __fadd_rn(h, rec.z));
+    return rec.x < exp_kind<EXP>(x);
+}
 
-    // ---- band neighbours: h -= (2s)*J  ==  h + (-(2s)*J); an empty slot adds -0.0 (identity)
-    const uint32_t neg_d = __float_as_uint(rec.y) & 0x80000000u;  // sign of -(2s), beta >= 0
-    tmem_wait_ld();  // the entry for p+2 was requested right after the previous attempt
-    const float a0 = __fadd_rn(r[(K + 6) & 7], __uint_as_float((bj.x ^ neg_d) | bm.x));
-    const float a1 = __fadd_rn(r[(K + 7) & 7], __uint_as_float((bj.y ^ neg_d) | bm.y));
-    const float a2 = __fadd_rn(r[(K + 1) & 7], __uint_as_float((bj.z ^ neg_d) | bm.z));
-    const float a3 = __fadd_rn(r[(K + 2) & 7], __uint_as_float((bj.w ^ neg_d) | bm.w));
+// Band neighbours of a flip: h -= (2s)*J  ==  h + (-(2s)*J), predicated register adds on the window
+// entries p-2, p-1, p+1, p+2.  The addend comes from the band_pm entry of the flipped spin's sign
+// (the sign bit of rec.y = -2*beta*s picks it); an empty slot adds -0.0.
+template <int K>
+__device__ __forceinline__ void band_update(float (&r)[kUnroll], bool accept, uint32_t band_addr, float rec_y) {
+    const uint32_t sel = ((__float_as_uint(rec_y) >> 27) & 16u) | band_addr;  // band_addr is 32-byte aligned
+    const uint4 op = lds128(sel + K * 32);
+    const float a0 = __fadd_rn(r[(K + 6) & 7], __uint_as_float(op.x));
+    const float a1 = __fadd_rn(r[(K + 7) & 7], __uint_as_float(op.y));
+    const float a2 = __fadd_rn(r[(K + 1) & 7], __uint_as_float(op.z));
+    const float a3 = __fadd_rn(r[(K + 2) & 7], __uint_as_float(op.w));
     r[(K + 6) & 7] = accept ? a0 : r[(K + 6) & 7];
     r[(K + 7) & 7] = accept ? a1 : r[(K + 7) & 7];
     r[(K + 1) & 7] = accept ? a2 : r[(K + 1) & 7];
     r[(K + 2) & 7] = accept ? a3 : r[(K + 2) & 7];
+}
+
+// Addresses of the stage the sweep warp is consuming (shared-memory window addresses).
+struct StageAddr {
+    uint32_t rec_x;    // this lane's rec.x of attempt 0 (attempts are 512 B apart)
+    uint32_t ballots;  // ballot of attempt 0
+    uint32_t band;     // band_pm pair of position p0
+};
+
+// One attempt at position p = p0 + K of a CAREFUL chunk (K is the compile-time index inside the
+// unrolled chunk; the register window r[] is indexed by position & 7): the window moves one column
+// per attempt, and near forward far targets are updated in Tensor Memory before they enter it.
+template <int EXP, int K>
+__device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, const StageAddr& sa, uint32_t far_info,
+                                        PostSync& ps, uint32_t chunks_before, uint32_t p0, uint32_t P, uint32_t tm,
+                                        const uint2* far, uint32_t lane) {
+    const float h = r[K];
+    const bool accept = decide<EXP>(h, rec);
+    tmem_wait_ld();  // the entry for p+2 was requested right after the previous attempt
+    band_update<K>(r, accept, sa.band, rec.y);
     const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
-    rec_x[K * 128] = h;  // the helper needs the field this decision saw (energy bookkeeping)
-    if (lane == 0) ballots[K] = ballot;
+    sts32(sa.rec_x + K * 512, __float_as_uint(h));  // the post warp needs the field this decision saw
+    if (lane == 0) sts32(sa.ballots + K * 4, ballot);
 
     // ---- retire column p-2: no later attempt of this layer can reach it through the band
     if (K >= 2 || p0 != 0) tmem_st(tm + p0 + K - 2, r[(K + 6) & 7]);
 
-    // ---- far neighbours: read-modify-write in Tensor Memory, out of line to keep this loop small
-    // (near forward targets only: everything else is the post warp's; a near target may also have
-    // updates pending there, all from earlier chunks, which must land first)
+    // ---- near forward far neighbours: read-modify-write in Tensor Memory, out of line (a near
+    // target may also have updates pending in the far warp, all from earlier chunks: they land first)
     const uint32_t near_count = (far_info >> 16) & 15u;
     if (near_count != 0u && ballot != 0u) {
         wait_post(ps, chunks_before);
-        far_update(tm, far + (far_info & 0xffffu), near_count, neg_d, accept);
+        far_update(tm, far + (far_info & 0xffffu), near_count, __float_as_uint(rec.y) & 0x80000000u, accept);
     }
-}
-
-// Feeds the window entry for position p+3 after attempt p (it is first needed by attempt p+1).
-// The post warp may still owe that column updates from attempts at least two chunks back:
-// far_info carries how many chunks of this layer it must have finished.
-template <int K>
-__device__ __forceinline__ void feed(float (&r)[kUnroll], uint32_t far_info, PostSync& ps, uint32_t p0, uint32_t P,
-                                     uint32_t tm) {
-    // (checked once per chunk, before its first attempt: see sweep_warp)
+    // ---- the window entry for p+3 (first needed by attempt p+1)
     if (K <= 4 || p0 + kUnroll < P) r[(K + 3) & 7] = tmem_ld(tm + p0 + K + 3);
 }
 
-#define ISING_ATTEMPT(K)                                                                                   \
-    {                                                                                                      \
-        const uint32_t far_info = g.pos[p0 + K].z;                                                         \
-        attempt<EXP, K>(r, rec##K, g.band_j2[p0 + K], g.band_mask[p0 + K], far_info, ps, chunk_seq, p0, tm,  \
-                        g.far, rec_x, ballots, lane);                                                      \
-        feed<K>(r, far_info, ps, p0, P, tm);                                                               \
-    }
+// One attempt of a LEAN chunk (no near forward far targets, not the first or last chunk of the
+// layer): the eight columns entering the window were loaded together (nx), the eight leaving it
+// are collected (out) and stored together, so the attempt touches no Tensor Memory at all.
+template <int EXP, int K>
+__device__ __forceinline__ void attempt_lean(float (&r)[kUnroll], float (&out)[kUnroll], float (&nx)[kUnroll],
+                                             const float4 rec, const StageAddr& sa, uint32_t lane) {
+    const float h = r[K];
+    const bool accept = decide<EXP>(h, rec);
+    if (K == 0) tmem_wait_ld8(nx);  // in flight during the first decision
+    band_update<K>(r, accept, sa.band, rec.y);
+    const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+    sts32(sa.rec_x + K * 512, __float_as_uint(h));
+    if (lane == 0) sts32(sa.ballots + K * 4, ballot);
+    out[K] = r[(K + 6) & 7];  // column p-2 is final
+    r[(K + 3) & 7] = nx[K];   // column p+3 enters
+}
+
+#define ISING_ATTEMPT(K) \
+    attempt<EXP, K>(r, rec##K, sa, g.pos[p0 + K].z, ps, chunk_seq, p0, P, tm, g.far, lane);
+#define ISING_ATTEMPT_LEAN(K) attempt_lean<EXP, K>(r, out, nx, rec##K, sa, lane);
 
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
@@ -651,6 +686,7 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
     float* hs_g = b.hs + size_t(tile) * n * 32 + lane;
     float* hs_prev = nullptr;
     uint32_t p0 = 0;
+    const uint32_t band_base = smem_u32(g.band_pm);
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
@@ -682,18 +718,36 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 // finished those (it cannot be more than one chunk behind)
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
-                float* rec_x = reinterpret_cast<float*>(s.recs + size_t(st) * kUnroll * 32 + lane);
-                uint32_t* ballots = s.ballots + st * kUnroll;
+                StageAddr sa;
+                sa.rec_x = smem_u32(recs);
+                sa.ballots = smem_u32(s.ballots + st * kUnroll);
+                sa.band = band_base + p0 * 32;
+                const bool careful = (g.pos[p0].z >> 20) & 1u;
                 const float4 rec0 = recs[0 * 32], rec1 = recs[1 * 32], rec2 = recs[2 * 32], rec3 = recs[3 * 32];
                 const float4 rec4 = recs[4 * 32], rec5 = recs[5 * 32], rec6 = recs[6 * 32], rec7 = recs[7 * 32];
-                ISING_ATTEMPT(0)
-                ISING_ATTEMPT(1)
-                ISING_ATTEMPT(2)
-                ISING_ATTEMPT(3)
-                ISING_ATTEMPT(4)
-                ISING_ATTEMPT(5)
-                ISING_ATTEMPT(6)
-                ISING_ATTEMPT(7)
+                if (!careful) {
+                    float nx[kUnroll], out[kUnroll];
+                    tmem_ld8(tm + p0 + 3, nx);  // columns p0+3 .. p0+10: final (see delegated() in batch.cpp)
+                    ISING_ATTEMPT_LEAN(0)
+                    ISING_ATTEMPT_LEAN(1)
+                    ISING_ATTEMPT_LEAN(2)
+                    ISING_ATTEMPT_LEAN(3)
+                    ISING_ATTEMPT_LEAN(4)
+                    ISING_ATTEMPT_LEAN(5)
+                    ISING_ATTEMPT_LEAN(6)
+                    ISING_ATTEMPT_LEAN(7)
+                    tmem_st8(tm + p0 - 2, out);  // columns p0-2 .. p0+5 leave the window
+                } else {
+                    ISING_ATTEMPT(0)
+                    ISING_ATTEMPT(1)
+                    ISING_ATTEMPT(2)
+                    ISING_ATTEMPT(3)
+                    ISING_ATTEMPT(4)
+                    ISING_ATTEMPT(5)
+                    ISING_ATTEMPT(6)
+                    ISING_ATTEMPT(7)
+                    tmem_wait_ld();  // entries requested by the last attempts
+                }
                 // the post warp may now update columns this chunk retired: they must have landed
                 tmem_wait_st();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -717,10 +771,11 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
     __syncwarp();
 }
 #undef ISING_ATTEMPT
+#undef ISING_ATTEMPT_LEAN
 
 template <int EXP>
 __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBatch b, uint32_t sweeps) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 16);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
