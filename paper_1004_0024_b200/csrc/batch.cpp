@@ -39,6 +39,122 @@ void upload(DeviceBuffer& buf, const std::vector<T>& host, size_t& tally, cudaSt
     }
 }
 
+// Host-side image of DevLayerGraph (see device_batch.hpp for the meaning of every array).
+struct HostLayerGraph {
+    std::vector<uint4> pos, band_pm, chunks;
+    std::vector<uint2> far;        // {target position | attempt index in its chunk << 16, bits of 2J}
+    std::vector<uint32_t> groups;  // edge begin | edge count << 16
+};
+
+bool is_band(uint32_t p, uint32_t t) { return (t > p ? t - p : p - t) <= 2; }
+
+uint32_t bits(float v) {
+    uint32_t b;
+    std::memcpy(&b, &v, sizeof b);
+    return b;
+}
+
+HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
+    const uint32_t P = m.per_layer;
+    HostLayerGraph out;
+    out.pos.resize(P);
+    out.band_pm.resize(2 * size_t(P));
+    out.chunks.resize(P / 8);
+    std::vector<uint4>&pos = out.pos, &band_pm = out.band_pm, &chunks = out.chunks;
+    std::vector<uint2>& far = out.far;
+    std::vector<uint32_t>& groups = out.groups;
+        // Far (non-band) edges are split by who applies them.  The FAR warp, which trails the sweep
+    // warp by whole 8-attempt chunks, takes every target the sweep warp is not going to read
+    // soon: backward targets (already out of its register window) and forward targets that
+    // enter the window at least two chunks after the flipping attempt's chunk.  The sweep warp
+    // keeps the NEAR forward targets.  A near target inside the columns the chunk has already
+    // loaded (<= 8c+10) makes the chunk CAREFUL: it runs the per-attempt loop, with per-position
+    // near lists.  Otherwise the chunk is LEAN and applies its near edges, like the far warp,
+    // in groups after its last attempt.
+    const auto delegated = [](uint32_t p, uint32_t t) { return t < p || (t - 3) / 8 >= p / 8 + 2; };
+    struct Edge { uint32_t k, t, j2; };
+    // a group is up to 8 edges with distinct targets, applied with their loads batched
+    // A group is padded to 8 edges when the layer has columns to spare for it: a padding edge
+    // is tied to attempt 8 (no such attempt: nobody accepts it, it adds -0.0) and targets a
+    // column that no real edge of the group uses and that the sweep warp does not write while
+    // the group can be applied (it retires columns up to 8c+13 meanwhile): one at least a chunk
+    // behind chunk c, else one at least three chunks ahead.
+    const auto emit_groups = [&](const std::vector<Edge>& edges, uint32_t chunk) {
+        const uint32_t first_group = uint32_t(groups.size());
+        std::vector<Edge> cur;
+        const auto close = [&]() {
+            if (cur.empty()) return;
+            const uint32_t begin = uint32_t(far.size());
+            std::vector<uint32_t> used;
+            for (const Edge& e : cur) used.push_back(e.t);
+            for (uint32_t col = 0; col < P && cur.size() < 8; ++col) {
+                const bool safe = col + 9 <= 8 * chunk || col >= 8 * chunk + 24;
+                if (!safe || std::find(used.begin(), used.end(), col) != used.end()) continue;
+                cur.push_back({8, col, 0x80000000u});
+                used.push_back(col);
+            }
+            for (const Edge& e : cur) far.push_back(make_uint2(e.t | e.k << 16, e.j2));
+            groups.push_back(begin | uint32_t(cur.size()) << 16);
+            cur.clear();
+        };
+        for (const Edge& e : edges) {
+            const bool clash = std::any_of(cur.begin(), cur.end(), [&](const Edge& o) { return o.t == e.t; });
+            if (cur.size() == 8 || clash) close();
+            cur.push_back(e);
+        }
+        close();
+        return first_group | (uint32_t(groups.size()) - first_group) << 16;
+    };
+    for (uint32_t p0 = 0; p0 < P; p0 += 8) {
+        std::vector<Edge> for_far_warp, near_all;
+        std::vector<std::vector<Edge>> near_of(8);
+        bool careful = p0 == 0 || p0 + 8 >= P;
+        for (uint32_t k = 0; k < 8; ++k) {
+            const uint32_t p = p0 + k;
+            uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
+            for (uint32_t e = m.layer_offsets[p]; e < m.layer_offsets[p + 1]; ++e) {
+                const uint32_t t = m.layer_targets[e];
+                const uint32_t doubled = bits(2.0f * m.layer_couplings[e]);  // exact
+                if (is_band(p, t)) {
+                    const int off = int(t) - int(p);             // -2, -1, +1, +2
+                    const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
+                    j2[slot] = doubled;
+                    mask[slot] = 0;
+                } else if (delegated(p, t)) {
+                    for_far_warp.push_back({k, t, doubled});
+                } else {
+                    near_of[k].push_back({k, t, doubled});
+                    near_all.push_back({k, t, doubled});
+                    careful = careful || t <= p0 + 10;
+                }
+            }
+            const float tau2 = 2.0f * m.layer_tau[p];
+            const float tau2g = tau_scale * tau2;  // f32 product, as gamma * h_tau in the reference
+            pos[p] = make_uint4(bits(tau2g), bits(tau2), 0, 0);
+            // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign
+            // of -s; an empty slot adds -0.0.  Entry 2p is for s = -1 (sign bit of -2*beta*s
+            // clear), entry 2p+1 for s = +1.
+            for (uint32_t neg = 0; neg < 2; ++neg) {
+                const uint32_t flip = neg ? 0x80000000u : 0u;
+                band_pm[2 * size_t(p) + neg] = make_uint4((j2[0] ^ flip) | mask[0], (j2[1] ^ flip) | mask[1],
+                                                         (j2[2] ^ flip) | mask[2], (j2[3] ^ flip) | mask[3]);
+            }
+        }
+        uint32_t near_groups = 0;
+        if (careful) {
+            for (uint32_t k = 0; k < 8; ++k) {
+                pos[p0 + k].z = uint32_t(far.size()) | uint32_t(near_of[k].size()) << 16;
+                for (const Edge& e : near_of[k]) far.push_back(make_uint2(e.t | e.k << 16, e.j2));
+            }
+        } else {
+            near_groups = emit_groups(near_all, p0 / 8);
+        }
+        chunks[p0 / 8] = make_uint4(emit_groups(for_far_warp, p0 / 8), near_groups, careful ? 1u : 0u, 0u);
+    }
+    if (far.size() > 0xffffu || groups.size() > 0xffffu) throw Error("init_state: layer graph too large for the layered kernel");
+    return out;
+}
+
 }  // namespace
 
 void Batch::bind_device() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
@@ -74,26 +190,31 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     if (cfg.kernel < 0 || cfg.kernel > 2) throw Error("invalid kernel value " + std::to_string(cfg.kernel));
     // The layered family needs every model to qualify (HostModel::layered_uniform) and one layer
     // to fit the on-chip window: <= 512 positions (TMEM columns) and the graph within shared memory.
-    uint32_t max_per_layer = 0, max_far_edges = 0;
+    uint32_t max_per_layer = 0, max_far_edges = 0, max_groups = 0;
     bool layered_ok = true;
-    const auto is_band = [](uint32_t p, uint32_t t) { return (t > p ? t - p : p - t) <= 2; };
     for (const HostModel* m : models) {
         layered_ok = layered_ok && m->layered_uniform && m->per_layer % 8 == 0;
         max_per_layer = std::max(max_per_layer, m->per_layer);
         if (!m->layered_uniform) continue;
-        uint32_t far = 0;
         for (uint32_t p = 0; p < m->per_layer; ++p) {
             uint32_t far_here = 0;
             for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
                 far_here += is_band(p, m->layer_targets[e]) ? 0u : 1u;
             }
             layered_ok = layered_ok && far_here < 16;  // 4-bit edge counts in DevLayerGraph::pos
-            far += far_here;
         }
-        max_far_edges = std::max(max_far_edges, far);
+    }
+    std::vector<HostLayerGraph> host_graphs;
+    if (layered_ok && cfg.kernel != int(KernelFamily::generic)) {
+        for (const HostModel* m : models) {
+            host_graphs.push_back(build_layer_graph(*m, cfg.tau_scale));
+            layered_ok = layered_ok && host_graphs.back().far.size() <= 0xffffu && host_graphs.back().groups.size() <= 0xffffu;
+            max_far_edges = std::max(max_far_edges, uint32_t(host_graphs.back().far.size()));
+            max_groups = std::max(max_groups, uint32_t(host_graphs.back().groups.size()));
+        }
     }
     const bool graph_shared = models.size() == 1;
-    const size_t layered_smem = layered_ok ? layered_smem_bytes(max_per_layer, max_far_edges, graph_shared) : 0;
+    const size_t layered_smem = layered_ok ? layered_smem_bytes(max_per_layer, max_far_edges, max_groups, graph_shared) : 0;
     layered_ok = layered_ok && layered_smem != 0;
     if (cfg.kernel == int(KernelFamily::layered) && !layered_ok) {
         throw Error("init_state: the layered kernel needs identical-layer models with equal tau couplings "
@@ -160,82 +281,31 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         if (prop.major != 10) throw CudaError("the layered kernel needs an sm_100 device (tcgen05 tensor memory)");
         sm_count_ = prop.multiProcessorCount;
         std::vector<DevLayerGraph> graphs;
-        const auto bits = [](float v) {
-            uint32_t b;
-            std::memcpy(&b, &v, sizeof b);
-            return b;
-        };
-        for (const HostModel* m : models) {
-            const uint32_t P = m->per_layer;
-            std::vector<uint4> pos(P), band_pm(2 * size_t(P));
-            std::vector<uint2> far;
-            // Far edges are split by who applies them.  The FAR warp, which trails the sweep warp by
-            // whole 8-attempt chunks, takes every target the sweep warp is not going to read soon:
-            // backward targets (already out of its register window) and forward targets that enter the
-            // window at least two chunks after the flipping attempt's chunk.  The sweep warp keeps the
-            // near forward targets; a chunk without any (and not the first or last of the layer) runs
-            // its lean loop, which moves the window in and out of Tensor Memory eight columns at a time.
-            const auto delegated = [](uint32_t p, uint32_t t) { return t < p || (t - 3) / 8 >= p / 8 + 2; };
-            std::vector<uint32_t> near_counts(P, 0);
-            for (uint32_t p = 0; p < P; ++p) {
-                uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
-                std::vector<uint2> for_far_warp;
-                const uint32_t near_begin = uint32_t(far.size());
-                for (uint32_t e = m->layer_offsets[p]; e < m->layer_offsets[p + 1]; ++e) {
-                    const uint32_t t = m->layer_targets[e];
-                    const float doubled = 2.0f * m->layer_couplings[e];  // exact
-                    if (is_band(p, t)) {
-                        const int off = int(t) - int(p);             // -2, -1, +1, +2
-                        const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
-                        j2[slot] = bits(doubled);
-                        mask[slot] = 0;
-                    } else if (delegated(p, t)) {
-                        for_far_warp.push_back(make_uint2(t, bits(doubled)));
-                    } else {
-                        far.push_back(make_uint2(t, bits(doubled)));
-                    }
-                }
-                const uint32_t near_count = uint32_t(far.size()) - near_begin;
-                near_counts[p] = near_count;
-                const uint32_t far_begin = uint32_t(far.size());
-                far.insert(far.end(), for_far_warp.begin(), for_far_warp.end());
-                const float tau2 = 2.0f * m->layer_tau[p];
-                const float tau2g = cfg.tau_scale * tau2;  // f32 product, as gamma * h_tau in the reference
-                pos[p] = make_uint4(bits(tau2g), bits(tau2), near_begin | near_count << 16,
-                                    far_begin | uint32_t(for_far_warp.size()) << 24);
-                // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign of
-                // -s; an empty slot adds -0.0.  Entry 2p is for s = -1 (sign bit of -2*beta*s clear),
-                // entry 2p+1 for s = +1.
-                for (uint32_t neg = 0; neg < 2; ++neg) {
-                    const uint32_t flip = neg ? 0x80000000u : 0u;
-                    band_pm[2 * size_t(p) + neg] = make_uint4((j2[0] ^ flip) | mask[0], (j2[1] ^ flip) | mask[1],
-                                                             (j2[2] ^ flip) | mask[2], (j2[3] ^ flip) | mask[3]);
-                }
-            }
-            // bit 20 of the chunk's first position: the chunk needs the careful (per-attempt) loop
-            for (uint32_t p0 = 0; p0 < P; p0 += 8) {
-                bool careful = p0 == 0 || p0 + 8 >= P;
-                for (uint32_t k = 0; k < 8; ++k) careful = careful || near_counts[p0 + k] != 0;
-                if (careful) pos[p0].z |= 1u << 20;
-            }
+        for (size_t k = 0; k < models.size(); ++k) {
+            HostLayerGraph& hg = host_graphs[k];
             DevLayerGraph g{};
-            g.per_layer = P;
-            g.layers = m->layers;
-            g.n_far = uint32_t(far.size());
-            if (far.empty()) far.push_back(make_uint2(0, 0));
-            g.pos = keep(pos)->as<uint4>();
-            g.band_pm = keep(band_pm)->as<uint4>();
-            g.far = keep(far)->as<uint2>();
+            g.per_layer = models[k]->per_layer;
+            g.layers = models[k]->layers;
+            g.n_far = uint32_t(hg.far.size());
+            g.n_groups = uint32_t(hg.groups.size());
+            if (hg.far.empty()) hg.far.push_back(make_uint2(0, 0));
+            if (hg.groups.empty()) hg.groups.push_back(0);
+            g.pos = keep(hg.pos)->as<uint4>();
+            g.band_pm = keep(hg.band_pm)->as<uint4>();
+            g.chunks = keep(hg.chunks)->as<uint4>();
+            g.groups = keep(hg.groups)->as<uint32_t>();
+            g.far = keep(hg.far)->as<uint2>();
             graphs.push_back(g);
-            cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");  // temporaries die here
         }
+        cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");  // host_graphs die with the constructor
         upload(layer_graphs_, graphs, device_bytes_, stream_);
         cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");
         dev_.layer_graphs = layer_graphs_.as<DevLayerGraph>();
         dev_.max_far_edges = max_far_edges;
+        dev_.max_groups = max_groups;
         dev_.max_per_layer = max_per_layer;
         dev_.graph_shared = graph_shared ? 1u : 0u;
-        dev_.layered_stages = layered_stage_count(max_per_layer, max_far_edges, graph_shared);
+        dev_.layered_stages = layered_stage_count(max_per_layer, max_far_edges, max_groups, graph_shared);
         dev_.layered_smem = uint32_t(layered_smem);
         cuda_check(prepare_layered_kernels(layered_smem), "cudaFuncSetAttribute");
     }

@@ -41,19 +41,25 @@ struct DevLayerGraph {
     uint32_t layers;
     uint32_t n_far;
     // per position: {bits of tau2g, bits of tau2,
-    //                near forward far edges: begin | count << 16 | careful-chunk flag << 20,
-    //                far-warp edges: begin | count << 24}  (indices into `far`)
+    //                near forward edges of a CAREFUL chunk: begin | count << 16 (indices into `far`), 0}
     const uint4* pos;
+    // per chunk of 8 positions: {far-warp groups: begin | count << 16 (indices into `groups`),
+    //                            near groups of a LEAN chunk: begin | count << 16, 1 if careful, 0}
+    const uint4* chunks;
+    // a group is up to 8 edges with distinct targets: edge begin | edge count << 16
+    const uint32_t* groups;
+    uint32_t n_groups;
     // per position two entries (2p: flipped spin was -1, 2p+1: it was +1): what the flip adds to the
     // fields at p-2, p-1, p+1, p+2, i.e. -(2s)*J as bits; an empty slot holds -0.0, the additive
     // identity for every float bit pattern, so it costs no predicate.
     const uint4* band_pm;
-    const uint2* far;  // {position, bits of 2J}
+    const uint2* far;  // {target position | attempt index in its chunk << 16, bits of 2J}
 };
 
 struct DevBatch {
     const DevLayerGraph* layer_graphs;  // per model; nullptr unless the layered family is used
     uint32_t max_far_edges;             // largest n_far over the batch's models
+    uint32_t max_groups;                // largest n_groups over the batch's models
     uint32_t layered_smem;              // dynamic shared memory of one layered-kernel CTA
     uint32_t max_per_layer;             // largest per_layer over the batch's models
     uint32_t graph_shared;              // 1: all tiles use model 0, one shared-memory copy per CTA
@@ -95,8 +101,8 @@ cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_
 // Layered family: needs b.layer_graphs; `sm_count` persistent CTAs of 4 sweep warps.
 cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_count, cudaStream_t stream);
 // Bytes of dynamic shared memory one CTA of the layered kernel needs (0: does not fit).
-size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared);
-uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared);
+size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared);
+uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared);
 cudaError_t prepare_layered_kernels(size_t smem_bytes);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);

@@ -149,14 +149,16 @@ __device__ __forceinline__ void chunk_barrier(uint32_t id) {
 struct GraphSmem {
     uint4* pos;      // P : DevLayerGraph::pos
     uint4* band_pm;  // 2P : DevLayerGraph::band_pm (32-byte aligned: the entry pair of a position)
-    uint2* far;      // max_far
+    uint4* chunks;   // P/8 : DevLayerGraph::chunks
+    uint2* far;      // max_far edges
+    uint32_t* groups;  // max_far groups at most
 };
 struct PairSmem {
     uint2* agree_sign;  // P : per layer, {~(up ^ dn), up} spin words
     uint32_t* words;    // 3 * P : ring of spin-bit layers
     float4* recs;       // stages * 8 * 32 prep records {u | h, -2*beta*s, gamma*h_tau, h_tau}
     uint32_t* ballots;  // stages * 8
-    uint32_t* stage_p0; // stages : chunk start position of the content of every stage
+    uint32_t* signs;    // stages * 32 : per lane, bit k = sign bit of rec.y of the stage's attempt k
 };
 
 // header: tmem slot (16 B) + per pair full[8] + consumed[8] + empty[8] barriers (192 B) x 4
@@ -164,19 +166,23 @@ constexpr size_t kRingBarriers = kSweepWarps * 3 * kMaxStages;
 constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one post-progress counter per pair
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
-__host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far) {
-    return (size_t(P) * 48 + size_t(max_far ? max_far : 1) * 8 + 31) / 32 * 32;  // keeps band_pm pairs 32-byte aligned
+__host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far, uint32_t max_groups) {
+    // pos + band_pm + chunks + far edges + groups; a multiple of 32 keeps band_pm pairs 32-byte aligned
+    return (size_t(P) * 48 + size_t(P) * 2 + size_t(max_far ? max_far : 1) * 8 +
+            size_t(max_groups ? max_groups : 1) * 4 + 31) / 32 * 32;
 }
 __host__ __device__ inline size_t pair_bytes(uint32_t P, uint32_t stages) {
     return align16(size_t(P) * 8) + align16(size_t(P) * 12) + size_t(stages) * kUnroll * 32 * 16 +
-           align16(size_t(stages) * kUnroll * 4) + align16(size_t(stages) * 4);
+           align16(size_t(stages) * kUnroll * 4) + size_t(stages) * 32 * 4;
 }
 
 __device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P) {
     GraphSmem g;
     g.pos = reinterpret_cast<uint4*>(base);
     g.band_pm = g.pos + P;
-    g.far = reinterpret_cast<uint2*>(g.band_pm + 2 * size_t(P));
+    g.chunks = g.band_pm + 2 * size_t(P);
+    g.far = reinterpret_cast<uint2*>(g.chunks + P / 8);
+    g.groups = nullptr;  // set by the caller: it follows the far edges (max_far of them)
     return g;
 }
 __device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P, uint32_t stages) {
@@ -189,7 +195,7 @@ __device__ __forceinline__ PairSmem carve_pair(unsigned char* base, uint32_t P, 
     base += size_t(stages) * kUnroll * 32 * 16;
     s.ballots = reinterpret_cast<uint32_t*>(base);
     base += align16(size_t(stages) * kUnroll * 4);
-    s.stage_p0 = reinterpret_cast<uint32_t*>(base);
+    s.signs = reinterpret_cast<uint32_t*>(base);
     return s;
 }
 
@@ -200,7 +206,9 @@ __device__ __forceinline__ void load_graph(const GraphSmem& dst, const DevLayerG
         dst.band_pm[2 * k] = g.band_pm[2 * k];
         dst.band_pm[2 * k + 1] = g.band_pm[2 * k + 1];
     }
+    for (uint32_t k = tid; k < g.per_layer / 8; k += nthreads) dst.chunks[k] = g.chunks[k];
     for (uint32_t k = tid; k < g.n_far; k += nthreads) dst.far[k] = g.far[k];
+    for (uint32_t k = tid; k < g.n_groups; k += nthreads) dst.groups[k] = g.groups[k];
 }
 
 __device__ __forceinline__ void words_copy(uint32_t* dst, const uint32_t* src, uint32_t P, uint32_t lane) {
@@ -317,6 +325,7 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
                     cursor.waited();
                 }
                 uint32_t raw[kUnroll];
+                uint32_t signs = 0;
                 mt_generate8(h, raw);
                 mt_load_operands(h);  // operands of the next chunk: in flight while this one is prepared
 #pragma unroll
@@ -332,11 +341,13 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
                     rec.x = h.active ? u32_to_unit(raw[k]) : 2.0f;  // padding lanes never accept
                     // x = -beta*((2s)*v) == (-2*beta*s)*v: doubling is exact, one rounding either way
                     rec.y = __uint_as_float(h.nb2 ^ sgn_s);
+                    signs |= ((h.nb2 ^ sgn_s) >> 31) << k;
                     // tau field J*(s_up + s_dn) in {+2J, +0, -2J}: scaled by gamma, and raw
                     rec.z = __uint_as_float((tau.x ^ sgn_up) & agree);
                     rec.w = __uint_as_float((tau.y ^ sgn_up) & agree);
                     recs[k * 32] = rec;
                 }
+                s.signs[st * 32 + lane] = signs;
                 in_flight |= 1u << st;
                 mbar_arrive(&full[st]);
                 cursor.advance(stages);
@@ -473,6 +484,69 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
     __syncwarp();
 }
 
+// Applies the edge groups `ginfo` (begin | count << 16) of one finished chunk: h[t] -= (2s)*J for
+// every lane that accepted attempt k of the chunk, as Tensor Memory read-modify-writes on column t.
+// The targets of a group are distinct, so its loads go out together; all 32 lanes move data, a lane
+// that did not accept adds -0.0.  Groups are normally padded to 8 edges (the padding targets a
+// column nobody else writes meanwhile and belongs to no attempt that can accept: see batch.cpp).
+// `signs_addr`/`ballots_addr` are the chunk's stage (this lane's sign word, the 8 ballots).
+__device__ __forceinline__ uint32_t edge_addend(uint2 e, uint32_t acc_neg) {
+    // acc_neg: bit k = this lane accepted attempt k; bit 16+k = sign bit of rec.y = -2*beta*s, which
+    // is the sign of the addend -(2s)*J relative to 2J
+    const uint32_t t = acc_neg >> (e.x >> 16);
+    const uint32_t add = ((t << 15) & 0x80000000u) ^ e.y;
+    return (t & 1u) ? add : 0x80000000u;
+}
+__device__ __forceinline__ void apply_groups(uint32_t tm, const GraphSmem& g, uint32_t ginfo, uint32_t signs_addr,
+                                             uint32_t ballots_addr, uint32_t lane) {
+    uint32_t acc_neg;
+    {
+        uint4 b0, b1;
+        uint32_t neg;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b0.x), "=r"(b0.y), "=r"(b0.z), "=r"(b0.w) : "r"(ballots_addr) : "memory");
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b1.x), "=r"(b1.y), "=r"(b1.z), "=r"(b1.w) : "r"(ballots_addr + 16) : "memory");
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(neg) : "r"(signs_addr) : "memory");
+        const uint32_t bl[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        acc_neg = neg << 16;
+#pragma unroll
+        for (uint32_t k = 0; k < kUnroll; ++k) acc_neg |= ((bl[k] >> lane) & 1u) << k;
+    }
+    const uint32_t* grp = g.groups + (ginfo & 0xffffu);
+    const uint32_t n_groups = ginfo >> 16;
+#pragma unroll 1
+    for (uint32_t q = 0; q < n_groups; ++q) {
+        const uint32_t info = grp[q];
+        const uint2* fe = g.far + (info & 0xffffu);
+        const uint32_t n = info >> 16;
+        if (n == kUnroll) {
+            uint2 e[kUnroll];
+            float v[kUnroll];
+#pragma unroll
+            for (uint32_t i = 0; i < kUnroll; ++i) e[i] = fe[i];
+#pragma unroll
+            for (uint32_t i = 0; i < kUnroll; ++i) v[i] = tmem_ld(tm + (e[i].x & 0xffffu));
+            tmem_wait_ld();
+#pragma unroll
+            for (uint32_t i = 0; i < kUnroll; ++i) {
+                tmem_st(tm + (e[i].x & 0xffffu), __fadd_rn(v[i], __uint_as_float(edge_addend(e[i], acc_neg))));
+            }
+        } else {  // unpadded group (layers too short to find padding columns): one edge at a time
+#pragma unroll 1
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint2 e = fe[i];
+                const float v = tmem_ld(tm + (e.x & 0xffffu));
+                tmem_wait_ld();
+                tmem_st(tm + (e.x & 0xffffu), __fadd_rn(v, __uint_as_float(edge_addend(e, acc_neg))));
+            }
+        }
+        tmem_wait_st();  // the next group may hit one of these columns again
+    }
+}
+__device__ __noinline__ void apply_groups_outlined(uint32_t tm, const GraphSmem& g, uint32_t ginfo, uint32_t signs_addr,
+                                                   uint32_t ballots_addr, uint32_t lane) {
+    apply_groups(tm, g, ginfo, signs_addr, ballots_addr, lane);
+}
+
 // Far: applies the far-neighbour updates the sweep warp does not need soon — every BACKWARD target
 // (its column left the register window before the flipping attempt ran) and every FORWARD target
 // that enters the window at least two chunks later.  It trails the sweep warp by whole chunks,
@@ -493,41 +567,11 @@ __device__ void far_warp(float* hs_g, uint32_t sweeps, uint32_t lane, const Grap
                 const uint32_t st = cursor.stage;
                 chunk_barrier(bar_id);  // the sweep warp has finished this chunk
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const float* rec_y = reinterpret_cast<const float*>(s.recs + size_t(st) * kUnroll * 32 + lane) + 1;
-                const uint32_t* ballots = s.ballots + st * kUnroll;
-                bool stored = false;
-#pragma unroll 1
-                for (uint32_t k = 0; k < kUnroll; ++k) {
-                    const uint32_t ballot = ballots[k];
-                    const uint32_t info = g.pos[p0 + k].w;
-                    const uint32_t count = info >> 24;
-                    if (count == 0u || ballot == 0u) continue;
-                    const bool mine = (ballot >> lane) & 1u;
-                    const uint32_t neg_d = __float_as_uint(rec_y[k * 128]) & 0x80000000u;
-                    const uint2* fe = g.far + (info & 0xffffffu);
-                    if (stored) tmem_wait_st();  // an earlier attempt of this stage may have hit the same column
-                    // the targets of one attempt are distinct: load them together (first two), then store
-                    const uint2 e0 = fe[0];
-                    const uint2 e1 = fe[count > 1u ? 1 : 0];
-                    const float v0 = tmem_ld(tm + e0.x);
-                    float v1 = 0.0f;
-                    if (count > 1u) v1 = tmem_ld(tm + e1.x);
-                    tmem_wait_ld();
-                    const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
-                    const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
-                    tmem_st(tm + e0.x, mine ? n0 : v0);
-                    if (count > 1u) tmem_st(tm + e1.x, mine ? n1 : v1);
-#pragma unroll 1
-                    for (uint32_t e = 2; e < count; ++e) {
-                        const uint2 ed = fe[e];
-                        const float v = tmem_ld(tm + ed.x);
-                        tmem_wait_ld();
-                        const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
-                        tmem_st(tm + ed.x, mine ? nv : v);
-                    }
-                    stored = true;
+                const uint32_t ginfo = g.chunks[p0 / kUnroll].x;
+                if ((ginfo >> 16) != 0u) {
+                    apply_groups(tm, g, ginfo, smem_u32(s.signs + st * 32 + lane), smem_u32(s.ballots + st * kUnroll),
+                                 lane);
                 }
-                if (stored) tmem_wait_st();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);
@@ -557,21 +601,23 @@ __device__ __noinline__ void far_update(uint32_t tm, const uint2* fe, uint32_t f
     tmem_wait_st();  // a column retired by an earlier attempt may be a target
     const uint2 e0 = fe[0];
     const uint2 e1 = fe[far_count > 1u ? 1 : 0];
-    const float v0 = tmem_ld(tm + e0.x);
+    const uint32_t c0 = tm + (e0.x & 0xffffu), c1 = tm + (e1.x & 0xffffu);
+    const float v0 = tmem_ld(c0);
     float v1 = 0.0f;
-    if (far_count > 1u) v1 = tmem_ld(tm + e1.x);
+    if (far_count > 1u) v1 = tmem_ld(c1);
     tmem_wait_ld();
     const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
     const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
-    tmem_st(tm + e0.x, accept ? n0 : v0);
-    if (far_count > 1u) tmem_st(tm + e1.x, accept ? n1 : v1);
+    tmem_st(c0, accept ? n0 : v0);
+    if (far_count > 1u) tmem_st(c1, accept ? n1 : v1);
 #pragma unroll 1
     for (uint32_t e = 2; e < far_count; ++e) {
         const uint2 ed = fe[e];
-        const float v = tmem_ld(tm + ed.x);
+        const uint32_t c = tm + (ed.x & 0xffffu);
+        const float v = tmem_ld(c);
         tmem_wait_ld();
         const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
-        tmem_st(tm + ed.x, accept ? nv : v);
+        tmem_st(c, accept ? nv : v);
     }
     tmem_wait_st();  // a target may be the next column to enter the window
 }
@@ -722,7 +768,8 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 sa.rec_x = smem_u32(recs);
                 sa.ballots = smem_u32(s.ballots + st * kUnroll);
                 sa.band = band_base + p0 * 32;
-                const bool careful = (g.pos[p0].z >> 20) & 1u;
+                const uint4 chunk_info = g.chunks[p0 / kUnroll];
+                const bool careful = chunk_info.z != 0u;
                 const float4 rec0 = recs[0 * 32], rec1 = recs[1 * 32], rec2 = recs[2 * 32], rec3 = recs[3 * 32];
                 const float4 rec4 = recs[4 * 32], rec5 = recs[5 * 32], rec6 = recs[6 * 32], rec7 = recs[7 * 32];
                 if (!careful) {
@@ -736,6 +783,13 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                     ISING_ATTEMPT_LEAN(5)
                     ISING_ATTEMPT_LEAN(6)
                     ISING_ATTEMPT_LEAN(7)
+                    if ((chunk_info.y >> 16) != 0u) {
+                        // near forward targets (columns 8c+11 .. 8c+18, not loaded yet): the far warp may
+                        // still owe them updates from the chunk before this one, which must land first
+                        __syncwarp();
+                        wait_post(ps, chunk_seq);
+                        apply_groups_outlined(tm, g, chunk_info.y, smem_u32(s.signs + st * 32 + lane), sa.ballots, lane);
+                    }
                     tmem_st8(tm + p0 - 2, out);  // columns p0-2 .. p0+5 leave the window
                 } else {
                     ISING_ATTEMPT(0)
@@ -788,11 +842,12 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
 
     const uint32_t maxP = b.max_per_layer;
     const uint32_t stages = b.layered_stages;
-    const size_t gbytes = graph_bytes(maxP, b.max_far_edges);
+    const size_t gbytes = graph_bytes(maxP, b.max_far_edges, b.max_groups);
     unsigned char* graph_base = smem_raw + kHeaderBytes + (b.graph_shared ? 0 : size_t(pair) * gbytes);
     unsigned char* pair_base = smem_raw + kHeaderBytes + (b.graph_shared ? 1 : kSweepWarps) * gbytes +
                                size_t(pair) * pair_bytes(maxP, stages);
-    const GraphSmem gs = carve_graph(graph_base, maxP);
+    GraphSmem gs = carve_graph(graph_base, maxP);
+    gs.groups = reinterpret_cast<uint32_t*>(gs.far + (b.max_far_edges ? b.max_far_edges : 1));
     const PairSmem s = carve_pair(pair_base, maxP, stages);
 
     if (warp == 0) tmem_alloc(tmem_slot, kTmemColumns);
@@ -846,9 +901,10 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
 }  // namespace
 
 // Ring depth: 8 stages when they fit, otherwise 4 (multi-model batches keep a graph copy per pair).
-static uint32_t pick_stages(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared, size_t* bytes_out) {
+static uint32_t pick_stages(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared,
+                            size_t* bytes_out) {
     for (uint32_t stages : {8u, 4u, 2u}) {
-        const size_t bytes = kHeaderBytes + (graph_shared ? 1 : kSweepWarps) * graph_bytes(per_layer, max_far_edges) +
+        const size_t bytes = kHeaderBytes + (graph_shared ? 1 : kSweepWarps) * graph_bytes(per_layer, max_far_edges, max_groups) +
                              kSweepWarps * pair_bytes(per_layer, stages);
         if (bytes <= 227 * 1024) {
             *bytes_out = bytes;
@@ -859,16 +915,16 @@ static uint32_t pick_stages(uint32_t per_layer, uint32_t max_far_edges, bool gra
     return 0;
 }
 
-size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared) {
+size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared) {
     if (per_layer == 0 || per_layer > kTmemColumns || per_layer % kUnroll != 0) return 0;
     size_t bytes = 0;
-    pick_stages(per_layer, max_far_edges, graph_shared, &bytes);
+    pick_stages(per_layer, max_far_edges, max_groups, graph_shared, &bytes);
     return bytes;
 }
 
-uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, bool graph_shared) {
+uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared) {
     size_t bytes = 0;
-    return pick_stages(per_layer, max_far_edges, graph_shared, &bytes);
+    return pick_stages(per_layer, max_far_edges, max_groups, graph_shared, &bytes);
 }
 
 cudaError_t prepare_layered_kernels(size_t smem_bytes) {
