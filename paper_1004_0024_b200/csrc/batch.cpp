@@ -79,7 +79,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
     // column that no real edge of the group uses and that the sweep warp does not write while
     // the group can be applied (it retires columns up to 8c+13 meanwhile): one at least a chunk
     // behind chunk c, else one at least three chunks ahead.
-    const auto emit_groups = [&](const std::vector<Edge>& edges, uint32_t chunk) {
+    const auto emit_groups = [&](const std::vector<Edge>& edges, uint32_t chunk, bool pad) {
         const uint32_t first_group = uint32_t(groups.size());
         std::vector<Edge> cur;
         const auto close = [&]() {
@@ -87,7 +87,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
             const uint32_t begin = uint32_t(far.size());
             std::vector<uint32_t> used;
             for (const Edge& e : cur) used.push_back(e.t);
-            for (uint32_t col = 0; col < P && cur.size() < 8; ++col) {
+            for (uint32_t col = 0; pad && col < P && cur.size() < 8; ++col) {
                 const bool safe = col + 9 <= 8 * chunk || col >= 8 * chunk + 24;
                 if (!safe || std::find(used.begin(), used.end(), col) != used.end()) continue;
                 cur.push_back({8, col, 0x80000000u});
@@ -108,7 +108,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
     for (uint32_t p0 = 0; p0 < P; p0 += 8) {
         std::vector<Edge> for_far_warp, near_all;
         std::vector<std::vector<Edge>> near_of(8);
-        bool careful = p0 == 0 || p0 + 8 >= P;
+        bool careful = false;
         for (uint32_t k = 0; k < 8; ++k) {
             const uint32_t p = p0 + k;
             uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
@@ -147,9 +147,9 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
                 for (const Edge& e : near_of[k]) far.push_back(make_uint2(e.t | e.k << 16, e.j2));
             }
         } else {
-            near_groups = emit_groups(near_all, p0 / 8);
+            near_groups = emit_groups(near_all, p0 / 8, false);  // rare and short: not worth padding
         }
-        chunks[p0 / 8] = make_uint4(emit_groups(for_far_warp, p0 / 8), near_groups, careful ? 1u : 0u, 0u);
+        chunks[p0 / 8] = make_uint4(emit_groups(for_far_warp, p0 / 8, true), near_groups, careful ? 1u : 0u, 0u);
     }
     if (far.size() > 0xffffu || groups.size() > 0xffffu) throw Error("init_state: layer graph too large for the layered kernel");
     return out;

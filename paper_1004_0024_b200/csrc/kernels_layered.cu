@@ -309,6 +309,8 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
             const uint32_t* w_cur = s.words + slot_cur * P;
+            // the words of layer l+2 are read at the end of this layer: have them in L2 by then
+            if (lane * 32 < P) prefetch_l2(words_g + size_t((l + 2) % L) * P + lane * 32);
             {   // the tau field of this whole layer is fixed while it is swept: previous layer already
                 // visited, next layer not yet.  agree = neighbours equal, sign = their common spin bit.
                 const uint32_t* w_up = s.words + slot_up * P;
@@ -774,7 +776,14 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 const float4 rec4 = recs[4 * 32], rec5 = recs[5 * 32], rec6 = recs[6 * 32], rec7 = recs[7 * 32];
                 if (!careful) {
                     float nx[kUnroll], out[kUnroll];
-                    tmem_ld8(tm + p0 + 3, nx);  // columns p0+3 .. p0+10: final (see delegated() in batch.cpp)
+                    // columns p0+3 .. p0+10 enter: final by now (see delegated() in batch.cpp); the last
+                    // chunk of a layer has only five left
+                    if (p0 + kUnroll < P) {
+                        tmem_ld8(tm + p0 + 3, nx);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < int(kUnroll); ++k) nx[k] = k < 5 ? tmem_ld(tm + p0 + 3 + k) : 0.0f;
+                    }
                     ISING_ATTEMPT_LEAN(0)
                     ISING_ATTEMPT_LEAN(1)
                     ISING_ATTEMPT_LEAN(2)
@@ -790,7 +799,13 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                         wait_post(ps, chunk_seq);
                         apply_groups_outlined(tm, g, chunk_info.y, smem_u32(s.signs + st * 32 + lane), sa.ballots, lane);
                     }
-                    tmem_st8(tm + p0 - 2, out);  // columns p0-2 .. p0+5 leave the window
+                    // columns p0-2 .. p0+5 leave the window (the first chunk has no p0-2, p0-1)
+                    if (p0 != 0) {
+                        tmem_st8(tm + p0 - 2, out);
+                    } else {
+#pragma unroll
+                        for (int k = 2; k < int(kUnroll); ++k) tmem_st(tm + k - 2, out[k]);
+                    }
                 } else {
                     ISING_ATTEMPT(0)
                     ISING_ATTEMPT(1)
