@@ -42,7 +42,7 @@ void upload(DeviceBuffer& buf, const std::vector<T>& host, size_t& tally, cudaSt
 // Host-side image of DevLayerGraph (see device_batch.hpp for the meaning of every array).
 struct HostLayerGraph {
     std::vector<uint4> pos, band_pm, chunks;
-    std::vector<uint2> far;        // {target position | attempt index in its chunk << 16, bits of 2J}
+    std::vector<uint4> far;        // {target position, 7 - attempt index in its chunk, bits of 2J, 0}
     std::vector<uint32_t> groups;  // edge begin | edge count << 16
 };
 
@@ -61,7 +61,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
     out.band_pm.resize(2 * size_t(P));
     out.chunks.resize(P / 8);
     std::vector<uint4>&pos = out.pos, &band_pm = out.band_pm, &chunks = out.chunks;
-    std::vector<uint2>& far = out.far;
+    std::vector<uint4>& far = out.far;
     std::vector<uint32_t>& groups = out.groups;
         // Far (non-band) edges are split by who applies them.  The FAR warp, which trails the sweep
     // warp by whole 8-attempt chunks, takes every target the sweep warp is not going to read
@@ -93,7 +93,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
                 cur.push_back({8, col, 0x80000000u});
                 used.push_back(col);
             }
-            for (const Edge& e : cur) far.push_back(make_uint2(e.t | e.k << 16, e.j2));
+            for (const Edge& e : cur) far.push_back(make_uint4(e.t, e.k < 8 ? 7u - e.k : 15u, e.j2, 0u));  // shift 15: a bit nobody sets
             groups.push_back(begin | uint32_t(cur.size()) << 16);
             cur.clear();
         };
@@ -144,7 +144,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
         if (careful) {
             for (uint32_t k = 0; k < 8; ++k) {
                 pos[p0 + k].z = uint32_t(far.size()) | uint32_t(near_of[k].size()) << 16;
-                for (const Edge& e : near_of[k]) far.push_back(make_uint2(e.t | e.k << 16, e.j2));
+                for (const Edge& e : near_of[k]) far.push_back(make_uint4(e.t, e.k < 8 ? 7u - e.k : 15u, e.j2, 0u));  // shift 15: a bit nobody sets
             }
         } else {
             near_groups = emit_groups(near_all, p0 / 8, false);  // rare and short: not worth padding
@@ -288,13 +288,13 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             g.layers = models[k]->layers;
             g.n_far = uint32_t(hg.far.size());
             g.n_groups = uint32_t(hg.groups.size());
-            if (hg.far.empty()) hg.far.push_back(make_uint2(0, 0));
+            if (hg.far.empty()) hg.far.push_back(make_uint4(0, 0, 0, 0));
             if (hg.groups.empty()) hg.groups.push_back(0);
             g.pos = keep(hg.pos)->as<uint4>();
             g.band_pm = keep(hg.band_pm)->as<uint4>();
             g.chunks = keep(hg.chunks)->as<uint4>();
             g.groups = keep(hg.groups)->as<uint32_t>();
-            g.far = keep(hg.far)->as<uint2>();
+            g.far = keep(hg.far)->as<uint4>();
             graphs.push_back(g);
         }
         cuda_check(cudaStreamSynchronize(stream_), "upload layer graphs");  // host_graphs die with the constructor

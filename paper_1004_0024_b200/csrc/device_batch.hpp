@@ -53,7 +53,7 @@ struct DevLayerGraph {
     // fields at p-2, p-1, p+1, p+2, i.e. -(2s)*J as bits; an empty slot holds -0.0, the additive
     // identity for every float bit pattern, so it costs no predicate.
     const uint4* band_pm;
-    const uint2* far;  // {target position | attempt index in its chunk << 16, bits of 2J}
+    const uint4* far;  // {target position, 7 - attempt index in its chunk, bits of 2J, 0}
 };
 
 struct DevBatch {

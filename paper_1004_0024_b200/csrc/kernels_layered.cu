@@ -150,7 +150,7 @@ struct GraphSmem {
     uint4* pos;      // P : DevLayerGraph::pos
     uint4* band_pm;  // 2P : DevLayerGraph::band_pm (32-byte aligned: the entry pair of a position)
     uint4* chunks;   // P/8 : DevLayerGraph::chunks
-    uint2* far;      // max_far edges
+    uint4* far;      // max_far edges
     uint32_t* groups;  // max_far groups at most
 };
 struct PairSmem {
@@ -158,7 +158,7 @@ struct PairSmem {
     uint32_t* words;    // 3 * P : ring of spin-bit layers
     float4* recs;       // stages * 8 * 32 prep records {u | h, -2*beta*s, gamma*h_tau, h_tau}
     uint32_t* ballots;  // stages * 8
-    uint32_t* signs;    // stages * 32 : per lane, bit k = sign bit of rec.y of the stage's attempt k
+    uint32_t* signs;    // stages * 32 : per lane, bit 7-k set <=> the spin of the stage's attempt k was -1
 };
 
 // header: tmem slot (16 B) + per pair full[8] + consumed[8] + empty[8] barriers (192 B) x 4
@@ -168,7 +168,7 @@ constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one post-prog
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far, uint32_t max_groups) {
     // pos + band_pm + chunks + far edges + groups; a multiple of 32 keeps band_pm pairs 32-byte aligned
-    return (size_t(P) * 48 + size_t(P) * 2 + size_t(max_far ? max_far : 1) * 8 +
+    return (size_t(P) * 48 + size_t(P) * 2 + size_t(max_far ? max_far : 1) * 16 +
             size_t(max_groups ? max_groups : 1) * 4 + 31) / 32 * 32;
 }
 __host__ __device__ inline size_t pair_bytes(uint32_t P, uint32_t stages) {
@@ -181,7 +181,7 @@ __device__ __forceinline__ GraphSmem carve_graph(unsigned char* base, uint32_t P
     g.pos = reinterpret_cast<uint4*>(base);
     g.band_pm = g.pos + P;
     g.chunks = g.band_pm + 2 * size_t(P);
-    g.far = reinterpret_cast<uint2*>(g.chunks + P / 8);
+    g.far = g.chunks + P / 8;
     g.groups = nullptr;  // set by the caller: it follows the far edges (max_far of them)
     return g;
 }
@@ -291,7 +291,8 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
     ProducerState h;
     h.active = lane < b.tile_count[tile];
     h.nb2 = __float_as_uint(h.active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
-    h.sh = 31u - lane;
+    h.sh = 1u << (31u - lane);  // word * sh moves this lane's bit to bit 31 (a multiply: FMA pipe, not ALU)
+    const float u_offset = h.active ? 0.0f : 2.0f;  // padding lanes draw u >= 2: they never accept
     h.mt = b.mt + size_t(tile) * kMtN * 32 + lane;
     h.pos = b.mt_pos[tile];
     h.cur = h.mt[size_t(h.pos) * 32];
@@ -336,14 +337,15 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
                     const uint32_t word = w_cur[p];
                     const uint2 as = s.agree_sign[p];
                     const uint2 tau = *reinterpret_cast<const uint2*>(g.pos + p);
-                    const uint32_t sgn_s = (word << h.sh) & 0x80000000u;  // sign bit set <=> s = -1
-                    const uint32_t sgn_up = (as.y << h.sh) & 0x80000000u;
-                    const uint32_t agree = uint32_t(int32_t(as.x << h.sh) >> 31);  // ones when s_up == s_dn
+                    const uint32_t spin_top = word * h.sh;  // bit 31 set <=> s = -1 (lower bits: other lanes)
+                    const uint32_t sgn_up = (as.y * h.sh) & 0x80000000u;
+                    const uint32_t agree = uint32_t(int32_t(as.x * h.sh) >> 31);  // ones when s_up == s_dn
                     float4 rec;
-                    rec.x = h.active ? u32_to_unit(raw[k]) : 2.0f;  // padding lanes never accept
+                    // u32_to_unit (x * 2^-32 is exact, so is adding +0); padding lanes get u + 2
+                    rec.x = __fmaf_rn(__uint2float_rz(raw[k]), 0x1p-32f, u_offset);
                     // x = -beta*((2s)*v) == (-2*beta*s)*v: doubling is exact, one rounding either way
-                    rec.y = __uint_as_float(h.nb2 ^ sgn_s);
-                    signs |= ((h.nb2 ^ sgn_s) >> 31) << k;
+                    rec.y = __uint_as_float(h.nb2 ^ (spin_top & 0x80000000u));
+                    signs = __funnelshift_l(spin_top, signs, 1);  // attempt k ends up at bit 7-k
                     // tau field J*(s_up + s_dn) in {+2J, +0, -2J}: scaled by gamma, and raw
                     rec.z = __uint_as_float((tau.x ^ sgn_up) & agree);
                     rec.w = __uint_as_float((tau.y ^ sgn_up) & agree);
@@ -492,11 +494,11 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
 // that did not accept adds -0.0.  Groups are normally padded to 8 edges (the padding targets a
 // column nobody else writes meanwhile and belongs to no attempt that can accept: see batch.cpp).
 // `signs_addr`/`ballots_addr` are the chunk's stage (this lane's sign word, the 8 ballots).
-__device__ __forceinline__ uint32_t edge_addend(uint2 e, uint32_t acc_neg) {
-    // acc_neg: bit k = this lane accepted attempt k; bit 16+k = sign bit of rec.y = -2*beta*s, which
-    // is the sign of the addend -(2s)*J relative to 2J
-    const uint32_t t = acc_neg >> (e.x >> 16);
-    const uint32_t add = ((t << 15) & 0x80000000u) ^ e.y;
+__device__ __forceinline__ uint32_t edge_addend(uint4 e, uint32_t acc_neg) {
+    // e = {column, 7 - attempt index, bits of 2J, 0}.  acc_neg: bit 7-k = this lane accepted attempt
+    // k; bit 16+7-k = sign bit of rec.y = -2*beta*s, the sign of the addend -(2s)*J relative to 2J
+    const uint32_t t = acc_neg >> e.y;
+    const uint32_t add = ((t << 15) & 0x80000000u) ^ e.z;
     return (t & 1u) ? add : 0x80000000u;
 }
 __device__ __forceinline__ void apply_groups(uint32_t tm, const GraphSmem& g, uint32_t ginfo, uint32_t signs_addr,
@@ -504,41 +506,43 @@ __device__ __forceinline__ void apply_groups(uint32_t tm, const GraphSmem& g, ui
     uint32_t acc_neg;
     {
         uint4 b0, b1;
-        uint32_t neg;
+        uint32_t spins;
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b0.x), "=r"(b0.y), "=r"(b0.z), "=r"(b0.w) : "r"(ballots_addr) : "memory");
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(b1.x), "=r"(b1.y), "=r"(b1.z), "=r"(b1.w) : "r"(ballots_addr + 16) : "memory");
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(neg) : "r"(signs_addr) : "memory");
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(spins) : "r"(signs_addr) : "memory");
         const uint32_t bl[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        acc_neg = neg << 16;
+        // rec.y = -2*beta*s is negative for s = +1, i.e. where the spin bit is clear (an accepting
+        // lane is never a padding lane, whose -2*beta is +0)
+        acc_neg = (~spins & 0xffu) << 16;
 #pragma unroll
-        for (uint32_t k = 0; k < kUnroll; ++k) acc_neg |= ((bl[k] >> lane) & 1u) << k;
+        for (uint32_t k = 0; k < kUnroll; ++k) acc_neg |= ((bl[k] >> lane) & 1u) << (7u - k);
     }
     const uint32_t* grp = g.groups + (ginfo & 0xffffu);
     const uint32_t n_groups = ginfo >> 16;
 #pragma unroll 1
     for (uint32_t q = 0; q < n_groups; ++q) {
         const uint32_t info = grp[q];
-        const uint2* fe = g.far + (info & 0xffffu);
+        const uint4* fe = g.far + (info & 0xffffu);
         const uint32_t n = info >> 16;
         if (n == kUnroll) {
-            uint2 e[kUnroll];
+            uint4 e[kUnroll];
             float v[kUnroll];
 #pragma unroll
             for (uint32_t i = 0; i < kUnroll; ++i) e[i] = fe[i];
 #pragma unroll
-            for (uint32_t i = 0; i < kUnroll; ++i) v[i] = tmem_ld(tm + (e[i].x & 0xffffu));
+            for (uint32_t i = 0; i < kUnroll; ++i) v[i] = tmem_ld(tm + e[i].x);
             tmem_wait_ld();
 #pragma unroll
             for (uint32_t i = 0; i < kUnroll; ++i) {
-                tmem_st(tm + (e[i].x & 0xffffu), __fadd_rn(v[i], __uint_as_float(edge_addend(e[i], acc_neg))));
+                tmem_st(tm + e[i].x, __fadd_rn(v[i], __uint_as_float(edge_addend(e[i], acc_neg))));
             }
-        } else {  // unpadded group (layers too short to find padding columns): one edge at a time
+        } else {  // unpadded group (near groups; layers too short to find padding columns): one edge at a time
 #pragma unroll 1
             for (uint32_t i = 0; i < n; ++i) {
-                const uint2 e = fe[i];
-                const float v = tmem_ld(tm + (e.x & 0xffffu));
+                const uint4 e = fe[i];
+                const float v = tmem_ld(tm + e.x);
                 tmem_wait_ld();
-                tmem_st(tm + (e.x & 0xffffu), __fadd_rn(v, __uint_as_float(edge_addend(e, acc_neg))));
+                tmem_st(tm + e.x, __fadd_rn(v, __uint_as_float(edge_addend(e, acc_neg))));
             }
         }
         tmem_wait_st();  // the next group may hit one of these columns again
@@ -598,27 +602,27 @@ __device__ void far_warp(float* hs_g, uint32_t sweeps, uint32_t lane, const Grap
 // =======================================================================================
 // Far neighbours of a flipped spin: h[t] -= (2s)*J as a Tensor Memory read-modify-write on column t
 // (the first two with their loads batched).  All 32 lanes move data; only accepting lanes change it.
-__device__ __noinline__ void far_update(uint32_t tm, const uint2* fe, uint32_t far_count, uint32_t neg_d,
+__device__ __noinline__ void far_update(uint32_t tm, const uint4* fe, uint32_t far_count, uint32_t neg_d,
                                         bool accept) {
     tmem_wait_st();  // a column retired by an earlier attempt may be a target
-    const uint2 e0 = fe[0];
-    const uint2 e1 = fe[far_count > 1u ? 1 : 0];
-    const uint32_t c0 = tm + (e0.x & 0xffffu), c1 = tm + (e1.x & 0xffffu);
+    const uint4 e0 = fe[0];
+    const uint4 e1 = fe[far_count > 1u ? 1 : 0];
+    const uint32_t c0 = tm + e0.x, c1 = tm + e1.x;
     const float v0 = tmem_ld(c0);
     float v1 = 0.0f;
     if (far_count > 1u) v1 = tmem_ld(c1);
     tmem_wait_ld();
-    const float n0 = __fadd_rn(v0, __uint_as_float(e0.y ^ neg_d));
-    const float n1 = __fadd_rn(v1, __uint_as_float(e1.y ^ neg_d));
+    const float n0 = __fadd_rn(v0, __uint_as_float(e0.z ^ neg_d));
+    const float n1 = __fadd_rn(v1, __uint_as_float(e1.z ^ neg_d));
     tmem_st(c0, accept ? n0 : v0);
     if (far_count > 1u) tmem_st(c1, accept ? n1 : v1);
 #pragma unroll 1
     for (uint32_t e = 2; e < far_count; ++e) {
-        const uint2 ed = fe[e];
-        const uint32_t c = tm + (ed.x & 0xffffu);
+        const uint4 ed = fe[e];
+        const uint32_t c = tm + ed.x;
         const float v = tmem_ld(c);
         tmem_wait_ld();
-        const float nv = __fadd_rn(v, __uint_as_float(ed.y ^ neg_d));
+        const float nv = __fadd_rn(v, __uint_as_float(ed.z ^ neg_d));
         tmem_st(c, accept ? nv : v);
     }
     tmem_wait_st();  // a target may be the next column to enter the window
@@ -681,7 +685,7 @@ struct StageAddr {
 template <int EXP, int K>
 __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, const StageAddr& sa, uint32_t far_info,
                                         PostSync& ps, uint32_t chunks_before, uint32_t p0, uint32_t P, uint32_t tm,
-                                        const uint2* far, uint32_t lane) {
+                                        const uint4* far, uint32_t lane) {
     const float h = r[K];
     const bool accept = decide<EXP>(h, rec);
     tmem_wait_ld();  // the entry for p+2 was requested right after the previous attempt
