@@ -448,6 +448,7 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
     const bool active = lane < b.tile_count[tile];
     double e_run = active ? b.e_run[chain] : 0.0;
     uint32_t flips = 0;
+    const uint32_t lane_top = 1u << (31u - lane);
     uint32_t slot_cur = 0;  // follows the producer's ring rotation: layer l lives in slot l % 3 of the visit order
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
@@ -460,17 +461,19 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                 chunk_barrier(bar_id);  // the sweep warp has finished this chunk
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
+                // spin words: lane k flips the bits of attempt k's accepting chains
+                if (lane < kUnroll) w_cur[p0 + lane] ^= ballots[lane];
 #pragma unroll
                 for (int k = 0; k < int(kUnroll); ++k) {
                     const uint32_t ballot = ballots[k];
                     const float4 rec = recs[k * 32];
-                    // rec.y = -2*beta*s carries the opposite of the spin's sign: 2s = 2.0 with the sign of s
-                    const float two_s = __uint_as_float(0x40000000u | (~__float_as_uint(rec.y) & 0x80000000u));
-                    const double de = double(__fmul_rn(two_s, __fadd_rn(rec.x, rec.w)));
-                    const bool mine = (ballot >> lane) & 1u;
+                    // (2s)*(h + h_tau): doubling is exact, and rec.y = -2*beta*s carries the opposite of
+                    // the spin's sign, so the product is 2*(h + h_tau) with its sign flipped where s = -1
+                    const float twice = __fmul_rn(__fadd_rn(rec.x, rec.w), 2.0f);
+                    const float de = __uint_as_float(__float_as_uint(twice) ^ (~__float_as_uint(rec.y) & 0x80000000u));
+                    const bool mine = int32_t(ballot * lane_top) < 0;  // bit `lane` of the ballot, moved to the sign
                     flips += mine ? 1u : 0u;
-                    e_run = mine ? __dadd_rn(e_run, de) : e_run;
-                    if (lane == 0 && ballot != 0u) w_cur[p0 + k] ^= ballot;
+                    e_run = __dadd_rn(e_run, double(mine ? de : 0.0f));  // + 0.0 changes nothing
                 }
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);
