@@ -149,7 +149,10 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
         } else {
             near_groups = emit_groups(near_all, p0 / 8, false);  // rare and short: not worth padding
         }
-        chunks[p0 / 8] = make_uint4(emit_groups(for_far_warp, p0 / 8, true), near_groups, careful ? 1u : 0u, 0u);
+        // flags: bit 0 careful; bit 1 lean but first or last chunk of the layer
+        const bool odd = !careful && (p0 == 0 || p0 + 8 >= P);
+        chunks[p0 / 8] = make_uint4(emit_groups(for_far_warp, p0 / 8, true), near_groups,
+                                    (careful ? 1u : 0u) | (odd ? 2u : 0u), 0u);
     }
     if (far.size() > 0xffffu || groups.size() > 0xffffu) throw Error("init_state: layer graph too large for the layered kernel");
     return out;

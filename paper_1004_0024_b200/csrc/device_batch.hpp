@@ -44,7 +44,8 @@ struct DevLayerGraph {
     //                near forward edges of a CAREFUL chunk: begin | count << 16 (indices into `far`), 0}
     const uint4* pos;
     // per chunk of 8 positions: {far-warp groups: begin | count << 16 (indices into `groups`),
-    //                            near groups of a LEAN chunk: begin | count << 16, 1 if careful, 0}
+    //                            near groups of a LEAN chunk: begin | count << 16,
+    //                            flags (1 careful, 2 lean but first/last of the layer), 0}
     const uint4* chunks;
     // a group is up to 8 edges with distinct targets: edge begin | edge count << 16
     const uint32_t* groups;

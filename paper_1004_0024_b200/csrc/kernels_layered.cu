@@ -111,6 +111,12 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
+// the volatile flavour, for data other warps write (prep records)
+__device__ __forceinline__ float4 lds_rec(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -551,10 +557,6 @@ __device__ __forceinline__ void apply_groups(uint32_t tm, const GraphSmem& g, ui
         tmem_wait_st();  // the next group may hit one of these columns again
     }
 }
-__device__ __noinline__ void apply_groups_outlined(uint32_t tm, const GraphSmem& g, uint32_t ginfo, uint32_t signs_addr,
-                                                   uint32_t ballots_addr, uint32_t lane) {
-    apply_groups(tm, g, ginfo, signs_addr, ballots_addr, lane);
-}
 
 // Far: applies the far-neighbour updates the sweep warp does not need soon — every BACKWARD target
 // (its column left the register window before the flipping attempt ran) and every FORWARD target
@@ -732,9 +734,84 @@ __device__ __forceinline__ void attempt_lean(float (&r)[kUnroll], float (&out)[k
     attempt<EXP, K>(r, rec##K, sa, g.pos[p0 + K].z, ps, chunk_seq, p0, P, tm, g.far, lane);
 #define ISING_ATTEMPT_LEAN(K) attempt_lean<EXP, K>(r, out, nx, rec##K, sa, lane);
 
+// Near groups of a lean chunk (columns 8c+11 .. 8c+18, not loaded yet): the far warp may still owe
+// them updates from the chunk before this one, which must land first.
+__device__ __noinline__ void apply_near_groups(uint32_t tm, const GraphSmem& g, uint32_t ginfo, uint32_t signs_addr,
+                                               uint32_t ballots_addr, uint32_t post_done_addr, uint32_t chunk_seq,
+                                               uint32_t lane) {
+    PostSync ps{post_done_addr, 0u, 0u};
+    __syncwarp();
+    wait_post(ps, chunk_seq);
+    apply_groups(tm, g, ginfo, signs_addr, ballots_addr, lane);
+}
+
+// The register window of the sweep warp, passed by value to the out-of-line chunk below.
+struct Window {
+    float r[kUnroll];
+};
+
+// A chunk that is not plain lean: careful (per-attempt window traffic and near updates), or lean
+// but first / last of its layer.  Out of line, so that the sweep
+// warp's hot loop (plain lean chunks, ~97 % of them) stays a few KB of straight code.
+template <int EXP>
+__device__ __noinline__ Window special_chunk(Window w, const GraphSmem g, const PairSmem s, uint32_t post_done_addr,
+                                             uint32_t chunk_seq, uint32_t st, uint32_t p0, uint32_t P, uint32_t tm,
+                                             uint32_t band_base, uint32_t lane) {
+    float (&r)[kUnroll] = w.r;
+    PostSync ps{post_done_addr, 0u, 0u};
+    const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
+    StageAddr sa;
+    sa.rec_x = smem_u32(recs);
+    sa.ballots = smem_u32(s.ballots + st * kUnroll);
+    sa.band = band_base + p0 * 32;
+    const uint4 chunk_info = g.chunks[p0 / kUnroll];
+    const float4 rec0 = recs[0 * 32], rec1 = recs[1 * 32], rec2 = recs[2 * 32], rec3 = recs[3 * 32];
+    const float4 rec4 = recs[4 * 32], rec5 = recs[5 * 32], rec6 = recs[6 * 32], rec7 = recs[7 * 32];
+    if ((chunk_info.z & 1u) == 0u) {
+        float nx[kUnroll], out[kUnroll];
+        // columns p0+3 .. p0+10 enter; the last chunk of a layer has only five left
+        if (p0 + kUnroll < P) {
+            tmem_ld8(tm + p0 + 3, nx);
+        } else {
+#pragma unroll
+            for (int k = 0; k < int(kUnroll); ++k) nx[k] = k < 5 ? tmem_ld(tm + p0 + 3 + k) : 0.0f;
+        }
+        ISING_ATTEMPT_LEAN(0)
+        ISING_ATTEMPT_LEAN(1)
+        ISING_ATTEMPT_LEAN(2)
+        ISING_ATTEMPT_LEAN(3)
+        ISING_ATTEMPT_LEAN(4)
+        ISING_ATTEMPT_LEAN(5)
+        ISING_ATTEMPT_LEAN(6)
+        ISING_ATTEMPT_LEAN(7)
+        if ((chunk_info.y >> 16) != 0u) {
+            apply_near_groups(tm, g, chunk_info.y, smem_u32(s.signs + st * 32 + lane), sa.ballots, post_done_addr,
+                              chunk_seq, lane);
+        }
+        // columns p0-2 .. p0+5 leave the window (the first chunk has no p0-2, p0-1)
+        if (p0 != 0) {
+            tmem_st8(tm + p0 - 2, out);
+        } else {
+#pragma unroll
+            for (int k = 2; k < int(kUnroll); ++k) tmem_st(tm + k - 2, out[k]);
+        }
+    } else {
+        ISING_ATTEMPT(0)
+        ISING_ATTEMPT(1)
+        ISING_ATTEMPT(2)
+        ISING_ATTEMPT(3)
+        ISING_ATTEMPT(4)
+        ISING_ATTEMPT(5)
+        ISING_ATTEMPT(6)
+        ISING_ATTEMPT(7)
+        tmem_wait_ld();  // entries requested by the last attempts
+    }
+    return w;
+}
+
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint32_t bar_id, PostSync& ps,
+                           const PairSmem& s, uint64_t* full, uint32_t bar_id, uint32_t post_done_addr,
                            uint32_t& chunk_seq, RingCursor& cursor, uint32_t stages, uint32_t tile,
                            uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
@@ -742,6 +819,8 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
     float* hs_prev = nullptr;
     uint32_t p0 = 0;
     const uint32_t band_base = smem_u32(g.band_pm);
+    const uint32_t recs_u32 = smem_u32(s.recs + lane), ballots_u32 = smem_u32(s.ballots);
+    const uint32_t signs_u32 = smem_u32(s.signs + lane);
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
@@ -755,7 +834,8 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             hs_prev = hs_l;
 
             // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
-            float r[kUnroll];
+            Window w;
+            float (&r)[kUnroll] = w.r;
 #pragma unroll
             for (int k = 0; k < int(kUnroll); ++k) r[k] = 0.0f;
             r[0] = tmem_ld(tm + 0);
@@ -763,7 +843,6 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
             r[2] = tmem_ld(tm + 2);
             tmem_wait_ld();
 
-            ps.layer_base = chunk_seq;
             for (p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
                 mbar_wait(&full[st], cursor.parity(), 0);
@@ -772,25 +851,21 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                 // attempts at least two chunks back: the chunk rendezvous below guarantees it has
                 // finished those (it cannot be more than one chunk behind)
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
-                const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
-                StageAddr sa;
-                sa.rec_x = smem_u32(recs);
-                sa.ballots = smem_u32(s.ballots + st * kUnroll);
-                sa.band = band_base + p0 * 32;
                 const uint4 chunk_info = g.chunks[p0 / kUnroll];
-                const bool careful = chunk_info.z != 0u;
-                const float4 rec0 = recs[0 * 32], rec1 = recs[1 * 32], rec2 = recs[2 * 32], rec3 = recs[3 * 32];
-                const float4 rec4 = recs[4 * 32], rec5 = recs[5 * 32], rec6 = recs[6 * 32], rec7 = recs[7 * 32];
-                if (!careful) {
+                const uint32_t special = chunk_info.z;
+                StageAddr sa;
+                sa.rec_x = recs_u32 + st * (kUnroll * 32 * 16);
+                sa.ballots = ballots_u32 + st * (kUnroll * 4);
+                sa.band = band_base + p0 * 32;
+                // (requested before the branch on `special`, whose own load is still in flight)
+                const float4 rec0 = lds_rec(sa.rec_x + 0 * 512), rec1 = lds_rec(sa.rec_x + 1 * 512);
+                const float4 rec2 = lds_rec(sa.rec_x + 2 * 512), rec3 = lds_rec(sa.rec_x + 3 * 512);
+                const float4 rec4 = lds_rec(sa.rec_x + 4 * 512), rec5 = lds_rec(sa.rec_x + 5 * 512);
+                const float4 rec6 = lds_rec(sa.rec_x + 6 * 512), rec7 = lds_rec(sa.rec_x + 7 * 512);
+                if (__builtin_expect(special == 0u, 1)) {
+                    // plain lean chunk: eight columns in, eight attempts, eight columns out
                     float nx[kUnroll], out[kUnroll];
-                    // columns p0+3 .. p0+10 enter: final by now (see delegated() in batch.cpp); the last
-                    // chunk of a layer has only five left
-                    if (p0 + kUnroll < P) {
-                        tmem_ld8(tm + p0 + 3, nx);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < int(kUnroll); ++k) nx[k] = k < 5 ? tmem_ld(tm + p0 + 3 + k) : 0.0f;
-                    }
+                    tmem_ld8(tm + p0 + 3, nx);  // columns p0+3 .. p0+10: final by now (see delegated() in batch.cpp)
                     ISING_ATTEMPT_LEAN(0)
                     ISING_ATTEMPT_LEAN(1)
                     ISING_ATTEMPT_LEAN(2)
@@ -799,32 +874,15 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                     ISING_ATTEMPT_LEAN(5)
                     ISING_ATTEMPT_LEAN(6)
                     ISING_ATTEMPT_LEAN(7)
-                    if ((chunk_info.y >> 16) != 0u) {
-                        // near forward targets (columns 8c+11 .. 8c+18, not loaded yet): the far warp may
-                        // still owe them updates from the chunk before this one, which must land first
-                        __syncwarp();
-                        wait_post(ps, chunk_seq);
-                        apply_groups_outlined(tm, g, chunk_info.y, smem_u32(s.signs + st * 32 + lane), sa.ballots, lane);
+                    if (__builtin_expect((chunk_info.y >> 16) != 0u, 0)) {
+                        apply_near_groups(tm, g, chunk_info.y, signs_u32 + st * 128, sa.ballots, post_done_addr,
+                                          chunk_seq, lane);
                     }
-                    // columns p0-2 .. p0+5 leave the window (the first chunk has no p0-2, p0-1)
-                    if (p0 != 0) {
-                        tmem_st8(tm + p0 - 2, out);
-                    } else {
-#pragma unroll
-                        for (int k = 2; k < int(kUnroll); ++k) tmem_st(tm + k - 2, out[k]);
-                    }
+                    tmem_st8(tm + p0 - 2, out);  // columns p0-2 .. p0+5 leave the window
                 } else {
-                    ISING_ATTEMPT(0)
-                    ISING_ATTEMPT(1)
-                    ISING_ATTEMPT(2)
-                    ISING_ATTEMPT(3)
-                    ISING_ATTEMPT(4)
-                    ISING_ATTEMPT(5)
-                    ISING_ATTEMPT(6)
-                    ISING_ATTEMPT(7)
-                    tmem_wait_ld();  // entries requested by the last attempts
+                    w = special_chunk<EXP>(w, g, s, post_done_addr, chunk_seq, st, p0, P, tm, band_base, lane);
                 }
-                // the post warp may now update columns this chunk retired: they must have landed
+                // the far warp may now update columns this chunk retired: they must have landed
                 tmem_wait_st();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 chunk_barrier(bar_id);
@@ -886,7 +944,6 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     const uint32_t tm = tmem_base + ((pair * 32u) << 16);
     RingCursor cursor;
     uint32_t chunk_seq = 0;  // chunks this role has finished, over the whole kernel
-    PostSync ps{smem_u32(post_done), 0u, 0u};
 
     // tiles are dealt round-robin: CTA c, pair w, round r -> tile c + grid*(w + 4r)
     for (uint32_t tile = blockIdx.x + gridDim.x * pair; tile < b.n_tiles; tile += gridDim.x * kSweepWarps) {
@@ -905,7 +962,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
                      cursor, stages, tm, g.per_layer,
                      g.layers);
         } else {
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, bar_id, ps, chunk_seq, cursor, stages, tile, tm,
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, bar_id, smem_u32(post_done), chunk_seq, cursor, stages, tile, tm,
                             g.per_layer, g.layers);
         }
         if (!b.graph_shared) asm volatile("bar.sync %0, 128;" ::"r"(pair + 1) : "memory");
