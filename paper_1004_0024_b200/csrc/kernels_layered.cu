@@ -1,42 +1,49 @@
 // Layered-model sweep kernel: the performance path for identical-layer ("QMC-style") models.
 //
-// One persistent CTA per SM; four SWEEP warps and four HELPER warps per CTA.  Sweep warp w and
-// helper warp 4+w share a tile of 32 chains (lane = chain) and — because warp_id % 4 picks the SM
-// sub-partition — the same scheduler.  The sweep of a chain is strictly sequential (attempt p+1
-// needs the flips of attempt p), so the sweep warp is latency bound; everything that does not
-// sit on that loop-carried chain is moved to the helper, whose instructions fill the issue
-// slots the chain leaves empty:
+// One persistent CTA per SM, 16 warps = 4 tiles x 4 roles.  A TILE is 32 chains (lane = chain); its
+// four warps share warp_id % 4, hence one SM sub-partition (scheduler, register file slice, TMEM lane
+// quarter).  A chain's sweep is strictly sequential (attempt p+1 needs the flips of attempt p), so
+// the SWEEP warp is latency bound; everything that is not on that loop-carried chain runs in the
+// other three warps, whose instructions fill the issue slots the chain leaves empty:
 //
-//   helper warp, ahead of the sweep   MT19937 regeneration (replica-interleaved state in HBM/L2),
-//                                     tempering, u32 -> unit float, and per attempt the lane's
-//                                     sign constants and tau field ("prep record")
-//   sweep warp                        decision, band-neighbour updates, ballot, far-neighbour
-//                                     updates, Tensor Memory window traffic
-//   helper warp, behind the sweep     accept counts, running energy, spin-word updates
+//   producer (ahead)   MT19937 regeneration in place (replica-interleaved state, HBM/L2 resident),
+//                      tempering, u32 -> unit float, and per attempt the PREP RECORD
+//                      {u, -2*beta*s, gamma*h_tau, h_tau} plus one sign word per chunk
+//   sweep              decision, band-neighbour updates in registers, ballot; moves the register
+//                      window through Tensor Memory eight columns at a time
+//   post (behind)      accept counts, running energy (f64), spin-word flips
+//   far (behind)       far-neighbour field updates as batched Tensor Memory read-modify-writes
 //
-// The two meet in a shared-memory ring of 8-attempt stages guarded by mbarriers: the helper
-// fills a stage with prep records {u, -2*beta*s, gamma*h_tau, h_tau}; the sweep warp consumes it,
-// writes back the field it decided on and the accept ballot, and hands the stage back; the helper
-// post-processes it before refilling.
+// Work moves in CHUNKS of 8 attempts through a shared-memory ring of stages: `full` mbarriers
+// (producer -> sweep), one named hardware barrier per tile (sweep -> post, far: they sleep in it, and
+// the sweep warp is never more than one chunk ahead of them), `empty` mbarriers (post + far -> producer).
 //
 // A chain's working set for one layer lives ON CHIP:
-//   * Tensor Memory holds the space fields of the layer being swept: column p of the warp's own
-//     32-lane TMEM quarter is h_eff_space[(layer, p)] of its 32 chains (512 columns x 128 lanes x
-//     4 B = the whole 256 KB TMEM of an SM for 4 warps x 512 positions).
-//   * A five-entry REGISTER WINDOW slides over the columns p-2..p+2 of the position being
-//     attempted.  Updates of the near ("band") neighbours are predicated register adds, so the
-//     loop-carried dependency from one attempt to the next is a single FADD; only the far
-//     neighbours of a flip are read-modify-written in Tensor Memory (tcgen05.ld / tcgen05.st).
+//   * Tensor Memory holds the space fields of the layer being swept: column p of the tile's 32-lane
+//     quarter is h_eff_space[(layer, p)] of its 32 chains (512 columns x 128 lanes x 4 B = the whole
+//     256 KB TMEM of an SM for 4 tiles x 512 positions).  All three TMEM roles of a tile change
+//     layers together (layer_transition: a third of the columns each, HBM <-> TMEM, streaming hints).
+//   * A REGISTER WINDOW of the sweep warp slides over the columns p-2..p+2 of the position being
+//     attempted.  Updates of these band neighbours are predicated register adds.  In a LEAN chunk
+//     (97 % of them) the eight columns that enter the window are loaded with one tcgen05.ld.x8 and
+//     the eight that leave it stored with one tcgen05.st.x8; the attempts themselves touch no TMEM.
+//   * Far (non-band) neighbours of a flip are updated in Tensor Memory by whoever can do it without
+//     stalling the sweep: the FAR warp for every target the sweep warp is not about to load
+//     (backward targets, forward targets two or more chunks ahead), in groups of 8 edges with
+//     distinct targets whose loads go out together; the sweep warp itself for the few NEAR forward
+//     targets — after the chunk for targets the next chunk will load, per attempt (CAREFUL chunk,
+//     out of line) for targets inside the columns already loaded.  See build_layer_graph (batch.cpp)
+//     for the split and the ordering argument.
 //   * The tau field is NOT stored.  For these models it only takes the values {2J, +0, -2J}
 //     and every incremental update of it is exact (HostModel::layered_uniform), so it is rebuilt
 //     from two spin bits of the adjacent layers.  That removes 8 of the 17 bytes per attempt the
 //     generic layout streams, and both tau read-modify-writes of every flip.
 //   * Spins are one bit per chain: a 32-bit word per (tile, spin) holds the 32 lanes' signs.
-//     Three layers of words (previous, current, next) sit in shared memory per pair.
-//   * One layer's graph (band couplings + far-edge list per position) sits in shared memory.
+//     Three layers of words (previous, current, next) sit in shared memory per tile.
+//   * One layer's graph (band addends per sign, edge groups per chunk) sits in shared memory.
 //
 // HBM traffic per sweep is one read and one write of the f32 space fields plus the bit words
-// (8.25 B per attempt) and the MT19937 state words (12 B per attempt while they miss L2).
+// (8.25 B per attempt); the MT19937 state (12 B per attempt if it missed) is pinned in L2.
 // The trajectory is the reference's (ref: proj/src/sweep_basic.cpp:12-56) bit for bit.
 #include "device_batch.hpp"
 #include "device_math.cuh"
@@ -167,7 +174,7 @@ struct PairSmem {
     uint32_t* signs;    // stages * 32 : per lane, bit 7-k set <=> the spin of the stage's attempt k was -1
 };
 
-// header: tmem slot (16 B) + per pair full[8] + consumed[8] + empty[8] barriers (192 B) x 4
+// header: tmem slot (16 B) + per tile full[8], (unused)[8], empty[8] mbarriers (192 B) x 4
 constexpr size_t kRingBarriers = kSweepWarps * 3 * kMaxStages;
 constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one post-progress counter per pair
 
