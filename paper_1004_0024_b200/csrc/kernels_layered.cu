@@ -486,7 +486,7 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                     const float de = __uint_as_float(__float_as_uint(twice) ^ (~__float_as_uint(rec.y) & 0x80000000u));
                     const bool mine = int32_t(ballot * lane_top) < 0;  // bit `lane` of the ballot, moved to the sign
                     flips += mine ? 1u : 0u;
-                    e_run = __dadd_rn(e_run, double(mine ? de : 0.0f));  // + 0.0 changes nothing
+                    e_run = __dadd_rn(e_run, double(mine ? de : -0.0f));  // -0.0: the identity for every value
                 }
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);

@@ -296,3 +296,60 @@ def test_layered_many_tiles_and_sweeps(lib, port):
     state, want = run_both(port, [csr], 45, betas, 24, 4, kernel=ib.KERNEL_LAYERED, chunks=[3, 9, 12])
     assert state.info()["kernel"] == ib.KERNEL_LAYERED and state.info()["n_tiles"] == 5
     assert_batch_matches(state, want, REL_ENERGY)
+
+
+def chord_spec(positions, seed, offsets, density=0.6, h_sigma=0.4):
+    """A layer that stresses every class of far edge of the layered kernel: the +/-1, +/-2 ring plus
+    chords at the given offsets (short ones land inside the columns a chunk has already loaded, medium
+    ones in the next chunk's, long and backward ones are the far warp's), several per position and
+    often several into the same target within one chunk; couplings are not powers of two."""
+    rng = ins.MT19937(seed)
+    present, far_deg, edges = set(), [0] * positions, []
+
+    def add(a, b, far):
+        key = (min(a, b), max(a, b))
+        if a == b or key in present or (far and (far_deg[a] >= 12 or far_deg[b] >= 12)):
+            return
+        present.add(key)
+        if far:
+            far_deg[a] += 1
+            far_deg[b] += 1
+        edges.append(key)
+
+    for off in (1, 2):
+        if positions > 2 * off:
+            for p in range(positions):
+                add(p, (p + off) % positions, False)
+    for p in range(positions):
+        for off in offsets:
+            if off < positions and rng.below(1000) < int(1000 * density):
+                add(p, (p + off) % positions, min(off, positions - off) > 2)
+    values = np.array([0.75, -1.25, 1.0, -0.5, 0.3, -0.7], np.float32)
+    coup = [float(values[rng.below(len(values))]) for _ in edges]
+    h = rng.normals(positions, h_sigma)
+    return positions, h, [(a, b, c) for (a, b), c in zip(edges, coup)]
+
+
+@pytest.mark.parametrize("positions,layers,offsets", [
+    (8, 4, (3, 4)), (16, 4, (3, 5, 7)), (24, 5, (3, 4, 9, 11)), (64, 4, (3, 5, 6, 9, 13, 17, 26, 31)),
+    (128, 4, (3, 7, 10, 12, 19, 40, 63)), (512, 4, (3, 4, 5, 8, 11, 16, 23, 100, 255)),
+])
+@pytest.mark.parametrize("exp_kind", [1, 2, 3])
+def test_layered_chord_graphs_every_edge_class(lib, port, positions, layers, offsets, exp_kind):
+    csr = ins.build_layered_csr(*chord_spec(positions, 100 + positions, offsets), layers, 0.8)
+    betas = ins.geometric_betas(0.25, 2.0, 5)
+    ladders = 9  # 45 chains: two tiles, the second ragged
+    sweeps = 12 if positions < 512 else 6
+    out = {}
+    for kernel in LAYERED_KERNELS:
+        state, want = run_both(port, [csr], ladders, betas, sweeps, 3, tau_scale=1.25, exp_kind=exp_kind,
+                               kernel=kernel, chunks=[sweeps // 2, sweeps - sweeps // 2])
+        assert state.info()["kernel"] == kernel
+        assert_batch_matches(state, want, REL_ENERGY)
+        for c in (0, 44):
+            hs, ht = state.fields(c)
+            out.setdefault(c, []).append((hs.copy(), ht.copy()))
+        state.close()
+    for c, (a, b) in out.items():  # both families leave identical fields behind, bit for bit
+        np.testing.assert_array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+        np.testing.assert_array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
