@@ -187,6 +187,19 @@ typedef struct ising_batch_info {
 /* timing = 1 brackets every sweep/swap launch with CUDA events on the batch's stream. */
 ISING_B200_API ising_status ising_batch_set_timing(ising_batch* batch, int timing);
 ISING_B200_API ising_status ising_batch_get_info(ising_batch* batch, ising_batch_info* out); /* synchronises */
+
+/* Wait statistics (ref: FlipStats::group_wait / collect_wait_stats, include/isingmc/sweep.hpp:31-53,
+ * src/sweep_state.cpp:33-44; ising_run_report.wait_*, include/isingmc.h:94-96).  The reference
+ * groups w consecutively processed spins of ONE chain (its SIMD lanes); here the lanes of a warp are
+ * w NEIGHBOURING CHAINS attempting the same spin in lockstep, so the probability that a w-wide group
+ * holds at least one flip is measured on the real ballots.  Widths 1, 2, 4, 8, 16, 32 (1 = the
+ * flip rate); tiles with fewer than 32 chains are not recorded.  record_wait(1) zeroes the counters
+ * and starts recording for the following ising_batch_run calls; record_wait(0) stops it.
+ * probability/groups/with_flip: n_widths entries each, any may be NULL. */
+ISING_B200_API ising_status ising_batch_record_wait(ising_batch* batch, int on);
+ISING_B200_API ising_status ising_batch_read_wait_stats(ising_batch* batch, uint32_t n_widths,
+                                                         const uint32_t* widths, double* probability,
+                                                         uint64_t* groups, uint64_t* with_flip);
 /* The batch's cudaStream_t, for callers that want to record their own events on it. */
 ISING_B200_API void* ising_batch_stream(ising_batch* batch);
 

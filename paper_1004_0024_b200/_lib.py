@@ -78,6 +78,8 @@ SIGNATURES = {
     "ising_batch_read_swap_stats": (C.c_int, [C.c_void_p, u64p, u64p]),
     "ising_batch_pack_results": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ising_batch_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "ising_batch_record_wait": (C.c_int, [C.c_void_p, C.c_int]),
+    "ising_batch_read_wait_stats": (C.c_int, [C.c_void_p, C.c_uint32, u32p, f64p, u64p, u64p]),
     "ising_batch_get_info": (C.c_int, [C.c_void_p, C.POINTER(BatchInfo)]),
     "ising_batch_stream": (C.c_void_p, [C.c_void_p]),
     "ising_b200_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(RunReport)]),

@@ -232,6 +232,19 @@ class BatchState:
     def pack_results(self, device_ptr: int) -> None:
         _check(L.load().ising_batch_pack_results(self._h, C.c_void_p(device_ptr)))
 
+    def record_wait(self, on: bool = True) -> None:
+        """Starts (counters zeroed) or stops recording wait statistics (ref: EngineConfig::stats_widths)."""
+        _check(L.load().ising_batch_record_wait(self._h, int(on)))
+
+    def wait_stats(self, widths=(1, 2, 4, 8, 16, 32)) -> dict:
+        """ref: collect_wait_stats, src/sweep_state.cpp:33-44 — {width: (probability, groups, with_flip)}."""
+        w = _arr(list(widths), np.uint32)
+        prob = np.empty(w.size, np.float64)
+        groups, flip = np.empty(w.size, np.uint64), np.empty(w.size, np.uint64)
+        _check(L.load().ising_batch_read_wait_stats(self._h, w.size, _p(w, C.c_uint32), _p(prob, C.c_double),
+                                                    _p(groups, C.c_uint64), _p(flip, C.c_uint64)))
+        return {int(k): (float(p), int(g), int(f)) for k, p, g, f in zip(w, prob, groups, flip)}
+
     def set_timing(self, on: bool) -> None:
         _check(L.load().ising_batch_set_timing(self._h, int(on)))
 

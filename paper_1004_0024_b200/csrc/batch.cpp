@@ -583,6 +583,40 @@ void Batch::read_stats(uint64_t* flips, uint64_t* attempts) {
     }
 }
 
+void Batch::record_wait(bool on) {
+    bind_device();
+    sync();
+    if (!on) {
+        dev_.wait_counts = nullptr;  // counters stay readable until recording is switched on again
+        return;
+    }
+    const size_t bytes = size_t(dev_.n_tiles) * kWaitSlots * sizeof(unsigned long long);
+    if (wait_counts_.bytes() < bytes) wait_counts_.allocate(bytes, device_bytes_);
+    cuda_check(cudaMemsetAsync(wait_counts_.as<void>(), 0, bytes, stream_), "cudaMemsetAsync");
+    dev_.wait_counts = wait_counts_.as<unsigned long long>();
+}
+
+void Batch::read_wait(uint32_t n_widths, const uint32_t* widths, uint64_t* groups, uint64_t* with_flip) {
+    bind_device();
+    if (n_widths != 0 && (widths == nullptr || groups == nullptr || with_flip == nullptr)) throw Error("null argument");
+    if (wait_counts_.bytes() == 0) throw Error("collect_wait_stats: wait statistics were not recorded");
+    std::vector<unsigned long long> host(size_t(dev_.n_tiles) * kWaitSlots);
+    download(host.data(), wait_counts_.as<void>(), host.size(), stream_);
+    unsigned long long total[kWaitSlots] = {};
+    for (uint32_t t = 0; t < dev_.n_tiles; ++t) {
+        for (uint32_t k = 0; k < kWaitSlots; ++k) total[k] += host[size_t(t) * kWaitSlots + k];
+    }
+    for (uint32_t i = 0; i < n_widths; ++i) {
+        uint32_t slot = 0;
+        while (slot < 6 && (1u << slot) != widths[i]) ++slot;
+        if (slot == 6) {  // ref: collect_wait_stats throws for widths that were not recorded
+            throw Error("collect_wait_stats: width " + std::to_string(widths[i]) + " was not recorded");
+        }
+        groups[i] = total[6] * (32u >> slot);  // attempts per lane x groups of that width in a tile
+        with_flip[i] = total[slot];
+    }
+}
+
 void Batch::read_checksums(uint64_t* out) {
     bind_device();
     if (out == nullptr) throw Error("null argument");

@@ -78,6 +78,10 @@ class Batch {
     void pack_results(void* device_out);
 
     void set_timing(bool on) { timing_ = on; }
+    // wait statistics (ref: FlipStats::group_wait): recording starts (counters zeroed) or stops
+    void record_wait(bool on);
+    // per requested width (1, 2, 4, 8, 16 or 32): groups seen, groups with at least one flip
+    void read_wait(uint32_t n_widths, const uint32_t* widths, uint64_t* groups, uint64_t* with_flip);
     cudaStream_t stream() const { return stream_; }
 
     // introspection
@@ -117,7 +121,7 @@ class Batch {
     DeviceBuffer models_, tile_first_, tile_count_, tile_model_, chain_loc_, seeds_, betas_;
     DeviceBuffer slot_of_chain_, chain_at_slot_, hs_, ht_, spin_bits_, mt_, mt_pos_, e_run_, flips_;
     DeviceBuffer swap_seeds_, swap_mt_, swap_pos_, swap_acc_, swap_att_;
-    DeviceBuffer layer_graphs_;
+    DeviceBuffer layer_graphs_, wait_counts_;
     DeviceBuffer scratch_;  // readout staging
     int sm_count_ = 0;
 

@@ -304,6 +304,27 @@ ising_status ising_batch_set_timing(ising_batch* batch, int timing) {
     });
 }
 
+ising_status ising_batch_record_wait(ising_batch* batch, int on) {
+    return guarded([&]() {
+        impl_of(batch).record_wait(on != 0);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_batch_read_wait_stats(ising_batch* batch, uint32_t n_widths, const uint32_t* widths,
+                                         double* probability, uint64_t* groups, uint64_t* with_flip) {
+    return guarded([&]() {
+        std::vector<uint64_t> g(n_widths), f(n_widths);
+        impl_of(batch).read_wait(n_widths, widths, g.data(), f.data());
+        for (uint32_t i = 0; i < n_widths; ++i) {
+            if (probability != nullptr) probability[i] = g[i] ? double(f[i]) / double(g[i]) : 0.0;
+            if (groups != nullptr) groups[i] = g[i];
+            if (with_flip != nullptr) with_flip[i] = f[i];
+        }
+        return ISING_OK;
+    });
+}
+
 ising_status ising_batch_get_info(ising_batch* batch, ising_batch_info* out) {
     return guarded([&]() {
         Batch& b = impl_of(batch);

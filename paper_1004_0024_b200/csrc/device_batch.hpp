@@ -16,6 +16,7 @@
 
 namespace isingb200 {
 
+constexpr uint32_t kWaitSlots = 7;  // widths 1, 2, 4, 8, 16, 32, then the attempts (per lane) recorded
 constexpr uint32_t kMtWords = 624;  // MT19937 state words per chain (ref: rng.hpp:11)
 
 struct DevModel {
@@ -88,6 +89,10 @@ struct DevBatch {
     uint32_t* mt_pos;
     double* e_run;
     unsigned long long* flips;
+    // wait statistics (ref: FlipStats::group_wait, sweep.hpp:31-44), per tile: groups of w = 1, 2, 4, 8,
+    // 16, 32 neighbouring lanes (chains attempting the same spin in lockstep) that held at least one
+    // flip, and the attempts recorded; nullptr unless recording was requested
+    unsigned long long* wait_counts;  // [tile][kWaitSlots]
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]

@@ -64,6 +64,21 @@ __device__ __forceinline__ float exp_accurate(float x) {
 // only when that value sits within ~1e-16 (relative) of an f32 rounding boundary.
 __device__ __forceinline__ float exp_exact(float x) { return __double2float_rn(exp(double(x))); }
 
+// Wait statistics of one lockstep attempt of 32 chains: adds, for w = 1, 2, 4, 8, 16, 32, the
+// number of aligned w-lane groups of `ballot` that hold at least one accepting lane.
+__device__ __forceinline__ void wait_fold(uint32_t ballot, uint32_t (&c)[6]) {
+    const uint32_t a2 = (ballot | (ballot >> 1)) & 0x55555555u;
+    const uint32_t a4 = (a2 | (a2 >> 2)) & 0x11111111u;
+    const uint32_t a8 = (a4 | (a4 >> 4)) & 0x01010101u;
+    const uint32_t a16 = (a8 | (a8 >> 8)) & 0x00010001u;
+    c[0] += __popc(ballot);
+    c[1] += __popc(a2);
+    c[2] += __popc(a4);
+    c[3] += __popc(a8);
+    c[4] += __popc(a16);
+    c[5] += ballot != 0u ? 1u : 0u;
+}
+
 template <int EXP>
 __device__ __forceinline__ float exp_kind(float x) {
     if constexpr (EXP == kExpExact) return exp_exact(x);

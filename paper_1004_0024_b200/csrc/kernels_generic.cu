@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
     const float gamma = b.tau_scale;
     double e_run = t.active ? b.e_run[t.chain] : 0.0;
     unsigned long long flips = 0;
+    const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
+    uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
 
     MtLane g;
     g.open(t.mt, 32, b.mt_pos[t.tile]);
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
                 const float p = exp_kind<EXP>(x);
                 const bool accept = t.active && (u[k] < p);
                 const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+                if (record_wait) wait_fold(ballot, wait);
                 if (ballot != 0u) {
                     const uint32_t end = m.offsets[i + 1];
                     const uint32_t mid = TAU ? end - m.tau_counts[i] : end;
@@ -211,6 +214,15 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
             }
         }
         __syncwarp();  // lane 0's spin-word stores become visible to the whole warp
+        if (record_wait) {  // flushed per sweep: the 32-bit partial counts cannot overflow (n < 2^27)
+            unsigned long long* out = b.wait_counts + size_t(t.tile) * kWaitSlots;
+#pragma unroll
+            for (int w = 0; w < 6; ++w) {
+                if (t.lane == 0) out[w] += wait[w];
+                wait[w] = 0;
+            }
+            if (t.lane == 0) out[6] += n;
+        }
     }
 
     if (t.lane == 0) b.mt_pos[t.tile] = g.pos;

@@ -452,6 +452,7 @@ __device__ __forceinline__ void layer_transition(uint32_t part, uint32_t tm, flo
 // Post: accept counts, running energy and spin words of every consumed stage (ref:
 // sweep_basic.cpp:47-48; the energy bookkeeping is the tempering definition of
 // oracle/ising_oracle.h).
+template <bool WAIT>
 __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const PairSmem& s,
                           uint32_t bar_id, uint64_t* empty, RingCursor& cursor, uint32_t stages,
                           uint32_t tile, uint32_t tm, uint32_t P, uint32_t L) {
@@ -462,6 +463,9 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
     double e_run = active ? b.e_run[chain] : 0.0;
     uint32_t flips = 0;
     const uint32_t lane_top = 1u << (31u - lane);
+    // wait statistics: lane k folds the ballot of attempt k of every chunk (full tiles only)
+    const bool record_wait = WAIT && b.wait_counts != nullptr && b.tile_count[tile] == 32;
+    uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
     uint32_t slot_cur = 0;  // follows the producer's ring rotation: layer l lives in slot l % 3 of the visit order
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
@@ -475,7 +479,11 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                 const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
                 const uint32_t* ballots = s.ballots + st * kUnroll;
                 // spin words: lane k flips the bits of attempt k's accepting chains
-                if (lane < kUnroll) w_cur[p0 + lane] ^= ballots[lane];
+                if (lane < kUnroll) {
+                    const uint32_t mine_ballot = ballots[lane];
+                    w_cur[p0 + lane] ^= mine_ballot;
+                    if (WAIT && record_wait) wait_fold(mine_ballot, wait);
+                }
 #pragma unroll
                 for (int k = 0; k < int(kUnroll); ++k) {
                     const uint32_t ballot = ballots[k];
@@ -493,6 +501,17 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
             }
             chunk_barrier(bar_id);  // layer rendezvous (the sweep warp waits for the far warp here)
             slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
+            if (WAIT && record_wait) {  // flushed per layer (lanes 0..7 hold partial sums of at most 64 * 32 each)
+                unsigned long long* out = b.wait_counts + size_t(tile) * kWaitSlots;
+#pragma unroll
+                for (int w = 0; w < 6; ++w) {
+                    uint32_t v = wait[w];
+                    for (int off = 4; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+                    if (lane == 0) out[w] += v;
+                    wait[w] = 0;
+                }
+                if (lane == 0) out[6] += P;
+            }
         }
     }
     layer_transition(1, tm, hs_prev, nullptr, P);
@@ -914,7 +933,7 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
 #undef ISING_ATTEMPT
 #undef ISING_ATTEMPT_LEAN
 
-template <int EXP>
+template <int EXP, bool WAIT>
 __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBatch b, uint32_t sweeps) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
@@ -963,7 +982,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         if (role == 1) {
             producer_warp(b, sweeps, lane, gs, s, full, empty, cursor, stages, tile, g.per_layer, g.layers);
         } else if (role == 2) {
-            post_warp(b, sweeps, lane, s, bar_id, empty, cursor, stages, tile, tm, g.per_layer, g.layers);
+            post_warp<WAIT>(b, sweeps, lane, s, bar_id, empty, cursor, stages, tile, tm, g.per_layer, g.layers);
         } else if (role == 3) {
             far_warp(b.hs + size_t(tile) * b.n_spins * 32 + lane, sweeps, lane, gs, s, bar_id, empty, post_done, chunk_seq,
                      cursor, stages, tm, g.per_layer,
@@ -1013,15 +1032,29 @@ uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, uint32_
     return pick_stages(per_layer, max_far_edges, max_groups, graph_shared, &bytes);
 }
 
+namespace {
+template <int EXP, bool WAIT>
+cudaError_t prepare_one(size_t smem_bytes) {
+    return cudaFuncSetAttribute(sweep_layered_kernel<EXP, WAIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem_bytes));
+}
+template <int EXP>
+void launch_one(const DevBatch& b, uint32_t sweeps, dim3 grid, size_t smem, cudaStream_t stream) {
+    // the wait-statistics variant is a separate instantiation: the default kernel carries none of it
+    if (b.wait_counts != nullptr) sweep_layered_kernel<EXP, true><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps);
+    else sweep_layered_kernel<EXP, false><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps);
+}
+}  // namespace
+
 cudaError_t prepare_layered_kernels(size_t smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_layered_kernel<kExpExact>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(sweep_layered_kernel<kExpFast>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_bytes));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(sweep_layered_kernel<kExpAccurate>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = prepare_one<kExpExact, false>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_one<kExpExact, true>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_one<kExpFast, false>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_one<kExpFast, true>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_one<kExpAccurate, false>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_one<kExpAccurate, true>(smem_bytes);
+    return e;
 }
 
 cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_count, cudaStream_t stream) {
@@ -1029,9 +1062,9 @@ cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_coun
     const uint32_t ctas = uint32_t(sm_count) < b.n_tiles ? uint32_t(sm_count) : b.n_tiles;
     const dim3 grid(ctas ? ctas : 1);
     switch (b.exp_kind) {
-        case kExpExact: sweep_layered_kernel<kExpExact><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps); break;
-        case kExpFast: sweep_layered_kernel<kExpFast><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps); break;
-        default: sweep_layered_kernel<kExpAccurate><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps); break;
+        case kExpExact: launch_one<kExpExact>(b, sweeps, grid, smem, stream); break;
+        case kExpFast: launch_one<kExpFast>(b, sweeps, grid, smem, stream); break;
+        default: launch_one<kExpAccurate>(b, sweeps, grid, smem, stream); break;
     }
     return cudaGetLastError();
 }

@@ -353,3 +353,48 @@ def test_layered_chord_graphs_every_edge_class(lib, port, positions, layers, off
     for c, (a, b) in out.items():  # both families leave identical fields behind, bit for bit
         np.testing.assert_array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
         np.testing.assert_array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("kernel", LAYERED_KERNELS)
+def test_wait_statistics_from_real_ballots(lib, port, kernel):
+    """probability that a group of w neighbouring lanes (chains attempting the same spin
+    in lockstep) holds at least one flip, measured on the warp's ballots, against the same quantity
+    computed from the oracle's per-sweep flip flags (ref: accumulate_group_flags, sweep_state.cpp:356-372,
+    with the group taken across chains instead of along one chain)."""
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 5), 4, 1.5)  # 64 spins
+    betas = ins.geometric_betas(0.3, 2.0, 4)
+    ladders, sweeps = 24, 9  # 96 chains = 3 full tiles
+    seeds = (ins.CHAIN_SEED_BASE + np.arange(ladders * betas.size)).astype(np.uint32)
+    with ib.init_state(product_model(csr), betas, ladders, seeds=seeds, kernel=kernel) as st:
+        with pytest.raises(ib.IsingError, match="not recorded"):
+            st.wait_stats()
+        st.run(2)                      # not recorded
+        st.record_wait(True)
+        st.run(4)
+        st.run(sweeps - 4)
+        got = st.wait_stats()
+        flips_recorded = st.stats()[0].sum()
+        with pytest.raises(ib.IsingError, match="width 3 was not recorded"):
+            st.wait_stats([3])
+    # oracle: every chain on its own, a flip flag per (sweep, spin) = the spin changed in that sweep
+    model = port.model(csr)
+    n = csr["n_spins"]
+    flags = np.zeros((sweeps, n, ladders * betas.size), bool)
+    flips_before = 0
+    for c in range(ladders * betas.size):
+        chain = port.chain(model, int(seeds[c]), float(betas[c % betas.size]), 1.0, 2, None)
+        chain.sweep(2)
+        flips_before += chain.flips
+        prev = chain.spins
+        for s in range(sweeps):
+            chain.sweep(1)
+            cur = chain.spins
+            flags[s, :, c] = cur != prev
+            prev = cur
+    for w in (1, 2, 4, 8, 16, 32):
+        grouped = flags.reshape(sweeps, n, -1, w).any(axis=3)
+        prob, groups, with_flip = got[w]
+        assert groups == grouped.size and with_flip == int(grouped.sum())
+        assert prob == pytest.approx(grouped.mean())
+    assert got[1][2] == int(flags.sum()) == int(flips_recorded) - flips_before
+    assert got[32][0] >= got[16][0] >= got[1][0]  # wider groups wait more often
