@@ -226,6 +226,26 @@ typedef struct ising_b200_run_report {
 
 ISING_B200_API ising_status ising_b200_run(const ising_b200_model* model, const ising_b200_run_params* params,
                             ising_b200_run_report* out);
+/* ref: ising_run_json, include/isingmc.h:108-112, src/capi.cpp:230-262: the same run, plus a JSON
+ * document with the reference's keys (engine, exp, spins, sweeps, beta, tau_scale, seed, workers,
+ * final_cost, flip_rate, flips, attempts, wait, checksum as 16 hex digits, environment).  `engine`
+ * names the kernel family used ("b200-generic" / "b200-layered"); `wait` is empty for a single
+ * chain (see ising_batch_read_wait_stats).  *out_json is freed with ising_b200_string_free;
+ * out_report may be NULL. */
+ISING_B200_API ising_status ising_b200_run_json(const ising_b200_model* model, const ising_b200_run_params* params,
+                                                 ising_b200_run_report* out_report, char** out_json);
+
+/* ------------------------------------------------------- model text documents ---- */
+/* `ising-model v1` documents (ref: include/isingmc/model_io.hpp:10-28, src/model_io.cpp:45-226;
+ * C entry points ising_model_load / _from_string / _to_string / ising_string_free, include/isingmc.h:
+ * 40-53).  Hex-float literals: save -> load is bit-exact; the loader canonicalises the adjacency
+ * order and validates.  Malformed documents -> ISING_ERR_PARSE with "line N: ..." (N 1-based),
+ * unreadable / unwritable files -> ISING_ERR_IO, structurally invalid models -> ISING_ERR_ARGUMENT. */
+ISING_B200_API ising_status ising_b200_model_from_string(const char* text, ising_b200_model** out);
+ISING_B200_API ising_status ising_b200_model_to_string(const ising_b200_model* model, char** out);
+ISING_B200_API ising_status ising_b200_model_load(const char* path, ising_b200_model** out);
+ISING_B200_API ising_status ising_b200_model_save(const ising_b200_model* model, const char* path);
+ISING_B200_API void ising_b200_string_free(char* text);
 
 #ifdef __cplusplus
 }

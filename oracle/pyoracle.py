@@ -256,6 +256,10 @@ class Reference:
         lib.ref_model_half_edges.restype = C.c_uint64
         lib.ref_model_half_edges.argtypes = [C.c_void_p]
         lib.ref_model_export.argtypes = [C.c_void_p, f32p, u32p, u32p, f32p, u8p]
+        lib.ref_model_to_string.restype = C.c_long
+        lib.ref_model_to_string.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+        lib.ref_model_from_string.restype = C.c_void_p
+        lib.ref_model_from_string.argtypes = [C.c_char_p]
         lib.ref_total_cost.restype = C.c_double
         lib.ref_total_cost.argtypes = [C.c_void_p, f32p]
         lib.ref_checksum.restype = C.c_uint64
@@ -380,6 +384,23 @@ class RefModel:
     def validate(self):
         """None when valid, otherwise the reference's error message."""
         return None if self.ref.lib.ref_model_validate(self.handle) == 0 else self.ref.error()
+
+    def to_string(self) -> str:
+        """The reference's model_to_string (model_io.cpp:45-72)."""
+        size = self.ref.lib.ref_model_to_string(self.handle, None, 0)
+        if size < 0:
+            raise ValueError(self.ref.error())
+        buf = C.create_string_buffer(size + 1)
+        self.ref.lib.ref_model_to_string(self.handle, buf, size)
+        return buf.raw[:size].decode()
+
+    @classmethod
+    def from_string(cls, ref, text: str):
+        """The reference's model_from_string (model_io.cpp:74-205); raises ValueError with its message."""
+        handle = ref.lib.ref_model_from_string(text.encode())
+        if not handle:
+            raise ValueError(ref.error())
+        return cls(ref, None, handle)
 
     def csr(self) -> dict:
         n, e = self.n_spins, self.ref.lib.ref_model_half_edges(self.handle)

@@ -15,6 +15,7 @@
 
 #include "isingmc/fastexp.hpp"
 #include "isingmc/model.hpp"
+#include "isingmc/model_io.hpp"
 #include "isingmc/rng.hpp"
 #include "isingmc/sweep.hpp"
 
@@ -91,6 +92,27 @@ void* ref_build_layered(uint32_t positions, const float* h, uint32_t n_edges, co
 }
 
 void ref_model_free(void* m) { delete static_cast<SpinModel*>(m); }
+
+// `ising-model v1` documents through the reference's own reader and writer (model_io.cpp).
+// to_string: returns the length, copies at most `capacity` bytes; -1 on error.
+long ref_model_to_string(const void* m, char* out, size_t capacity) {
+    try {
+        const std::string text = model_to_string(*static_cast<const SpinModel*>(m));
+        if (out != nullptr && capacity != 0) std::memcpy(out, text.data(), std::min(capacity, text.size()));
+        return long(text.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+void* ref_model_from_string(const char* text) {
+    try {
+        return new SpinModel(model_from_string(text));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
 
 int ref_model_validate(const void* m) {
     try {

@@ -7,11 +7,13 @@ reference's sweep interface.  There is no CPU fallback: importing works anywhere
 batch needs the built library and a CUDA device.
 """
 from .api import (BatchState, ExpKind, IsingError, LayerSpec, SpinModel, SweepParams,
-                  build_layered_model, init_state, run_single, run_sweeps, state_checksum, total_cost)
+                  build_layered_model, init_state, run_single, run_single_json, run_sweeps, state_checksum,
+                  total_cost)
 from ._lib import KERNEL_AUTO, KERNEL_GENERIC, KERNEL_LAYERED
 
 __all__ = [
     "BatchState", "ExpKind", "IsingError", "LayerSpec", "SpinModel", "SweepParams",
-    "build_layered_model", "init_state", "run_single", "run_sweeps", "state_checksum", "total_cost",
+    "build_layered_model", "init_state", "run_single", "run_single_json", "run_sweeps", "state_checksum",
+    "total_cost",
     "KERNEL_AUTO", "KERNEL_GENERIC", "KERNEL_LAYERED",
 ]

@@ -83,6 +83,13 @@ SIGNATURES = {
     "ising_batch_get_info": (C.c_int, [C.c_void_p, C.POINTER(BatchInfo)]),
     "ising_batch_stream": (C.c_void_p, [C.c_void_p]),
     "ising_b200_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(RunReport)]),
+    "ising_b200_run_json": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(RunReport),
+                                      C.POINTER(C.c_void_p)]),
+    "ising_b200_model_from_string": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ising_b200_model_to_string": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ising_b200_model_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ising_b200_model_save": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "ising_b200_string_free": (None, [C.c_void_p]),
 }
 
 _lib = None

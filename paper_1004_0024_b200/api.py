@@ -86,6 +86,30 @@ class SpinModel:
             _p(couplings, C.c_float), _p(tau, C.c_uint8), layers, per_layer, C.byref(out)))
         return cls(out.value)
 
+    # --- `ising-model v1` documents (ref: model_io.hpp:10-28; ising_model_from_string / _load / _to_string)
+    @classmethod
+    def from_string(cls, text: str) -> "SpinModel":
+        out = C.c_void_p()
+        _check(L.load().ising_b200_model_from_string(text.encode(), C.byref(out)))
+        return cls(out.value)
+
+    @classmethod
+    def load(cls, path) -> "SpinModel":
+        out = C.c_void_p()
+        _check(L.load().ising_b200_model_load(str(path).encode(), C.byref(out)))
+        return cls(out.value)
+
+    def to_string(self) -> str:
+        out = C.c_void_p()
+        _check(L.load().ising_b200_model_to_string(self._h, C.byref(out)))
+        try:
+            return C.string_at(out.value).decode()
+        finally:
+            L.load().ising_b200_string_free(out)
+
+    def save(self, path) -> None:
+        _check(L.load().ising_b200_model_save(self._h, str(path).encode()))
+
     @property
     def n_spins(self) -> int:
         return L.load().ising_b200_model_spins(self._h)
@@ -311,3 +335,17 @@ def run_single(model: SpinModel, sweeps: int, beta: float, seed: int, tau_scale:
     r = L.RunReport()
     _check(L.load().ising_b200_run(model._h, C.byref(p), C.byref(r)))
     return {name: getattr(r, name) for name, _ in L.RunReport._fields_}
+
+
+def run_single_json(model: SpinModel, sweeps: int, beta: float, seed: int, tau_scale: float = 1.0,
+                    exp_kind: int = ExpKind.default, device: int = 0):
+    """ref: ising_run_json, include/isingmc.h:108-112 — (report dict, JSON text with the reference's keys)."""
+    p = L.RunParams(sweeps=sweeps, beta=beta, tau_scale=tau_scale, exp_kind=exp_kind, seed=seed, device=device)
+    r = L.RunReport()
+    out = C.c_void_p()
+    _check(L.load().ising_b200_run_json(model._h, C.byref(p), C.byref(r), C.byref(out)))
+    try:
+        text = C.string_at(out.value).decode()
+    finally:
+        L.load().ising_b200_string_free(out)
+    return {name: getattr(r, name) for name, _ in L.RunReport._fields_}, text

@@ -4,13 +4,17 @@
 // ISING_ERR_ARGUMENT and everything else (CUDA failures included) to ISING_ERR_INTERNAL.
 #include "isingmc_b200.h"
 
+#include <cinttypes>
+#include <cstdio>
 #include <cstring>
+#include <sys/utsname.h>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "batch.hpp"
 #include "host_model.hpp"
+#include "model_text.hpp"
 
 using namespace isingb200;
 
@@ -31,6 +35,12 @@ template <typename F>
 ising_status guarded(F&& body) {
     try {
         return body();
+    } catch (const ParseError& e) {
+        g_last_error = e.what();
+        return ISING_ERR_PARSE;
+    } catch (const IoError& e) {
+        g_last_error = e.what();
+        return ISING_ERR_IO;
     } catch (const Error& e) {
         g_last_error = e.what();
         return ISING_ERR_ARGUMENT;
@@ -50,6 +60,63 @@ void require(const void* p) {
 Batch& impl_of(ising_batch* b) {
     require(b);
     return *b->impl;
+}
+
+char* dup_string(const std::string& text) {
+    char* out = new (std::nothrow) char[text.size() + 1];
+    if (out != nullptr) std::memcpy(out, text.c_str(), text.size() + 1);
+    return out;
+}
+
+// One chain on the device: what ising_b200_run and ising_b200_run_json share.
+struct SingleRun {
+    ising_b200_run_report report;
+    int exp_kind;
+    int family;
+};
+
+int resolve_exp_kind(int kind);
+
+SingleRun run_single(const ising_b200_model* model, const ising_b200_run_params* params) {
+    require(model);
+    require(params);
+    BatchConfig cfg;
+    cfg.n_ladders = 1;
+    cfg.n_betas = 1;
+    cfg.betas = {params->beta};
+    cfg.seeds = {params->seed};
+    cfg.swap_seeds = {0u};
+    cfg.tau_scale = params->tau_scale;
+    cfg.exp_kind = resolve_exp_kind(params->exp_kind);
+    cfg.device = params->device;
+    Batch batch({&model->model}, {0u}, cfg, nullptr);
+    batch.run(params->sweeps, 0);
+    uint64_t flips = 0, attempts = 0, checksum = 0;
+    double cost = 0.0;
+    batch.read_stats(&flips, &attempts);
+    batch.read_energies(&cost);
+    batch.read_checksums(&checksum);
+    SingleRun out{};
+    out.report.final_cost = cost;
+    out.report.flips = flips;
+    out.report.attempts = attempts;
+    out.report.flip_rate = attempts ? double(flips) / double(attempts) : 0.0;
+    out.report.checksum = checksum;
+    out.exp_kind = cfg.exp_kind;
+    out.family = int(batch.family());
+    return out;
+}
+
+// Shortest decimal text that reads back as the same double (JSON number).
+std::string json_number(double v) {
+    char buf[40];
+    for (int digits = 1; digits <= 17; ++digits) {
+        std::snprintf(buf, sizeof buf, "%.*g", digits, v);
+        if (std::strtod(buf, nullptr) == v) break;
+    }
+    std::string text = buf;
+    if (text.find_first_of(".eEn") == std::string::npos) text += ".0";
+    return text;
 }
 
 int resolve_exp_kind(int kind) {
@@ -354,30 +421,86 @@ void* ising_batch_stream(ising_batch* batch) {
 ising_status ising_b200_run(const ising_b200_model* model, const ising_b200_run_params* params,
                             ising_b200_run_report* out) {
     return guarded([&]() {
-        require(model);
-        require(params);
         require(out);
-        BatchConfig cfg;
-        cfg.n_ladders = 1;
-        cfg.n_betas = 1;
-        cfg.betas = {params->beta};
-        cfg.seeds = {params->seed};
-        cfg.swap_seeds = {0u};
-        cfg.tau_scale = params->tau_scale;
-        cfg.exp_kind = resolve_exp_kind(params->exp_kind);
-        cfg.device = params->device;
-        Batch batch({&model->model}, {0u}, cfg, nullptr);
-        batch.run(params->sweeps, 0);
-        uint64_t flips = 0, attempts = 0, checksum = 0;
-        double cost = 0.0;
-        batch.read_stats(&flips, &attempts);
-        batch.read_energies(&cost);
-        batch.read_checksums(&checksum);
-        out->final_cost = cost;
-        out->flips = flips;
-        out->attempts = attempts;
-        out->flip_rate = attempts ? double(flips) / double(attempts) : 0.0;
-        out->checksum = checksum;
+        *out = run_single(model, params).report;
+        return ISING_OK;
+    });
+}
+
+ising_status ising_b200_run_json(const ising_b200_model* model, const ising_b200_run_params* params,
+                                 ising_b200_run_report* out_report, char** out_json) {
+    return guarded([&]() {
+        require(out_json);
+        const SingleRun run = run_single(model, params);
+        if (out_report != nullptr) *out_report = run.report;
+        static const char* const exp_names[] = {"?", "exact", "fast", "accurate"};
+        utsname u{};
+        std::string env = "unknown";
+        if (uname(&u) == 0) env = std::string(u.nodename) + " " + u.sysname + " " + u.release + " " + u.machine;
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, params->device) == cudaSuccess) env += std::string("; device=") + prop.name;
+        env += "; build=optimized; compiler=nvcc " + std::to_string(__CUDACC_VER_MAJOR__) + "." +
+               std::to_string(__CUDACC_VER_MINOR__);
+        char checksum[24];
+        std::snprintf(checksum, sizeof checksum, "%016" PRIx64, run.report.checksum);
+        // the keys of the reference's report (ref: capi.cpp:237-258), in its (alphabetical) dump order
+        std::string j = "{\n";
+        j += "  \"attempts\": " + std::to_string(run.report.attempts) + ",\n";
+        j += "  \"beta\": " + json_number(double(params->beta)) + ",\n";
+        j += std::string("  \"checksum\": \"") + checksum + "\",\n";
+        j += std::string("  \"engine\": \"") + (run.family == 2 ? "b200-layered" : "b200-generic") + "\",\n";
+        j += "  \"environment\": \"" + env + "\",\n";
+        j += std::string("  \"exp\": \"") + exp_names[run.exp_kind] + "\",\n";
+        j += "  \"final_cost\": " + json_number(run.report.final_cost) + ",\n";
+        j += "  \"flip_rate\": " + json_number(run.report.flip_rate) + ",\n";
+        j += "  \"flips\": " + std::to_string(run.report.flips) + ",\n";
+        j += "  \"seed\": " + std::to_string(params->seed) + ",\n";
+        j += "  \"spins\": " + std::to_string(model->model.n_spins) + ",\n";
+        j += "  \"sweeps\": " + std::to_string(params->sweeps) + ",\n";
+        j += "  \"tau_scale\": " + json_number(double(params->tau_scale)) + ",\n";
+        j += "  \"wait\": {},\n";  // one chain fills one lane: no lockstep groups to wait in
+        j += "  \"workers\": 1\n}";
+        *out_json = dup_string(j);
+        return *out_json != nullptr ? ISING_OK : ISING_ERR_INTERNAL;
+    });
+}
+
+// ---------------------------------------------------------------- model text I/O
+
+void ising_b200_string_free(char* text) { delete[] text; }
+
+ising_status ising_b200_model_from_string(const char* text, ising_b200_model** out) {
+    return guarded([&]() {
+        require(text);
+        require(out);
+        *out = new ising_b200_model{model_from_text(text)};
+        return ISING_OK;
+    });
+}
+
+ising_status ising_b200_model_to_string(const ising_b200_model* model, char** out) {
+    return guarded([&]() {
+        require(model);
+        require(out);
+        *out = dup_string(model_to_text(model->model));
+        return *out != nullptr ? ISING_OK : ISING_ERR_INTERNAL;
+    });
+}
+
+ising_status ising_b200_model_load(const char* path, ising_b200_model** out) {
+    return guarded([&]() {
+        require(path);
+        require(out);
+        *out = new ising_b200_model{load_model_text(path)};
+        return ISING_OK;
+    });
+}
+
+ising_status ising_b200_model_save(const ising_b200_model* model, const char* path) {
+    return guarded([&]() {
+        require(model);
+        require(path);
+        save_model_text(model->model, path);
         return ISING_OK;
     });
 }

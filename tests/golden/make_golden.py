@@ -109,10 +109,20 @@ def layered_builder(ref):
                         j_tau=np.float32(1.5), **{f"csr_{k}": v for k, v in csr.items()})
 
 
+def model_documents(ref):
+    """`ising-model v1` documents written by the reference's model_to_string (tests/test_model_text.py)."""
+    sys.path.insert(0, str(OUT.parent))
+    from test_model_text import sample_csrs
+    for name, csr in sample_csrs().items():
+        (OUT / f"model_{name}.txt").write_text(ref.model(csr).to_string())
+
+
 if __name__ == "__main__":
     po.build()
     reference = po.Reference()
-    primitives(reference)
-    trajectories(reference)
-    layered_builder(reference)
+    if "--documents-only" not in sys.argv:
+        primitives(reference)
+        trajectories(reference)
+        layered_builder(reference)
+    model_documents(reference)
     print("golden vectors written to", OUT)

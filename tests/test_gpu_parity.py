@@ -398,3 +398,28 @@ def test_wait_statistics_from_real_ballots(lib, port, kernel):
         assert prob == pytest.approx(grouped.mean())
     assert got[1][2] == int(flags.sum()) == int(flips_recorded) - flips_before
     assert got[32][0] >= got[16][0] >= got[1][0]  # wider groups wait more often
+
+
+def test_one_shot_run_json_has_the_reference_report_keys(lib, port, tmp_path):
+    """model file -> device run -> JSON report with the keys of ising_run_json
+    (ref: proj/src/capi.cpp:230-262)."""
+    import json
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 9), 4, 1.5)
+    path = tmp_path / "model.ising"
+    product_model(csr).save(path)
+    model = ib.SpinModel.load(path)
+    report, text = ib.run_single_json(model, 25, 0.7, 4321, tau_scale=1.25, exp_kind=ib.ExpKind.fast)
+    doc = json.loads(text)
+    assert set(doc) == {"engine", "exp", "spins", "sweeps", "beta", "tau_scale", "seed", "workers", "final_cost",
+                        "flip_rate", "flips", "attempts", "wait", "checksum", "environment"}
+    chain = port.chain(port.model(csr), 4321, 0.7, 1.25, 2, None)
+    chain.sweep(25)
+    assert doc["flips"] == report["flips"] == chain.flips and doc["attempts"] == 25 * 64
+    assert doc["checksum"] == f"{report['checksum']:016x}" == f"{port.checksum(chain.spins):016x}"
+    assert doc["final_cost"] == report["final_cost"]  # shortest round-trip decimal: same double
+    assert doc["final_cost"] == pytest.approx(port.total_cost(port.model(csr), chain.spins), rel=REL_ENERGY)
+    assert doc["flip_rate"] == report["flips"] / report["attempts"]
+    head = (doc["engine"], doc["exp"], doc["spins"], doc["sweeps"], doc["seed"], doc["workers"])
+    assert head == ("b200-layered", "fast", 64, 25, 4321, 1)
+    assert doc["beta"] == float(np.float32(0.7)) and doc["tau_scale"] == 1.25 and doc["wait"] == {}
+    assert "device=" in doc["environment"]
