@@ -349,3 +349,151 @@ int orc_pt_run(const orc_model* const* models, uint32_t n_ladders, uint32_t n_be
     pthread_mutex_destroy(&job.lock);
     return job.failed ? -1 : 0;
 }
+
+
+/* ======================================================================================
+ * The coalesced schedule (ref: proj/src/sweep_coalesced.cpp).
+ * ====================================================================================== */
+orc_coalesced* orc_coalesced_create(const orc_model* m, uint32_t seed, float beta, float tau_scale,
+                                    int exp_kind, const int8_t* initial) {
+    if (m->layers < 4 || m->layers % 2 != 0 || (uint64_t)m->layers * m->per_layer != m->n_spins) return NULL;
+    orc_coalesced* c = (orc_coalesced*)calloc(1, sizeof *c);
+    if (!c) return NULL;
+    const uint32_t n = m->n_spins, W = m->layers / 2, P = m->per_layer;
+    c->n = n;
+    c->lanes = W;
+    c->per_layer = P;
+    c->beta = beta;
+    c->tau_scale = tau_scale;
+    c->exp_kind = exp_kind;
+    /* coalesce_permutation, model.cpp:190-215 */
+    c->forward = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    uint32_t* inverse = (uint32_t*)malloc(sizeof(uint32_t) * n);
+    for (uint32_t l = 0; l < m->layers; ++l) {
+        for (uint32_t p = 0; p < P; ++p) {
+            const uint32_t old_index = l * P + p, new_index = W * ((l % 2) * P + p) + l / 2;
+            c->forward[old_index] = new_index;
+            inverse[new_index] = old_index;
+        }
+    }
+    /* apply_permutation, model.cpp:217-245: spin new_index takes the edge list of its old spin,
+     * in the old order, with the targets renamed */
+    orc_model* q = &c->permuted;
+    const uint32_t edges = m->offsets[n];
+    q->n_spins = n;
+    q->layers = m->layers;
+    q->per_layer = P;
+    float* h = (float*)malloc(sizeof(float) * n);
+    uint32_t* offsets = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t* targets = (uint32_t*)malloc(sizeof(uint32_t) * (edges ? edges : 1));
+    float* couplings = (float*)malloc(sizeof(float) * (edges ? edges : 1));
+    uint8_t* tau_counts = (uint8_t*)malloc(n);
+    uint32_t k = 0;
+    for (uint32_t ni = 0; ni < n; ++ni) {
+        const uint32_t oi = inverse[ni];
+        h[ni] = m->h[oi];
+        offsets[ni] = k;
+        tau_counts[ni] = m->tau_counts ? m->tau_counts[oi] : 0;
+        for (uint32_t e = m->offsets[oi]; e < m->offsets[oi + 1]; ++e) {
+            targets[k] = c->forward[m->targets[e]];
+            couplings[k] = m->couplings[e];
+            ++k;
+        }
+    }
+    offsets[n] = k;
+    free(inverse);
+    q->h = h;
+    q->offsets = offsets;
+    q->targets = targets;
+    q->couplings = couplings;
+    q->tau_counts = tau_counts;
+    /* init_state on the permuted model: spins drawn / taken in the NEW order (sweep_state.cpp:218-234) */
+    c->spins = (float*)malloc(sizeof(float) * 3 * (size_t)n);
+    c->hs = c->spins + n;
+    c->ht = c->hs + n;
+    c->flags = (uint8_t*)calloc(n, 1);
+    if (initial) {
+        for (uint32_t i = 0; i < n; ++i) c->spins[i] = (float)initial[i];
+    } else {
+        int8_t* tmp = (int8_t*)malloc(n);
+        orc_initial_spins(n, seed, tmp);
+        for (uint32_t i = 0; i < n; ++i) c->spins[i] = (float)tmp[i];
+        free(tmp);
+    }
+    orc_recompute_fields(q, c->spins, c->hs, c->ht);
+    /* InterlacedMt::with_base_seed(seed, W): lane k is Mt19937(seed + k) (rng.cpp:144-148) */
+    c->lane_rng = (orc_mt*)malloc(sizeof(orc_mt) * W);
+    for (uint32_t t = 0; t < W; ++t) orc_mt_seed(&c->lane_rng[t], seed + t);
+    return c;
+}
+
+void orc_coalesced_free(orc_coalesced* c) {
+    if (!c) return;
+    free((void*)c->permuted.h);
+    free((void*)c->permuted.offsets);
+    free((void*)c->permuted.targets);
+    free((void*)c->permuted.couplings);
+    free((void*)c->permuted.tau_counts);
+    free(c->forward);
+    free(c->spins);
+    free(c->flags);
+    free(c->lane_rng);
+    free(c);
+}
+
+/* flip_phase, sweep_coalesced.cpp:45-83.  The uniform of (region, p, lane t) is output number
+ * region*P + p of lane t's generator in this sweep (fill_unit_floats writes block b of all lanes
+ * at [b*W, (b+1)*W), rng.hpp:51-53): drawing lane by lane in p order is the same stream. */
+static void coalesced_flip_phase(orc_coalesced* c, uint32_t region_base) {
+    const orc_model* q = &c->permuted;
+    const uint32_t W = c->lanes, P = c->per_layer;
+    for (uint32_t p = 0; p < P; ++p) {
+        for (uint32_t t = 0; t < W; ++t) {
+            const uint32_t i = region_base + W * p + t;
+            const float u = orc_u32_to_unit(orc_mt_next(&c->lane_rng[t]));
+            const float s = c->spins[i];
+            const float x = -c->beta * (2.0f * s * (c->hs[i] + c->tau_scale * c->ht[i]));
+            const float prob = orc_exp_kind(c->exp_kind, x);
+            if (u < prob) {
+                const float two_s = 2.0f * s;
+                const uint32_t end = q->offsets[i + 1];
+                for (uint32_t e = q->offsets[i]; e < end - 2; ++e) c->hs[q->targets[e]] -= two_s * q->couplings[e];
+                c->ht[q->targets[end - 1]] -= two_s * q->couplings[end - 1]; /* previous layer now */
+                c->spins[i] = -s;
+                c->flags[i] = 1;
+                ++c->flips;
+            }
+        }
+    }
+}
+
+/* deferred_tau_phase, sweep_coalesced.cpp:87-104 */
+static void coalesced_deferred_phase(orc_coalesced* c, uint32_t region_base) {
+    const orc_model* q = &c->permuted;
+    const uint32_t W = c->lanes, P = c->per_layer;
+    for (uint32_t p = 0; p < P; ++p) {
+        for (uint32_t t = 0; t < W; ++t) {
+            const uint32_t i = region_base + W * p + t;
+            if (!c->flags[i]) continue;
+            const float two_s = -2.0f * c->spins[i]; /* twice the pre-flip spin */
+            const uint32_t up = q->offsets[i + 1] - 2;
+            c->ht[q->targets[up]] -= two_s * q->couplings[up];
+        }
+    }
+}
+
+void orc_coalesced_sweep(orc_coalesced* c, uint64_t sweeps) {
+    const uint32_t odd_base = c->lanes * c->per_layer;
+    for (uint64_t sw = 0; sw < sweeps; ++sw) {
+        coalesced_flip_phase(c, 0);
+        coalesced_deferred_phase(c, 0);
+        coalesced_flip_phase(c, odd_base);
+        coalesced_deferred_phase(c, odd_base);
+        c->attempts += c->n;
+        memset(c->flags, 0, c->n);
+    }
+}
+
+void orc_coalesced_read_spins(const orc_coalesced* c, int8_t* out) {
+    for (uint32_t i = 0; i < c->n; ++i) out[i] = c->spins[c->forward[i]] > 0.0f ? 1 : -1;
+}

@@ -55,6 +55,7 @@ typedef struct orc_model {
     const uint32_t* targets;    /* offsets[n] half-edges */
     const float* couplings;     /* offsets[n] */
     const uint8_t* tau_counts;  /* n_spins: trailing tau edges per spin */
+    uint32_t layers, per_layer; /* LayeredMeta (model.hpp:44-50); 0, 0 for generic models */
 } orc_model;
 
 /* src/sweep_state.cpp:211-216 */
@@ -101,6 +102,32 @@ void orc_chain_sweep(orc_chain* c, const orc_model* m, uint64_t sweeps);
  *   - E is the running energy: total_cost of the initial spins, plus
  *     (double)((2.0f*s)*(hs+ht)) at each accepted flip, in flip order.
  */
+/* ---- the intra-system "coalesced" schedule (ref: proj/src/sweep_coalesced.cpp:10-124; model
+ * permutation proj/src/model.cpp:190-215; init proj/src/sweep_state.cpp:120-146,193-199).
+ * W = layers/2 lanes; lane t owns layers 2t (even region) and 2t+1 (odd region); spin (l,p) lives
+ * at new index W*((l%2)*P + p) + l/2.  One sweep = even flips (space edges + tau edge down),
+ * deferred tau edges up, odd flips, deferred tau edges up; lane t draws from Mt19937(seed + t).
+ * The model given here is the ORIGINAL (identity-ordered) layered model; all arrays of the
+ * state are in the new index order, `forward[old] = new`. */
+typedef struct orc_coalesced {
+    uint32_t n, lanes, per_layer;
+    float beta, tau_scale;
+    int exp_kind;
+    orc_model permuted;   /* owned: CSR of the permuted model (edge order of the original lists) */
+    uint32_t* forward;    /* old index -> new index */
+    float *spins, *hs, *ht;
+    uint8_t* flags;
+    orc_mt* lane_rng;     /* lanes generators */
+    uint64_t flips, attempts;
+} orc_coalesced;
+
+orc_coalesced* orc_coalesced_create(const orc_model* m, uint32_t seed, float beta, float tau_scale,
+                                    int exp_kind, const int8_t* initial_new_order);
+void orc_coalesced_free(orc_coalesced* c);
+void orc_coalesced_sweep(orc_coalesced* c, uint64_t sweeps);
+/* spins in the ORIGINAL spin order (+1/-1) */
+void orc_coalesced_read_spins(const orc_coalesced* c, int8_t* out);
+
 typedef struct orc_pt_result {
     int8_t* spins;        /* n_chains * n : +/-1 */
     uint64_t* flips;      /* n_chains */

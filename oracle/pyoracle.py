@@ -40,7 +40,7 @@ def _p(a, ctype):
 
 class _Model(C.Structure):
     _fields_ = [("n_spins", C.c_uint32), ("h", f32p), ("offsets", u32p), ("targets", u32p),
-                ("couplings", f32p), ("tau_counts", u8p)]
+                ("couplings", f32p), ("tau_counts", u8p), ("layers", C.c_uint32), ("per_layer", C.c_uint32)]
 
 
 class _PtResult(C.Structure):
@@ -56,6 +56,13 @@ class _Chain(C.Structure):
     _fields_ = [("n", C.c_uint32), ("beta", C.c_float), ("tau_scale", C.c_float), ("exp_kind", C.c_int),
                 ("spins", f32p), ("hs", f32p), ("ht", f32p), ("rng", _Mt), ("flips", C.c_uint64),
                 ("attempts", C.c_uint64), ("e_run", C.c_double)]
+
+
+class _Coalesced(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("lanes", C.c_uint32), ("per_layer", C.c_uint32), ("beta", C.c_float),
+                ("tau_scale", C.c_float), ("exp_kind", C.c_int), ("permuted", _Model), ("forward", u32p),
+                ("spins", f32p), ("hs", f32p), ("ht", f32p), ("flags", u8p), ("lane_rng", C.c_void_p),
+                ("flips", C.c_uint64), ("attempts", C.c_uint64)]
 
 
 def _canon(csr: dict) -> dict:
@@ -98,6 +105,11 @@ class Port:
         lib.orc_chain_create.argtypes = [C.POINTER(_Model), C.c_uint32, C.c_float, C.c_float, C.c_int, i8p]
         lib.orc_chain_free.argtypes = [C.POINTER(_Chain)]
         lib.orc_chain_sweep.argtypes = [C.POINTER(_Chain), C.POINTER(_Model), C.c_uint64]
+        lib.orc_coalesced_create.restype = C.POINTER(_Coalesced)
+        lib.orc_coalesced_create.argtypes = [C.POINTER(_Model), C.c_uint32, C.c_float, C.c_float, C.c_int, i8p]
+        lib.orc_coalesced_free.argtypes = [C.POINTER(_Coalesced)]
+        lib.orc_coalesced_sweep.argtypes = [C.POINTER(_Coalesced), C.c_uint64]
+        lib.orc_coalesced_read_spins.argtypes = [C.POINTER(_Coalesced), i8p]
         lib.orc_pt_run.restype = C.c_int
         lib.orc_pt_run.argtypes = [C.POINTER(C.POINTER(_Model)), C.c_uint32, C.c_uint32, f32p, u32p, u32p,
                                    C.c_float, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, i8p,
@@ -126,7 +138,7 @@ class Port:
         keep = _canon(csr)
         m = _Model(keep["n_spins"], _p(keep["h"], C.c_float), _p(keep["offsets"], C.c_uint32),
                    _p(keep["targets"], C.c_uint32), _p(keep["couplings"], C.c_float),
-                   _p(keep["tau_counts"], C.c_uint8))
+                   _p(keep["tau_counts"], C.c_uint8), int(csr.get("layers") or 0), int(csr.get("per_layer") or 0))
         m._keep = keep
         return m
 
@@ -147,6 +159,9 @@ class Port:
     # --- one chain (SweepState)
     def chain(self, model, seed, beta, tau_scale=1.0, exp_kind=EXP_FAST, initial=None):
         return PortChain(self, model, seed, beta, tau_scale, exp_kind, initial)
+
+    def coalesced(self, model, seed, beta, tau_scale=1.0, exp_kind=EXP_FAST, initial_new_order=None):
+        return PortCoalesced(self, model, seed, beta, tau_scale, exp_kind, initial_new_order)
 
     # --- batch with tempering
     def pt_run(self, models, n_ladders, betas, seeds, swap_seeds, sweeps, swap_interval, tau_scale=1.0,
@@ -173,6 +188,60 @@ class Port:
         if rc != 0:
             raise RuntimeError("orc_pt_run failed")
         return res
+
+
+class PortCoalesced:
+    """The plain-C restatement of the reference's coalesced engine on one chain."""
+
+    def __init__(self, port, model, seed, beta, tau_scale, exp_kind, initial_new_order):
+        self.port, self.model = port, model
+        init = None if initial_new_order is None else np.ascontiguousarray(initial_new_order, np.int8)
+        self.ptr = port.lib.orc_coalesced_create(C.byref(model), seed, beta, tau_scale, exp_kind, _p(init, C.c_int8))
+        if not self.ptr:
+            raise ValueError("coalesced: needs a layered model with an even layer count >= 4")
+        self.n = model.n_spins
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            self.port.lib.orc_coalesced_free(self.ptr)
+            self.ptr = None
+
+    def sweep(self, sweeps: int = 1):
+        self.port.lib.orc_coalesced_sweep(self.ptr, sweeps)
+
+    def _new_order(self, p):
+        return np.ctypeslib.as_array(p, shape=(self.n,)).copy()
+
+    @property
+    def forward(self):
+        return self._new_order(self.ptr.contents.forward)
+
+    @property
+    def spins_new_order(self):
+        return self._new_order(self.ptr.contents.spins)
+
+    @property
+    def hs_new_order(self):
+        return self._new_order(self.ptr.contents.hs)
+
+    @property
+    def ht_new_order(self):
+        return self._new_order(self.ptr.contents.ht)
+
+    @property
+    def spins(self):
+        """+1/-1 in the ORIGINAL spin order."""
+        out = np.empty(self.n, np.int8)
+        self.port.lib.orc_coalesced_read_spins(self.ptr, _p(out, C.c_int8))
+        return out
+
+    @property
+    def flips(self):
+        return int(self.ptr.contents.flips)
+
+    @property
+    def attempts(self):
+        return int(self.ptr.contents.attempts)
 
 
 class PortChain:
@@ -256,6 +325,8 @@ class Reference:
         lib.ref_model_half_edges.restype = C.c_uint64
         lib.ref_model_half_edges.argtypes = [C.c_void_p]
         lib.ref_model_export.argtypes = [C.c_void_p, f32p, u32p, u32p, f32p, u8p]
+        lib.ref_prepare_model.restype = C.c_void_p
+        lib.ref_prepare_model.argtypes = [C.c_void_p, C.c_int, u32p]
         lib.ref_model_to_string.restype = C.c_long
         lib.ref_model_to_string.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
         lib.ref_model_from_string.restype = C.c_void_p
@@ -384,6 +455,14 @@ class RefModel:
     def validate(self):
         """None when valid, otherwise the reference's error message."""
         return None if self.ref.lib.ref_model_validate(self.handle) == 0 else self.ref.error()
+
+    def prepared_for(self, engine: int):
+        """The reference's prepare_model_for_engine (sweep_state.cpp:292-323): (permuted model, forward)."""
+        forward = np.empty(self.n_spins, np.uint32)
+        handle = self.ref.lib.ref_prepare_model(self.handle, engine, _p(forward, C.c_uint32))
+        if not handle:
+            raise ValueError(self.ref.error())
+        return type(self)(self.ref, None, handle), forward
 
     def to_string(self) -> str:
         """The reference's model_to_string (model_io.cpp:45-72)."""

@@ -93,6 +93,19 @@ void* ref_build_layered(uint32_t positions, const float* h, uint32_t n_edges, co
 
 void ref_model_free(void* m) { delete static_cast<SpinModel*>(m); }
 
+// prepare_model_for_engine (sweep_state.cpp:292-323): the permuted copy an engine needs, and the
+// permutation (forward[old] = new) it was built with.
+void* ref_prepare_model(const void* m, int engine, uint32_t* forward) {
+    try {
+        auto prepared = prepare_model_for_engine(*static_cast<const SpinModel*>(m), engine_of(engine));
+        if (forward != nullptr) std::copy(prepared.second.forward.begin(), prepared.second.forward.end(), forward);
+        return new SpinModel(std::move(prepared.first));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 // `ising-model v1` documents through the reference's own reader and writer (model_io.cpp).
 // to_string: returns the length, copies at most `capacity` bytes; -1 on error.
 long ref_model_to_string(const void* m, char* out, size_t capacity) {
