@@ -235,6 +235,52 @@ ISING_B200_API ising_status ising_b200_run(const ising_b200_model* model, const 
 ISING_B200_API ising_status ising_b200_run_json(const ising_b200_model* model, const ising_b200_run_params* params,
                                                  ising_b200_run_report* out_report, char** out_json);
 
+/* ------------------------------------------- coalesced (intra-system) batches ---- */
+/* The reference's `coalesced` engine on the device (ref: EngineKind::coalesced, include/isingmc/
+ * sweep.hpp:16; src/sweep_coalesced.cpp:10-124; prepare_model_for_engine + coalesce_permutation,
+ * src/sweep_state.cpp:292-323, src/model.cpp:190-215): one warp per chain, W = layers/2 lanes, lane t
+ * owns layers 2t and 2t+1 and draws from Mt19937(seed + t); four phases per sweep.  For few chains
+ * of a large layered system, where one chain per lane cannot fill the GPU.  The model is the
+ * ORIGINAL identity-ordered layered model (the permutation is applied internally, every readout is
+ * in the original spin order) and must stay alive as long as the batch.  Needs an even layer count
+ * <= 64 and half the spins within 227 KB of shared memory at 9 bytes per spin.  Chains are
+ * independent (this engine has no tempering in the reference either). */
+typedef struct ising_coalesced_params {
+    uint32_t n_chains;
+    const float* betas;          /* n_chains */
+    const uint32_t* seeds;       /* n_chains, or NULL: base_seed + c * (layers/2) (disjoint lane seeds) */
+    uint32_t base_seed;
+    float tau_scale;
+    int exp_kind;                /* ising_exp_kind */
+    int device;
+    const int8_t* initial_spins; /* NULL: initial_spins(n, seed) in the permuted order, exactly what the
+                                    reference's init_state(permuted model, cfg) draws; else
+                                    [n_chains][n_spins] of +/-1 in the ORIGINAL order */
+} ising_coalesced_params;
+
+typedef struct ising_coalesced_info {
+    uint64_t n_chains;
+    uint32_t n_spins;
+    uint32_t lanes;
+    uint64_t sweeps_done;
+    uint64_t launches;
+    double last_run_ms; /* CUDA-event time of the last ising_coalesced_run call */
+} ising_coalesced_info;
+
+typedef struct ising_coalesced ising_coalesced;
+
+ISING_B200_API ising_status ising_coalesced_create(const ising_b200_model* model,
+                                                    const ising_coalesced_params* params, ising_coalesced** out);
+ISING_B200_API void ising_coalesced_free(ising_coalesced* batch);
+/* ref: run_sweeps_coalesced, src/sweep_coalesced.cpp:139-178 (asynchronous; readouts synchronise) */
+ISING_B200_API ising_status ising_coalesced_run(ising_coalesced* batch, uint64_t sweeps);
+ISING_B200_API ising_status ising_coalesced_read_spins(ising_coalesced* batch, uint64_t chain, int8_t* out);
+ISING_B200_API ising_status ising_coalesced_read_fields(ising_coalesced* batch, uint64_t chain, float* hs, float* ht);
+ISING_B200_API ising_status ising_coalesced_read_stats(ising_coalesced* batch, uint64_t* flips, uint64_t* attempts);
+ISING_B200_API ising_status ising_coalesced_read_energies(ising_coalesced* batch, double* out);
+ISING_B200_API ising_status ising_coalesced_checksums(ising_coalesced* batch, uint64_t* out);
+ISING_B200_API ising_status ising_coalesced_get_info(ising_coalesced* batch, ising_coalesced_info* out);
+
 /* ------------------------------------------------------- model text documents ---- */
 /* `ising-model v1` documents (ref: include/isingmc/model_io.hpp:10-28, src/model_io.cpp:45-226;
  * C entry points ising_model_load / _from_string / _to_string / ising_string_free, include/isingmc.h:

@@ -6,13 +6,13 @@ in include/isingmc_b200.h); this package is the ctypes binding plus the host-sid
 reference's sweep interface.  There is no CPU fallback: importing works anywhere, creating a
 batch needs the built library and a CUDA device.
 """
-from .api import (BatchState, ExpKind, IsingError, LayerSpec, SpinModel, SweepParams,
+from .api import (BatchState, CoalescedState, init_coalesced, ExpKind, IsingError, LayerSpec, SpinModel, SweepParams,
                   build_layered_model, init_state, run_single, run_single_json, run_sweeps, state_checksum,
                   total_cost)
 from ._lib import KERNEL_AUTO, KERNEL_GENERIC, KERNEL_LAYERED
 
 __all__ = [
-    "BatchState", "ExpKind", "IsingError", "LayerSpec", "SpinModel", "SweepParams",
+    "BatchState", "CoalescedState", "init_coalesced", "ExpKind", "IsingError", "LayerSpec", "SpinModel", "SweepParams",
     "build_layered_model", "init_state", "run_single", "run_single_json", "run_sweeps", "state_checksum",
     "total_cost",
     "KERNEL_AUTO", "KERNEL_GENERIC", "KERNEL_LAYERED",

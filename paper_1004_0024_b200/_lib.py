@@ -37,6 +37,16 @@ class BatchInfo(C.Structure):
     ]
 
 
+class CoalescedParams(C.Structure):
+    _fields_ = [("n_chains", C.c_uint32), ("betas", f32p), ("seeds", u32p), ("base_seed", C.c_uint32),
+                ("tau_scale", C.c_float), ("exp_kind", C.c_int), ("device", C.c_int), ("initial_spins", i8p)]
+
+
+class CoalescedInfo(C.Structure):
+    _fields_ = [("n_chains", C.c_uint64), ("n_spins", C.c_uint32), ("lanes", C.c_uint32),
+                ("sweeps_done", C.c_uint64), ("launches", C.c_uint64), ("last_run_ms", C.c_double)]
+
+
 class RunParams(C.Structure):
     _fields_ = [("sweeps", C.c_uint64), ("beta", C.c_float), ("tau_scale", C.c_float),
                 ("exp_kind", C.c_int), ("seed", C.c_uint32), ("device", C.c_int)]
@@ -82,6 +92,15 @@ SIGNATURES = {
     "ising_batch_read_wait_stats": (C.c_int, [C.c_void_p, C.c_uint32, u32p, f64p, u64p, u64p]),
     "ising_batch_get_info": (C.c_int, [C.c_void_p, C.POINTER(BatchInfo)]),
     "ising_batch_stream": (C.c_void_p, [C.c_void_p]),
+    "ising_coalesced_create": (C.c_int, [C.c_void_p, C.POINTER(CoalescedParams), C.POINTER(C.c_void_p)]),
+    "ising_coalesced_free": (None, [C.c_void_p]),
+    "ising_coalesced_run": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "ising_coalesced_read_spins": (C.c_int, [C.c_void_p, C.c_uint64, i8p]),
+    "ising_coalesced_read_fields": (C.c_int, [C.c_void_p, C.c_uint64, f32p, f32p]),
+    "ising_coalesced_read_stats": (C.c_int, [C.c_void_p, u64p, u64p]),
+    "ising_coalesced_read_energies": (C.c_int, [C.c_void_p, f64p]),
+    "ising_coalesced_checksums": (C.c_int, [C.c_void_p, u64p]),
+    "ising_coalesced_get_info": (C.c_int, [C.c_void_p, C.POINTER(CoalescedInfo)]),
     "ising_b200_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(RunReport)]),
     "ising_b200_run_json": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.POINTER(RunReport),
                                       C.POINTER(C.c_void_p)]),

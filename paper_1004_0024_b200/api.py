@@ -278,6 +278,78 @@ class BatchState:
         return {name: getattr(info, name) for name, _ in L.BatchInfo._fields_}
 
 
+class CoalescedState:
+    """Device-resident chains swept with the intra-system schedule (ref: EngineKind::coalesced;
+    SweepState for that engine, sweep.hpp:85-121).  Readouts are in the original spin order."""
+
+    def __init__(self, handle: int, model: SpinModel, n_chains: int):
+        self._h, self._model, self.n_chains, self.n_spins = handle, model, n_chains, model.n_spins
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            L.load().ising_coalesced_free(h)
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def run(self, sweeps: int) -> None:
+        _check(L.load().ising_coalesced_run(self._h, sweeps))
+
+    def spins(self, chain: int = 0) -> np.ndarray:
+        out = np.empty(self.n_spins, np.int8)
+        _check(L.load().ising_coalesced_read_spins(self._h, chain, _p(out, C.c_int8)))
+        return out
+
+    def fields(self, chain: int = 0):
+        hs, ht = np.empty(self.n_spins, np.float32), np.empty(self.n_spins, np.float32)
+        _check(L.load().ising_coalesced_read_fields(self._h, chain, _p(hs, C.c_float), _p(ht, C.c_float)))
+        return hs, ht
+
+    def stats(self):
+        flips, attempts = np.empty(self.n_chains, np.uint64), np.empty(self.n_chains, np.uint64)
+        _check(L.load().ising_coalesced_read_stats(self._h, _p(flips, C.c_uint64), _p(attempts, C.c_uint64)))
+        return flips, attempts
+
+    def energies(self) -> np.ndarray:
+        out = np.empty(self.n_chains, np.float64)
+        _check(L.load().ising_coalesced_read_energies(self._h, _p(out, C.c_double)))
+        return out
+
+    def checksums(self) -> np.ndarray:
+        out = np.empty(self.n_chains, np.uint64)
+        _check(L.load().ising_coalesced_checksums(self._h, _p(out, C.c_uint64)))
+        return out
+
+    def info(self) -> dict:
+        info = L.CoalescedInfo()
+        _check(L.load().ising_coalesced_get_info(self._h, C.byref(info)))
+        return {name: getattr(info, name) for name, _ in L.CoalescedInfo._fields_}
+
+
+def init_coalesced(model: SpinModel, betas, *, seeds=None, base_seed: int = 1, params: SweepParams = SweepParams(),
+                   initial_spins=None, device: int = 0) -> CoalescedState:
+    """ref: prepare_model_for_engine(model, coalesced) + init_state per chain (sweep_state.cpp:218-323)."""
+    betas_a = _arr(np.atleast_1d(betas), np.float32)
+    seeds_a = None if seeds is None else _arr(seeds, np.uint32)
+    if seeds_a is not None and seeds_a.size != betas_a.size:
+        raise IsingError(L.ISING_ERR_ARGUMENT, "init_state: seed count mismatch")
+    init = None if initial_spins is None else _arr(initial_spins, np.int8)
+    if init is not None and init.size != betas_a.size * model.n_spins:
+        raise IsingError(L.ISING_ERR_ARGUMENT, "init_state: initial spin count mismatch")
+    p = L.CoalescedParams(n_chains=betas_a.size, betas=_p(betas_a, C.c_float), seeds=_p(seeds_a, C.c_uint32),
+                          base_seed=base_seed, tau_scale=params.tau_scale, exp_kind=int(params.exp_kind),
+                          device=device, initial_spins=_p(init, C.c_int8))
+    out = C.c_void_p()
+    _check(L.load().ising_coalesced_create(model._h, C.byref(p), C.byref(out)))
+    return CoalescedState(out.value, model, int(betas_a.size))
+
+
 def init_state(models, betas, n_ladders: int = 1, *, seeds=None, swap_seeds=None, base_seed: int = 1,
                swap_base_seed: int = 1, first_ladder: int = 0, params: SweepParams = SweepParams(),
                model_of_ladder=None, initial_spins=None, device: int = 0,

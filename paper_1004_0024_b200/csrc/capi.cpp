@@ -8,11 +8,13 @@
 #include <cstdio>
 #include <cstring>
 #include <sys/utsname.h>
+#include <memory>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "batch.hpp"
+#include "coalesced.hpp"
 #include "host_model.hpp"
 #include "model_text.hpp"
 
@@ -24,6 +26,9 @@ struct ising_b200_model {
 };
 struct ising_batch {
     Batch* impl;
+};
+struct ising_coalesced {
+    CoalescedBatch* impl;
 };
 }
 
@@ -462,6 +467,100 @@ ising_status ising_b200_run_json(const ising_b200_model* model, const ising_b200
         j += "  \"workers\": 1\n}";
         *out_json = dup_string(j);
         return *out_json != nullptr ? ISING_OK : ISING_ERR_INTERNAL;
+    });
+}
+
+// ---------------------------------------------------------------- coalesced (intra-system) batches
+
+ising_status ising_coalesced_create(const ising_b200_model* model, const ising_coalesced_params* params,
+                                    ising_coalesced** out) {
+    return guarded([&]() {
+        require(model);
+        require(params);
+        require(out);
+        if (params->n_chains == 0 || params->betas == nullptr) throw Error("null argument");
+        CoalescedConfig cfg;
+        cfg.betas.assign(params->betas, params->betas + params->n_chains);
+        cfg.seeds.resize(params->n_chains);
+        for (uint32_t c = 0; c < params->n_chains; ++c) {
+            cfg.seeds[c] = params->seeds != nullptr ? params->seeds[c] : params->base_seed + c * (model->model.layers / 2);
+        }
+        cfg.tau_scale = params->tau_scale;
+        cfg.exp_kind = resolve_exp_kind(params->exp_kind);
+        cfg.device = params->device;
+        auto impl = std::make_unique<CoalescedBatch>(model->model, cfg, params->initial_spins);
+        *out = new ising_coalesced{impl.release()};
+        return ISING_OK;
+    });
+}
+
+void ising_coalesced_free(ising_coalesced* batch) {
+    if (batch != nullptr) {
+        delete batch->impl;
+        delete batch;
+    }
+}
+
+namespace {
+CoalescedBatch& coalesced_of(ising_coalesced* b) {
+    require(b);
+    return *b->impl;
+}
+}  // namespace
+
+ising_status ising_coalesced_run(ising_coalesced* batch, uint64_t sweeps) {
+    return guarded([&]() {
+        coalesced_of(batch).run(sweeps);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_coalesced_read_spins(ising_coalesced* batch, uint64_t chain, int8_t* out) {
+    return guarded([&]() {
+        coalesced_of(batch).read_spins(chain, out);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_coalesced_read_fields(ising_coalesced* batch, uint64_t chain, float* hs, float* ht) {
+    return guarded([&]() {
+        coalesced_of(batch).read_fields(chain, hs, ht);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_coalesced_read_stats(ising_coalesced* batch, uint64_t* flips, uint64_t* attempts) {
+    return guarded([&]() {
+        coalesced_of(batch).read_stats(flips, attempts);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_coalesced_read_energies(ising_coalesced* batch, double* out) {
+    return guarded([&]() {
+        coalesced_of(batch).read_energies(out);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_coalesced_checksums(ising_coalesced* batch, uint64_t* out) {
+    return guarded([&]() {
+        coalesced_of(batch).read_checksums(out);
+        return ISING_OK;
+    });
+}
+
+ising_status ising_coalesced_get_info(ising_coalesced* batch, ising_coalesced_info* out) {
+    return guarded([&]() {
+        CoalescedBatch& b = coalesced_of(batch);
+        require(out);
+        out->n_chains = b.n_chains();
+        out->n_spins = b.n_spins();
+        out->lanes = b.lanes();
+        out->sweeps_done = b.sweeps_done();
+        out->launches = b.launches;
+        out->last_run_ms = b.last_run_ms();
+        return ISING_OK;
     });
 }
 

@@ -1,0 +1,78 @@
+"""The intra-system (`coalesced`) schedule on the device against the plain-C
+restatement of the reference's coalesced engine (itself pinned to the reference every sweep in
+tests/test_oracle_coalesced.py): spins, both field arrays and flip counts bit for bit."""
+import numpy as np
+import pytest
+
+import paper_1004_0024_b200 as ib
+from paper_1004_0024_b200 import _lib
+from helpers import ins, product_model
+
+pytestmark = pytest.mark.gpu
+
+
+def permuted_to_original(values, forward):
+    return values[forward]
+
+
+@pytest.mark.parametrize("positions,layers,exp_kind", [
+    (12, 4, 2), (16, 8, 1), (24, 6, 3), (40, 64, 2), (512, 64, 2), (96, 10, 2),
+])
+def test_coalesced_matches_the_oracle(lib, port, positions, layers, exp_kind):
+    csr = ins.build_layered_csr(*ins.layered_spec(positions, 31 + positions), layers, 1.25)
+    betas = [0.4, 0.9, 2.5]
+    seeds = [777, 5000, 123456]
+    sweeps = 9 if positions < 512 else 4
+    chains = [port.coalesced(port.model(csr), s, b, 1.5, exp_kind) for s, b in zip(seeds, betas)]
+    with ib.init_coalesced(product_model(csr), betas, seeds=seeds, params=ib.SweepParams(1.5, exp_kind)) as st:
+        assert st.info()["lanes"] == layers // 2
+        for part in (0, 1, sweeps - 1):   # the initial state, then two launches
+            if part:
+                st.run(part)
+                for c in chains:
+                    c.sweep(part)
+            for k, c in enumerate(chains):
+                np.testing.assert_array_equal(st.spins(k), c.spins)
+                hs, ht = st.fields(k)
+                np.testing.assert_array_equal(hs.view(np.uint32), c.hs_new_order[c.forward].view(np.uint32))
+                np.testing.assert_array_equal(ht.view(np.uint32), c.ht_new_order[c.forward].view(np.uint32))
+            flips, attempts = st.stats()
+            assert flips.tolist() == [c.flips for c in chains]
+            assert attempts.tolist() == [c.attempts for c in chains]
+        model = port.model(csr)
+        energies, checksums = st.energies(), st.checksums()
+        for k, c in enumerate(chains):
+            assert energies[k] == port.total_cost(model, c.spins)
+            assert int(checksums[k]) == port.checksum(c.spins)
+
+
+def test_coalesced_given_initial_spins_and_default_seeds(lib, port):
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 3), 6, 0.75)
+    n = csr["n_spins"]
+    rng = np.random.default_rng(5)
+    initial = (1 - 2 * rng.integers(0, 2, size=(2, n))).astype(np.int8)  # original order
+    with ib.init_coalesced(product_model(csr), [0.7, 1.1], base_seed=40, initial_spins=initial) as st:
+        np.testing.assert_array_equal(st.spins(1), initial[1])
+        st.run(6)
+        for k, beta in enumerate([0.7, 1.1]):
+            probe = port.coalesced(port.model(csr), 40 + 3 * k, beta, 1.0, 2)
+            ordered = np.empty(n, np.int8)
+            ordered[probe.forward] = initial[k]
+            chain = port.coalesced(port.model(csr), 40 + 3 * k, beta, 1.0, 2, ordered)
+            chain.sweep(6)
+            np.testing.assert_array_equal(st.spins(k), chain.spins)
+
+
+def test_coalesced_rejections(lib):
+    odd = product_model(ins.build_layered_csr(*ins.layered_spec(8, 3), 5, 1.0))
+    generic = product_model(ins.cubic_pm1(4, 5, 0.0))
+    too_deep = product_model(ins.build_layered_csr(*ins.layered_spec(8, 3), 66, 1.0))
+    for model, text in ((odd, "even layer count"), (generic, "needs a layered model"), (too_deep, "at most 64 layers")):
+        with pytest.raises(ib.IsingError) as err:
+            ib.init_coalesced(model, [1.0])
+        assert err.value.status == _lib.ISING_ERR_ARGUMENT and text in str(err.value)
+    ok = product_model(ins.build_layered_csr(*ins.layered_spec(8, 3), 4, 1.0))
+    with pytest.raises(ib.IsingError, match="beta must be finite"):
+        ib.init_coalesced(ok, [-1.0])
+    with pytest.raises(ib.IsingError, match="seed count"):
+        ib.init_coalesced(ok, [1.0, 2.0], seeds=[1])
