@@ -59,7 +59,35 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
             if (m.targets[e] / P != l) throw Error("init_state: coalesced model has a space edge leaving its layer");
         }
     }
-    smem_bytes_ = coalesced_smem_bytes(W, P);
+    // one layer's space graph, if every layer carries the same one (targets and coupling bits)
+    std::vector<uint32_t> layer_offsets(size_t(P) + 1, 0);
+    std::vector<uint2> layer_edges;
+    bool same_layers = true;
+    for (uint32_t pos = 0; pos < P; ++pos) {
+        layer_offsets[pos] = uint32_t(layer_edges.size());
+        for (uint32_t e = m.offsets[pos]; e + 2 < m.offsets[pos + 1]; ++e) {
+            uint32_t bits;
+            std::memcpy(&bits, &m.couplings[e], sizeof bits);
+            layer_edges.push_back(make_uint2(m.targets[e] % P, bits));
+        }
+    }
+    layer_offsets[P] = uint32_t(layer_edges.size());
+    for (uint32_t i = P; i < n && same_layers; ++i) {
+        const uint32_t pos = i % P, first = layer_offsets[pos], count = layer_offsets[pos + 1] - first;
+        same_layers = m.offsets[i + 1] - m.offsets[i] == count + 2;
+        for (uint32_t k = 0; k < count && same_layers; ++k) {
+            uint32_t bits;
+            std::memcpy(&bits, &m.couplings[m.offsets[i] + k], sizeof bits);
+            same_layers = m.targets[m.offsets[i] + k] % P == layer_edges[first + k].x && bits == layer_edges[first + k].y;
+        }
+    }
+    if (!same_layers) layer_edges.clear();
+    smem_bytes_ = coalesced_smem_bytes(W, P, uint32_t(layer_edges.size()));
+    if (smem_bytes_ == 0 && same_layers) {  // the graph copy does not fit next to the region: walk the CSR
+        same_layers = false;
+        layer_edges.clear();
+        smem_bytes_ = coalesced_smem_bytes(W, P, 0);
+    }
     if (smem_bytes_ == 0) {
         throw Error("init_state: the coalesced kernel needs at most 64 layers and one region (half the spins) "
                     "within 227 KB of shared memory at 9 bytes per spin");
@@ -99,6 +127,11 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
         }
     }
     offsets[n] = at;
+    std::vector<float> tau_up(n), tau_down(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        tau_up[i] = couplings[offsets[i + 1] - 2];
+        tau_down[i] = couplings[offsets[i + 1] - 1];
+    }
 
     // ---- init_state on the permuted model, per chain (sweep_state.cpp:160-234)
     const size_t chains = cfg.betas.size();
@@ -143,6 +176,10 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
     upload_vec(offsets_, offsets, device_bytes_, stream_);
     upload_vec(targets_, targets, device_bytes_, stream_);
     upload_vec(couplings_, couplings, device_bytes_, stream_);
+    upload_vec(tau_up_, tau_up, device_bytes_, stream_);
+    upload_vec(tau_down_, tau_down, device_bytes_, stream_);
+    upload_vec(layer_offsets_, layer_offsets, device_bytes_, stream_);
+    upload_vec(layer_edges_, layer_edges, device_bytes_, stream_);
     upload_vec(hs_, hs, device_bytes_, stream_);
     upload_vec(ht_, ht, device_bytes_, stream_);
     upload_vec(spins_, spins, device_bytes_, stream_);
@@ -161,6 +198,11 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
     dev_.offsets = offsets_.as<uint32_t>();
     dev_.targets = targets_.as<uint32_t>();
     dev_.couplings = couplings_.as<float>();
+    dev_.tau_up = tau_up_.as<float>();
+    dev_.tau_down = tau_down_.as<float>();
+    dev_.layer_offsets = same_layers ? layer_offsets_.as<uint32_t>() : nullptr;
+    dev_.layer_edges = same_layers ? layer_edges_.as<uint2>() : nullptr;
+    dev_.n_layer_edges = uint32_t(layer_edges.size());
     dev_.hs = hs_.as<float>();
     dev_.ht = ht_.as<float>();
     dev_.spins = spins_.as<int8_t>();

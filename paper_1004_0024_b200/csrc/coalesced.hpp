@@ -27,6 +27,14 @@ struct CoalescedDev {
     const uint32_t* offsets;
     const uint32_t* targets;
     const float* couplings;
+    // the two tau couplings of every spin (new index order): next layer, previous layer
+    const float* tau_up;
+    const float* tau_down;
+    // one layer's space graph when all layers carry the same one (else nullptr: the kernel walks the CSR):
+    // edges of position p are layer_edges[layer_offsets[p] .. layer_offsets[p+1]) = {position, bits of J}
+    const uint32_t* layer_offsets;  // per_layer + 1
+    const uint2* layer_edges;
+    uint32_t n_layer_edges;
     // per chain, new index order
     float* hs;        // [chain][n]
     float* ht;        // [chain][n]
@@ -37,7 +45,7 @@ struct CoalescedDev {
     unsigned long long* flips;      // [chain]
 };
 
-size_t coalesced_smem_bytes(uint32_t lanes, uint32_t per_layer);
+size_t coalesced_smem_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_layer_edges);
 cudaError_t prepare_coalesced_kernels(size_t smem_bytes);
 cudaError_t launch_sweep_coalesced(const CoalescedDev& d, uint32_t sweeps, size_t smem_bytes, cudaStream_t stream);
 
@@ -85,7 +93,8 @@ class CoalescedBatch {
     size_t smem_bytes_ = 0, device_bytes_ = 0;
     uint64_t sweeps_done_ = 0;
     std::vector<uint32_t> forward_;  // old index -> new index
-    DeviceBuffer offsets_, targets_, couplings_, hs_, ht_, spins_, mt_, mt_pos_, betas_, flips_;
+    DeviceBuffer offsets_, targets_, couplings_, tau_up_, tau_down_, layer_offsets_, layer_edges_;
+    DeviceBuffer hs_, ht_, spins_, mt_, mt_pos_, betas_, flips_;
 };
 
 }  // namespace isingb200

@@ -2,13 +2,16 @@
 //
 // The region being swept (even or odd layers: W*P spins) is staged in shared memory, so the
 // strictly sequential walk over the P positions pays shared-memory latency per step, not L2:
-//   hs, ht f32 [P][W], spins i8 [P][W], flip flags one bit per (p, lane).
+//   hs, ht f32 [P][W], spins i8 [P][W], flip flags one bit per (p, lane), and — when every layer
+//   carries the same space graph (GRAPH = true) — one layer's edge list, read warp-uniformly.
 // Lane t only ever touches column t of the staged region (space edges stay inside a layer), so a
 // phase needs no synchronisation.  The two tau updates of a flip leave the region (previous layer:
 // immediately; next layer: in the deferred phase, ref: sweep_coalesced.cpp:10-22): they go to the
 // OTHER region's h_tau in global memory as fire-and-forget `red.global.add.f32` of the negated
 // addend — h - d == h + (-d) bit for bit, every location receives at most one update per phase, and
 // a fence + warp barrier between phases keeps the reference's order (immediate, then deferred).
+// Everything a step needs from global memory (uniforms, tau couplings) is requested a chunk of 8
+// steps ahead and independent of the decisions, so no step waits on L2.
 #include "coalesced.hpp"
 #include "device_math.cuh"
 #include "device_mt.cuh"
@@ -17,29 +20,36 @@ namespace isingb200 {
 
 namespace {
 
-struct RegionSmem {
-    float* hs;
-    float* ht;
-    int8_t* spins;
-    uint32_t* flags;  // [ceil(P/32)][32]
-};
-
-__host__ __device__ inline size_t region_bytes(uint32_t lanes, uint32_t per_layer) {
+__host__ __device__ inline size_t region_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_layer_edges) {
     const size_t cells = size_t(lanes) * per_layer;
-    return cells * 4 * 2 + (cells + 15) / 16 * 16 + size_t((per_layer + 31) / 32) * 32 * 4;
+    size_t bytes = cells * 4 * 2 + (cells + 15) / 16 * 16 + size_t((per_layer + 31) / 32) * 32 * 4;
+    if (n_layer_edges != 0) bytes += (size_t(per_layer) + 1 + 3) / 4 * 16 + size_t(n_layer_edges) * 8;
+    return bytes;
 }
 
-template <int EXP>
+// A load the compiler may not sink into the branch that consumes it (it is issued where it stands).
+__device__ __forceinline__ float ld_stream(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+template <int EXP, bool GRAPH>
 __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uint32_t sweeps) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t chain = blockIdx.x, lane = threadIdx.x;
     const uint32_t W = d.lanes, P = d.per_layer, n = d.n_spins, cells = W * P;
     const bool active = lane < W;
-    RegionSmem s;
-    s.hs = reinterpret_cast<float*>(smem_raw);
-    s.ht = s.hs + cells;
-    s.spins = reinterpret_cast<int8_t*>(s.ht + cells);
-    s.flags = reinterpret_cast<uint32_t*>(smem_raw + size_t(cells) * 8 + (size_t(cells) + 15) / 16 * 16);
+    float* hs_s = reinterpret_cast<float*>(smem_raw);
+    float* ht_s = hs_s + cells;
+    int8_t* spins_s = reinterpret_cast<int8_t*>(ht_s + cells);
+    uint32_t* flags_s = reinterpret_cast<uint32_t*>(smem_raw + size_t(cells) * 8 + (size_t(cells) + 15) / 16 * 16);
+    uint32_t* graph_off = flags_s + (P + 31) / 32 * 32;
+    uint2* graph_edges = reinterpret_cast<uint2*>(graph_off + (P + 1 + 3) / 4 * 4);
+    if (GRAPH) {
+        for (uint32_t k = lane; k <= P; k += 32) graph_off[k] = d.layer_offsets[k];
+        for (uint32_t k = lane; k < d.n_layer_edges; k += 32) graph_edges[k] = d.layer_edges[k];
+    }
 
     float* hs_g = d.hs + size_t(chain) * n;
     float* ht_g = d.ht + size_t(chain) * n;
@@ -47,48 +57,81 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
     const float neg_beta = -d.betas[chain];
     const float gamma = d.tau_scale;
     unsigned long long flips = 0;
+    const uint32_t lane_c = active ? lane : 0u;  // idle lanes read column 0 and never accept
 
     MtLane g;
     if (active) g.open(d.mt + size_t(chain) * kMtN * W + lane, W, d.mt_pos[chain]);
 
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t region = 0; region < 2; ++region) {
-            const uint32_t base = region * cells;
-            // ---- stage the region in (the other region's tau updates of the previous phase pair
-            // have been fenced below)
+            const uint32_t base = region * cells, other = cells - base;
+            // tau targets of (p, lane) in the other region (ref: check_engine_model, sweep_state.cpp:131-141)
+            const uint32_t down_lane = region == 0 ? (lane_c + W - 1) % W : lane_c;
+            const uint32_t up_lane = region == 0 ? lane_c : (lane_c + 1) % W;
+
+            // ---- stage the region in (tau updates it received from the other region's phases were
+            // fenced before the warp barrier that ended them)
+#pragma unroll 8
             for (uint32_t k = lane; k < cells; k += 32) {
-                s.hs[k] = hs_g[base + k];
-                s.ht[k] = ht_g[base + k];
-                s.spins[k] = spins_g[base + k];
+                hs_s[k] = hs_g[base + k];
+                ht_s[k] = ht_g[base + k];
+                spins_s[k] = spins_g[base + k];
             }
-            for (uint32_t k = lane; k < (P + 31) / 32 * 32; k += 32) s.flags[k] = 0u;
+            for (uint32_t k = lane; k < (P + 31) / 32 * 32; k += 32) flags_s[k] = 0u;
             __syncwarp();
 
             // ---- flip phase (ref: flip_phase, sweep_coalesced.cpp:45-83)
             for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
                 const uint32_t count = min(uint32_t(kChunk), P - p0);
-                float u[kChunk];
+                float u[kChunk], j_down[kChunk];
+#pragma unroll
+                for (int k = 0; k < kChunk; ++k) {
+                    j_down[k] = uint32_t(k) < count ? ld_stream(d.tau_down + base + W * (p0 + k) + lane_c) : 0.0f;
+                    u[k] = 2.0f;
+                }
                 if (active) g.next_chunk(count, u);
 #pragma unroll
                 for (int k = 0; k < kChunk; ++k) {
                     if (uint32_t(k) >= count) break;
                     const uint32_t p = p0 + k;
-                    if (!active) continue;
-                    const uint32_t cell = W * p + lane;
-                    const float spin = float(s.spins[cell]);
-                    const float two_s = __fmul_rn(2.0f, spin);
-                    const float x = flip_exponent(neg_beta, gamma, two_s, s.hs[cell], s.ht[cell]);
-                    if (u[k] < exp_kind<EXP>(x)) {  // no clamp (ref: sweep_coalesced.cpp:66)
-                        const uint32_t i = base + cell;
-                        const uint32_t end = d.offsets[i + 1];
-                        for (uint32_t e = d.offsets[i]; e + 2 < end; ++e) {
-                            const uint32_t t = d.targets[e] - base;  // same layer: column `lane` of this region
-                            s.hs[t] = __fsub_rn(s.hs[t], __fmul_rn(two_s, d.couplings[e]));
+                    const uint32_t cell = W * p + lane_c;
+                    const int8_t spin_i = spins_s[cell];
+                    const float two_s = __fmul_rn(2.0f, float(spin_i));
+                    const float x = flip_exponent(neg_beta, gamma, two_s, hs_s[cell], ht_s[cell]);
+                    const bool accept = active && u[k] < exp_kind<EXP>(x);  // no clamp (ref: sweep_coalesced.cpp:66)
+                    if (GRAPH) {
+                        if (__any_sync(0xffffffffu, accept)) {
+                            // the targets of one position are distinct (validate_model rejects duplicate
+                            // edges): groups of four are read together, then written together
+                            const uint32_t end = graph_off[p + 1];
+                            for (uint32_t e0 = graph_off[p]; e0 < end; e0 += 4) {
+                                uint2 edge[4];
+                                float v[4];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    edge[q] = graph_edges[min(e0 + q, end - 1)];  // warp-uniform
+                                    v[q] = hs_s[W * edge[q].x + lane_c];
+                                }
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    if (accept && e0 + q < end) {
+                                        hs_s[W * edge[q].x + lane_c] = __fsub_rn(v[q], __fmul_rn(two_s, __uint_as_float(edge[q].y)));
+                                    }
+                                }
+                            }
                         }
+                    } else if (accept) {
+                        const uint32_t i = base + cell, end = d.offsets[i + 1];
+                        for (uint32_t e = d.offsets[i]; e + 2 < end; ++e) {
+                            const uint32_t t = d.targets[e] - base;  // same layer: this lane's column
+                            hs_s[t] = __fsub_rn(hs_s[t], __fmul_rn(two_s, d.couplings[e]));
+                        }
+                    }
+                    if (accept) {
                         // tau edge to the previous layer now; the one to the next layer waits
-                        atomicAdd(ht_g + d.targets[end - 1], -__fmul_rn(two_s, d.couplings[end - 1]));
-                        s.spins[cell] = int8_t(-s.spins[cell]);
-                        s.flags[(p >> 5) * 32 + lane] |= 1u << (p & 31u);
+                        atomicAdd(ht_g + other + W * p + down_lane, -__fmul_rn(two_s, j_down[k]));
+                        spins_s[cell] = int8_t(-spin_i);
+                        flags_s[(p >> 5) * 32 + lane] |= 1u << (p & 31u);
                         ++flips;
                     }
                 }
@@ -97,59 +140,77 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
             __syncwarp();
 
             // ---- deferred phase (ref: deferred_tau_phase, sweep_coalesced.cpp:87-104)
-            if (active) {
-                for (uint32_t p = 0; p < P; ++p) {
-                    if (((s.flags[(p >> 5) * 32 + lane] >> (p & 31u)) & 1u) == 0u) continue;
-                    const uint32_t cell = W * p + lane;
-                    const float two_s = __fmul_rn(-2.0f, float(s.spins[cell]));  // twice the pre-flip spin
-                    const uint32_t up = d.offsets[base + cell + 1] - 2;
-                    atomicAdd(ht_g + d.targets[up], -__fmul_rn(two_s, d.couplings[up]));
+            for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
+                const uint32_t count = min(uint32_t(kChunk), P - p0);
+                float j_up[kChunk];
+#pragma unroll
+                for (int k = 0; k < kChunk; ++k) {  // all eight requested before the first is used
+                    j_up[k] = uint32_t(k) < count ? ld_stream(d.tau_up + base + W * (p0 + k) + lane_c) : 0.0f;
+                }
+#pragma unroll
+                for (int k = 0; k < kChunk; ++k) {
+                    if (uint32_t(k) >= count) break;
+                    const uint32_t p = p0 + k;
+                    const bool flagged = active && ((flags_s[(p >> 5) * 32 + lane] >> (p & 31u)) & 1u) != 0u;
+                    if (flagged) {
+                        const float two_s = __fmul_rn(-2.0f, float(spins_s[W * p + lane_c]));  // twice the pre-flip spin
+                        atomicAdd(ht_g + other + W * p + up_lane, -__fmul_rn(two_s, j_up[k]));
+                    }
                 }
             }
             // ---- stage out
             __syncwarp();
+#pragma unroll 8
             for (uint32_t k = lane; k < cells; k += 32) {
-                hs_g[base + k] = s.hs[k];
-                ht_g[base + k] = s.ht[k];
-                spins_g[base + k] = s.spins[k];
+                hs_g[base + k] = hs_s[k];
+                ht_g[base + k] = ht_s[k];
+                spins_g[base + k] = spins_s[k];
             }
             __threadfence();
             __syncwarp();
         }
     }
-    if (active && lane == 0) {
-        d.mt_pos[chain] = g.pos;
-    }
-    // flips of all lanes
+    if (lane == 0) d.mt_pos[chain] = g.pos;
     for (int off = 16; off > 0; off >>= 1) flips += __shfl_down_sync(0xffffffffu, flips, off);
     if (lane == 0) d.flips[chain] += flips;
 }
 
+template <int EXP>
+cudaError_t prepare_exp(size_t smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_coalesced_kernel<EXP, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(sweep_coalesced_kernel<EXP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem_bytes));
+}
+
+template <int EXP>
+void launch_exp(const CoalescedDev& d, uint32_t sweeps, size_t smem_bytes, cudaStream_t stream) {
+    if (d.layer_edges != nullptr) sweep_coalesced_kernel<EXP, true><<<d.n_chains, 32, smem_bytes, stream>>>(d, sweeps);
+    else sweep_coalesced_kernel<EXP, false><<<d.n_chains, 32, smem_bytes, stream>>>(d, sweeps);
+}
+
 }  // namespace
 
-size_t coalesced_smem_bytes(uint32_t lanes, uint32_t per_layer) {
+size_t coalesced_smem_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_layer_edges) {
     if (lanes == 0 || lanes > 32 || per_layer == 0) return 0;
-    const size_t bytes = region_bytes(lanes, per_layer);
+    const size_t bytes = region_bytes(lanes, per_layer, n_layer_edges);
     return bytes <= 227 * 1024 ? bytes : 0;
 }
 
 cudaError_t prepare_coalesced_kernels(size_t smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_coalesced_kernel<kExpExact>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(sweep_coalesced_kernel<kExpFast>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_bytes));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(sweep_coalesced_kernel<kExpAccurate>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(smem_bytes));
+    cudaError_t e = prepare_exp<kExpExact>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_exp<kExpFast>(smem_bytes);
+    if (e == cudaSuccess) e = prepare_exp<kExpAccurate>(smem_bytes);
+    return e;
 }
 
 cudaError_t launch_sweep_coalesced(const CoalescedDev& d, uint32_t sweeps, size_t smem_bytes, cudaStream_t stream) {
     if (d.n_chains == 0) return cudaSuccess;
     switch (d.exp_kind) {
-        case kExpExact: sweep_coalesced_kernel<kExpExact><<<d.n_chains, 32, smem_bytes, stream>>>(d, sweeps); break;
-        case kExpFast: sweep_coalesced_kernel<kExpFast><<<d.n_chains, 32, smem_bytes, stream>>>(d, sweeps); break;
-        default: sweep_coalesced_kernel<kExpAccurate><<<d.n_chains, 32, smem_bytes, stream>>>(d, sweeps); break;
+        case kExpExact: launch_exp<kExpExact>(d, sweeps, smem_bytes, stream); break;
+        case kExpFast: launch_exp<kExpFast>(d, sweeps, smem_bytes, stream); break;
+        default: launch_exp<kExpAccurate>(d, sweeps, smem_bytes, stream); break;
     }
     return cudaGetLastError();
 }

@@ -76,3 +76,32 @@ def test_coalesced_rejections(lib):
         ib.init_coalesced(ok, [-1.0])
     with pytest.raises(ib.IsingError, match="seed count"):
         ib.init_coalesced(ok, [1.0, 2.0], seeds=[1])
+
+
+def test_coalesced_walks_the_csr_when_the_layer_graph_does_not_fit(lib, port):
+    """48,000 spins: one region (219 KB) fits shared memory, the staged layer graph next to it does
+    not, so the kernel falls back to walking the permuted CSR in global memory."""
+    csr = ins.build_layered_csr(*ins.layered_spec(750, 11), 64, 1.0)
+    chain = port.coalesced(port.model(csr), 9, 0.8, 1.0, 2)
+    with ib.init_coalesced(product_model(csr), [0.8], seeds=[9]) as st:
+        st.run(3)
+        chain.sweep(3)
+        np.testing.assert_array_equal(st.spins(0), chain.spins)
+        hs, ht = st.fields(0)
+        np.testing.assert_array_equal(hs.view(np.uint32), chain.hs_new_order[chain.forward].view(np.uint32))
+        np.testing.assert_array_equal(ht.view(np.uint32), chain.ht_new_order[chain.forward].view(np.uint32))
+        assert int(st.stats()[0][0]) == chain.flips
+
+
+def test_layers_must_be_identical_so_the_staged_graph_always_applies(lib):
+    """validate_model (ref: src/model.cpp:283-330) rejects layers that differ, couplings included."""
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 3), 6, 0.75)
+    csr = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in csr.items()}
+    a = 2 * 16 + 5
+    e = csr["offsets"][a]
+    b = int(csr["targets"][e])
+    csr["couplings"][e] = np.float32(0.625)
+    back = [k for k in range(csr["offsets"][b], csr["offsets"][b + 1]) if csr["targets"][k] == a][0]
+    csr["couplings"][back] = np.float32(0.625)
+    with pytest.raises(ib.IsingError, match="layers are not identical"):
+        product_model(csr)
