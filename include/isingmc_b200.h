@@ -243,7 +243,7 @@ ISING_B200_API ising_status ising_b200_run_json(const ising_b200_model* model, c
  * of a large layered system, where one chain per lane cannot fill the GPU.  The model is the
  * ORIGINAL identity-ordered layered model (the permutation is applied internally, every readout is
  * in the original spin order) and must stay alive as long as the batch.  Needs an even layer count
- * <= 64 and half the spins within 227 KB of shared memory at 9 bytes per spin.  Chains are
+ * <= 64 and half the spins within 227 KB of shared memory at 5 bytes per spin.  Chains are
  * independent (this engine has no tempering in the reference either). */
 typedef struct ising_coalesced_params {
     uint32_t n_chains;

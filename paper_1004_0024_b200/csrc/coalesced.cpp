@@ -90,7 +90,7 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
     }
     if (smem_bytes_ == 0) {
         throw Error("init_state: the coalesced kernel needs at most 64 layers and one region (half the spins) "
-                    "within 227 KB of shared memory at 9 bytes per spin");
+                    "within 227 KB of shared memory at 5 bytes per spin");
     }
 
     int count = 0;

@@ -2,7 +2,7 @@
 //
 // The region being swept (even or odd layers: W*P spins) is staged in shared memory, so the
 // strictly sequential walk over the P positions pays shared-memory latency per step, not L2:
-//   hs, ht f32 [P][W], spins i8 [P][W], flip flags one bit per (p, lane), and — when every layer
+//   hs f32 [P][W], spins i8 [P][W], flip flags one bit per (p, lane), and — when every layer
 //   carries the same space graph (GRAPH = true) — one layer's edge list, read warp-uniformly.
 // Lane t only ever touches column t of the staged region (space edges stay inside a layer), so a
 // phase needs no synchronisation.  The two tau updates of a flip leave the region (previous layer:
@@ -10,7 +10,8 @@
 // OTHER region's h_tau in global memory as fire-and-forget `red.global.add.f32` of the negated
 // addend — h - d == h + (-d) bit for bit, every location receives at most one update per phase, and
 // a fence + warp barrier between phases keeps the reference's order (immediate, then deferred).
-// Everything a step needs from global memory (uniforms, tau couplings) is requested a chunk of 8
+// The region's h_tau is only read (it changes in the OTHER region's phases), so it stays in global
+// memory.  Everything a step needs from there (uniforms, tau fields and couplings) is requested a chunk of 8
 // steps ahead and independent of the decisions, so no step waits on L2.
 #include "coalesced.hpp"
 #include "device_math.cuh"
@@ -22,7 +23,7 @@ namespace {
 
 __host__ __device__ inline size_t region_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_layer_edges) {
     const size_t cells = size_t(lanes) * per_layer;
-    size_t bytes = cells * 4 * 2 + (cells + 15) / 16 * 16 + size_t((per_layer + 31) / 32) * 32 * 4;
+    size_t bytes = cells * 4 + (cells + 15) / 16 * 16 + size_t((per_layer + 31) / 32) * 32 * 4;
     if (n_layer_edges != 0) bytes += (size_t(per_layer) + 1 + 3) / 4 * 16 + size_t(n_layer_edges) * 8;
     return bytes;
 }
@@ -34,6 +35,13 @@ __device__ __forceinline__ float ld_stream(const float* p) {
     return v;
 }
 
+// The same for data this kernel also updates with reductions in other phases: read at L2.
+__device__ __forceinline__ float ld_coherent(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <int EXP, bool GRAPH>
 __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uint32_t sweeps) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -41,9 +49,8 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
     const uint32_t W = d.lanes, P = d.per_layer, n = d.n_spins, cells = W * P;
     const bool active = lane < W;
     float* hs_s = reinterpret_cast<float*>(smem_raw);
-    float* ht_s = hs_s + cells;
-    int8_t* spins_s = reinterpret_cast<int8_t*>(ht_s + cells);
-    uint32_t* flags_s = reinterpret_cast<uint32_t*>(smem_raw + size_t(cells) * 8 + (size_t(cells) + 15) / 16 * 16);
+    int8_t* spins_s = reinterpret_cast<int8_t*>(hs_s + cells);
+    uint32_t* flags_s = reinterpret_cast<uint32_t*>(smem_raw + size_t(cells) * 4 + (size_t(cells) + 15) / 16 * 16);
     uint32_t* graph_off = flags_s + (P + 31) / 32 * 32;
     uint2* graph_edges = reinterpret_cast<uint2*>(graph_off + (P + 1 + 3) / 4 * 4);
     if (GRAPH) {
@@ -74,7 +81,6 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
 #pragma unroll 8
             for (uint32_t k = lane; k < cells; k += 32) {
                 hs_s[k] = hs_g[base + k];
-                ht_s[k] = ht_g[base + k];
                 spins_s[k] = spins_g[base + k];
             }
             for (uint32_t k = lane; k < (P + 31) / 32 * 32; k += 32) flags_s[k] = 0u;
@@ -83,10 +89,12 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
             // ---- flip phase (ref: flip_phase, sweep_coalesced.cpp:45-83)
             for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
                 const uint32_t count = min(uint32_t(kChunk), P - p0);
-                float u[kChunk], j_down[kChunk];
+                float u[kChunk], j_down[kChunk], ht[kChunk];
 #pragma unroll
                 for (int k = 0; k < kChunk; ++k) {
                     j_down[k] = uint32_t(k) < count ? ld_stream(d.tau_down + base + W * (p0 + k) + lane_c) : 0.0f;
+                    // this region's tau fields do not change while it is swept (only the other region's do)
+                    ht[k] = uint32_t(k) < count ? ld_coherent(ht_g + base + W * (p0 + k) + lane_c) : 0.0f;
                     u[k] = 2.0f;
                 }
                 if (active) g.next_chunk(count, u);
@@ -97,7 +105,7 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
                     const uint32_t cell = W * p + lane_c;
                     const int8_t spin_i = spins_s[cell];
                     const float two_s = __fmul_rn(2.0f, float(spin_i));
-                    const float x = flip_exponent(neg_beta, gamma, two_s, hs_s[cell], ht_s[cell]);
+                    const float x = flip_exponent(neg_beta, gamma, two_s, hs_s[cell], ht[k]);
                     const bool accept = active && u[k] < exp_kind<EXP>(x);  // no clamp (ref: sweep_coalesced.cpp:66)
                     if (GRAPH) {
                         if (__any_sync(0xffffffffu, accept)) {
@@ -163,7 +171,6 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
 #pragma unroll 8
             for (uint32_t k = lane; k < cells; k += 32) {
                 hs_g[base + k] = hs_s[k];
-                ht_g[base + k] = ht_s[k];
                 spins_g[base + k] = spins_s[k];
             }
             __threadfence();

@@ -79,9 +79,9 @@ def test_coalesced_rejections(lib):
 
 
 def test_coalesced_walks_the_csr_when_the_layer_graph_does_not_fit(lib, port):
-    """48,000 spins: one region (219 KB) fits shared memory, the staged layer graph next to it does
+    """86,400 spins: one region (219 KB) fits shared memory, the staged layer graph next to it does
     not, so the kernel falls back to walking the permuted CSR in global memory."""
-    csr = ins.build_layered_csr(*ins.layered_spec(750, 11), 64, 1.0)
+    csr = ins.build_layered_csr(*ins.layered_spec(1350, 11), 64, 1.0)
     chain = port.coalesced(port.model(csr), 9, 0.8, 1.0, 2)
     with ib.init_coalesced(product_model(csr), [0.8], seeds=[9]) as st:
         st.run(3)
