@@ -26,3 +26,20 @@ for chains in (1, 32, 148):
     st.run(20); ms = st.info()["last_run_ms"]
     print(f"layered  chains={chains:5d}  {ms:9.2f} ms for 20 sweeps -> {chains*n*20/ms*1e3:.3e} attempts/s")
     st.close()
+
+# the reference's own coalesced engine on one host core (oracle/_ref), same instance
+try:
+    from oracle import pyoracle
+    if pyoracle.Reference.available():
+        ref = pyoracle.Reference()
+        permuted, _ = ref.model(c).prepared_for(3)
+        chain = ref.chain(permuted, 1000, 1.0, 1.0, 2, None, engine=3)
+        chain.sweep(2)
+        t0 = time.perf_counter(); chain.sweep(20); dt = time.perf_counter() - t0
+        print(f"reference coalesced engine, 1 host thread: {20*n/dt:.3e} attempts/s ({dt/20*1e6:.0f} us/sweep)")
+        basic = ref.chain(ref.model(c), 1000, 1.0, 1.0, 2, None, engine=1)
+        basic.sweep(2)
+        t0 = time.perf_counter(); basic.sweep(20); dt = time.perf_counter() - t0
+        print(f"reference basic engine,     1 host thread: {20*n/dt:.3e} attempts/s ({dt/20*1e6:.0f} us/sweep)")
+except Exception as exc:  # the reference library is optional on the GPU box
+    print("reference timing skipped:", exc)
