@@ -2,17 +2,22 @@
 //
 // The region being swept (even or odd layers: W*P spins) is staged in shared memory, so the
 // strictly sequential walk over the P positions pays shared-memory latency per step, not L2:
-//   hs f32 [P][W], spins i8 [P][W], flip flags one bit per (p, lane), and — when every layer
-//   carries the same space graph (GRAPH = true) — one layer's edge list, read warp-uniformly.
+//   hs f32 [P][W], spins i8 [P][W], and — when the copy fits (GRAPH = true) — one layer's edge list,
+//   read warp-uniformly (validate_model guarantees identical layers).
 // Lane t only ever touches column t of the staged region (space edges stay inside a layer), so a
-// phase needs no synchronisation.  The two tau updates of a flip leave the region (previous layer:
-// immediately; next layer: in the deferred phase, ref: sweep_coalesced.cpp:10-22): they go to the
-// OTHER region's h_tau in global memory as fire-and-forget `red.global.add.f32` of the negated
-// addend — h - d == h + (-d) bit for bit, every location receives at most one update per phase, and
-// a fence + warp barrier between phases keeps the reference's order (immediate, then deferred).
-// The region's h_tau is only read (it changes in the OTHER region's phases), so it stays in global
-// memory.  Everything a step needs from there (uniforms, tau fields and couplings) is requested a chunk of 8
-// steps ahead and independent of the decisions, so no step waits on L2.
+// phase needs no synchronisation.  The region's h_tau is only read (it changes in the OTHER
+// region's phases), so it stays in global memory; everything a step needs from there (uniforms,
+// tau fields and couplings) is requested a chunk of 8 steps ahead, independent of the decisions.
+//
+// The two tau updates of a flip leave the region: the edge to the previous layer at once, the edge
+// to the next layer in the reference's DEFERRED phase (ref: sweep_coalesced.cpp:10-22, 87-104),
+// because a location of the other region can receive one of each in the same flip phase — from
+// two neighbouring lanes, both at the same position p — and the immediate one must round first.
+// Here the lane that owns the immediate update also applies its neighbour's deferred one: the
+// neighbour's addend arrives by warp shuffle in the same step, and the lane issues two
+// `red.global.add.f32` to that address in program order (same thread, same address: ordered).
+// That is the reference's order per location, without a second pass and without flip flags.
+// h - d == h + (-d) bit for bit, so the reductions add the negated addend.
 #include "coalesced.hpp"
 #include "device_math.cuh"
 #include "device_mt.cuh"
@@ -23,7 +28,7 @@ namespace {
 
 __host__ __device__ inline size_t region_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_layer_edges) {
     const size_t cells = size_t(lanes) * per_layer;
-    size_t bytes = cells * 4 + (cells + 15) / 16 * 16 + size_t((per_layer + 31) / 32) * 32 * 4;
+    size_t bytes = cells * 4 + (cells + 15) / 16 * 16;
     if (n_layer_edges != 0) bytes += (size_t(per_layer) + 1 + 3) / 4 * 16 + size_t(n_layer_edges) * 8;
     return bytes;
 }
@@ -50,8 +55,7 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
     const bool active = lane < W;
     float* hs_s = reinterpret_cast<float*>(smem_raw);
     int8_t* spins_s = reinterpret_cast<int8_t*>(hs_s + cells);
-    uint32_t* flags_s = reinterpret_cast<uint32_t*>(smem_raw + size_t(cells) * 4 + (size_t(cells) + 15) / 16 * 16);
-    uint32_t* graph_off = flags_s + (P + 31) / 32 * 32;
+    uint32_t* graph_off = reinterpret_cast<uint32_t*>(smem_raw + size_t(cells) * 4 + (size_t(cells) + 15) / 16 * 16);
     uint2* graph_edges = reinterpret_cast<uint2*>(graph_off + (P + 1 + 3) / 4 * 4);
     if (GRAPH) {
         for (uint32_t k = lane; k <= P; k += 32) graph_off[k] = d.layer_offsets[k];
@@ -73,8 +77,11 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
         for (uint32_t region = 0; region < 2; ++region) {
             const uint32_t base = region * cells, other = cells - base;
             // tau targets of (p, lane) in the other region (ref: check_engine_model, sweep_state.cpp:131-141)
+            // Location (p, j) of the other region gets the immediate update of lane `j + 1` (even
+            // region) or `j` (odd region) and the deferred one of lane `j` resp. `j - 1`: in both
+            // regions the deferred addend this lane applies comes from lane - 1.
             const uint32_t down_lane = region == 0 ? (lane_c + W - 1) % W : lane_c;
-            const uint32_t up_lane = region == 0 ? lane_c : (lane_c + 1) % W;
+            const uint32_t source_lane = (lane_c + W - 1) % W;
 
             // ---- stage the region in (tau updates it received from the other region's phases were
             // fenced before the warp barrier that ended them)
@@ -83,16 +90,16 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
                 hs_s[k] = hs_g[base + k];
                 spins_s[k] = spins_g[base + k];
             }
-            for (uint32_t k = lane; k < (P + 31) / 32 * 32; k += 32) flags_s[k] = 0u;
             __syncwarp();
 
             // ---- flip phase (ref: flip_phase, sweep_coalesced.cpp:45-83)
             for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
                 const uint32_t count = min(uint32_t(kChunk), P - p0);
-                float u[kChunk], j_down[kChunk], ht[kChunk];
+                float u[kChunk], j_down[kChunk], j_up[kChunk], ht[kChunk];
 #pragma unroll
                 for (int k = 0; k < kChunk; ++k) {
                     j_down[k] = uint32_t(k) < count ? ld_stream(d.tau_down + base + W * (p0 + k) + lane_c) : 0.0f;
+                    j_up[k] = uint32_t(k) < count ? ld_stream(d.tau_up + base + W * (p0 + k) + lane_c) : 0.0f;
                     // this region's tau fields do not change while it is swept (only the other region's do)
                     ht[k] = uint32_t(k) < count ? ld_coherent(ht_g + base + W * (p0 + k) + lane_c) : 0.0f;
                     u[k] = 2.0f;
@@ -135,39 +142,19 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
                             hs_s[t] = __fsub_rn(hs_s[t], __fmul_rn(two_s, d.couplings[e]));
                         }
                     }
+                    // tau edges: previous layer (mine, first), then next layer of the lane before me
+                    const uint32_t accepted = __ballot_sync(0xffffffffu, accept);
+                    const float deferred = __shfl_sync(0xffffffffu, -__fmul_rn(two_s, j_up[k]), source_lane);
+                    float* tau_cell = ht_g + other + W * p + down_lane;
                     if (accept) {
-                        // tau edge to the previous layer now; the one to the next layer waits
-                        atomicAdd(ht_g + other + W * p + down_lane, -__fmul_rn(two_s, j_down[k]));
+                        atomicAdd(tau_cell, -__fmul_rn(two_s, j_down[k]));
                         spins_s[cell] = int8_t(-spin_i);
-                        flags_s[(p >> 5) * 32 + lane] |= 1u << (p & 31u);
                         ++flips;
                     }
-                }
-            }
-            __threadfence();
-            __syncwarp();
-
-            // ---- deferred phase (ref: deferred_tau_phase, sweep_coalesced.cpp:87-104)
-            for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
-                const uint32_t count = min(uint32_t(kChunk), P - p0);
-                float j_up[kChunk];
-#pragma unroll
-                for (int k = 0; k < kChunk; ++k) {  // all eight requested before the first is used
-                    j_up[k] = uint32_t(k) < count ? ld_stream(d.tau_up + base + W * (p0 + k) + lane_c) : 0.0f;
-                }
-#pragma unroll
-                for (int k = 0; k < kChunk; ++k) {
-                    if (uint32_t(k) >= count) break;
-                    const uint32_t p = p0 + k;
-                    const bool flagged = active && ((flags_s[(p >> 5) * 32 + lane] >> (p & 31u)) & 1u) != 0u;
-                    if (flagged) {
-                        const float two_s = __fmul_rn(-2.0f, float(spins_s[W * p + lane_c]));  // twice the pre-flip spin
-                        atomicAdd(ht_g + other + W * p + up_lane, -__fmul_rn(two_s, j_up[k]));
-                    }
+                    if (active && ((accepted >> source_lane) & 1u)) atomicAdd(tau_cell, deferred);
                 }
             }
             // ---- stage out
-            __syncwarp();
 #pragma unroll 8
             for (uint32_t k = lane; k < cells; k += 32) {
                 hs_g[base + k] = hs_s[k];
