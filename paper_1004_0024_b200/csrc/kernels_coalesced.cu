@@ -92,18 +92,31 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
             }
             __syncwarp();
 
-            // ---- flip phase (ref: flip_phase, sweep_coalesced.cpp:45-83)
+            // ---- flip phase (ref: flip_phase, sweep_coalesced.cpp:45-83).  The global operands of a
+            // chunk (tau couplings, this region's tau fields — which do not change while it is swept)
+            // are requested while the chunk before it is processed.
+            float j_down_next[kChunk], j_up_next[kChunk], ht_next[kChunk];
+            const auto request = [&](uint32_t p0) {
+#pragma unroll
+                for (int k = 0; k < kChunk; ++k) {
+                    const uint32_t at = base + W * min(p0 + k, P - 1) + lane_c;
+                    j_down_next[k] = ld_stream(d.tau_down + at);
+                    j_up_next[k] = ld_stream(d.tau_up + at);
+                    ht_next[k] = ld_coherent(ht_g + at);
+                }
+            };
+            request(0);
             for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
                 const uint32_t count = min(uint32_t(kChunk), P - p0);
                 float u[kChunk], j_down[kChunk], j_up[kChunk], ht[kChunk];
 #pragma unroll
                 for (int k = 0; k < kChunk; ++k) {
-                    j_down[k] = uint32_t(k) < count ? ld_stream(d.tau_down + base + W * (p0 + k) + lane_c) : 0.0f;
-                    j_up[k] = uint32_t(k) < count ? ld_stream(d.tau_up + base + W * (p0 + k) + lane_c) : 0.0f;
-                    // this region's tau fields do not change while it is swept (only the other region's do)
-                    ht[k] = uint32_t(k) < count ? ld_coherent(ht_g + base + W * (p0 + k) + lane_c) : 0.0f;
+                    j_down[k] = j_down_next[k];
+                    j_up[k] = j_up_next[k];
+                    ht[k] = ht_next[k];
                     u[k] = 2.0f;
                 }
+                if (p0 + kChunk < P) request(p0 + kChunk);
                 if (active) g.next_chunk(count, u);
 #pragma unroll
                 for (int k = 0; k < kChunk; ++k) {
@@ -117,18 +130,18 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
                     if (GRAPH) {
                         if (__any_sync(0xffffffffu, accept)) {
                             // the targets of one position are distinct (validate_model rejects duplicate
-                            // edges): groups of four are read together, then written together
+                            // edges): groups of eight are read together, then written together
                             const uint32_t end = graph_off[p + 1];
-                            for (uint32_t e0 = graph_off[p]; e0 < end; e0 += 4) {
-                                uint2 edge[4];
-                                float v[4];
+                            for (uint32_t e0 = graph_off[p]; e0 < end; e0 += 8) {
+                                uint2 edge[8];
+                                float v[8];
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) {
+                                for (int q = 0; q < 8; ++q) {
                                     edge[q] = graph_edges[min(e0 + q, end - 1)];  // warp-uniform
                                     v[q] = hs_s[W * edge[q].x + lane_c];
                                 }
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) {
+                                for (int q = 0; q < 8; ++q) {
                                     if (accept && e0 + q < end) {
                                         hs_s[W * edge[q].x + lane_c] = __fsub_rn(v[q], __fmul_rn(two_s, __uint_as_float(edge[q].y)));
                                     }
