@@ -38,11 +38,10 @@ struct MtLane {
         return mt_temper(v);
     }
 
-    // `count` (<= kChunk) draws with every load issued before the first store: none of the
-    // words read here is rewritten inside the chunk (the far word is 227 draws old or newer
-    // by a whole block), so the loads overlap instead of serialising on L2 latency.
-    __device__ __forceinline__ void next_chunk(uint32_t count, float (&u)[kChunk]) {
-        uint32_t nxt[kChunk], far[kChunk];
+    // The recurrence operands of the next `count` (<= kChunk) draws.  None of them is a word the
+    // draws before them in the same or the previous chunk rewrite (the `next` words lie ahead, the
+    // `far` words 227 draws behind or 397 ahead), so they may be requested a whole chunk early.
+    __device__ __forceinline__ void load_operands(uint32_t count, uint32_t (&nxt)[kChunk], uint32_t (&far)[kChunk]) const {
 #pragma unroll
         for (int k = 0; k < kChunk; ++k) {
             if (uint32_t(k) < count) {
@@ -54,6 +53,11 @@ struct MtLane {
                 far[k] = w[size_t(jf) * stride];
             }
         }
+    }
+
+    // Regenerates `count` words in place from operands loaded by load_operands at this position.
+    __device__ __forceinline__ void generate(uint32_t count, const uint32_t (&nxt)[kChunk],
+                                             const uint32_t (&far)[kChunk], float (&u)[kChunk]) {
 #pragma unroll
         for (int k = 0; k < kChunk; ++k) {
             if (uint32_t(k) < count) {
@@ -67,6 +71,14 @@ struct MtLane {
         }
         pos += count;
         pos = pos >= kMtN ? pos - kMtN : pos;
+    }
+
+    // `count` (<= kChunk) draws with every load issued before the first store, so the loads
+    // overlap instead of serialising on L2 latency.
+    __device__ __forceinline__ void next_chunk(uint32_t count, float (&u)[kChunk]) {
+        uint32_t nxt[kChunk], far[kChunk];
+        load_operands(count, nxt, far);
+        generate(count, nxt, far, u);
     }
 };
 

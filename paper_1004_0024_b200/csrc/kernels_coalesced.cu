@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
                 }
             };
             request(0);
+            uint32_t mt_next[kChunk], mt_far[kChunk];
+            if (active) g.load_operands(min(uint32_t(kChunk), P), mt_next, mt_far);
             for (uint32_t p0 = 0; p0 < P; p0 += kChunk) {
                 const uint32_t count = min(uint32_t(kChunk), P - p0);
                 float u[kChunk], j_down[kChunk], j_up[kChunk], ht[kChunk];
@@ -116,8 +118,11 @@ __global__ void __launch_bounds__(32) sweep_coalesced_kernel(CoalescedDev d, uin
                     ht[k] = ht_next[k];
                     u[k] = 2.0f;
                 }
-                if (p0 + kChunk < P) request(p0 + kChunk);
-                if (active) g.next_chunk(count, u);
+                if (active) g.generate(count, mt_next, mt_far, u);
+                if (p0 + kChunk < P) {
+                    request(p0 + kChunk);
+                    if (active) g.load_operands(min(uint32_t(kChunk), P - p0 - kChunk), mt_next, mt_far);
+                }
 #pragma unroll
                 for (int k = 0; k < kChunk; ++k) {
                     if (uint32_t(k) >= count) break;
