@@ -269,6 +269,14 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         DevModel d{};
         d.n_spins = m->n_spins;
         d.has_tau = m->has_tau ? 1u : 0u;
+        d.distinct_targets = 1u;
+        for (uint32_t i = 0; i < m->n_spins && d.distinct_targets; ++i) {
+            for (uint32_t a = m->offsets[i]; a < m->offsets[i + 1] && d.distinct_targets; ++a) {
+                for (uint32_t b = a + 1; b < m->offsets[i + 1]; ++b) {
+                    if (m->targets[a] == m->targets[b]) d.distinct_targets = 0u;
+                }
+            }
+        }
         d.h = keep(m->h)->as<float>();
         d.offsets = keep(m->offsets)->as<uint32_t>();
         d.targets = keep(m->targets)->as<uint32_t>();

@@ -22,6 +22,7 @@ constexpr uint32_t kMtWords = 624;  // MT19937 state words per chain (ref: rng.h
 struct DevModel {
     uint32_t n_spins;
     uint32_t has_tau;
+    uint32_t distinct_targets;  // 1: no spin lists a neighbour twice, so a flip's updates may be batched
     const float* h;
     const uint32_t* offsets;
     const uint32_t* targets;

@@ -146,6 +146,28 @@ __global__ void init_swap_kernel(DevBatch b) {
 // The sweep.  TAU selects models with tau edges (two field arrays); generic models keep
 // h_eff_tau == +0 forever, and hs + gamma*(+0) only differs from hs in the sign of a zero,
 // which no exp_kind can see, so the tau array is neither stored nor read for them.
+// h[target] -= two_s * J for the edges [first, last) of a flipped spin, whose targets are distinct:
+// groups of eight, loads before stores.  Every lane moves data, only accepting lanes change it.
+__device__ __forceinline__ void flip_updates(float* field, const DevModel& m, uint32_t first, uint32_t last,
+                                             float two_s, bool accept) {
+    for (uint32_t e0 = first; e0 < last; e0 += 8) {
+        size_t at[8];
+        float coupling[8], value[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t e = min(e0 + q, last - 1);
+            at[q] = size_t(__ldg(m.targets + e)) * 32;
+            coupling[q] = __ldg(m.couplings + e);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) value[q] = field[at[q]];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (accept && e0 + q < last) field[at[q]] = __fsub_rn(value[q], __fmul_rn(two_s, coupling[q]));
+        }
+    }
+}
+
 template <int EXP, bool TAU>
 __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uint32_t sweeps) {
     TileView t;
@@ -193,16 +215,23 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
                 if (ballot != 0u) {
                     const uint32_t end = m.offsets[i + 1];
                     const uint32_t mid = TAU ? end - m.tau_counts[i] : end;
-                    for (uint32_t e = m.offsets[i]; e < mid; ++e) {
-                        const size_t at = size_t(m.targets[e]) * 32;
-                        const float d = __fmul_rn(two_s, m.couplings[e]);
-                        if (accept) t.hs[at] = __fsub_rn(t.hs[at], d);
-                    }
-                    if constexpr (TAU) {
-                        for (uint32_t e = mid; e < end; ++e) {
+                    if (m.distinct_targets) {
+                        // the neighbours of one spin are distinct: their fields are read together (one
+                        // L2 round trip for up to eight instead of one each), then written together
+                        flip_updates(t.hs, m, m.offsets[i], mid, two_s, accept);
+                        if constexpr (TAU) flip_updates(t.ht, m, mid, end, two_s, accept);
+                    } else {
+                        for (uint32_t e = m.offsets[i]; e < mid; ++e) {
                             const size_t at = size_t(m.targets[e]) * 32;
                             const float d = __fmul_rn(two_s, m.couplings[e]);
-                            if (accept) t.ht[at] = __fsub_rn(t.ht[at], d);
+                            if (accept) t.hs[at] = __fsub_rn(t.hs[at], d);
+                        }
+                        if constexpr (TAU) {
+                            for (uint32_t e = mid; e < end; ++e) {
+                                const size_t at = size_t(m.targets[e]) * 32;
+                                const float d = __fmul_rn(two_s, m.couplings[e]);
+                                if (accept) t.ht[at] = __fsub_rn(t.ht[at], d);
+                            }
                         }
                     }
                     if (accept) {
