@@ -66,7 +66,7 @@ struct DevBatch {
     uint32_t layered_smem;              // dynamic shared memory of one layered-kernel CTA
     uint32_t max_per_layer;             // largest per_layer over the batch's models
     uint32_t graph_shared;              // 1: all tiles use model 0, one shared-memory copy per CTA
-    uint32_t layered_stages;            // depth of the helper/sweep stage ring (2, 4 or 8)
+    uint32_t layered_stages;            // depth of the producer/sweep stage ring (2, 4 or 8)
     uint32_t n_spins;
     uint32_t n_tiles;
     uint32_t n_chains;

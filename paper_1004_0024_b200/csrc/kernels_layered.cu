@@ -240,7 +240,7 @@ struct RingCursor {
 };
 
 // =======================================================================================
-// Producer warp (ahead of the sweep) and post warp (behind it)
+// Producer warp (ahead of the sweep), post and far warps (behind it)
 // =======================================================================================
 struct ProducerState {
     uint32_t* mt;      // this lane's MT19937 state column
@@ -336,7 +336,7 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
                 float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
-                if ((in_flight >> st) & 1u) {  // recycle: the post warp must be done with it
+                if ((in_flight >> st) & 1u) {  // recycle: the post and far warps must be done with it
                     mbar_wait(&empty[st], cursor.parity(), 400);
                     cursor.waited();
                 }
@@ -659,14 +659,14 @@ __device__ __noinline__ void far_update(uint32_t tm, const uint4* fe, uint32_t f
     tmem_wait_st();  // a target may be the next column to enter the window
 }
 
-// Progress of the post warp as seen by the sweep warp.  Chunks are counted over the whole kernel
+// Progress of the FAR warp as seen by the sweep warp.  Chunks are counted over the whole kernel
 // (both warps walk the same sequence), `cached` is the last value read.
 struct PostSync {
     uint32_t addr;        // shared-memory address of the pair's counter
     uint32_t cached;
     uint32_t layer_base;  // chunks finished before this layer began
 };
-// Blocks until the post warp has finished `need_abs` chunks; then its Tensor Memory updates of
+// Blocks until the far warp has finished `need_abs` chunks; then its Tensor Memory updates of
 // those chunks are ordered before whatever this warp does next.
 __device__ __forceinline__ void wait_post(PostSync& ps, uint32_t need_abs) {
     if (int32_t(need_abs - ps.cached) > 0) {
