@@ -176,7 +176,7 @@ struct PairSmem {
 
 // header: tmem slot (16 B) + per tile full[8], (unused)[8], empty[8] mbarriers (192 B) x 4
 constexpr size_t kRingBarriers = kSweepWarps * 3 * kMaxStages;
-constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one post-progress counter per pair
+constexpr size_t kHeaderBytes = 16 + kRingBarriers * 8 + 16;  // + one far-warp progress counter per tile
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 __host__ __device__ inline size_t graph_bytes(uint32_t P, uint32_t max_far, uint32_t max_groups) {
@@ -661,14 +661,14 @@ __device__ __noinline__ void far_update(uint32_t tm, const uint4* fe, uint32_t f
 
 // Progress of the FAR warp as seen by the sweep warp.  Chunks are counted over the whole kernel
 // (both warps walk the same sequence), `cached` is the last value read.
-struct PostSync {
+struct FarProgress {
     uint32_t addr;        // shared-memory address of the pair's counter
     uint32_t cached;
     uint32_t layer_base;  // chunks finished before this layer began
 };
 // Blocks until the far warp has finished `need_abs` chunks; then its Tensor Memory updates of
 // those chunks are ordered before whatever this warp does next.
-__device__ __forceinline__ void wait_post(PostSync& ps, uint32_t need_abs) {
+__device__ __forceinline__ void wait_far(FarProgress& ps, uint32_t need_abs) {
     if (int32_t(need_abs - ps.cached) > 0) {
         uint32_t v;
         do {
@@ -715,7 +715,7 @@ struct StageAddr {
 // per attempt, and near forward far targets are updated in Tensor Memory before they enter it.
 template <int EXP, int K>
 __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, const StageAddr& sa, uint32_t far_info,
-                                        PostSync& ps, uint32_t chunks_before, uint32_t p0, uint32_t P, uint32_t tm,
+                                        FarProgress& ps, uint32_t chunks_before, uint32_t p0, uint32_t P, uint32_t tm,
                                         const uint4* far, uint32_t lane) {
     const float h = r[K];
     const bool accept = decide<EXP>(h, rec);
@@ -732,7 +732,7 @@ __device__ __forceinline__ void attempt(float (&r)[kUnroll], const float4 rec, c
     // target may also have updates pending in the far warp, all from earlier chunks: they land first)
     const uint32_t near_count = (far_info >> 16) & 15u;
     if (near_count != 0u && ballot != 0u) {
-        wait_post(ps, chunks_before);
+        wait_far(ps, chunks_before);
         far_update(tm, far + (far_info & 0xffffu), near_count, __float_as_uint(rec.y) & 0x80000000u, accept);
     }
     // ---- the window entry for p+3 (first needed by attempt p+1)
@@ -763,11 +763,11 @@ __device__ __forceinline__ void attempt_lean(float (&r)[kUnroll], float (&out)[k
 // Near groups of a lean chunk (columns 8c+11 .. 8c+18, not loaded yet): the far warp may still owe
 // them updates from the chunk before this one, which must land first.
 __device__ __noinline__ void apply_near_groups(uint32_t tm, const GraphSmem& g, uint32_t ginfo, uint32_t signs_addr,
-                                               uint32_t ballots_addr, uint32_t post_done_addr, uint32_t chunk_seq,
+                                               uint32_t ballots_addr, uint32_t far_done_addr, uint32_t chunk_seq,
                                                uint32_t lane) {
-    PostSync ps{post_done_addr, 0u, 0u};
+    FarProgress ps{far_done_addr, 0u, 0u};
     __syncwarp();
-    wait_post(ps, chunk_seq);
+    wait_far(ps, chunk_seq);
     apply_groups(tm, g, ginfo, signs_addr, ballots_addr, lane);
 }
 
@@ -780,11 +780,11 @@ struct Window {
 // but first / last of its layer.  Out of line, so that the sweep
 // warp's hot loop (plain lean chunks, ~97 % of them) stays a few KB of straight code.
 template <int EXP>
-__device__ __noinline__ Window special_chunk(Window w, const GraphSmem g, const PairSmem s, uint32_t post_done_addr,
+__device__ __noinline__ Window special_chunk(Window w, const GraphSmem g, const PairSmem s, uint32_t far_done_addr,
                                              uint32_t chunk_seq, uint32_t st, uint32_t p0, uint32_t P, uint32_t tm,
                                              uint32_t band_base, uint32_t lane) {
     float (&r)[kUnroll] = w.r;
-    PostSync ps{post_done_addr, 0u, 0u};
+    FarProgress ps{far_done_addr, 0u, 0u};
     const float4* recs = s.recs + size_t(st) * kUnroll * 32 + lane;
     StageAddr sa;
     sa.rec_x = smem_u32(recs);
@@ -811,7 +811,7 @@ __device__ __noinline__ Window special_chunk(Window w, const GraphSmem g, const 
         ISING_ATTEMPT_LEAN(6)
         ISING_ATTEMPT_LEAN(7)
         if ((chunk_info.y >> 16) != 0u) {
-            apply_near_groups(tm, g, chunk_info.y, smem_u32(s.signs + st * 32 + lane), sa.ballots, post_done_addr,
+            apply_near_groups(tm, g, chunk_info.y, smem_u32(s.signs + st * 32 + lane), sa.ballots, far_done_addr,
                               chunk_seq, lane);
         }
         // columns p0-2 .. p0+5 leave the window (the first chunk has no p0-2, p0-1)
@@ -837,7 +837,7 @@ __device__ __noinline__ Window special_chunk(Window w, const GraphSmem g, const 
 
 template <int EXP>
 __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, const GraphSmem& g,
-                           const PairSmem& s, uint64_t* full, uint32_t bar_id, uint32_t post_done_addr,
+                           const PairSmem& s, uint64_t* full, uint32_t bar_id, uint32_t far_done_addr,
                            uint32_t& chunk_seq, RingCursor& cursor, uint32_t stages, uint32_t tile,
                            uint32_t tm, uint32_t P, uint32_t L) {
     const uint32_t n = b.n_spins;
@@ -901,12 +901,12 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
                     ISING_ATTEMPT_LEAN(6)
                     ISING_ATTEMPT_LEAN(7)
                     if (__builtin_expect((chunk_info.y >> 16) != 0u, 0)) {
-                        apply_near_groups(tm, g, chunk_info.y, signs_u32 + st * 128, sa.ballots, post_done_addr,
+                        apply_near_groups(tm, g, chunk_info.y, signs_u32 + st * 128, sa.ballots, far_done_addr,
                                           chunk_seq, lane);
                     }
                     tmem_st8(tm + p0 - 2, out);  // columns p0-2 .. p0+5 leave the window
                 } else {
-                    w = special_chunk<EXP>(w, g, s, post_done_addr, chunk_seq, st, p0, P, tm, band_base, lane);
+                    w = special_chunk<EXP>(w, g, s, far_done_addr, chunk_seq, st, p0, P, tm, band_base, lane);
                 }
                 // the far warp may now update columns this chunk retired: they must have landed
                 tmem_wait_st();
@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
     uint64_t* full = bars + pair * 3 * kMaxStages;   // producer -> sweep
     uint64_t* empty = full + 2 * kMaxStages;         // post + far -> producer
     const uint32_t bar_id = 5 + pair;                // named barrier of the tile's sweep/post/far rendezvous
-    uint32_t* post_done = reinterpret_cast<uint32_t*>(bars + kRingBarriers) + pair;  // post -> sweep progress
+    uint32_t* far_done = reinterpret_cast<uint32_t*>(bars + kRingBarriers) + pair;  // far -> sweep progress
 
     const uint32_t maxP = b.max_per_layer;
     const uint32_t stages = b.layered_stages;
@@ -984,11 +984,11 @@ __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBa
         } else if (role == 2) {
             post_warp<WAIT>(b, sweeps, lane, s, bar_id, empty, cursor, stages, tile, tm, g.per_layer, g.layers);
         } else if (role == 3) {
-            far_warp(b.hs + size_t(tile) * b.n_spins * 32 + lane, sweeps, lane, gs, s, bar_id, empty, post_done, chunk_seq,
+            far_warp(b.hs + size_t(tile) * b.n_spins * 32 + lane, sweeps, lane, gs, s, bar_id, empty, far_done, chunk_seq,
                      cursor, stages, tm, g.per_layer,
                      g.layers);
         } else {
-            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, bar_id, smem_u32(post_done), chunk_seq, cursor, stages, tile, tm,
+            sweep_warp<EXP>(b, sweeps, lane, gs, s, full, bar_id, smem_u32(far_done), chunk_seq, cursor, stages, tile, tm,
                             g.per_layer, g.layers);
         }
         if (!b.graph_shared) asm volatile("bar.sync %0, 128;" ::"r"(pair + 1) : "memory");
