@@ -2,6 +2,8 @@
 properties (the oracle cannot finish them): agreement of the two kernel families, the running
 energy against the recomputed energy, determinism (a checksum of checksums), shard invariance,
 and bit parity with the oracle on a subsample of ladders inside the full batch."""
+import os
+
 import numpy as np
 import pytest
 
@@ -149,3 +151,61 @@ def test_more_tiles_than_warp_slots_each_pair_sweeps_several_tiles(lib, port):
     want = oracle_batch(port, [csr], 2, betas, sharding.chain_seeds(31, 5000, 2, 4),
                         sharding.ladder_seeds(32, 5000, 2), 12, 3)
     np.testing.assert_array_equal(sample, want["spins"])
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ISING_FUZZ_SEEDS", "12"))))
+def test_random_layer_graphs_both_families_bit_identical(lib, seed):
+    """Seeded fuzz of the layered kernel's edge classification (band / near in the loaded columns /
+    near in the next chunk's / far warp, group splitting on repeated targets, padding): random layer
+    graphs with chords at random distances, both kernel families must leave identical spins, flip
+    counts, slots, running energies and FIELDS (bit for bit) behind."""
+    rng = np.random.default_rng(1000 + seed)
+    positions = int(rng.choice([8, 16, 24, 40, 64, 104, 160, 256, 512]))
+    layers = int(rng.integers(4, 8))
+    present, far_deg, edges = set(), [0] * positions, []
+    for off in (1, 2):
+        if positions > 2 * off:
+            for p in range(positions):
+                key = (min(p, (p + off) % positions), max(p, (p + off) % positions))
+                if key not in present and key[0] != key[1]:
+                    present.add(key)
+                    edges.append(key)
+    scale = int(rng.choice([4, 12, 40, positions]))
+    for _ in range(int(positions * rng.uniform(0.3, 2.5))):
+        a = int(rng.integers(0, positions))
+        b = (a + int(rng.integers(3, max(4, min(scale, positions - 2))))) % positions
+        key = (min(a, b), max(a, b))
+        index_distance = key[1] - key[0]
+        if key[0] == key[1] or key in present or index_distance <= 2:
+            continue
+        if far_deg[key[0]] >= 13 or far_deg[key[1]] >= 13:
+            continue
+        present.add(key)
+        far_deg[key[0]] += 1
+        far_deg[key[1]] += 1
+        edges.append(key)
+    couplings = rng.choice(np.array([1.0, -1.0, 0.5, -0.75, 0.3, -1.3], np.float32), size=len(edges))
+    h = rng.normal(0.0, 0.4, positions).astype(np.float32)
+    csr = ins.build_layered_csr(positions, h, [(a, b, float(j)) for (a, b), j in zip(edges, couplings)], layers,
+                                float(rng.choice([0.5, 1.0, 1.5])))
+    model = product_model(csr)
+    betas = ins.geometric_betas(0.2, 3.0, int(rng.integers(2, 7)))
+    ladders = int(rng.integers(3, 20))
+    sweeps, interval = int(rng.integers(4, 12)), int(rng.integers(1, 4))
+    gamma = float(rng.choice([1.0, 1.25]))
+    out = {}
+    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC):
+        with ib.init_state(model, betas, ladders, base_seed=7 + seed, swap_base_seed=99 + seed, kernel=family,
+                           params=ib.SweepParams(gamma, 2)) as st:
+            assert st.info()["kernel"] == family
+            st.run(sweeps, interval)
+            st.run(3, interval)
+            chain = int(rng.integers(0, ladders * betas.size)) if family == ib.KERNEL_LAYERED else out["chain"]
+            hs, ht = st.fields(chain)
+            got = (st.spins(), st.stats()[0], st.slots(), st.running_energies().view(np.uint64),
+                   hs.view(np.uint32), ht.view(np.uint32))
+            if family == ib.KERNEL_LAYERED:
+                out["chain"], out["layered"] = chain, got
+            else:
+                for a, b in zip(out["layered"], got):
+                    np.testing.assert_array_equal(a, b)
