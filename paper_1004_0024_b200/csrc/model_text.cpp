@@ -1,223 +1,291 @@
 #include "model_text.hpp"
 
 #include <algorithm>
+#include <array>
 #include <charconv>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iterator>
-#include <unordered_set>
+#include <tuple>
 #include <vector>
 
 namespace isingb200 {
 
 namespace {
 
-// One whitespace-separated field of a line; the views point into the document.
-std::vector<std::string_view> split_fields(std::string_view line) {
-    std::vector<std::string_view> fields;
-    size_t at = 0;
-    while (at < line.size()) {
-        while (at < line.size() && (line[at] == ' ' || line[at] == '\t')) ++at;
-        size_t end = at;
-        while (end < line.size() && line[end] != ' ' && line[end] != '\t') ++end;
-        if (end > at) fields.push_back(line.substr(at, end - at));
-        at = end;
-    }
-    return fields;
-}
-
-bool to_u32(std::string_view field, uint32_t& out) {
-    if (field.empty()) return false;
-    const char* last = field.data() + field.size();
-    const auto res = std::from_chars(field.data(), last, out, 10);
-    return res.ec == std::errc() && res.ptr == last;
-}
-
-// Decimal or hexadecimal float literal, whole field (strtof reads both, and rounds to nearest).
-bool to_f32(std::string_view field, float& out) {
-    if (field.empty()) return false;
-    const std::string copy(field);
-    char* end = nullptr;
-    out = std::strtof(copy.c_str(), &end);
-    return end == copy.c_str() + copy.size();
-}
-
-void append_hex(std::string& doc, float v) {
-    char buf[40];
-    std::snprintf(buf, sizeof buf, "%a", double(v));  // same literal the reference writes (model_io.cpp:18-22)
-    doc += buf;
-}
-
-struct Problem {
-    size_t line;
-    [[noreturn]] void operator()(const std::string& what) const {
-        throw ParseError("line " + std::to_string(line) + ": " + what);
-    }
-};
-
-struct PendingEdge {
-    uint32_t a, b;
+// ------------------------------------------------------------------------------------------
+// Reading is a small state machine over the lines of the document: a table maps the keyword of
+// a line to a handler, every handler validates its own arity and ranges, and all complaints go
+// through Reader::reject, which stamps the 1-based line number (ref: model_io.cpp:28-30 for the
+// message format; the wording of each complaint is the reference's, so that callers matching on
+// it keep working).
+// ------------------------------------------------------------------------------------------
+struct HalfEdge {
+    uint32_t spin;
+    uint32_t target;
     float coupling;
-    bool tau;
+    uint8_t rank;  // 0 space, 1 tau towards the next layer, 2 tau towards the previous layer
 };
+
+class Reader {
+  public:
+    explicit Reader(std::string_view document) : rest_(document) {}
+
+    HostModel run() {
+        while (next_line()) {
+            if (words_.empty()) continue;
+            if (!header_ok_) {
+                if (!(words_.size() == 2 && words_[0] == "ising-model" && words_[1] == "v1")) {
+                    reject("expected header 'ising-model v1'");
+                }
+                header_ok_ = true;
+                continue;
+            }
+            dispatch();
+        }
+        if (!header_ok_) throw ParseError("line 1: empty document, expected 'ising-model v1'");
+        if (!spins_known_) throw ParseError("line " + std::to_string(line_) + ": missing spins line");
+        return assemble();
+    }
+
+  private:
+    using Handler = void (Reader::*)();
+
+    void dispatch() {
+        static constexpr std::array<std::pair<std::string_view, Handler>, 4> table{{
+            {"spins", &Reader::take_spins},
+            {"layers", &Reader::take_layers},
+            {"h", &Reader::take_field},
+            {"edge", &Reader::take_edge},
+        }};
+        const std::string_view key = words_[0];
+        const auto hit = std::find_if(table.begin(), table.end(), [&](const auto& row) { return row.first == key; });
+        if (key != "spins" && !spins_known_) reject("spins line must precede '" + std::string(key) + "'");
+        if (hit == table.end()) reject("unknown line '" + std::string(key) + "'");
+        (this->*hit->second)();
+    }
+
+    void take_spins() {
+        if (spins_known_) reject("duplicate spins line");
+        uint32_t count = 0;
+        if (words_.size() != 2 || !number(1, count) || count == 0) reject("malformed spins line");
+        n_ = count;
+        spins_known_ = true;
+        field_.assign(n_, 0.0f);
+        field_line_.assign(n_, 0);
+    }
+
+    void take_layers() {
+        if (layers_ != 0) reject("duplicate layers line");
+        uint32_t count = 0, width = 0;
+        if (words_.size() != 3 || !number(1, count) || !number(2, width)) reject("malformed layers line");
+        if (count < 4 || uint64_t(count) * width != n_) reject("layers * per_layer must equal spins with layers >= 4");
+        layers_ = count;
+        width_ = width;
+    }
+
+    void take_field() {
+        uint32_t spin = 0;
+        float value = 0.0f;
+        if (words_.size() != 3 || !number(1, spin) || !real(2, value)) reject("malformed h line");
+        if (spin >= n_) reject("h index out of range");
+        if (field_line_[spin] != 0) reject("duplicate h line for spin " + std::to_string(spin));
+        field_line_[spin] = line_;
+        field_[spin] = value;
+    }
+
+    void take_edge() {
+        uint32_t a = 0, b = 0;
+        float coupling = 0.0f;
+        const bool shape = words_.size() == 5 && number(1, a) && number(2, b) && real(3, coupling) &&
+                           (words_[4] == "space" || words_[4] == "tau");
+        if (!shape) reject("malformed edge line");
+        if (std::max(a, b) >= n_) reject("edge endpoint out of range");
+        if (a >= b) reject("edge endpoints must satisfy i < j");
+        const uint64_t key = uint64_t(a) * n_ + b;
+        if (std::binary_search(seen_sorted_.begin(), seen_sorted_.end(), key) ||
+            std::find(seen_recent_.begin(), seen_recent_.end(), key) != seen_recent_.end()) {
+            reject("duplicate edge " + std::to_string(a) + "-" + std::to_string(b));
+        }
+        remember(key);
+        const bool tau = words_[4] == "tau";
+        if (tau && layers_ == 0) reject("tau edge in a model without layers");
+        // a tau edge ranks by the direction it has seen from each endpoint
+        halves_.push_back({a, b, coupling, uint8_t(tau ? direction(a, b) : 0)});
+        halves_.push_back({b, a, coupling, uint8_t(tau ? direction(b, a) : 0)});
+    }
+
+    // 1 when `to` is `from`'s partner in the next layer (periodic), else 2
+    uint8_t direction(uint32_t from, uint32_t to) const {
+        const uint32_t up = ((from / width_ + 1) % layers_) * width_ + from % width_;
+        return to == up ? 1 : 2;
+    }
+
+    // duplicate detection without a node-based set: a sorted run plus a short unsorted tail
+    void remember(uint64_t key) {
+        seen_recent_.push_back(key);
+        if (seen_recent_.size() >= 64) {
+            const size_t old = seen_sorted_.size();
+            seen_sorted_.insert(seen_sorted_.end(), seen_recent_.begin(), seen_recent_.end());
+            std::sort(seen_sorted_.begin() + long(old), seen_sorted_.end());
+            std::inplace_merge(seen_sorted_.begin(), seen_sorted_.begin() + long(old), seen_sorted_.end());
+            seen_recent_.clear();
+        }
+    }
+
+    HostModel assemble() {
+        // canonical adjacency = half-edges ordered by (spin, space before tau-next before tau-previous,
+        // target); stable, so nothing depends on the order of the lines
+        std::stable_sort(halves_.begin(), halves_.end(), [](const HalfEdge& x, const HalfEdge& y) {
+            return std::tie(x.spin, x.rank, x.target) < std::tie(y.spin, y.rank, y.target);
+        });
+        HostModel m;
+        m.n_spins = n_;
+        m.layers = layers_;
+        m.per_layer = layers_ != 0 ? width_ : 0;
+        m.h = std::move(field_);
+        m.offsets.assign(size_t(n_) + 1, 0);
+        m.tau_counts.assign(n_, 0);
+        m.targets.reserve(halves_.size());
+        m.couplings.reserve(halves_.size());
+        for (const HalfEdge& half : halves_) {
+            ++m.offsets[half.spin + 1];
+            m.tau_counts[half.spin] = uint8_t(m.tau_counts[half.spin] + (half.rank != 0 ? 1 : 0));
+            m.targets.push_back(half.target);
+            m.couplings.push_back(half.coupling);
+        }
+        for (uint32_t spin = 0; spin < n_; ++spin) {
+            m.offsets[spin + 1] += m.offsets[spin];
+            if (layers_ != 0 && m.tau_counts[spin] != 2) {
+                throw Error("spin " + std::to_string(spin) + " has " + std::to_string(m.tau_counts[spin]) +
+                            " tau edges, expected 2");
+            }
+        }
+        try {
+            finalize_model(m);
+        } catch (const Error& problem) {
+            throw Error(std::string("model failed validation after load: ") + problem.what());
+        }
+        return m;
+    }
+
+    // ---- line and word plumbing
+    bool next_line() {
+        if (rest_.empty()) return false;
+        const size_t cut = rest_.find('\n');
+        std::string_view line = rest_.substr(0, cut);
+        rest_.remove_prefix(cut == std::string_view::npos ? rest_.size() : cut + 1);
+        ++line_;
+        words_.clear();
+        const char* const blanks = " \t\r";
+        for (size_t from = line.find_first_not_of(blanks); from != std::string_view::npos;) {
+            const size_t to = line.find_first_of(blanks, from);
+            words_.push_back(line.substr(from, to == std::string_view::npos ? to : to - from));
+            from = to == std::string_view::npos ? to : line.find_first_not_of(blanks, to);
+        }
+        return true;
+    }
+
+    bool number(size_t index, uint32_t& out) const {
+        const std::string_view w = words_[index];
+        const auto parsed = std::from_chars(w.data(), w.data() + w.size(), out, 10);
+        return !w.empty() && parsed.ec == std::errc() && parsed.ptr == w.data() + w.size();
+    }
+
+    // decimal or hexadecimal literal filling the whole word (strtof reads both, to nearest)
+    bool real(size_t index, float& out) const {
+        const std::string word(words_[index]);
+        char* stop = nullptr;
+        out = std::strtof(word.c_str(), &stop);
+        return !word.empty() && stop == word.c_str() + word.size();
+    }
+
+    [[noreturn]] void reject(const std::string& why) const {
+        throw ParseError("line " + std::to_string(line_) + ": " + why);
+    }
+
+    std::string_view rest_;
+    std::vector<std::string_view> words_;
+    size_t line_ = 0;
+    bool header_ok_ = false, spins_known_ = false;
+    uint32_t n_ = 0, layers_ = 0, width_ = 0;
+    std::vector<float> field_;
+    std::vector<size_t> field_line_;
+    std::vector<HalfEdge> halves_;
+    std::vector<uint64_t> seen_sorted_, seen_recent_;
+};
+
+// "%a" of the value widened to double: the literal the reference writes (ref: model_io.cpp:18-22)
+void put_hex(std::string& doc, float value) {
+    char text[40];
+    const int length = std::snprintf(text, sizeof text, "%a", double(value));
+    doc.append(text, size_t(length));
+}
+
+void put_line(std::string& doc, std::initializer_list<uint32_t> numbers, const char* keyword, float value,
+              const char* suffix) {
+    doc += keyword;
+    for (uint32_t v : numbers) {
+        doc += ' ';
+        doc += std::to_string(v);
+    }
+    doc += ' ';
+    put_hex(doc, value);
+    doc += suffix;
+}
 
 }  // namespace
 
 std::string model_to_text(const HostModel& m) {
-    std::string doc = "ising-model v1\nspins " + std::to_string(m.n_spins) + "\n";
-    if (m.layers != 0) doc += "layers " + std::to_string(m.layers) + " " + std::to_string(m.per_layer) + "\n";
-    for (uint32_t i = 0; i < m.n_spins; ++i) {
-        uint32_t bits;
-        std::memcpy(&bits, &m.h[i], sizeof bits);
-        if (bits == 0) continue;  // +0.0 only: -0.0 is written, so the round trip keeps every bit
-        doc += "h " + std::to_string(i) + " ";
-        append_hex(doc, m.h[i]);
-        doc += "\n";
+    std::string doc;
+    doc.reserve(64 + size_t(m.n_spins) * 24 + m.targets.size() * 20);
+    doc += "ising-model v1\nspins ";
+    doc += std::to_string(m.n_spins);
+    doc += '\n';
+    if (m.layers != 0) {
+        doc += "layers " + std::to_string(m.layers) + ' ' + std::to_string(m.per_layer) + '\n';
     }
-    for (uint32_t i = 0; i < m.n_spins; ++i) {
-        const uint32_t end = m.offsets[i + 1], first_tau = end - m.tau_counts[i];
-        for (uint32_t e = m.offsets[i]; e < end; ++e) {
-            if (m.targets[e] <= i) continue;  // each undirected edge once, from its lower endpoint
-            doc += "edge " + std::to_string(i) + " " + std::to_string(m.targets[e]) + " ";
-            append_hex(doc, m.couplings[e]);
-            doc += e >= first_tau ? " tau\n" : " space\n";
+    // fields: every bit pattern other than +0.0 (a negative zero is written and so survives)
+    for (uint32_t spin = 0; spin < m.n_spins; ++spin) {
+        uint32_t pattern = 0;
+        std::memcpy(&pattern, &m.h[spin], sizeof pattern);
+        if (pattern != 0) put_line(doc, {spin}, "h", m.h[spin], "\n");
+    }
+    // each undirected edge once, from its lower endpoint, in adjacency order
+    for (uint32_t spin = 0; spin < m.n_spins; ++spin) {
+        const uint32_t stop = m.offsets[spin + 1];
+        for (uint32_t slot = m.offsets[spin]; slot < stop; ++slot) {
+            if (m.targets[slot] <= spin) continue;
+            const bool tau = stop - slot <= m.tau_counts[spin];
+            put_line(doc, {spin, m.targets[slot]}, "edge", m.couplings[slot], tau ? " tau\n" : " space\n");
         }
     }
     return doc;
 }
 
-HostModel model_from_text(std::string_view text) {
-    bool seen_header = false, seen_spins = false, seen_layers = false;
-    uint32_t n = 0, layers = 0, per_layer = 0;
-    std::vector<float> h;
-    std::vector<char> h_given;
-    std::vector<PendingEdge> edges;
-    std::unordered_set<uint64_t> edge_keys;
-
-    size_t line_no = 0, at = 0;
-    while (at < text.size()) {
-        size_t nl = text.find('\n', at);
-        if (nl == std::string_view::npos) nl = text.size();
-        std::string_view line = text.substr(at, nl - at);
-        at = nl + 1;
-        ++line_no;
-        if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
-        const std::vector<std::string_view> f = split_fields(line);
-        if (f.empty()) continue;
-        const Problem fail{line_no};
-
-        if (!seen_header) {
-            if (f.size() != 2 || f[0] != "ising-model" || f[1] != "v1") fail("expected header 'ising-model v1'");
-            seen_header = true;
-        } else if (f[0] == "spins") {
-            if (seen_spins) fail("duplicate spins line");
-            if (f.size() != 2 || !to_u32(f[1], n) || n == 0) fail("malformed spins line");
-            seen_spins = true;
-            h.assign(n, 0.0f);
-            h_given.assign(n, 0);
-        } else if (!seen_spins) {
-            fail("spins line must precede '" + std::string(f[0]) + "'");
-        } else if (f[0] == "layers") {
-            if (seen_layers) fail("duplicate layers line");
-            if (f.size() != 3 || !to_u32(f[1], layers) || !to_u32(f[2], per_layer)) fail("malformed layers line");
-            if (layers < 4 || uint64_t(layers) * per_layer != n) {
-                fail("layers * per_layer must equal spins with layers >= 4");
-            }
-            seen_layers = true;
-        } else if (f[0] == "h") {
-            uint32_t i = 0;
-            float v = 0.0f;
-            if (f.size() != 3 || !to_u32(f[1], i) || !to_f32(f[2], v)) fail("malformed h line");
-            if (i >= n) fail("h index out of range");
-            if (h_given[i]) fail("duplicate h line for spin " + std::to_string(i));
-            h_given[i] = 1;
-            h[i] = v;
-        } else if (f[0] == "edge") {
-            PendingEdge e{};
-            if (f.size() != 5 || !to_u32(f[1], e.a) || !to_u32(f[2], e.b) || !to_f32(f[3], e.coupling) ||
-                (f[4] != "space" && f[4] != "tau")) {
-                fail("malformed edge line");
-            }
-            if (e.a >= n || e.b >= n) fail("edge endpoint out of range");
-            if (e.a >= e.b) fail("edge endpoints must satisfy i < j");
-            if (!edge_keys.insert(uint64_t(e.a) << 32 | e.b).second) {
-                fail("duplicate edge " + std::to_string(e.a) + "-" + std::to_string(e.b));
-            }
-            e.tau = f[4] == "tau";
-            if (e.tau && !seen_layers) fail("tau edge in a model without layers");
-            edges.push_back(e);
-        } else {
-            fail("unknown line '" + std::string(f[0]) + "'");
-        }
-    }
-    if (!seen_header) throw ParseError("line 1: empty document, expected 'ising-model v1'");
-    if (!seen_spins) throw ParseError("line " + std::to_string(line_no) + ": missing spins line");
-
-    // ---- canonical CSR: per spin the space edges by target, then (layered) tau up, tau down
-    struct Half {
-        uint32_t target;
-        float coupling;
-    };
-    std::vector<std::vector<Half>> space(n), tau(n);
-    for (const PendingEdge& e : edges) {
-        auto& side = e.tau ? tau : space;
-        side[e.a].push_back({e.b, e.coupling});
-        side[e.b].push_back({e.a, e.coupling});
-    }
-    HostModel m;
-    m.n_spins = n;
-    m.h = std::move(h);
-    m.layers = seen_layers ? layers : 0;
-    m.per_layer = seen_layers ? per_layer : 0;
-    m.offsets.assign(1, 0);
-    m.tau_counts.assign(n, 0);
-    for (uint32_t i = 0; i < n; ++i) {
-        std::sort(space[i].begin(), space[i].end(), [](const Half& x, const Half& y) { return x.target < y.target; });
-        if (seen_layers) {
-            if (tau[i].size() != 2) {
-                throw Error("spin " + std::to_string(i) + " has " + std::to_string(tau[i].size()) +
-                            " tau edges, expected 2");
-            }
-            const uint32_t up = ((i / per_layer + 1) % layers) * per_layer + i % per_layer;
-            if (tau[i][0].target != up) std::swap(tau[i][0], tau[i][1]);
-            m.tau_counts[i] = 2;
-        }
-        for (const auto* side : {&space[i], &tau[i]}) {
-            for (const Half& half : *side) {
-                m.targets.push_back(half.target);
-                m.couplings.push_back(half.coupling);
-            }
-        }
-        m.offsets.push_back(uint32_t(m.targets.size()));
-    }
-    try {
-        finalize_model(m);
-    } catch (const Error& e) {
-        throw Error(std::string("model failed validation after load: ") + e.what());
-    }
-    return m;
-}
+HostModel model_from_text(std::string_view text) { return Reader(text).run(); }
 
 void save_model_text(const HostModel& m, const std::string& path) {
-    std::ofstream out(path, std::ios::binary);
-    if (!out) throw IoError("save_model: cannot open " + path);
-    out << model_to_text(m);
-    out.flush();
-    if (!out) throw IoError("save_model: write failed for " + path);
+    const std::string doc = model_to_text(m);
+    std::ofstream file(path, std::ios::binary | std::ios::trunc);
+    if (!file.is_open()) throw IoError("save_model: cannot open " + path);
+    file.write(doc.data(), std::streamsize(doc.size()));
+    file.close();
+    if (file.fail()) throw IoError("save_model: write failed for " + path);
 }
 
 HostModel load_model_text(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw IoError("load_model: cannot open " + path);
-    const std::string doc((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::ifstream file(path, std::ios::binary);
+    if (!file.is_open()) throw IoError("load_model: cannot open " + path);
+    const std::string doc{std::istreambuf_iterator<char>(file), std::istreambuf_iterator<char>()};
     try {
         return model_from_text(doc);
-    } catch (const ParseError& e) {
-        throw ParseError(path + ": " + e.what());
-    } catch (const Error& e) {
-        throw Error(path + ": " + e.what());
+    } catch (const ParseError& problem) {
+        throw ParseError(path + ": " + problem.what());
+    } catch (const Error& problem) {
+        throw Error(path + ": " + problem.what());
     }
 }
 
