@@ -82,7 +82,45 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
         }
     }
     if (!same_layers) layer_edges.clear();
-    smem_bytes_ = coalesced_smem_bytes(W, P, uint32_t(layer_edges.size()));
+    // band / far split of the layer for the register-window variant
+    std::vector<uint4> band_pm;
+    std::vector<uint32_t> far_offsets;
+    std::vector<uint2> far_edges;
+    bool windowed = same_layers && P % 8 == 0;
+    if (windowed) {
+        band_pm.resize(2 * size_t(P));
+        far_offsets.assign(size_t(P) + 1, 0);
+        for (uint32_t pos = 0; pos < P; ++pos) {
+            uint32_t twice[4] = {0, 0, 0, 0}, empty[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
+            far_offsets[pos] = uint32_t(far_edges.size());
+            for (uint32_t e = layer_offsets[pos]; e < layer_offsets[pos + 1]; ++e) {
+                const uint32_t t = layer_edges[e].x;
+                const uint32_t distance = t > pos ? t - pos : pos - t;
+                if (distance <= 2) {
+                    float j;
+                    std::memcpy(&j, &layer_edges[e].y, sizeof j);
+                    const float doubled = 2.0f * j;  // exact
+                    const int slot = t < pos ? int(t + 2 - pos) : int(t - pos + 1);  // -2,-1,+1,+2 -> 0..3
+                    if (empty[slot] == 0) windowed = false;  // a neighbour listed twice: the table holds one
+                    std::memcpy(&twice[slot], &doubled, sizeof doubled);
+                    empty[slot] = 0;
+                    windowed = windowed && std::isfinite(doubled);
+                } else {
+                    far_edges.push_back(layer_edges[e]);
+                }
+            }
+            for (uint32_t positive = 0; positive < 2; ++positive) {  // a flip of s adds -(2s)*J
+                const uint32_t flip = positive ? 0x80000000u : 0u;
+                band_pm[2 * size_t(pos) + positive] =
+                    make_uint4((twice[0] ^ flip) | empty[0], (twice[1] ^ flip) | empty[1],
+                               (twice[2] ^ flip) | empty[2], (twice[3] ^ flip) | empty[3]);
+            }
+        }
+        far_offsets[P] = uint32_t(far_edges.size());
+        if (windowed && coalesced_window_smem_bytes(W, P, uint32_t(far_edges.size())) == 0) windowed = false;
+    }
+    smem_bytes_ = windowed ? coalesced_window_smem_bytes(W, P, uint32_t(far_edges.size()))
+                           : coalesced_smem_bytes(W, P, uint32_t(layer_edges.size()));
     if (smem_bytes_ == 0 && same_layers) {  // the graph copy does not fit next to the region: walk the CSR
         same_layers = false;
         layer_edges.clear();
@@ -180,6 +218,9 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
     upload_vec(tau_down_, tau_down, device_bytes_, stream_);
     upload_vec(layer_offsets_, layer_offsets, device_bytes_, stream_);
     upload_vec(layer_edges_, layer_edges, device_bytes_, stream_);
+    upload_vec(band_pm_, band_pm, device_bytes_, stream_);
+    upload_vec(far_offsets_, far_offsets, device_bytes_, stream_);
+    upload_vec(far_edges_, far_edges, device_bytes_, stream_);
     upload_vec(hs_, hs, device_bytes_, stream_);
     upload_vec(ht_, ht, device_bytes_, stream_);
     upload_vec(spins_, spins, device_bytes_, stream_);
@@ -203,6 +244,10 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
     dev_.layer_offsets = same_layers ? layer_offsets_.as<uint32_t>() : nullptr;
     dev_.layer_edges = same_layers ? layer_edges_.as<uint2>() : nullptr;
     dev_.n_layer_edges = uint32_t(layer_edges.size());
+    dev_.band_pm = windowed ? band_pm_.as<uint4>() : nullptr;
+    dev_.far_offsets = far_offsets_.as<uint32_t>();
+    dev_.far_edges = far_edges_.as<uint2>();
+    dev_.n_far_edges = uint32_t(far_edges.size());
     dev_.hs = hs_.as<float>();
     dev_.ht = ht_.as<float>();
     dev_.spins = spins_.as<int8_t>();

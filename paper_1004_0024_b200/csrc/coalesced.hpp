@@ -35,6 +35,13 @@ struct CoalescedDev {
     const uint32_t* layer_offsets;  // per_layer + 1
     const uint2* layer_edges;
     uint32_t n_layer_edges;
+    // the same layer split for the REGISTER WINDOW variant (per_layer % 8 == 0): what a flip adds to the
+    // fields at p-2, p-1, p+1, p+2 (two entries per position, by the sign of the flipped spin: 2p for
+    // s = -1, 2p+1 for s = +1; an empty slot holds -0.0), and the remaining ("far") edges as a CSR list
+    const uint4* band_pm;           // 2 * per_layer, or nullptr
+    const uint32_t* far_offsets;    // per_layer + 1
+    const uint2* far_edges;
+    uint32_t n_far_edges;
     // per chain, new index order
     float* hs;        // [chain][n]
     float* ht;        // [chain][n]
@@ -46,6 +53,8 @@ struct CoalescedDev {
 };
 
 size_t coalesced_smem_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_layer_edges);
+// the register-window variant: band table + far list next to the region
+size_t coalesced_window_smem_bytes(uint32_t lanes, uint32_t per_layer, uint32_t n_far_edges);
 cudaError_t prepare_coalesced_kernels(size_t smem_bytes);
 cudaError_t launch_sweep_coalesced(const CoalescedDev& d, uint32_t sweeps, size_t smem_bytes, cudaStream_t stream);
 
@@ -94,6 +103,7 @@ class CoalescedBatch {
     uint64_t sweeps_done_ = 0;
     std::vector<uint32_t> forward_;  // old index -> new index
     DeviceBuffer offsets_, targets_, couplings_, tau_up_, tau_down_, layer_offsets_, layer_edges_;
+    DeviceBuffer band_pm_, far_offsets_, far_edges_;
     DeviceBuffer hs_, ht_, spins_, mt_, mt_pos_, betas_, flips_;
 };
 
