@@ -250,14 +250,18 @@ __device__ __forceinline__ void window_step(float (&r)[8], const WindowSmem& s, 
     if (K <= 4 || p0 + 8 < P) r[(K + 3) & 7] = s.hs[W * (p + 3) + lane_c];
 
     // tau edges: previous layer (mine, first), then next layer of the lane before me (see the file header)
-    const float deferred = __shfl_sync(0xffffffffu, -__fmul_rn(two_s, j_up), source_lane);
-    float* tau_cell = tau_row + W * p + down_lane;
-    if (accept) {
-        atomicAdd(tau_cell, -__fmul_rn(two_s, j_down));
-        s.spins[cell] = int8_t(-spin_i);
-        ++flips;
+    // (branch-free: a lane without an update adds -0.0, the identity for every value, when any lane has one)
+    const float mine_up = accept ? -__fmul_rn(two_s, j_up) : -0.0f;
+    const float deferred = __shfl_sync(0xffffffffu, mine_up, source_lane);
+    if (accepted != 0u) {
+        float* tau_cell = tau_row + W * p + down_lane;
+        if (active) {
+            atomicAdd(tau_cell, accept ? -__fmul_rn(two_s, j_down) : -0.0f);
+            atomicAdd(tau_cell, deferred);
+        }
+        s.spins[cell] = accept ? int8_t(-spin_i) : spin_i;
+        flips += accept ? 1u : 0u;
     }
-    if (active && ((accepted >> source_lane) & 1u)) atomicAdd(tau_cell, deferred);
 }
 
 template <int EXP>
