@@ -44,7 +44,9 @@ def parse_args():
     ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--ladders", type=int, default=0, help="override ladders per GPU (0: the workload's)")
     ap.add_argument("--exp", default="fast", choices=["exact", "fast", "accurate"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "layered"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "layered", "coalesced"],
+                    help="coalesced: the intra-system schedule (one warp per chain; layered workloads, 1 GPU)")
+    ap.add_argument("--chains", type=int, default=148, help="chains for --kernel coalesced")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-ladders", type=int, default=0, help="CPU sample size in ladders (0: auto)")
@@ -162,6 +164,89 @@ def exp_kind_name(k):
     return {1: "exact", 2: "fast", 3: "accurate"}[k]
 
 
+def bench_coalesced(args, wl, exp_kind):
+    """The intra-system (coalesced) family on a layered workload: `--chains` independent chains of the
+    workload's first instance, one warp each.  One JSON line in the same shape as the main arm; the
+    CPU baseline is the reference's own coalesced engine on one host thread per chain sample."""
+    import paper_1004_0024_b200 as ib
+    from paper_1004_0024_b200 import instances as ins
+    c = wl.make_csrs()[0]
+    if not c["layers"]:
+        raise SystemExit("--kernel coalesced needs a layered workload (c4 or c5)")
+    n = c["n_spins"]
+    model = ib.SpinModel.from_csr(n, c["h"], c["offsets"], c["targets"], c["couplings"], c["tau_counts"],
+                                  c["layers"], c["per_layer"])
+    betas = np.resize(np.asarray(wl.betas, np.float32), args.chains)
+    sweeps_per_step = 10
+    state = ib.init_coalesced(model, betas, base_seed=ins.CHAIN_SEED_BASE, params=ib.SweepParams(1.0, exp_kind))
+    for _ in range(args.warmup):
+        state.run(sweeps_per_step)
+    state.info()
+    sampler = ClockSampler(0)
+    sampler.start()
+    state.run(sweeps_per_step * args.steps)
+    ms = state.info()["last_run_ms"]
+    clocks = sampler.stop()
+    flips, attempts = state.stats()
+    value = args.chains * n * sweeps_per_step * args.steps / (ms * 1e-3)
+    t0 = time.perf_counter()
+    again = ib.init_coalesced(model, betas, base_seed=ins.CHAIN_SEED_BASE, params=ib.SweepParams(1.0, exp_kind))
+    for _ in range(args.steps):
+        again.run(sweeps_per_step)
+        again.stats()
+    energies = again.energies()
+    wall = time.perf_counter() - t0
+    again.close()
+    flip_rate = float(flips.sum()) / float(attempts.sum())
+    dbar = float(len(c["targets"])) / n
+    bytes_per_attempt = 9.0 + flip_rate * (1.0 + 8.0 * dbar)
+    peak, peak_src = peak_hbm()
+    achieved = bytes_per_attempt * value / 1e9
+    base = None
+    if not args.no_cpu_baseline:
+        from oracle import pyoracle
+        pyoracle.build(ref=True)
+        sample = min(args.chains, 4)
+        if pyoracle.Reference.available():
+            ref = pyoracle.Reference()
+            permuted, _ = ref.model(c).prepared_for(3)
+            chains = [ref.chain(permuted, ins.CHAIN_SEED_BASE + 32 * k, float(betas[k]), 1.0, exp_kind, None, engine=3)
+                      for k in range(sample)]
+            kind = "reference"
+        else:
+            port = pyoracle.Port()
+            chains = [port.coalesced(port.model(c), ins.CHAIN_SEED_BASE + 32 * k, float(betas[k]), 1.0, exp_kind)
+                      for k in range(sample)]
+            kind = "port"
+        t1 = time.perf_counter()
+        for ch in chains:
+            ch.sweep(40)
+        secs = time.perf_counter() - t1
+        base = {"value": sample * n * 40 / secs, "unit": UNIT, "cores": 1, "kind": kind,
+                "sample": f"{sample} chains x 40 sweeps of the coalesced engine, one host thread"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{wl.name} instance, {args.chains} independent chains, intra-system (coalesced) "
+                                   f"schedule, {sweeps_per_step * args.steps} sweeps", "chains_per_gpu": args.chains,
+                       "n_spins": n, "sweeps_per_step": sweeps_per_step, "exp_kind": args.exp,
+                       "kernel_family": "sweep_coalesced",
+                       "l2": "state of the chains is L2 resident; the kernel is latency bound (see DESIGN.md 4.5)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src, "bytes_per_attempt": bytes_per_attempt,
+                         "flip_rate": flip_rate, "mean_degree": dbar, "kernel": "sweep_coalesced",
+                         "kernel_ms_per_launch": ms},
+            "cpu_baseline": base,
+            "e2e": {"value": args.chains * n * sweeps_per_step * args.steps / wall, "unit": UNIT,
+                    "h2d_bytes_per_step": (state.n_chains * n * 9 + model_bytes([c])) / args.steps,
+                    "d2h_bytes_per_step": 16 * args.chains + energies.nbytes / args.steps,
+                    "includes": "host init_state (permutation, fields), upload, K steps with per-step flip counts, "
+                                "final energies (host f64 from downloaded spins)"},
+            "gpu_launches": int(state.info()["launches"]) - args.warmup, "clocks": clocks}
+    state.close()
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -171,6 +256,10 @@ def main():
 
     from paper_1004_0024_b200 import workloads
     wl = workloads.get(args.workload)
+    if args.kernel == "coalesced":
+        if rank == 0 and args.impl == "ours":
+            bench_coalesced(args, wl, exp_kind)
+        return
     if args.ladders:
         wl.n_ladders = args.ladders
     sweeps_per_step = wl.swap_interval if wl.swap_interval else 10
