@@ -162,6 +162,30 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
 
 void Batch::bind_device() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
 
+// total_cost (ref: model.cpp:108-126) as the flat sequence of terms its two loops visit: for every
+// spin the field term, then its edges towards higher indices in adjacency order.  Terms with a zero
+// field are left out (cost - (+-0) == cost for every cost the sum can hold), the tail is padded
+// with zero coefficients to a multiple of 32 so that a warp can always take 32 terms at a time.
+static std::vector<uint4> build_cost_terms(const HostModel& m) {
+    std::vector<uint4> terms;
+    terms.reserve(size_t(m.n_spins) + m.targets.size() / 2 + 32);
+    const auto bits = [](float v) {
+        uint32_t pattern;
+        std::memcpy(&pattern, &v, sizeof pattern);
+        return pattern;
+    };
+    for (uint32_t i = 0; i < m.n_spins; ++i) {
+        if (m.h[i] != 0.0f) terms.push_back(make_uint4(i, kFieldTerm, bits(m.h[i]), 0));
+        for (uint32_t e = m.offsets[i]; e < m.offsets[i + 1]; ++e) {
+            if (m.targets[e] > i) terms.push_back(make_uint4(i, m.targets[e], bits(m.couplings[e]), 0));
+        }
+    }
+    do {
+        terms.push_back(make_uint4(0, kFieldTerm, 0, 0));
+    } while (terms.size() % 32 != 0);
+    return terms;
+}
+
 Batch::Batch(const std::vector<const HostModel*>& models,
              const std::vector<uint32_t>& model_of_ladder, const BatchConfig& cfg,
              const int8_t* initial_spins) {
@@ -282,6 +306,9 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         d.targets = keep(m->targets)->as<uint32_t>();
         d.couplings = keep(m->couplings)->as<float>();
         d.tau_counts = keep(m->tau_counts)->as<uint8_t>();
+        const std::vector<uint4> terms = build_cost_terms(*m);
+        d.cost_terms = keep(terms)->as<uint4>();
+        d.n_cost_terms = uint32_t(terms.size());
         dev_models.push_back(d);
     }
     upload(models_, dev_models, device_bytes_, stream_);

@@ -28,7 +28,13 @@ struct DevModel {
     const uint32_t* targets;
     const float* couplings;
     const uint8_t* tau_counts;
+    // total_cost as a flat list in the reference's summation order (batch.cpp: build_cost_terms):
+    // {spin, partner or kFieldTerm, bits of the coefficient, 0}, padded to a multiple of 32 with
+    // zero coefficients.
+    const uint4* cost_terms;
+    uint32_t n_cost_terms;
 };
+constexpr uint32_t kFieldTerm = 0xffffffffu;
 
 // One layer of an identical-layer model, as the layered kernel keeps it in shared memory.
 // Edge e of position p (layer_offsets[p] <= e < layer_offsets[p+1]) goes to position

@@ -80,6 +80,25 @@ struct MtLane {
         load_operands(count, nxt, far);
         generate(count, nxt, far, u);
     }
+
+    // The same chunk as tempered 32-bit outputs (initial_spins reads bit 31 of each).
+    __device__ __forceinline__ void next_chunk_raw(uint32_t count, uint32_t (&raw)[kChunk]) {
+        uint32_t nxt[kChunk], far[kChunk];
+        load_operands(count, nxt, far);
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            if (uint32_t(k) < count) {
+                const uint32_t v = mt_recurrence(cur, nxt[k], far[k]);
+                uint32_t j = pos + k;
+                j = j >= kMtN ? j - kMtN : j;
+                w[size_t(j) * stride] = v;
+                cur = nxt[k];
+                raw[k] = mt_temper(v);
+            }
+        }
+        pos += count;
+        pos = pos >= kMtN ? pos - kMtN : pos;
+    }
 };
 
 // ref: Mt19937::reseed, rng.cpp:37-44

@@ -60,18 +60,36 @@ __device__ __forceinline__ void fields_of_spin(const DevModel& m, const uint32_t
 }
 
 // ref: total_cost, model.cpp:108-126 — f64, index order, each undirected edge once (t > i).
+// The whole warp calls this for its tile: the terms come as a flat list in that order
+// (DevModel::cost_terms); lane l fetches term l of each block of 32 and the two spin words it needs,
+// one block ahead (terms two blocks ahead), and the block is then summed term by term from
+// shuffles, every lane for its own chain.  (double(c) * s_i) * s_t is +-double(c) exactly, so a
+// term is the coefficient with the sign bit of s_i * s_t.
 __device__ double chain_cost(const DevModel& m, const uint32_t* words, uint32_t lane) {
+    const uint32_t blocks = m.n_cost_terms / 32;
+    const uint4* terms = m.cost_terms + lane;
+    const auto signs_of = [&](const uint4& term) {  // bit c: s_i * s_t < 0 in chain c
+        const uint32_t wi = words[term.x];
+        return term.y == kFieldTerm ? wi : wi ^ words[term.y];
+    };
     double cost = 0.0;
-    for (uint32_t i = 0; i < m.n_spins; ++i) {
-        const double si = double(spin_of(words[i], lane));
-        cost = __dsub_rn(cost, __dmul_rn(double(m.h[i]), si));
-        for (uint32_t e = m.offsets[i]; e < m.offsets[i + 1]; ++e) {
-            const uint32_t t = m.targets[e];
-            if (t > i) {
-                const double st = double(spin_of(words[t], lane));
-                cost = __dsub_rn(cost, __dmul_rn(__dmul_rn(double(m.couplings[e]), si), st));
-            }
+    uint4 ahead = terms[0];
+    uint32_t signs = signs_of(ahead);
+    uint32_t coef = ahead.z;
+    ahead = blocks > 1 ? terms[32] : ahead;
+    for (uint32_t blk = 0; blk < blocks; ++blk) {
+        const uint4 next = ahead;
+        if (blk + 2 < blocks) ahead = terms[size_t(blk + 2) * 32];
+        uint32_t next_signs = 0;
+        if (blk + 1 < blocks) next_signs = signs_of(next);
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t flip = (__shfl_sync(0xffffffffu, signs, k) >> lane) << 31;
+            const float c = __uint_as_float(__shfl_sync(0xffffffffu, coef, k) ^ flip);
+            cost = __dsub_rn(cost, double(c));
         }
+        signs = next_signs;
+        coef = next.z;
     }
     return cost;
 }
@@ -87,7 +105,8 @@ __device__ unsigned long long chain_checksum(const uint32_t* words, uint32_t n, 
 }
 
 // ---------------------------------------------------------------------------------------
-// init_state for every chain of a tile (ref: sweep_state.cpp:160-234).
+// init_state for every chain of a tile (ref: sweep_state.cpp:160-234), in two launches: the spin
+// words, generators and energies by one warp per tile, then the fields by one warp per (tile, spin).
 __global__ void __launch_bounds__(kThreads) init_kernel(DevBatch b, const int8_t* initial) {
     TileView t;
     if (!open_tile(b, t)) return;
@@ -99,10 +118,17 @@ __global__ void __launch_bounds__(kThreads) init_kernel(DevBatch b, const int8_t
         mt_seed_lane(t.mt, 32, seed ^ kInitSpinSeedMix);
         MtLane g;
         g.open(t.mt, 32, 0);
-        for (uint32_t i = 0; i < n; ++i) {
-            const bool neg = t.active && (g.next_raw() >> 31);
-            const uint32_t word = __ballot_sync(0xffffffffu, neg);
-            if (t.lane == 0) t.words[i] = word;
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk) {
+            const uint32_t count = min(uint32_t(kChunk), n - i0);
+            uint32_t raw[kChunk];
+            g.next_chunk_raw(count, raw);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (uint32_t(k) < count) {
+                    const uint32_t word = __ballot_sync(0xffffffffu, t.active && (raw[k] >> 31));
+                    if (t.lane == uint32_t(k)) t.words[i0 + k] = word;
+                }
+            }
         }
     } else {
         const int8_t* mine = initial + size_t(t.chain) * n;
@@ -116,16 +142,21 @@ __global__ void __launch_bounds__(kThreads) init_kernel(DevBatch b, const int8_t
     mt_seed_lane(t.mt, 32, seed);
     if (t.lane == 0) b.mt_pos[t.tile] = 0;
 
-    for (uint32_t i = 0; i < n; ++i) {
-        float a, c;
-        fields_of_spin(t.model, t.words, t.lane, i, a, c);
-        t.hs[size_t(i) * 32] = a;
-        if (t.ht) t.ht[size_t(i) * 32] = c;
-    }
+    const double cost = chain_cost(t.model, t.words, t.lane);
     if (t.active) {
-        b.e_run[t.chain] = chain_cost(t.model, t.words, t.lane);
+        b.e_run[t.chain] = cost;
         b.flips[t.chain] = 0ull;
     }
+}
+
+__global__ void __launch_bounds__(256) init_fields_kernel(DevBatch b) {
+    const size_t pair = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (pair >= size_t(b.n_tiles) * b.n_spins) return;
+    const uint32_t tile = uint32_t(pair / b.n_spins), i = uint32_t(pair % b.n_spins), lane = threadIdx.x & 31u;
+    float a, c;
+    fields_of_spin(b.models[b.tile_model[tile]], b.spin_bits + size_t(tile) * b.n_spins, lane, i, a, c);
+    b.hs[pair * 32 + lane] = a;
+    if (b.ht) b.ht[pair * 32 + lane] = c;
 }
 
 // Swap generators: one thread per ladder.
@@ -294,8 +325,9 @@ __global__ void swap_kernel(DevBatch b, unsigned long long round) {
 // Readout.
 __global__ void __launch_bounds__(kThreads) energies_kernel(DevBatch b, double* out) {
     TileView t;
-    if (!open_tile(b, t) || !t.active) return;
-    out[t.chain] = chain_cost(t.model, t.words, t.lane);
+    if (!open_tile(b, t)) return;
+    const double cost = chain_cost(t.model, t.words, t.lane);  // the whole warp, see chain_cost
+    if (t.active) out[t.chain] = cost;
 }
 
 __global__ void __launch_bounds__(kThreads) checksums_kernel(DevBatch b, unsigned long long* out) {
@@ -362,9 +394,10 @@ struct ResultRecord {  // 32 bytes per chain, see ising_batch_pack_results
 
 __global__ void __launch_bounds__(kThreads) pack_results_kernel(DevBatch b, ResultRecord* out) {
     TileView t;
-    if (!open_tile(b, t) || !t.active) return;
+    if (!open_tile(b, t)) return;
     ResultRecord r;
-    r.energy = chain_cost(t.model, t.words, t.lane);
+    r.energy = chain_cost(t.model, t.words, t.lane);  // the whole warp, see chain_cost
+    if (!t.active) return;
     r.e_run = b.e_run[t.chain];
     r.flips = b.flips[t.chain];
     r.checksum = chain_checksum(t.words, b.n_spins, t.lane);
@@ -383,6 +416,8 @@ void launch_sweep_exp(const DevBatch& b, uint32_t sweeps, cudaStream_t s) {
 
 cudaError_t launch_init(const DevBatch& b, const int8_t* initial, cudaStream_t s) {
     init_kernel<<<tile_grid(b), kThreads, 0, s>>>(b, initial);
+    const size_t field_threads = size_t(b.n_tiles) * b.n_spins * 32;
+    if (field_threads) init_fields_kernel<<<unsigned((field_threads + 255) / 256), 256, 0, s>>>(b);
     init_swap_kernel<<<(b.n_ladders + 127) / 128, 128, 0, s>>>(b);
     return cudaGetLastError();
 }
