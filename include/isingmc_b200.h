@@ -183,6 +183,10 @@ typedef struct ising_batch_info {
     double sweep_ms;         /* CUDA-event time summed over sweep launches (needs timing on) */
     double swap_ms;
     double last_run_ms;      /* CUDA-event time of the last ising_batch_run call, whole call */
+    /* generic family only: 0 read-modify-write updates (some coupling or field is below 2^-100 in
+     * magnitude), 1 updates as f32 reductions, 2 reductions + own-field window for every model */
+    uint32_t generic_variant;
+    uint32_t reserved;
 } ising_batch_info;
 /* timing = 1 brackets every sweep/swap launch with CUDA events on the batch's stream. */
 ISING_B200_API ising_status ising_batch_set_timing(ising_batch* batch, int timing);

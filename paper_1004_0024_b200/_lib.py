@@ -33,7 +33,7 @@ class BatchInfo(C.Structure):
         ("kernel", C.c_int), ("sweeps_done", C.c_uint64), ("device_bytes", C.c_uint64),
         ("sweep_launches", C.c_uint64), ("swap_launches", C.c_uint64),
         ("other_launches", C.c_uint64), ("sweep_ms", C.c_double), ("swap_ms", C.c_double),
-        ("last_run_ms", C.c_double),
+        ("last_run_ms", C.c_double), ("generic_variant", C.c_uint32), ("reserved", C.c_uint32),
     ]
 
 

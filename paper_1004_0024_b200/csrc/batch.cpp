@@ -301,6 +301,26 @@ Batch::Batch(const std::vector<const HostModel*>& models,
                 }
             }
         }
+        d.reduction_safe = 1u;
+        const auto tiny = [](float v) { return v != 0.0f && std::fabs(v) < 0x1p-100f; };
+        for (float v : m->h) d.reduction_safe &= tiny(v) ? 0u : 1u;
+        for (float v : m->couplings) d.reduction_safe &= tiny(v) ? 0u : 1u;
+        d.window = nullptr;
+        if (family_ == KernelFamily::generic && d.reduction_safe) {
+            std::vector<float> window(size_t(m->n_spins) * 8, 0.0f);
+            bool usable = true;
+            for (uint32_t i = 0; i < m->n_spins && usable; ++i) {
+                const uint32_t end = m->offsets[i + 1], first_tau = end - m->tau_counts[i];
+                for (uint32_t e = m->offsets[i]; e < end; ++e) {
+                    const uint32_t t = m->targets[e];
+                    if (t <= i || t / 8 != i / 8) continue;
+                    float& slot = window[size_t(i) * 8 + (t - i)];
+                    if (e >= first_tau || slot != 0.0f) usable = false;
+                    slot = m->couplings[e];
+                }
+            }
+            if (usable) d.window = keep(window)->as<float>();
+        }
         d.h = keep(m->h)->as<float>();
         d.offsets = keep(m->offsets)->as<uint32_t>();
         d.targets = keep(m->targets)->as<uint32_t>();
@@ -312,6 +332,13 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         dev_models.push_back(d);
     }
     upload(models_, dev_models, device_bytes_, stream_);
+    dev_.generic_reduce = 1u;
+    bool all_windows = true;
+    for (const DevModel& d : dev_models) {
+        dev_.generic_reduce &= d.reduction_safe;
+        all_windows = all_windows && d.window != nullptr;
+    }
+    generic_variant_ = family_ != KernelFamily::generic ? 0u : !dev_.generic_reduce ? 0u : all_windows ? 2u : 1u;
 
     if (family_ == KernelFamily::layered) {
         cudaDeviceProp prop{};

@@ -89,6 +89,8 @@ class Batch {
     uint32_t n_spins() const { return dev_.n_spins; }
     uint32_t n_tiles() const { return dev_.n_tiles; }
     KernelFamily family() const { return family_; }
+    // generic family: 0 read-modify-write, 1 reductions, 2 reductions + own-field window in every model
+    uint32_t generic_variant() const { return generic_variant_; }
     uint64_t sweeps_done() const { return sweeps_done_; }
     uint64_t device_bytes() const { return device_bytes_; }
     uint64_t sweep_launches = 0, swap_launches = 0, other_launches = 0;
@@ -111,6 +113,7 @@ class Batch {
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
     KernelFamily family_ = KernelFamily::generic;
+    uint32_t generic_variant_ = 0;
     DevBatch dev_{};
     size_t device_bytes_ = 0;
     uint64_t sweeps_done_ = 0;

@@ -413,6 +413,8 @@ ising_status ising_batch_get_info(ising_batch* batch, ising_batch_info* out) {
         out->sweep_ms = b.sweep_ms();
         out->swap_ms = b.swap_ms();
         out->last_run_ms = b.last_run_ms();
+        out->generic_variant = b.generic_variant();
+        out->reserved = 0;
         return ISING_OK;
     });
 }

@@ -48,6 +48,12 @@ CoalescedBatch::CoalescedBatch(const HostModel& m, const CoalescedConfig& cfg, c
         if (!(beta >= 0.0f) || !std::isfinite(beta)) throw Error("init_state: beta must be finite and >= 0");
     }
     if (!std::isfinite(cfg.tau_scale)) throw Error("init_state: tau_scale must be finite");
+    // the kernel applies tau updates as global f32 reductions, which flush subnormals: with every
+    // non-zero value at least 2^-100 no field (a sum of multiples of 2^-123) can be subnormal
+    const auto tiny = [](float v) { return v != 0.0f && std::fabs(v) < 0x1p-100f; };
+    if (std::any_of(m.h.begin(), m.h.end(), tiny) || std::any_of(m.couplings.begin(), m.couplings.end(), tiny)) {
+        throw Error("init_state: the coalesced kernel needs non-zero fields and couplings of magnitude >= 2^-100");
+    }
     if (cfg.exp_kind < 1 || cfg.exp_kind > 3) throw Error("invalid exp_kind value " + std::to_string(cfg.exp_kind));
     for (uint32_t i = 0; i < n; ++i) {
         const uint32_t l = i / P, pos = i % P, end = m.offsets[i + 1];

@@ -23,6 +23,14 @@ struct DevModel {
     uint32_t n_spins;
     uint32_t has_tau;
     uint32_t distinct_targets;  // 1: no spin lists a neighbour twice, so a flip's updates may be batched
+    // 1: every non-zero field and coupling is at least 2^-100 in magnitude, so no effective field can
+    // ever be subnormal (they are sums of multiples of 2^-123) and h[t] -= d may be issued as a global
+    // f32 reduction, which rounds like the subtraction but flushes subnormals
+    uint32_t reduction_safe;
+    // Generic family, own-field window: window[i*8 + q] is the space coupling from spin i to spin i+q
+    // when both lie in the same chunk of eight attempts (else 0).  nullptr when the window cannot be
+    // used (not reduction_safe, a repeated in-chunk neighbour, an in-chunk tau edge).
+    const float* window;
     const float* h;
     const uint32_t* offsets;
     const uint32_t* targets;
@@ -100,6 +108,7 @@ struct DevBatch {
     // 16, 32 neighbouring lanes (chains attempting the same spin in lockstep) that held at least one
     // flip, and the attempts recorded; nullptr unless recording was requested
     unsigned long long* wait_counts;  // [tile][kWaitSlots]
+    uint32_t generic_reduce;          // every model is reduction_safe: the generic family uses sweep_reduce_kernel
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]

@@ -293,6 +293,143 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
 }
 
 // ---------------------------------------------------------------------------------------
+// The same sweep for batches whose models are all DevModel::reduction_safe: a flip's updates
+// h[t] -= (2s)*J go out as f32 reductions at L2 — h + (-(2s*J)) rounds exactly like the subtraction,
+// reductions of one thread to one address apply in program order, and nothing has to come back, so a
+// flip costs no round trip.  The fields are read past L1 (the reductions land in L2).  What is left of
+// the latency is taken off the attempt's critical path: the chunk's CSR offsets and (DevModel::window)
+// its eight own fields are requested together at the start of the chunk — every update of an earlier
+// chunk precedes them in program order, and a flip inside the chunk patches the register copies of
+// its in-chunk neighbours with the very subtraction its reduction performs — and an attempt's edges
+// are requested before its decision, which nine times out of ten needs them.
+__device__ __forceinline__ float ld_field(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void reduce_field(float* p, float addend) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(addend) : "memory");
+}
+
+template <int EXP, bool TAU>
+__global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint32_t sweeps) {
+    TileView t;
+    if (!open_tile(b, t)) return;
+    const uint32_t n = b.n_spins;
+    const DevModel& m = t.model;
+    const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
+    const float gamma = b.tau_scale;
+    double e_run = t.active ? b.e_run[t.chain] : 0.0;
+    unsigned long long flips = 0;
+    const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
+    uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
+    const bool window = m.window != nullptr;
+
+    MtLane g;
+    g.open(t.mt, 32, b.mt_pos[t.tile]);
+
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk) {
+            const uint32_t count = min(uint32_t(kChunk), n - i0);
+            float u[kChunk], own[kChunk], own_tau[kChunk];
+            uint32_t word[kChunk], off[kChunk + 1];
+            g.next_chunk(count, u);
+#pragma unroll
+            for (int k = 0; k <= kChunk; ++k) {
+                if (uint32_t(k) <= count) off[k] = __ldg(m.offsets + i0 + k);
+            }
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (uint32_t(k) < count) {
+                    word[k] = t.words[i0 + k];
+                    if (window) {
+                        own[k] = ld_field(t.hs + size_t(i0 + k) * 32);
+                        if constexpr (TAU) own_tau[k] = ld_field(t.ht + size_t(i0 + k) * 32);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (uint32_t(k) >= count) break;
+                const uint32_t i = i0 + k;
+                const uint32_t first = off[k], end = off[k + 1];
+                const uint32_t mid = TAU ? end - m.tau_counts[i] : end;
+                // the attempt's first eight edges and its window couplings, ahead of the decision
+                uint32_t target[8];
+                float coupling[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const bool have = first + q < end;
+                    target[q] = have ? __ldg(m.targets + first + q) : 0u;
+                    coupling[q] = have ? __ldg(m.couplings + first + q) : 0.0f;
+                }
+                float4 near_lo = make_float4(0.f, 0.f, 0.f, 0.f), near_hi = near_lo;
+                if (window && k + 1 < kChunk) {
+                    near_lo = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i) * 8));
+                    near_hi = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i) * 8 + 4));
+                }
+                const float two_s = (word[k] >> t.lane) & 1u ? -2.0f : 2.0f;
+                const float hsi = window ? own[k] : ld_field(t.hs + size_t(i) * 32);
+                float hti = 0.0f;
+                float x;
+                if constexpr (TAU) {
+                    hti = window ? own_tau[k] : ld_field(t.ht + size_t(i) * 32);
+                    x = flip_exponent(neg_beta, gamma, two_s, hsi, hti);
+                } else {
+                    x = __fmul_rn(neg_beta, __fmul_rn(two_s, hsi));
+                }
+                const float p = exp_kind<EXP>(x);
+                const bool accept = t.active && (u[k] < p);
+                const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+                if (record_wait) wait_fold(ballot, wait);
+                if (ballot != 0u) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        float* field = (!TAU || first + q < mid) ? t.hs : t.ht;
+                        if (accept && first + q < end) {
+                            reduce_field(field + size_t(target[q]) * 32, __fmul_rn(-two_s, coupling[q]));
+                        }
+                    }
+                    for (uint32_t e = first + 8; e < end; ++e) {  // degree > 8
+                        float* field = (!TAU || e < mid) ? t.hs : t.ht;
+                        const size_t at = size_t(__ldg(m.targets + e)) * 32;
+                        const float d = __fmul_rn(-two_s, __ldg(m.couplings + e));
+                        if (accept) reduce_field(field + at, d);
+                    }
+                    const float near[8] = {near_lo.x, near_lo.y, near_lo.z, near_lo.w,
+                                           near_hi.x, near_hi.y, near_hi.z, near_hi.w};
+#pragma unroll
+                    for (int q = 1; k + q < kChunk; ++q) {
+                        own[k + q] = accept ? __fsub_rn(own[k + q], __fmul_rn(two_s, near[q])) : own[k + q];
+                    }
+                    if (accept) {
+                        ++flips;
+                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(hsi, hti))));
+                    }
+                    if (t.lane == 0) t.words[i] = word[k] ^ ballot;
+                }
+            }
+        }
+        __syncwarp();  // lane 0's spin-word stores become visible to the whole warp
+        if (record_wait) {  // flushed per sweep: the 32-bit partial counts cannot overflow (n < 2^27)
+            unsigned long long* out = b.wait_counts + size_t(t.tile) * kWaitSlots;
+#pragma unroll
+            for (int w = 0; w < 6; ++w) {
+                if (t.lane == 0) out[w] += wait[w];
+                wait[w] = 0;
+            }
+            if (t.lane == 0) out[6] += n;
+        }
+    }
+
+    if (t.lane == 0) b.mt_pos[t.tile] = g.pos;
+    if (t.active) {
+        b.e_run[t.chain] = e_run;
+        b.flips[t.chain] += flips;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Tempering swap round (new semantics, oracle/ising_oracle.h): pairs of
 // slots (k,k+1), k = round&1, +2, ...; one draw per pair from the ladder's own generator;
 // accept iff u < exp_kind(float((beta_k - beta_k1) * (E_a - E_b))); the chains exchange slots.
@@ -408,8 +545,14 @@ inline dim3 tile_grid(const DevBatch& b) { return dim3((b.n_tiles + kWarpsPerBlo
 
 template <int EXP>
 void launch_sweep_exp(const DevBatch& b, uint32_t sweeps, cudaStream_t s) {
-    if (b.ht) sweep_generic_kernel<EXP, true><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
-    else sweep_generic_kernel<EXP, false><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+    if (b.generic_reduce) {
+        if (b.ht) sweep_reduce_kernel<EXP, true><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+        else sweep_reduce_kernel<EXP, false><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+    } else if (b.ht) {
+        sweep_generic_kernel<EXP, true><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+    } else {
+        sweep_generic_kernel<EXP, false><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+    }
 }
 
 }  // namespace

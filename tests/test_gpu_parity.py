@@ -423,3 +423,39 @@ def test_one_shot_run_json_has_the_reference_report_keys(lib, port, tmp_path):
     assert head == ("b200-layered", "fast", 64, 25, 4321, 1)
     assert doc["beta"] == float(np.float32(0.7)) and doc["tau_scale"] == 1.25 and doc["wait"] == {}
     assert "device=" in doc["environment"]
+
+
+def _with_coupling(csr, spin, slot, value):
+    """The same graph with the coupling of `spin`'s `slot`-th edge (both directions) replaced."""
+    out = dict(csr)
+    out["couplings"] = csr["couplings"].copy()
+    e = int(csr["offsets"][spin]) + slot
+    t = int(csr["targets"][e])
+    out["couplings"][e] = value
+    back = [k for k in range(int(csr["offsets"][t]), int(csr["offsets"][t + 1])) if int(csr["targets"][k]) == spin]
+    out["couplings"][back[0]] = value
+    return out
+
+
+def test_generic_family_update_variants(lib, port):
+    """The generic family's three ways of applying a flip's updates land on the same bits as the oracle:
+    f32 reductions with the own-field window (the default), reductions without it (a model whose window
+    is unusable: an in-chunk tau edge), and read-modify-write (a coupling so small that a field could be
+    subnormal, which a reduction would flush)."""
+    betas = ins.geometric_betas(0.2, 3.0, 8)
+    base = ins.cubic_mixed_degree(8, ins.INSTANCE_SEED + 40)
+    state, want = run_both(port, [base], 6, betas, 80, 1, kernel=ib.KERNEL_GENERIC)
+    assert state.info()["generic_variant"] == 2
+    assert_batch_matches(state, want, REL_ENERGY)
+
+    # four positions per layer: the tau partner of spin i is i + 4, inside i's chunk of eight attempts
+    narrow = ins.build_layered_csr(*ins.layered_spec(4, 77), 6, 1.25)
+    state, want = run_both(port, [narrow], 40, [0.7], 100, 0, tau_scale=0.75, kernel=ib.KERNEL_GENERIC)
+    assert state.info()["generic_variant"] == 1
+    assert_batch_matches(state, want, REL_ENERGY)
+
+    # a subnormal coupling: fields of the two spins it joins carry subnormal parts
+    tiny = _with_coupling(base, 5, 0, np.float32(3e-39))
+    state, want = run_both(port, [tiny, base], 2, betas, 80, 1, kernel=ib.KERNEL_GENERIC)
+    assert state.info()["generic_variant"] == 0
+    assert_batch_matches(state, want, REL_ENERGY)
