@@ -328,46 +328,72 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
     MtLane g;
     g.open(t.mt, 32, b.mt_pos[t.tile]);
 
+    // What a chunk needs and no attempt before it can change is requested one chunk ahead: the
+    // generator's recurrence operands, the CSR offsets, the spin words (a word changes only at its own
+    // attempt; with a single chunk per sweep the request has to wait for the chunk's own attempts).
+    uint32_t mt_next[kChunk], mt_far[kChunk], off_ahead[kChunk + 1], word_ahead[kChunk];
+    const auto request = [&](uint32_t first) {
+        const uint32_t cnt = min(uint32_t(kChunk), n - first);
+#pragma unroll
+        for (int k = 0; k <= kChunk; ++k) {
+            if (uint32_t(k) <= cnt) off_ahead[k] = __ldg(m.offsets + first + k);
+            if (uint32_t(k) < cnt) word_ahead[k] = t.words[first + k];
+        }
+    };
+    const bool early = n > uint32_t(kChunk);
+    g.load_operands(min(uint32_t(kChunk), n), mt_next, mt_far);
+    request(0);
+
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t i0 = 0; i0 < n; i0 += kChunk) {
             const uint32_t count = min(uint32_t(kChunk), n - i0);
+            const uint32_t i0_ahead = i0 + kChunk < n ? i0 + kChunk : 0u;
             float u[kChunk], own[kChunk], own_tau[kChunk];
             uint32_t word[kChunk], off[kChunk + 1];
-            g.next_chunk(count, u);
 #pragma unroll
             for (int k = 0; k <= kChunk; ++k) {
-                if (uint32_t(k) <= count) off[k] = __ldg(m.offsets + i0 + k);
+                off[k] = off_ahead[k];
+                if (k < kChunk) word[k] = word_ahead[k];
             }
+            g.generate(count, mt_next, mt_far, u);
 #pragma unroll
             for (int k = 0; k < kChunk; ++k) {
-                if (uint32_t(k) < count) {
-                    word[k] = t.words[i0 + k];
-                    if (window) {
-                        own[k] = ld_field(t.hs + size_t(i0 + k) * 32);
-                        if constexpr (TAU) own_tau[k] = ld_field(t.ht + size_t(i0 + k) * 32);
-                    }
+                if (window && uint32_t(k) < count) {
+                    own[k] = ld_field(t.hs + size_t(i0 + k) * 32);
+                    if constexpr (TAU) own_tau[k] = ld_field(t.ht + size_t(i0 + k) * 32);
                 }
             }
+            g.load_operands(min(uint32_t(kChunk), n - i0_ahead), mt_next, mt_far);
+            if (early) {
+                __syncwarp();  // lane 0's spin-word stores of the previous sweep
+                request(i0_ahead);
+            }
+            // an attempt's first eight edges and its window couplings, one attempt ahead
+            uint32_t target[2][8];
+            float coupling[2][8];
+            float4 near_lo[2], near_hi[2];
+            const auto fetch_edges = [&](int k, int slot) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const bool have = off[k] + q < off[k + 1];
+                    target[slot][q] = have ? __ldg(m.targets + off[k] + q) : 0u;
+                    coupling[slot][q] = have ? __ldg(m.couplings + off[k] + q) : 0.0f;
+                }
+                if (window && k + 1 < kChunk) {
+                    near_lo[slot] = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i0 + k) * 8));
+                    near_hi[slot] = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i0 + k) * 8 + 4));
+                } else {
+                    near_lo[slot] = near_hi[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            };
+            fetch_edges(0, 0);
 #pragma unroll
             for (int k = 0; k < kChunk; ++k) {
                 if (uint32_t(k) >= count) break;
                 const uint32_t i = i0 + k;
                 const uint32_t first = off[k], end = off[k + 1];
                 const uint32_t mid = TAU ? end - m.tau_counts[i] : end;
-                // the attempt's first eight edges and its window couplings, ahead of the decision
-                uint32_t target[8];
-                float coupling[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const bool have = first + q < end;
-                    target[q] = have ? __ldg(m.targets + first + q) : 0u;
-                    coupling[q] = have ? __ldg(m.couplings + first + q) : 0.0f;
-                }
-                float4 near_lo = make_float4(0.f, 0.f, 0.f, 0.f), near_hi = near_lo;
-                if (window && k + 1 < kChunk) {
-                    near_lo = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i) * 8));
-                    near_hi = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i) * 8 + 4));
-                }
+                if (k + 1 < kChunk && uint32_t(k + 1) < count) fetch_edges(k + 1, (k + 1) & 1);
                 const float two_s = (word[k] >> t.lane) & 1u ? -2.0f : 2.0f;
                 const float hsi = window ? own[k] : ld_field(t.hs + size_t(i) * 32);
                 float hti = 0.0f;
@@ -387,7 +413,7 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
                     for (int q = 0; q < 8; ++q) {
                         float* field = (!TAU || first + q < mid) ? t.hs : t.ht;
                         if (accept && first + q < end) {
-                            reduce_field(field + size_t(target[q]) * 32, __fmul_rn(-two_s, coupling[q]));
+                            reduce_field(field + size_t(target[k & 1][q]) * 32, __fmul_rn(-two_s, coupling[k & 1][q]));
                         }
                     }
                     for (uint32_t e = first + 8; e < end; ++e) {  // degree > 8
@@ -396,8 +422,8 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
                         const float d = __fmul_rn(-two_s, __ldg(m.couplings + e));
                         if (accept) reduce_field(field + at, d);
                     }
-                    const float near[8] = {near_lo.x, near_lo.y, near_lo.z, near_lo.w,
-                                           near_hi.x, near_hi.y, near_hi.z, near_hi.w};
+                    const float4 lo = near_lo[k & 1], hi = near_hi[k & 1];
+                    const float near[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
                     for (int q = 1; k + q < kChunk; ++q) {
                         own[k + q] = accept ? __fsub_rn(own[k + q], __fmul_rn(two_s, near[q])) : own[k + q];
@@ -411,6 +437,7 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
             }
         }
         __syncwarp();  // lane 0's spin-word stores become visible to the whole warp
+        if (!early) request(0);
         if (record_wait) {  // flushed per sweep: the 32-bit partial counts cannot overflow (n < 2^27)
             unsigned long long* out = b.wait_counts + size_t(t.tile) * kWaitSlots;
 #pragma unroll
