@@ -375,9 +375,12 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
             const auto fetch_edges = [&](int k, int slot) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const bool have = off[k] + q < off[k + 1];
-                    target[slot][q] = have ? __ldg(m.targets + off[k] + q) : 0u;
-                    coupling[slot][q] = have ? __ldg(m.couplings + off[k] + q) : 0.0f;
+                    // (left unset past the spin's last edge: a default would make the compiler wait for
+                    // the load right here, to select between the two)
+                    if (off[k] + q < off[k + 1]) {
+                        target[slot][q] = __ldg(m.targets + off[k] + q);
+                        coupling[slot][q] = __ldg(m.couplings + off[k] + q);
+                    }
                 }
                 if (window && k + 1 < kChunk) {
                     near_lo[slot] = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i0 + k) * 8));
