@@ -415,8 +415,11 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         float* field = (!TAU || first + q < mid) ? t.hs : t.ht;
-                        if (accept && first + q < end) {
-                            reduce_field(field + size_t(target[k & 1][q]) * 32, __fmul_rn(-two_s, coupling[k & 1][q]));
+                        // every lane takes part (a lane that did not accept adds -0.0, the identity for
+                        // every bit pattern), so the warp does not diverge once per edge
+                        if (first + q < end) {
+                            reduce_field(field + size_t(target[k & 1][q]) * 32,
+                                         accept ? __fmul_rn(-two_s, coupling[k & 1][q]) : -0.0f);
                         }
                     }
                     for (uint32_t e = first + 8; e < end; ++e) {  // degree > 8
