@@ -108,7 +108,7 @@ struct DevBatch {
     // 16, 32 neighbouring lanes (chains attempting the same spin in lockstep) that held at least one
     // flip, and the attempts recorded; nullptr unless recording was requested
     unsigned long long* wait_counts;  // [tile][kWaitSlots]
-    uint32_t generic_reduce;          // every model is reduction_safe: the generic family uses sweep_reduce_kernel
+    uint32_t generic_reduce;          // every model is reduction_safe: the generic family uses sweep_split_kernel
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]

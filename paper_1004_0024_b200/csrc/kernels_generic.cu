@@ -296,12 +296,10 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
 // The same sweep for batches whose models are all DevModel::reduction_safe: a flip's updates
 // h[t] -= (2s)*J go out as f32 reductions at L2 — h + (-(2s*J)) rounds exactly like the subtraction,
 // reductions of one thread to one address apply in program order, and nothing has to come back, so a
-// flip costs no round trip.  The fields are read past L1 (the reductions land in L2).  What is left of
-// the latency is taken off the attempt's critical path: the chunk's CSR offsets and (DevModel::window)
-// its eight own fields are requested together at the start of the chunk — every update of an earlier
-// chunk precedes them in program order, and a flip inside the chunk patches the register copies of
-// its in-chunk neighbours with the very subtraction its reduction performs — and an attempt's edges
-// are requested before its decision, which nine times out of ten needs them.
+// flip costs no round trip.  The fields are read past L1 (the reductions land in L2).  The chunk's
+// eight own fields are requested together at the start of the chunk (DevModel::window) — every update
+// of an earlier chunk precedes them in program order, and a flip inside the chunk patches the register
+// copies of its in-chunk neighbours with the very subtraction its reduction performs.
 __device__ __forceinline__ float ld_field(const float* p) {
     float v;
     asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
@@ -311,10 +309,115 @@ __device__ __forceinline__ void reduce_field(float* p, float addend) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(addend) : "memory");
 }
 
+// ---------------------------------------------------------------------------------------
+// Two warps per tile.  The PRODUCER warp runs ahead and fills a ring of
+// shared-memory stages, one per chunk of eight attempts, with everything that does not depend on the
+// chain's state: the eight uniform draws of every lane, and (warp-uniform) each attempt's first eight
+// edges, its window couplings and its edge counts.  The SWEEP warp keeps the state: spin words, own
+// fields, decisions, reductions, bookkeeping — about a third of the instructions of a one-warp
+// version (2.2x slower on c3), on a path that is one in-order warp's instruction latency.  Stages change hands through a
+// pair of mbarriers each (full: producer -> sweep, empty: sweep -> producer).
+constexpr int kSplitStages = 4;
+constexpr int kSplitThreads = 64;
+struct SplitStage {
+    float u[kChunk][32];
+    uint32_t target[kChunk][8];
+    float coupling[kChunk][8];
+    float near[kChunk][8];
+    uint32_t degree[kChunk];  // edges of attempt k
+    uint32_t space[kChunk];   // the first `space` of them update h_eff_space, the rest h_eff_tau
+    uint32_t first[kChunk];   // CSR offset of attempt k's edges (degree > 8: the tail is read from there)
+    uint32_t pad[kChunk];
+};
+
+__device__ __forceinline__ uint32_t split_smem(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void split_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(split_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void split_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(split_smem(bar)), "r"(parity)
+            : "memory");
+    } while (done == 0u);
+}
+
+template <bool TAU>
+__device__ void split_producer(const DevBatch& b, const TileView& t, uint32_t sweeps, SplitStage* stages,
+                               uint64_t* full, uint64_t* empty) {
+    const uint32_t n = b.n_spins;
+    const DevModel& m = t.model;
+    const bool window = m.window != nullptr;
+    MtLane g;
+    g.open(t.mt, 32, b.mt_pos[t.tile]);
+    uint32_t mt_next[kChunk], mt_far[kChunk];
+    g.load_operands(min(uint32_t(kChunk), n), mt_next, mt_far);
+    // lane l <= 8 keeps offsets[i0 + l] of the chunk, requested one chunk ahead
+    uint32_t off_ahead = t.lane <= min(uint32_t(kChunk), n) ? __ldg(m.offsets + t.lane) : 0u;
+    uint32_t chunk = 0;
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk, ++chunk) {
+            const uint32_t count = min(uint32_t(kChunk), n - i0);
+            const uint32_t i0_ahead = i0 + kChunk < n ? i0 + kChunk : 0u;
+            const uint32_t st = chunk % kSplitStages;
+            SplitStage& stage = stages[st];
+            float u[kChunk];
+            g.generate(count, mt_next, mt_far, u);
+            g.load_operands(min(uint32_t(kChunk), n - i0_ahead), mt_next, mt_far);
+            const uint32_t off_mine = off_ahead;
+            off_ahead = t.lane <= min(uint32_t(kChunk), n - i0_ahead) ? __ldg(m.offsets + i0_ahead + t.lane) : 0u;
+            // (attempt, edge) pairs: this lane fills (lane / 8, lane % 8) and (lane / 8 + 4, lane % 8)
+            uint32_t tg[2];
+            float cp[2], nr[2];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t k = (t.lane >> 3) + 4u * half, q = t.lane & 7u;
+                const uint32_t lo = __shfl_sync(0xffffffffu, off_mine, k);
+                const uint32_t hi = __shfl_sync(0xffffffffu, off_mine, k + 1);
+                const bool have = k < count && lo + q < hi;
+                tg[half] = have ? __ldg(m.targets + lo + q) : 0u;
+                cp[half] = have ? __ldg(m.couplings + lo + q) : 0.0f;
+                nr[half] = (window && k < count) ? __ldg(m.window + size_t(i0 + k) * 8 + q) : 0.0f;
+            }
+            uint32_t degree = 0, space = 0;
+            {
+                const uint32_t hi = __shfl_sync(0xffffffffu, off_mine, min(t.lane + 1, uint32_t(kChunk)));
+                if (t.lane < count) {
+                    degree = hi - off_mine;
+                    space = TAU ? degree - m.tau_counts[i0 + t.lane] : degree;
+                }
+            }
+            if (chunk >= uint32_t(kSplitStages)) split_wait(&empty[st], ((chunk / kSplitStages) - 1u) & 1u);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) stage.u[k][t.lane] = u[k];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t k = (t.lane >> 3) + 4u * half, q = t.lane & 7u;
+                stage.target[k][q] = tg[half];
+                stage.coupling[k][q] = cp[half];
+                stage.near[k][q] = nr[half];
+            }
+            if (t.lane < uint32_t(kChunk)) {
+                stage.degree[t.lane] = degree;
+                stage.space[t.lane] = space;
+                stage.first[t.lane] = off_mine;
+            }
+            split_arrive(&full[st]);
+        }
+    }
+    if (t.lane == 0) b.mt_pos[t.tile] = g.pos;
+}
+
 template <int EXP, bool TAU>
-__global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint32_t sweeps) {
-    TileView t;
-    if (!open_tile(b, t)) return;
+__device__ void split_sweep(const DevBatch& b, const TileView& t, uint32_t sweeps, const SplitStage* stages,
+                            uint64_t* full, uint64_t* empty) {
     const uint32_t n = b.n_spins;
     const DevModel& m = t.model;
     const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
@@ -324,79 +427,39 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
     const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
     const bool window = m.window != nullptr;
-
-    MtLane g;
-    g.open(t.mt, 32, b.mt_pos[t.tile]);
-
-    // What a chunk needs and no attempt before it can change is requested one chunk ahead: the
-    // generator's recurrence operands, the CSR offsets, the spin words (a word changes only at its own
-    // attempt; with a single chunk per sweep the request has to wait for the chunk's own attempts).
-    uint32_t mt_next[kChunk], mt_far[kChunk], off_ahead[kChunk + 1], word_ahead[kChunk];
-    const auto request = [&](uint32_t first) {
-        const uint32_t cnt = min(uint32_t(kChunk), n - first);
-#pragma unroll
-        for (int k = 0; k <= kChunk; ++k) {
-            if (uint32_t(k) <= cnt) off_ahead[k] = __ldg(m.offsets + first + k);
-            if (uint32_t(k) < cnt) word_ahead[k] = t.words[first + k];
-        }
-    };
-    const bool early = n > uint32_t(kChunk);
-    g.load_operands(min(uint32_t(kChunk), n), mt_next, mt_far);
-    request(0);
-
+    uint32_t chunk = 0;
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
-        for (uint32_t i0 = 0; i0 < n; i0 += kChunk) {
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk, ++chunk) {
             const uint32_t count = min(uint32_t(kChunk), n - i0);
-            const uint32_t i0_ahead = i0 + kChunk < n ? i0 + kChunk : 0u;
-            float u[kChunk], own[kChunk], own_tau[kChunk];
-            uint32_t word[kChunk], off[kChunk + 1];
-#pragma unroll
-            for (int k = 0; k <= kChunk; ++k) {
-                off[k] = off_ahead[k];
-                if (k < kChunk) word[k] = word_ahead[k];
-            }
-            g.generate(count, mt_next, mt_far, u);
+            const uint32_t st = chunk % kSplitStages;
+            const SplitStage& stage = stages[st];
+            float own[kChunk], own_tau[kChunk], u[kChunk];
+            uint32_t word[kChunk];
 #pragma unroll
             for (int k = 0; k < kChunk; ++k) {
-                if (window && uint32_t(k) < count) {
-                    own[k] = ld_field(t.hs + size_t(i0 + k) * 32);
-                    if constexpr (TAU) own_tau[k] = ld_field(t.ht + size_t(i0 + k) * 32);
-                }
-            }
-            g.load_operands(min(uint32_t(kChunk), n - i0_ahead), mt_next, mt_far);
-            if (early) {
-                __syncwarp();  // lane 0's spin-word stores of the previous sweep
-                request(i0_ahead);
-            }
-            // an attempt's first eight edges and its window couplings, one attempt ahead
-            uint32_t target[2][8];
-            float coupling[2][8];
-            float4 near_lo[2], near_hi[2];
-            const auto fetch_edges = [&](int k, int slot) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    // (left unset past the spin's last edge: a default would make the compiler wait for
-                    // the load right here, to select between the two)
-                    if (off[k] + q < off[k + 1]) {
-                        target[slot][q] = __ldg(m.targets + off[k] + q);
-                        coupling[slot][q] = __ldg(m.couplings + off[k] + q);
+                if (uint32_t(k) < count) {
+                    word[k] = t.words[i0 + k];
+                    if (window) {
+                        own[k] = ld_field(t.hs + size_t(i0 + k) * 32);
+                        if constexpr (TAU) own_tau[k] = ld_field(t.ht + size_t(i0 + k) * 32);
                     }
                 }
-                if (window && k + 1 < kChunk) {
-                    near_lo[slot] = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i0 + k) * 8));
-                    near_hi[slot] = __ldg(reinterpret_cast<const float4*>(m.window + size_t(i0 + k) * 8 + 4));
-                } else {
-                    near_lo[slot] = near_hi[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            };
-            fetch_edges(0, 0);
+            }
+            split_wait(&full[st], (chunk / kSplitStages) & 1u);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) u[k] = stage.u[k][t.lane];
 #pragma unroll
             for (int k = 0; k < kChunk; ++k) {
                 if (uint32_t(k) >= count) break;
                 const uint32_t i = i0 + k;
-                const uint32_t first = off[k], end = off[k + 1];
-                const uint32_t mid = TAU ? end - m.tau_counts[i] : end;
-                if (k + 1 < kChunk && uint32_t(k + 1) < count) fetch_edges(k + 1, (k + 1) & 1);
+                // warp-uniform operands of this attempt, ahead of the decision
+                const uint4 tg_lo = *reinterpret_cast<const uint4*>(&stage.target[k][0]);
+                const uint4 tg_hi = *reinterpret_cast<const uint4*>(&stage.target[k][4]);
+                const float4 cp_lo = *reinterpret_cast<const float4*>(&stage.coupling[k][0]);
+                const float4 cp_hi = *reinterpret_cast<const float4*>(&stage.coupling[k][4]);
+                const float4 nr_lo = *reinterpret_cast<const float4*>(&stage.near[k][0]);
+                const float4 nr_hi = *reinterpret_cast<const float4*>(&stage.near[k][4]);
+                const uint32_t degree = stage.degree[k], space = stage.space[k];
                 const float two_s = (word[k] >> t.lane) & 1u ? -2.0f : 2.0f;
                 const float hsi = window ? own[k] : ld_field(t.hs + size_t(i) * 32);
                 float hti = 0.0f;
@@ -412,24 +475,27 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
                 const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
                 if (record_wait) wait_fold(ballot, wait);
                 if (ballot != 0u) {
+                    const uint32_t target[8] = {tg_lo.x, tg_lo.y, tg_lo.z, tg_lo.w, tg_hi.x, tg_hi.y, tg_hi.z, tg_hi.w};
+                    const float coupling[8] = {cp_lo.x, cp_lo.y, cp_lo.z, cp_lo.w, cp_hi.x, cp_hi.y, cp_hi.z, cp_hi.w};
+                    const float near[8] = {nr_lo.x, nr_lo.y, nr_lo.z, nr_lo.w, nr_hi.x, nr_hi.y, nr_hi.z, nr_hi.w};
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        float* field = (!TAU || first + q < mid) ? t.hs : t.ht;
+                        float* field = (!TAU || uint32_t(q) < space) ? t.hs : t.ht;
                         // every lane takes part (a lane that did not accept adds -0.0, the identity for
                         // every bit pattern), so the warp does not diverge once per edge
-                        if (first + q < end) {
-                            reduce_field(field + size_t(target[k & 1][q]) * 32,
-                                         accept ? __fmul_rn(-two_s, coupling[k & 1][q]) : -0.0f);
+                        if (uint32_t(q) < degree) {
+                            reduce_field(field + size_t(target[q]) * 32, accept ? __fmul_rn(-two_s, coupling[q]) : -0.0f);
                         }
                     }
-                    for (uint32_t e = first + 8; e < end; ++e) {  // degree > 8
-                        float* field = (!TAU || e < mid) ? t.hs : t.ht;
-                        const size_t at = size_t(__ldg(m.targets + e)) * 32;
-                        const float d = __fmul_rn(-two_s, __ldg(m.couplings + e));
-                        if (accept) reduce_field(field + at, d);
+                    if (degree > 8u) {
+                        const uint32_t first = stage.first[k];
+                        for (uint32_t e = 8; e < degree; ++e) {
+                            float* field = (!TAU || e < space) ? t.hs : t.ht;
+                            const size_t at = size_t(__ldg(m.targets + first + e)) * 32;
+                            const float d = __fmul_rn(-two_s, __ldg(m.couplings + first + e));
+                            reduce_field(field + at, accept ? d : -0.0f);
+                        }
                     }
-                    const float4 lo = near_lo[k & 1], hi = near_hi[k & 1];
-                    const float near[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
                     for (int q = 1; k + q < kChunk; ++q) {
                         own[k + q] = accept ? __fsub_rn(own[k + q], __fmul_rn(two_s, near[q])) : own[k + q];
@@ -441,9 +507,9 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
                     if (t.lane == 0) t.words[i] = word[k] ^ ballot;
                 }
             }
+            split_arrive(&empty[st]);
         }
         __syncwarp();  // lane 0's spin-word stores become visible to the whole warp
-        if (!early) request(0);
         if (record_wait) {  // flushed per sweep: the 32-bit partial counts cannot overflow (n < 2^27)
             unsigned long long* out = b.wait_counts + size_t(t.tile) * kWaitSlots;
 #pragma unroll
@@ -454,11 +520,35 @@ __global__ void __launch_bounds__(kThreads) sweep_reduce_kernel(DevBatch b, uint
             if (t.lane == 0) out[6] += n;
         }
     }
-
-    if (t.lane == 0) b.mt_pos[t.tile] = g.pos;
     if (t.active) {
         b.e_run[t.chain] = e_run;
         b.flips[t.chain] += flips;
+    }
+}
+
+template <int EXP, bool TAU>
+__global__ void __launch_bounds__(kSplitThreads) sweep_split_kernel(DevBatch b, uint32_t sweeps) {
+    __shared__ __align__(16) SplitStage stages[kSplitStages];
+    __shared__ __align__(8) uint64_t bars[2 * kSplitStages];
+    TileView t;
+    t.tile = blockIdx.x;
+    t.lane = threadIdx.x & 31u;
+    t.active = t.lane < b.tile_count[t.tile];
+    t.chain = b.tile_first[t.tile] + t.lane;
+    t.model = b.models[b.tile_model[t.tile]];
+    const size_t base = size_t(t.tile) * b.n_spins;
+    t.hs = b.hs + base * 32 + t.lane;
+    t.ht = b.ht ? b.ht + base * 32 + t.lane : nullptr;
+    t.words = b.spin_bits + base;
+    t.mt = b.mt + size_t(t.tile) * kMtN * 32 + t.lane;
+    if (threadIdx.x < 2 * kSplitStages) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(split_smem(&bars[threadIdx.x])), "r"(32) : "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        split_sweep<EXP, TAU>(b, t, sweeps, stages, bars, bars + kSplitStages);
+    } else {
+        split_producer<TAU>(b, t, sweeps, stages, bars, bars + kSplitStages);
     }
 }
 
@@ -578,9 +668,9 @@ inline dim3 tile_grid(const DevBatch& b) { return dim3((b.n_tiles + kWarpsPerBlo
 
 template <int EXP>
 void launch_sweep_exp(const DevBatch& b, uint32_t sweeps, cudaStream_t s) {
-    if (b.generic_reduce) {
-        if (b.ht) sweep_reduce_kernel<EXP, true><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
-        else sweep_reduce_kernel<EXP, false><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
+    if (b.generic_reduce && b.n_tiles != 0) {
+        if (b.ht) sweep_split_kernel<EXP, true><<<b.n_tiles, kSplitThreads, 0, s>>>(b, sweeps);
+        else sweep_split_kernel<EXP, false><<<b.n_tiles, kSplitThreads, 0, s>>>(b, sweeps);
     } else if (b.ht) {
         sweep_generic_kernel<EXP, true><<<tile_grid(b), kThreads, 0, s>>>(b, sweeps);
     } else {
