@@ -55,4 +55,20 @@ def assert_batch_matches(state, want, rel_energy=1e-5):
     return e
 
 
-__all__ = ["csr_from_npz", "product_model", "bits", "oracle_batch", "assert_batch_matches", "ins", "ib"]
+def random_graph(n, mean_degree, seed, repeats=0):
+    """A seeded random multigraph: `mean_degree * n / 2` distinct edges plus `repeats` repeated ones,
+    Gaussian couplings and fields (tests only: degrees well beyond eight, a ragged last chunk)."""
+    rng = np.random.default_rng(seed)
+    pairs = set()
+    while len(pairs) < mean_degree * n // 2:
+        a, b = (int(v) for v in rng.integers(0, n, 2))
+        if a != b:
+            pairs.add((min(a, b), max(a, b)))
+    edges = sorted(pairs)
+    edges += [edges[int(k)] for k in rng.integers(0, len(edges), repeats)]
+    coup = rng.normal(0.0, 1.0, len(edges)).astype(np.float32)
+    h = rng.normal(0.0, 0.3, n).astype(np.float32)
+    return ins.csr_from_adjacency(h, ins._adjacency(n, np.array(edges, np.int64), coup))
+
+
+__all__ = ["random_graph", "csr_from_npz", "product_model", "bits", "oracle_batch", "assert_batch_matches", "ins", "ib"]

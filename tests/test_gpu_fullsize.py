@@ -9,7 +9,7 @@ import pytest
 
 import paper_1004_0024_b200 as ib
 from paper_1004_0024_b200 import sharding, workloads
-from helpers import ins, oracle_batch, product_model
+from helpers import assert_batch_matches, ins, oracle_batch, product_model, random_graph
 
 pytestmark = pytest.mark.gpu
 
@@ -209,3 +209,53 @@ def test_random_layer_graphs_both_families_bit_identical(lib, seed):
             else:
                 for a, b in zip(out["layered"], got):
                     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ISING_FUZZ_SEEDS", "12"))))
+def test_random_multigraphs_generic_family_matches_the_oracle(lib, port, seed):
+    """Seeded fuzz of the generic family against the oracle: random multigraphs (sizes off the chunk
+    grid, degrees from sparse to ~25, repeated edges, zero fields, now and then a subnormal coupling
+    that sends the batch through the read-modify-write kernel), random ladders, all exp kinds."""
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.choice([5, 8, 9, 31, 64, 77, 130, 257]))
+    n_models = int(rng.integers(1, 4))
+    csrs = []
+    for k in range(n_models):
+        degree = int(rng.integers(2, min(15, n - 1)))
+        g = random_graph(n, degree, 7000 + 10 * seed + k, repeats=int(rng.choice([0, 0, 6])))
+        if rng.random() < 0.3:
+            g["h"] = np.zeros(n, np.float32)
+        csrs.append(g)
+    tiny = rng.random() < 0.25
+    if tiny:
+        g = csrs[0]
+        e = int(rng.integers(0, g["targets"].size))
+        a = int(np.searchsorted(g["offsets"], e, side="right") - 1)
+        t = int(g["targets"][e])
+        value = np.float32(2e-39)
+        g["couplings"] = g["couplings"].copy()
+        for x, y in ((a, t), (t, a)):  # every copy of the edge, both directions
+            lo, hi = int(g["offsets"][x]), int(g["offsets"][x + 1])
+            hit = lo + np.flatnonzero(g["targets"][lo:hi] == y)
+            g["couplings"][hit] = value
+    betas = ins.geometric_betas(0.1, 3.0, int(rng.integers(1, 9)))
+    ladders = int(rng.integers(1, 12))
+    model_of_ladder = [int(v) for v in rng.integers(0, n_models, ladders)]
+    used = sorted(set(model_of_ladder))
+    csrs = [csrs[k] for k in used]
+    model_of_ladder = [used.index(k) for k in model_of_ladder]
+    chains = ladders * betas.size
+    seeds = (31 * seed + 1 + np.arange(chains)).astype(np.uint32)
+    swap_seeds = (17 * seed + 5 + np.arange(ladders)).astype(np.uint32)
+    sweeps, interval = int(rng.integers(20, 60)), int(rng.integers(0, 4))
+    exp_kind = int(rng.integers(1, 4))
+    want = oracle_batch(port, csrs, ladders, betas, seeds, swap_seeds, sweeps, interval, 1.0, exp_kind, model_of_ladder)
+    with ib.init_state([product_model(c) for c in csrs], betas, ladders, seeds=seeds, swap_seeds=swap_seeds,
+                       params=ib.SweepParams(1.0, exp_kind), model_of_ladder=model_of_ladder,
+                       kernel=ib.KERNEL_GENERIC) as st:
+        if tiny and 0 in used:
+            assert st.info()["generic_variant"] == 0
+        split = int(rng.integers(1, sweeps))
+        st.run(split, interval)
+        st.run(sweeps - split, interval)
+        assert_batch_matches(st, want, 1e-5)

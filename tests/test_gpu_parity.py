@@ -7,7 +7,7 @@ import pytest
 
 import paper_1004_0024_b200 as ib
 from paper_1004_0024_b200 import _lib
-from helpers import assert_batch_matches, bits, csr_from_npz, ins, oracle_batch, product_model
+from helpers import assert_batch_matches, bits, csr_from_npz, ins, oracle_batch, product_model, random_graph
 
 pytestmark = pytest.mark.gpu
 
@@ -461,29 +461,13 @@ def test_generic_family_update_variants(lib, port):
     assert_batch_matches(state, want, REL_ENERGY)
 
 
-def _random_graph(n, mean_degree, seed, repeats=0):
-    """A seeded random multigraph: `mean_degree * n / 2` distinct edges plus `repeats` repeated ones,
-    Gaussian couplings and fields (tests only: degrees well beyond eight, a ragged last chunk)."""
-    rng = np.random.default_rng(seed)
-    pairs = set()
-    while len(pairs) < mean_degree * n // 2:
-        a, b = (int(v) for v in rng.integers(0, n, 2))
-        if a != b:
-            pairs.add((min(a, b), max(a, b)))
-    edges = sorted(pairs)
-    edges += [edges[int(k)] for k in rng.integers(0, len(edges), repeats)]
-    coup = rng.normal(0.0, 1.0, len(edges)).astype(np.float32)
-    h = rng.normal(0.0, 0.3, n).astype(np.float32)
-    return ins.csr_from_adjacency(h, ins._adjacency(n, np.array(edges, np.int64), coup))
-
-
 @pytest.mark.parametrize("exp_kind", [1, 2, 3])
 def test_generic_family_high_degree_ragged_and_repeated_edges(lib, port, exp_kind):
     """Degrees up to ~20 (the split kernel's tail past eight edges), n = 77 (a last chunk of five
     attempts), ragged tiles, and a second model with repeated edges (own-field window unusable)."""
-    plain = _random_graph(77, 11, 901)
+    plain = random_graph(77, 11, 901)
     assert int(np.diff(plain["offsets"]).max()) > 12
-    repeated = _random_graph(77, 9, 902, repeats=12)
+    repeated = random_graph(77, 9, 902, repeats=12)
     betas = ins.geometric_betas(0.15, 2.5, 11)
     state, want = run_both(port, [plain, repeated], 7, betas, 150, 1, exp_kind=exp_kind, kernel=ib.KERNEL_GENERIC,
                            model_of_ladder=[0, 1, 0, 1, 1, 0, 0])
