@@ -338,6 +338,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         dev_.generic_reduce &= d.reduction_safe;
         all_windows = all_windows && d.window != nullptr;
     }
+    dev_.generic_windows = dev_.generic_reduce && all_windows ? 1u : 0u;
     generic_variant_ = family_ != KernelFamily::generic ? 0u : !dev_.generic_reduce ? 0u : all_windows ? 2u : 1u;
 
     if (family_ == KernelFamily::layered) {

@@ -109,6 +109,7 @@ struct DevBatch {
     // flip, and the attempts recorded; nullptr unless recording was requested
     unsigned long long* wait_counts;  // [tile][kWaitSlots]
     uint32_t generic_reduce;          // every model is reduction_safe: the generic family uses sweep_split_kernel
+    uint32_t generic_windows;         // ... and every model has an own-field window: sweep_trio_kernel
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]

@@ -553,6 +553,219 @@ __global__ void __launch_bounds__(kSplitThreads) sweep_split_kernel(DevBatch b, 
 }
 
 // ---------------------------------------------------------------------------------------
+// Three warps per tile, for batches in which every model has an own-field window.  The reductions and
+// the own-field loads are the two kinds of access whose order matters (a load must come after every
+// reduction that can reach it), so both move to one thread each lane: the REDUCER warp.  The sweep
+// warp publishes every decision (the ballot, and which of the accepting lanes held s = -1) through a
+// 16-slot ring with one mbarrier per slot; the reducer issues that attempt's reductions, and after the
+// last attempt of a chunk requests the next chunk's own fields and hands them back through shared
+// memory.  The sweep warp is left with the decision, the in-chunk patches and the bookkeeping.
+constexpr int kTrioThreads = 96;
+struct TrioShared {
+    SplitStage stages[kSplitStages];
+    float own[2][kChunk][32];
+    float own_tau[2][kChunk][32];
+    uint2 decided[2 * kChunk];
+    uint64_t full[kSplitStages], empty[kSplitStages];
+    uint64_t decided_bar[2 * kChunk];
+    uint64_t own_bar[2];
+};
+
+template <int EXP, bool TAU>
+__device__ void trio_sweep(const DevBatch& b, const TileView& t, uint32_t sweeps, TrioShared& sh) {
+    const uint32_t n = b.n_spins;
+    const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
+    const float gamma = b.tau_scale;
+    double e_run = t.active ? b.e_run[t.chain] : 0.0;
+    unsigned long long flips = 0;
+    const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
+    uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
+    uint32_t chunk = 0;
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk, ++chunk) {
+            const uint32_t count = min(uint32_t(kChunk), n - i0);
+            const uint32_t st = chunk % kSplitStages, half = chunk & 1u, phase = (chunk >> 1) & 1u;
+            const SplitStage& stage = sh.stages[st];
+            float own[kChunk], own_tau[kChunk], u[kChunk];
+            uint32_t word[kChunk];
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (uint32_t(k) < count) word[k] = t.words[i0 + k];
+            }
+            split_wait(&sh.own_bar[half], phase);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                own[k] = sh.own[half][k][t.lane];
+                if constexpr (TAU) own_tau[k] = sh.own_tau[half][k][t.lane];
+            }
+            split_wait(&sh.full[st], (chunk / kSplitStages) & 1u);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) u[k] = stage.u[k][t.lane];
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                const uint32_t slot = half * kChunk + k;
+                if (uint32_t(k) >= count) {  // keep every slot's barrier in step with the chunk count
+                    if (t.lane == 0) split_arrive(&sh.decided_bar[slot]);
+                    continue;
+                }
+                const uint32_t i = i0 + k;
+                const float4 nr_lo = *reinterpret_cast<const float4*>(&stage.near[k][0]);
+                const float4 nr_hi = *reinterpret_cast<const float4*>(&stage.near[k][4]);
+                const float two_s = (word[k] >> t.lane) & 1u ? -2.0f : 2.0f;
+                const float hsi = own[k];
+                float hti = 0.0f;
+                float x;
+                if constexpr (TAU) {
+                    hti = own_tau[k];
+                    x = flip_exponent(neg_beta, gamma, two_s, hsi, hti);
+                } else {
+                    x = __fmul_rn(neg_beta, __fmul_rn(two_s, hsi));
+                }
+                const float p = exp_kind<EXP>(x);
+                const bool accept = t.active && (u[k] < p);
+                const uint32_t ballot = __ballot_sync(0xffffffffu, accept);
+                if (t.lane == 0) {
+                    sh.decided[slot] = make_uint2(ballot, ballot & word[k]);
+                    split_arrive(&sh.decided_bar[slot]);
+                }
+                if (record_wait) wait_fold(ballot, wait);
+                if (ballot != 0u) {
+                    const float near[8] = {nr_lo.x, nr_lo.y, nr_lo.z, nr_lo.w, nr_hi.x, nr_hi.y, nr_hi.z, nr_hi.w};
+#pragma unroll
+                    for (int q = 1; k + q < kChunk; ++q) {
+                        own[k + q] = accept ? __fsub_rn(own[k + q], __fmul_rn(two_s, near[q])) : own[k + q];
+                    }
+                    if (accept) {
+                        ++flips;
+                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(hsi, hti))));
+                    }
+                    if (t.lane == 0) t.words[i] = word[k] ^ ballot;
+                }
+            }
+            split_arrive(&sh.empty[st]);
+        }
+        __syncwarp();  // lane 0's spin-word stores become visible to the whole warp
+        if (record_wait) {  // flushed per sweep: the 32-bit partial counts cannot overflow (n < 2^27)
+            unsigned long long* out = b.wait_counts + size_t(t.tile) * kWaitSlots;
+#pragma unroll
+            for (int w = 0; w < 6; ++w) {
+                if (t.lane == 0) out[w] += wait[w];
+                wait[w] = 0;
+            }
+            if (t.lane == 0) out[6] += n;
+        }
+    }
+    if (t.active) {
+        b.e_run[t.chain] = e_run;
+        b.flips[t.chain] += flips;
+    }
+}
+
+template <bool TAU>
+__device__ void trio_reducer(const DevBatch& b, const TileView& t, uint32_t sweeps, TrioShared& sh) {
+    const uint32_t n = b.n_spins;
+    const DevModel& m = t.model;
+    const uint32_t chunks_per_sweep = (n + kChunk - 1) / kChunk;
+    const uint32_t total_chunks = chunks_per_sweep * sweeps;
+    // the own fields of chunk `c` (first spin `first`), requested after every reduction issued so far
+    const auto hand_over = [&](uint32_t c, uint32_t first) {
+        const uint32_t cnt = min(uint32_t(kChunk), n - first), half = c & 1u;
+        float own[kChunk], own_tau[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            own[k] = uint32_t(k) < cnt ? ld_field(t.hs + size_t(first + k) * 32) : 0.0f;
+            if constexpr (TAU) own_tau[k] = uint32_t(k) < cnt ? ld_field(t.ht + size_t(first + k) * 32) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            sh.own[half][k][t.lane] = own[k];
+            if constexpr (TAU) sh.own_tau[half][k][t.lane] = own_tau[k];
+        }
+        split_arrive(&sh.own_bar[half]);
+    };
+    if (total_chunks != 0) hand_over(0, 0);
+    uint32_t chunk = 0;
+    for (uint32_t sw = 0; sw < sweeps; ++sw) {
+        for (uint32_t i0 = 0; i0 < n; i0 += kChunk, ++chunk) {
+            const uint32_t count = min(uint32_t(kChunk), n - i0);
+            const uint32_t st = chunk % kSplitStages, half = chunk & 1u, phase = (chunk >> 1) & 1u;
+            const SplitStage& stage = sh.stages[st];
+            split_wait(&sh.full[st], (chunk / kSplitStages) & 1u);
+#pragma unroll 1
+            for (uint32_t k = 0; k < count; ++k) {
+                const uint32_t slot = half * kChunk + k;
+                split_wait(&sh.decided_bar[slot], phase);
+                const uint2 decision = sh.decided[slot];
+                if (decision.x == 0u) continue;
+                const bool accept = (decision.x >> t.lane) & 1u;
+                const float minus_two_s = (decision.y >> t.lane) & 1u ? 2.0f : -2.0f;
+                const uint4 tg_lo = *reinterpret_cast<const uint4*>(&stage.target[k][0]);
+                const uint4 tg_hi = *reinterpret_cast<const uint4*>(&stage.target[k][4]);
+                const float4 cp_lo = *reinterpret_cast<const float4*>(&stage.coupling[k][0]);
+                const float4 cp_hi = *reinterpret_cast<const float4*>(&stage.coupling[k][4]);
+                const uint32_t degree = stage.degree[k], space = stage.space[k];
+                const uint32_t target[8] = {tg_lo.x, tg_lo.y, tg_lo.z, tg_lo.w, tg_hi.x, tg_hi.y, tg_hi.z, tg_hi.w};
+                const float coupling[8] = {cp_lo.x, cp_lo.y, cp_lo.z, cp_lo.w, cp_hi.x, cp_hi.y, cp_hi.z, cp_hi.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float* field = (!TAU || uint32_t(q) < space) ? t.hs : t.ht;
+                    // every lane takes part (a lane that did not accept adds -0.0, the identity for
+                    // every bit pattern), so the warp does not diverge once per edge
+                    if (uint32_t(q) < degree) {
+                        reduce_field(field + size_t(target[q]) * 32, accept ? __fmul_rn(minus_two_s, coupling[q]) : -0.0f);
+                    }
+                }
+                if (degree > 8u) {
+                    const uint32_t first = stage.first[k];
+                    for (uint32_t e = 8; e < degree; ++e) {
+                        float* field = (!TAU || e < space) ? t.hs : t.ht;
+                        const size_t at = size_t(__ldg(m.targets + first + e)) * 32;
+                        const float d = __fmul_rn(minus_two_s, __ldg(m.couplings + first + e));
+                        reduce_field(field + at, accept ? d : -0.0f);
+                    }
+                }
+            }
+            split_arrive(&sh.empty[st]);
+            if (chunk + 1 < total_chunks) hand_over(chunk + 1, i0 + kChunk < n ? i0 + kChunk : 0u);
+        }
+    }
+}
+
+template <int EXP, bool TAU>
+__global__ void __launch_bounds__(kTrioThreads) sweep_trio_kernel(DevBatch b, uint32_t sweeps) {
+    __shared__ __align__(16) TrioShared sh;
+    TileView t;
+    t.tile = blockIdx.x;
+    t.lane = threadIdx.x & 31u;
+    t.active = t.lane < b.tile_count[t.tile];
+    t.chain = b.tile_first[t.tile] + t.lane;
+    t.model = b.models[b.tile_model[t.tile]];
+    const size_t base = size_t(t.tile) * b.n_spins;
+    t.hs = b.hs + base * 32 + t.lane;
+    t.ht = b.ht ? b.ht + base * 32 + t.lane : nullptr;
+    t.words = b.spin_bits + base;
+    t.mt = b.mt + size_t(t.tile) * kMtN * 32 + t.lane;
+    const auto init = [](uint64_t* bar, uint32_t count) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(split_smem(bar)), "r"(count) : "memory");
+    };
+    if (threadIdx.x < kSplitStages) {
+        init(&sh.full[threadIdx.x], 32);
+        init(&sh.empty[threadIdx.x], 64);  // the sweep warp and the reducer both read a stage
+    }
+    if (threadIdx.x < 2 * kChunk) init(&sh.decided_bar[threadIdx.x], 1);
+    if (threadIdx.x < 2) init(&sh.own_bar[threadIdx.x], 32);
+    __syncthreads();
+    const uint32_t role = threadIdx.x >> 5;
+    if (role == 0) {
+        trio_sweep<EXP, TAU>(b, t, sweeps, sh);
+    } else if (role == 1) {
+        split_producer<TAU>(b, t, sweeps, sh.stages, sh.full, sh.empty);
+    } else {
+        trio_reducer<TAU>(b, t, sweeps, sh);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Tempering swap round (new semantics, oracle/ising_oracle.h): pairs of
 // slots (k,k+1), k = round&1, +2, ...; one draw per pair from the ladder's own generator;
 // accept iff u < exp_kind(float((beta_k - beta_k1) * (E_a - E_b))); the chains exchange slots.
@@ -668,7 +881,10 @@ inline dim3 tile_grid(const DevBatch& b) { return dim3((b.n_tiles + kWarpsPerBlo
 
 template <int EXP>
 void launch_sweep_exp(const DevBatch& b, uint32_t sweeps, cudaStream_t s) {
-    if (b.generic_reduce && b.n_tiles != 0) {
+    if (b.generic_reduce && b.generic_windows && b.n_tiles != 0) {
+        if (b.ht) sweep_trio_kernel<EXP, true><<<b.n_tiles, kTrioThreads, 0, s>>>(b, sweeps);
+        else sweep_trio_kernel<EXP, false><<<b.n_tiles, kTrioThreads, 0, s>>>(b, sweeps);
+    } else if (b.generic_reduce && b.n_tiles != 0) {
         if (b.ht) sweep_split_kernel<EXP, true><<<b.n_tiles, kSplitThreads, 0, s>>>(b, sweeps);
         else sweep_split_kernel<EXP, false><<<b.n_tiles, kSplitThreads, 0, s>>>(b, sweeps);
     } else if (b.ht) {
