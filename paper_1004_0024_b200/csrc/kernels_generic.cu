@@ -308,6 +308,17 @@ __device__ __forceinline__ float ld_field(const float* p) {
 __device__ __forceinline__ void reduce_field(float* p, float addend) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(addend) : "memory");
 }
+// The same under a (warp-uniform) predicate instead of a branch.
+__device__ __forceinline__ void reduce_field_if(bool on, float* p, float addend) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.u32 p, %2, 0;\n"
+        "@p red.global.add.f32 [%0], %1;\n"
+        "}\n" ::"l"(p),
+        "f"(addend), "r"(uint32_t(on))
+        : "memory");
+}
 
 // ---------------------------------------------------------------------------------------
 // Two warps per tile.  The PRODUCER warp runs ahead and fills a ring of
@@ -706,15 +717,18 @@ __device__ void trio_reducer(const DevBatch& b, const TileView& t, uint32_t swee
                 const uint32_t degree = stage.degree[k], space = stage.space[k];
                 const uint32_t target[8] = {tg_lo.x, tg_lo.y, tg_lo.z, tg_lo.w, tg_hi.x, tg_hi.y, tg_hi.z, tg_hi.w};
                 const float coupling[8] = {cp_lo.x, cp_lo.y, cp_lo.z, cp_lo.w, cp_hi.x, cp_hi.y, cp_hi.z, cp_hi.w};
+                // addresses and addends first, then the eight reductions back to back (a lane that did
+                // not accept adds -0.0, the identity for every bit pattern: full 128-byte reductions, no
+                // divergence; past the spin's last edge the reduction is predicated off)
+                float* at[8];
+                float addend[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    float* field = (!TAU || uint32_t(q) < space) ? t.hs : t.ht;
-                    // every lane takes part (a lane that did not accept adds -0.0, the identity for
-                    // every bit pattern), so the warp does not diverge once per edge
-                    if (uint32_t(q) < degree) {
-                        reduce_field(field + size_t(target[q]) * 32, accept ? __fmul_rn(minus_two_s, coupling[q]) : -0.0f);
-                    }
+                    at[q] = ((!TAU || uint32_t(q) < space) ? t.hs : t.ht) + size_t(target[q]) * 32;
+                    addend[q] = accept ? __fmul_rn(minus_two_s, coupling[q]) : -0.0f;
                 }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) reduce_field_if(uint32_t(q) < degree, at[q], addend[q]);
                 if (degree > 8u) {
                     const uint32_t first = stage.first[k];
                     for (uint32_t e = 8; e < degree; ++e) {
