@@ -705,16 +705,18 @@ __device__ void trio_reducer(const DevBatch& b, const TileView& t, uint32_t swee
 #pragma unroll 1
             for (uint32_t k = 0; k < count; ++k) {
                 const uint32_t slot = half * kChunk + k;
+                // the attempt's operands are in the stage already: requested before the wait for its decision
+                const uint4 tg_lo = *reinterpret_cast<const uint4*>(&stage.target[k][0]);
+                const uint4 tg_hi = *reinterpret_cast<const uint4*>(&stage.target[k][4]);
+                const float4 cp_lo = *reinterpret_cast<const float4*>(&stage.coupling[k][0]);
+                const float4 cp_hi = *reinterpret_cast<const float4*>(&stage.coupling[k][4]);
+                const uint32_t degree = stage.degree[k];
+                const uint32_t space = stage.space[k];
                 split_wait(&sh.decided_bar[slot], phase);
                 const uint2 decision = sh.decided[slot];
                 if (decision.x == 0u) continue;
                 const bool accept = (decision.x >> t.lane) & 1u;
                 const float minus_two_s = (decision.y >> t.lane) & 1u ? 2.0f : -2.0f;
-                const uint4 tg_lo = *reinterpret_cast<const uint4*>(&stage.target[k][0]);
-                const uint4 tg_hi = *reinterpret_cast<const uint4*>(&stage.target[k][4]);
-                const float4 cp_lo = *reinterpret_cast<const float4*>(&stage.coupling[k][0]);
-                const float4 cp_hi = *reinterpret_cast<const float4*>(&stage.coupling[k][4]);
-                const uint32_t degree = stage.degree[k], space = stage.space[k];
                 const uint32_t target[8] = {tg_lo.x, tg_lo.y, tg_lo.z, tg_lo.w, tg_hi.x, tg_hi.y, tg_hi.z, tg_hi.w};
                 const float coupling[8] = {cp_lo.x, cp_lo.y, cp_lo.z, cp_lo.w, cp_hi.x, cp_hi.y, cp_hi.z, cp_hi.w};
                 // addresses and addends first, then the eight reductions back to back (a lane that did
