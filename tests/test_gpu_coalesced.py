@@ -76,6 +76,13 @@ def test_coalesced_rejections(lib):
         ib.init_coalesced(ok, [-1.0])
     with pytest.raises(ib.IsingError, match="seed count"):
         ib.init_coalesced(ok, [1.0, 2.0], seeds=[1])
+    # tau updates go out as global f32 reductions, which flush subnormals: a model that could hold a
+    # subnormal field is refused (the batch API runs it through the read-modify-write kernel instead)
+    tiny = ins.build_layered_csr(*ins.layered_spec(8, 3), 4, 1.0)
+    tiny["h"] = tiny["h"].copy()
+    tiny["h"][3::8] = np.float32(1e-39)  # the same position of every layer: layers stay identical
+    with pytest.raises(ib.IsingError, match="2\\^-100"):
+        ib.init_coalesced(product_model(tiny), [1.0])
 
 
 def test_coalesced_walks_the_csr_when_the_layer_graph_does_not_fit(lib, port):
