@@ -602,9 +602,9 @@ __device__ void far_warp(float* hs_g, uint32_t sweeps, uint32_t lane, const Grap
             hs_prev = hs_g + size_t(l) * P * 32;
             for (uint32_t p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
+                const uint32_t ginfo = g.chunks[p0 / kUnroll].x;  // (static: requested before the rendezvous)
                 chunk_barrier(bar_id);  // the sweep warp has finished this chunk
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t ginfo = g.chunks[p0 / kUnroll].x;
                 if ((ginfo >> 16) != 0u) {
                     apply_groups(tm, g, ginfo, smem_u32(s.signs + st * 32 + lane), smem_u32(s.ballots + st * kUnroll),
                                  lane);
@@ -871,13 +871,13 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
 
             for (p0 = 0; p0 < P; p0 += kUnroll) {
                 const uint32_t st = cursor.stage;
+                const uint4 chunk_info = g.chunks[p0 / kUnroll];  // (static: requested before the wait)
                 mbar_wait(&full[st], cursor.parity(), 0);
                 cursor.waited();
                 // columns entering the window during this chunk may be owed updates by the far warp from
                 // attempts at least two chunks back: the chunk rendezvous below guarantees it has
                 // finished those (it cannot be more than one chunk behind)
                 if ((p0 & 31u) == 0 && p0 + lane < P) prefetch_l2(hs_next + size_t(p0 + lane) * 32);
-                const uint4 chunk_info = g.chunks[p0 / kUnroll];
                 const uint32_t special = chunk_info.z;
                 StageAddr sa;
                 sa.rec_x = recs_u32 + st * (kUnroll * 32 * 16);
