@@ -5,12 +5,14 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import numpy as np, paper_1004_0024_b200 as ib
 from paper_1004_0024_b200 import workloads, instances as ins
 
-wl = workloads.get("c5")
-c = wl.make_csrs()[0]
+name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+wl = workloads.get(name)
+csrs = wl.make_csrs()
 for rep in range(2):
     t = [time.perf_counter()]
-    model = ib.SpinModel.from_csr(c["n_spins"], c["h"], c["offsets"], c["targets"], c["couplings"], c["tau_counts"],
-                                  c["layers"], c["per_layer"])
+    model = [ib.SpinModel.from_csr(c["n_spins"], c["h"], c["offsets"], c["targets"], c["couplings"], c["tau_counts"],
+                                   c["layers"], c["per_layer"]) for c in csrs]
+    model = model[0] if len(model) == 1 else model
     t.append(time.perf_counter())
     st = ib.init_state(model, wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE, swap_base_seed=ins.SWAP_SEED_BASE)
     t.append(time.perf_counter())
