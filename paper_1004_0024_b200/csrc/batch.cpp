@@ -2,7 +2,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
 
 namespace isingb200 {
 
@@ -160,6 +164,35 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
 
 }  // namespace
 
+// Runs fn(0) .. fn(count - 1) on up to 16 host threads (the per-model graph analysis of a batch with
+// many distinct instances); the first exception is rethrown on the calling thread.
+template <typename Fn>
+static void parallel_for(size_t count, Fn&& fn) {
+    const size_t workers = std::min<size_t>({count, size_t(std::max(1u, std::thread::hardware_concurrency())), size_t(16)});
+    if (workers <= 1) {
+        for (size_t k = 0; k < count; ++k) fn(k);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::exception_ptr failure;
+    std::mutex failure_lock;
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < workers; ++w) {
+        pool.emplace_back([&]() {
+            for (size_t k = next.fetch_add(1); k < count; k = next.fetch_add(1)) {
+                try {
+                    fn(k);
+                } catch (...) {
+                    std::lock_guard<std::mutex> hold(failure_lock);
+                    if (!failure) failure = std::current_exception();
+                }
+            }
+        });
+    }
+    for (std::thread& t : pool) t.join();
+    if (failure) std::rethrow_exception(failure);
+}
+
 void Batch::bind_device() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
 
 // total_cost (ref: model.cpp:108-126) as the flat sequence of terms its two loops visit: for every
@@ -233,11 +266,12 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     }
     std::vector<HostLayerGraph> host_graphs;
     if (layered_ok && cfg.kernel != int(KernelFamily::generic)) {
-        for (const HostModel* m : models) {
-            host_graphs.push_back(build_layer_graph(*m, cfg.tau_scale));
-            layered_ok = layered_ok && host_graphs.back().far.size() <= 0xffffu && host_graphs.back().groups.size() <= 0xffffu;
-            max_far_edges = std::max(max_far_edges, uint32_t(host_graphs.back().far.size()));
-            max_groups = std::max(max_groups, uint32_t(host_graphs.back().groups.size()));
+        host_graphs.resize(models.size());
+        parallel_for(models.size(), [&](size_t k) { host_graphs[k] = build_layer_graph(*models[k], cfg.tau_scale); });
+        for (const HostLayerGraph& hg : host_graphs) {
+            layered_ok = layered_ok && hg.far.size() <= 0xffffu && hg.groups.size() <= 0xffffu;
+            max_far_edges = std::max(max_far_edges, uint32_t(hg.far.size()));
+            max_groups = std::max(max_groups, uint32_t(hg.groups.size()));
         }
     }
     const bool graph_shared = models.size() == 1;
@@ -289,46 +323,59 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         upload(*model_storage_.back(), host_vec, device_bytes_, stream_);
         return model_storage_.back().get();
     };
-    for (const HostModel* m : models) {
-        DevModel d{};
-        d.n_spins = m->n_spins;
-        d.has_tau = m->has_tau ? 1u : 0u;
-        d.distinct_targets = 1u;
-        for (uint32_t i = 0; i < m->n_spins && d.distinct_targets; ++i) {
-            for (uint32_t a = m->offsets[i]; a < m->offsets[i + 1] && d.distinct_targets; ++a) {
+    struct Prepared {  // what the kernels want to know about a model, worked out on the host
+        uint32_t distinct_targets = 1u, reduction_safe = 1u;
+        std::vector<float> window;  // empty: unusable
+        std::vector<uint4> terms;
+    };
+    std::vector<Prepared> prepared(models.size());
+    const bool generic_family = family_ == KernelFamily::generic;
+    parallel_for(models.size(), [&](size_t k) {
+        const HostModel* m = models[k];
+        Prepared& out = prepared[k];
+        for (uint32_t i = 0; i < m->n_spins && out.distinct_targets; ++i) {
+            for (uint32_t a = m->offsets[i]; a < m->offsets[i + 1] && out.distinct_targets; ++a) {
                 for (uint32_t b = a + 1; b < m->offsets[i + 1]; ++b) {
-                    if (m->targets[a] == m->targets[b]) d.distinct_targets = 0u;
+                    if (m->targets[a] == m->targets[b]) out.distinct_targets = 0u;
                 }
             }
         }
-        d.reduction_safe = 1u;
         const auto tiny = [](float v) { return v != 0.0f && std::fabs(v) < 0x1p-100f; };
-        for (float v : m->h) d.reduction_safe &= tiny(v) ? 0u : 1u;
-        for (float v : m->couplings) d.reduction_safe &= tiny(v) ? 0u : 1u;
-        d.window = nullptr;
-        if (family_ == KernelFamily::generic && d.reduction_safe) {
-            std::vector<float> window(size_t(m->n_spins) * 8, 0.0f);
+        for (float v : m->h) out.reduction_safe &= tiny(v) ? 0u : 1u;
+        for (float v : m->couplings) out.reduction_safe &= tiny(v) ? 0u : 1u;
+        if (generic_family && out.reduction_safe) {
+            out.window.assign(size_t(m->n_spins) * 8, 0.0f);
             bool usable = true;
             for (uint32_t i = 0; i < m->n_spins && usable; ++i) {
                 const uint32_t end = m->offsets[i + 1], first_tau = end - m->tau_counts[i];
                 for (uint32_t e = m->offsets[i]; e < end; ++e) {
                     const uint32_t t = m->targets[e];
                     if (t <= i || t / 8 != i / 8) continue;
-                    float& slot = window[size_t(i) * 8 + (t - i)];
+                    float& slot = out.window[size_t(i) * 8 + (t - i)];
                     if (e >= first_tau || slot != 0.0f) usable = false;
                     slot = m->couplings[e];
                 }
             }
-            if (usable) d.window = keep(window)->as<float>();
+            if (!usable) out.window.clear();
         }
+        out.terms = build_cost_terms(*m);
+    });
+    for (size_t k = 0; k < models.size(); ++k) {
+        const HostModel* m = models[k];
+        const Prepared& ready = prepared[k];
+        DevModel d{};
+        d.n_spins = m->n_spins;
+        d.has_tau = m->has_tau ? 1u : 0u;
+        d.distinct_targets = ready.distinct_targets;
+        d.reduction_safe = ready.reduction_safe;
+        d.window = ready.window.empty() ? nullptr : keep(ready.window)->as<float>();
         d.h = keep(m->h)->as<float>();
         d.offsets = keep(m->offsets)->as<uint32_t>();
         d.targets = keep(m->targets)->as<uint32_t>();
         d.couplings = keep(m->couplings)->as<float>();
         d.tau_counts = keep(m->tau_counts)->as<uint8_t>();
-        const std::vector<uint4> terms = build_cost_terms(*m);
-        d.cost_terms = keep(terms)->as<uint4>();
-        d.n_cost_terms = uint32_t(terms.size());
+        d.cost_terms = keep(ready.terms)->as<uint4>();
+        d.n_cost_terms = uint32_t(ready.terms.size());
         dev_models.push_back(d);
     }
     upload(models_, dev_models, device_bytes_, stream_);
