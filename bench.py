@@ -113,9 +113,18 @@ class ClockSampler:
 
 
 def build_models(wl, csrs):
+    """One product model per instance (validation and layer analysis run in C++ with the GIL released, so
+    workloads with many distinct instances build them on a few host threads)."""
     import paper_1004_0024_b200 as ib
-    return [ib.SpinModel.from_csr(c["n_spins"], c["h"], c["offsets"], c["targets"], c["couplings"],
-                                  c["tau_counts"], c["layers"], c["per_layer"]) for c in csrs]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(c):
+        return ib.SpinModel.from_csr(c["n_spins"], c["h"], c["offsets"], c["targets"], c["couplings"],
+                                     c["tau_counts"], c["layers"], c["per_layer"])
+    if len(csrs) < 4:
+        return [one(c) for c in csrs]
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+        return list(pool.map(one, csrs))
 
 
 def model_bytes(csrs) -> int:
