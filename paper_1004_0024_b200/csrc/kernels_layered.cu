@@ -933,14 +933,18 @@ __device__ void sweep_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, co
 #undef ISING_ATTEMPT
 #undef ISING_ATTEMPT_LEAN
 
-template <int EXP, bool WAIT>
+template <int EXP, bool WAIT, bool SPREAD>
 __global__ void __launch_bounds__(kLayeredThreads, 1) sweep_layered_kernel(DevBatch b, uint32_t sweeps) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 16);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t pair = warp & 3u;
-    const uint32_t role = warp >> 2;  // 0 sweep, 1 producer, 2 post, 3 far — all four on scheduler `pair`
+    const uint32_t role = warp >> 2;  // 0 sweep, 1 producer, 2 post, 3 far
+    // A tile's sweep, post and far warps must sit on scheduler `pair` (it is also the TMEM lane quarter
+    // they may touch); the producer touches no Tensor Memory.  SPREAD (the host picks it when a CTA has
+    // at most two tiles, pairs 0 and 1): their producers run on the two schedulers that would otherwise
+    // idle — a tile is 14 % faster without its producer's 43 instructions per attempt in its issue port.
+    const uint32_t pair = (SPREAD && role == 1) ? (warp + 2u) & 3u : warp & 3u;  // 0 sweep, 1 producer, 2 post, 3 far — all four on scheduler `pair`
     uint64_t* full = bars + pair * 3 * kMaxStages;   // producer -> sweep
     uint64_t* empty = full + 2 * kMaxStages;         // post + far -> producer
     const uint32_t bar_id = 5 + pair;                // named barrier of the tile's sweep/post/far rendezvous
@@ -1035,14 +1039,26 @@ uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, uint32_
 namespace {
 template <int EXP, bool WAIT>
 cudaError_t prepare_one(size_t smem_bytes) {
-    return cudaFuncSetAttribute(sweep_layered_kernel<EXP, WAIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep_layered_kernel<EXP, WAIT, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(sweep_layered_kernel<EXP, WAIT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(smem_bytes));
 }
-template <int EXP>
+template <int EXP, bool SPREAD>
 void launch_one(const DevBatch& b, uint32_t sweeps, dim3 grid, size_t smem, cudaStream_t stream) {
     // the wait-statistics variant is a separate instantiation: the default kernel carries none of it
-    if (b.wait_counts != nullptr) sweep_layered_kernel<EXP, true><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps);
-    else sweep_layered_kernel<EXP, false><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps);
+    if (b.wait_counts != nullptr) {
+        sweep_layered_kernel<EXP, true, SPREAD><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps);
+    } else {
+        sweep_layered_kernel<EXP, false, SPREAD><<<grid, kLayeredThreads, smem, stream>>>(b, sweeps);
+    }
+}
+template <int EXP>
+void launch_either(const DevBatch& b, uint32_t sweeps, dim3 grid, size_t smem, cudaStream_t stream) {
+    // at most two tiles per CTA: the producers move to the idle schedulers (see the kernel)
+    if (b.n_tiles <= 2u * grid.x) launch_one<EXP, true>(b, sweeps, grid, smem, stream);
+    else launch_one<EXP, false>(b, sweeps, grid, smem, stream);
 }
 }  // namespace
 
@@ -1062,9 +1078,9 @@ cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_coun
     const uint32_t ctas = uint32_t(sm_count) < b.n_tiles ? uint32_t(sm_count) : b.n_tiles;
     const dim3 grid(ctas ? ctas : 1);
     switch (b.exp_kind) {
-        case kExpExact: launch_one<kExpExact>(b, sweeps, grid, smem, stream); break;
-        case kExpFast: launch_one<kExpFast>(b, sweeps, grid, smem, stream); break;
-        default: launch_one<kExpAccurate>(b, sweeps, grid, smem, stream); break;
+        case kExpExact: launch_either<kExpExact>(b, sweeps, grid, smem, stream); break;
+        case kExpFast: launch_either<kExpFast>(b, sweeps, grid, smem, stream); break;
+        default: launch_either<kExpAccurate>(b, sweeps, grid, smem, stream); break;
     }
     return cudaGetLastError();
 }
