@@ -124,6 +124,23 @@ double orc_total_cost(const orc_model* m, const float* spins) {
     return cost;
 }
 
+/* The energy whose Boltzmann weight the sweeps sample, exp(-beta * (E_space + gamma * E_tau)):
+ * total_cost with every tau coupling replaced by the f32 product gamma * J (new: see orc_pt_run;
+ * equal to orc_total_cost bit for bit when gamma == 1). */
+double orc_tempering_cost(const orc_model* m, const float* spins, float tau_scale) {
+    double cost = 0.0;
+    for (uint32_t i = 0; i < m->n_spins; ++i) {
+        cost -= (double)m->h[i] * (double)spins[i];
+        const uint32_t end = m->offsets[i + 1], mid = end - m->tau_counts[i];
+        for (uint32_t e = m->offsets[i]; e < end; ++e) {
+            uint32_t t = m->targets[e];
+            const float j = e >= mid ? tau_scale * m->couplings[e] : m->couplings[e];
+            if (t > i) cost -= (double)j * (double)spins[i] * (double)spins[t];
+        }
+    }
+    return cost;
+}
+
 uint64_t orc_checksum(const float* spins, uint32_t n) {
     uint64_t h = 1469598103934665603ull;
     for (uint32_t i = 0; i < n; ++i) {
@@ -184,7 +201,8 @@ orc_chain* orc_chain_create(const orc_model* m, uint32_t seed, float beta, float
     }
     orc_recompute_fields(m, c->spins, c->hs, c->ht);
     orc_mt_seed(&c->rng, seed);
-    c->e_run = orc_total_cost(m, c->spins);
+    c->e_run = orc_tempering_cost(m, c->spins, tau_scale);
+    c->energy_block = (m->layers != 0 && m->per_layer != 0) ? m->per_layer : m->n_spins;
     return c;
 }
 
@@ -199,7 +217,9 @@ void orc_chain_free(orc_chain* c) {
  * stream is the same as one next_u32 per attempt. */
 void orc_chain_sweep(orc_chain* c, const orc_model* m, uint64_t sweeps) {
     const float beta = c->beta, gamma = c->tau_scale;
+    const uint32_t block = c->energy_block ? c->energy_block : c->n;
     for (uint64_t sw = 0; sw < sweeps; ++sw) {
+        double e_block = 0.0; /* new: see orc_pt_run */
         for (uint32_t i = 0; i < c->n; ++i) {
             const float u = orc_u32_to_unit(orc_mt_next(&c->rng));
             const float s = c->spins[i];
@@ -215,7 +235,11 @@ void orc_chain_sweep(orc_chain* c, const orc_model* m, uint64_t sweeps) {
                     c->ht[m->targets[e]] -= two_s * m->couplings[e];
                 c->spins[i] = -s;
                 ++c->flips;
-                c->e_run += (double)(two_s * (hs + ht)); /* new: see orc_pt_run */
+                e_block += (double)(two_s * (hs + gamma * ht)); /* the inner factor of x above */
+            }
+            if ((i + 1) % block == 0 || i + 1 == c->n) {
+                c->e_run += e_block;
+                e_block = 0.0;
             }
         }
         c->attempts += c->n;

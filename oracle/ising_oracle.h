@@ -64,6 +64,8 @@ void orc_initial_spins(uint32_t n, uint32_t seed, int8_t* out);
 void orc_recompute_fields(const orc_model* m, const float* spins, float* hs, float* ht);
 /* src/model.cpp:108-126 */
 double orc_total_cost(const orc_model* m, const float* spins);
+/* new (tempering): total_cost with the tau couplings scaled by gamma in f32 (see orc_pt_run) */
+double orc_tempering_cost(const orc_model* m, const float* spins, float tau_scale);
 /* src/sweep_state.cpp:325-336 (identity permutation) */
 uint64_t orc_checksum(const float* spins, uint32_t n);
 /* src/sweep_state.cpp:338-354 */
@@ -81,6 +83,7 @@ typedef struct orc_chain {
     orc_mt rng;
     uint64_t flips, attempts;
     double e_run; /* running energy used by the tempering swap (see orc_pt_run) */
+    uint32_t energy_block; /* spins per partial sum of the running energy (see orc_pt_run) */
 } orc_chain;
 
 /* init_state(model, cfg[, initial]) — src/sweep_state.cpp:218-234.  initial may be NULL. */
@@ -99,8 +102,14 @@ void orc_chain_sweep(orc_chain* c, const orc_model* m, uint64_t sweeps);
  *     ladder's own Mt19937(swap_seed ^ 0x85EBCA6B), x = (float)((double(beta_k) -
  *     double(beta_k1)) * (E_a - E_b)), accept iff u < exp_kind(x); on accept the two
  *     chains exchange beta slots (spin arrays and sweep RNG streams stay put);
- *   - E is the running energy: total_cost of the initial spins, plus
- *     (double)((2.0f*s)*(hs+ht)) at each accepted flip, in flip order.
+ *   - E is the running value of the energy the sweeps sample, E_space + gamma * E_tau: it starts as
+ *     orc_tempering_cost of the initial spins (total_cost with the tau couplings scaled by gamma;
+ *     total_cost itself when gamma == 1) and receives, after every ENERGY BLOCK of attempts, the
+ *     block's partial sum: starting from 0.0, (double)((2.0f*s)*(hs + gamma*ht)) — the inner factor
+ *     of the flip exponent, an f32 — added at each accepted flip in flip order.  A block is one
+ *     layer (per_layer spins) of a layered model, the whole sweep otherwise.  Summing per block is
+ *     what lets the layers of one chain be swept by different warps (a block's partial sum needs
+ *     nothing from the blocks before it); the blocks are added in index order.
  */
 /* ---- the intra-system "coalesced" schedule (ref: proj/src/sweep_coalesced.cpp:10-124; model
  * permutation proj/src/model.cpp:190-215; init proj/src/sweep_state.cpp:120-146,193-199).

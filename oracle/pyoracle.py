@@ -55,7 +55,7 @@ class _Mt(C.Structure):
 class _Chain(C.Structure):
     _fields_ = [("n", C.c_uint32), ("beta", C.c_float), ("tau_scale", C.c_float), ("exp_kind", C.c_int),
                 ("spins", f32p), ("hs", f32p), ("ht", f32p), ("rng", _Mt), ("flips", C.c_uint64),
-                ("attempts", C.c_uint64), ("e_run", C.c_double)]
+                ("attempts", C.c_uint64), ("e_run", C.c_double), ("energy_block", C.c_uint32)]
 
 
 class _Coalesced(C.Structure):
@@ -97,6 +97,8 @@ class Port:
         lib.orc_recompute_fields.argtypes = [C.POINTER(_Model), f32p, f32p, f32p]
         lib.orc_total_cost.restype = C.c_double
         lib.orc_total_cost.argtypes = [C.POINTER(_Model), f32p]
+        lib.orc_tempering_cost.restype = C.c_double
+        lib.orc_tempering_cost.argtypes = [C.POINTER(_Model), f32p, C.c_float]
         lib.orc_checksum.restype = C.c_uint64
         lib.orc_checksum.argtypes = [f32p, C.c_uint32]
         lib.orc_field_coherence_ulp.restype = C.c_uint64
@@ -145,6 +147,11 @@ class Port:
     def total_cost(self, model, spins) -> float:
         s = np.ascontiguousarray(spins, np.float32)
         return self.lib.orc_total_cost(C.byref(model), _p(s, C.c_float))
+
+    def tempering_cost(self, model, spins, tau_scale) -> float:
+        """total_cost with the tau couplings scaled by gamma in f32: what the running energy tracks."""
+        s = np.ascontiguousarray(spins, np.float32)
+        return self.lib.orc_tempering_cost(C.byref(model), _p(s, C.c_float), float(tau_scale))
 
     def checksum(self, spins) -> int:
         s = np.ascontiguousarray(spins, np.float32)

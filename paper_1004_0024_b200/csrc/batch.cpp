@@ -199,7 +199,7 @@ void Batch::bind_device() const { cuda_check(cudaSetDevice(device_), "cudaSetDev
 // spin the field term, then its edges towards higher indices in adjacency order.  Terms with a zero
 // field are left out (cost - (+-0) == cost for every cost the sum can hold), the tail is padded
 // with zero coefficients to a multiple of 32 so that a warp can always take 32 terms at a time.
-static std::vector<uint4> build_cost_terms(const HostModel& m) {
+static std::vector<uint4> build_cost_terms(const HostModel& m, float tau_scale = 1.0f) {
     std::vector<uint4> terms;
     terms.reserve(size_t(m.n_spins) + m.targets.size() / 2 + 32);
     const auto bits = [](float v) {
@@ -209,8 +209,11 @@ static std::vector<uint4> build_cost_terms(const HostModel& m) {
     };
     for (uint32_t i = 0; i < m.n_spins; ++i) {
         if (m.h[i] != 0.0f) terms.push_back(make_uint4(i, kFieldTerm, bits(m.h[i]), 0));
+        const uint32_t first_tau = m.offsets[i + 1] - m.tau_counts[i];
         for (uint32_t e = m.offsets[i]; e < m.offsets[i + 1]; ++e) {
-            if (m.targets[e] > i) terms.push_back(make_uint4(i, m.targets[e], bits(m.couplings[e]), 0));
+            // tempering energy: the tau coupling as the sweep sees it, gamma * J in f32
+            const float j = e >= first_tau ? tau_scale * m.couplings[e] : m.couplings[e];
+            if (m.targets[e] > i) terms.push_back(make_uint4(i, m.targets[e], bits(j), 0));
         }
     }
     do {
@@ -326,7 +329,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     struct Prepared {  // what the kernels want to know about a model, worked out on the host
         uint32_t distinct_targets = 1u, reduction_safe = 1u;
         std::vector<float> window;  // empty: unusable
-        std::vector<uint4> terms;
+        std::vector<uint4> terms, tempering_terms;  // the second stays empty when tau_scale is 1
     };
     std::vector<Prepared> prepared(models.size());
     const bool generic_family = family_ == KernelFamily::generic;
@@ -359,6 +362,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             if (!usable) out.window.clear();
         }
         out.terms = build_cost_terms(*m);
+        if (cfg.tau_scale != 1.0f && m->has_tau) out.tempering_terms = build_cost_terms(*m, cfg.tau_scale);
     });
     for (size_t k = 0; k < models.size(); ++k) {
         const HostModel* m = models[k];
@@ -376,6 +380,9 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         d.tau_counts = keep(m->tau_counts)->as<uint8_t>();
         d.cost_terms = keep(ready.terms)->as<uint4>();
         d.n_cost_terms = uint32_t(ready.terms.size());
+        // (scaling a coupling never changes which terms exist: the two lists have one length)
+        d.tempering_terms = ready.tempering_terms.empty() ? d.cost_terms : keep(ready.tempering_terms)->as<uint4>();
+        d.energy_block = (m->layers != 0 && m->per_layer != 0) ? m->per_layer : m->n_spins;
         dev_models.push_back(d);
     }
     upload(models_, dev_models, device_bytes_, stream_);

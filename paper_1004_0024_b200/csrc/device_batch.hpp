@@ -41,6 +41,12 @@ struct DevModel {
     // zero coefficients.
     const uint4* cost_terms;
     uint32_t n_cost_terms;
+    // The same list with every tau coupling replaced by fl32(tau_scale * J): the energy the sweeps
+    // sample, which the tempering swap compares (== cost_terms when tau_scale is 1).
+    const uint4* tempering_terms;
+    // Attempts per partial sum of the running energy: per_layer for layered models, n_spins otherwise
+    // (tempering definition, oracle/ising_oracle.h).
+    uint32_t energy_block;
 };
 constexpr uint32_t kFieldTerm = 0xffffffffu;
 

@@ -65,9 +65,9 @@ __device__ __forceinline__ void fields_of_spin(const DevModel& m, const uint32_t
 // one block ahead (terms two blocks ahead), and the block is then summed term by term from
 // shuffles, every lane for its own chain.  (double(c) * s_i) * s_t is +-double(c) exactly, so a
 // term is the coefficient with the sign bit of s_i * s_t.
-__device__ double chain_cost(const DevModel& m, const uint32_t* words, uint32_t lane) {
+__device__ double chain_cost(const DevModel& m, const uint4* term_list, const uint32_t* words, uint32_t lane) {
     const uint32_t blocks = m.n_cost_terms / 32;
-    const uint4* terms = m.cost_terms + lane;
+    const uint4* terms = term_list + lane;
     const auto signs_of = [&](const uint4& term) {  // bit c: s_i * s_t < 0 in chain c
         const uint32_t wi = words[term.x];
         return term.y == kFieldTerm ? wi : wi ^ words[term.y];
@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(kThreads) init_kernel(DevBatch b, const int8_t
     mt_seed_lane(t.mt, 32, seed);
     if (t.lane == 0) b.mt_pos[t.tile] = 0;
 
-    const double cost = chain_cost(t.model, t.words, t.lane);
+    // the running energy of the tempering swap starts as the energy the sweeps sample (tau couplings
+    // scaled by gamma: DevModel::tempering_terms)
+    const double cost = chain_cost(t.model, t.model.tempering_terms, t.words, t.lane);
     if (t.active) {
         b.e_run[t.chain] = cost;
         b.flips[t.chain] = 0ull;
@@ -208,6 +210,11 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
     const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
     const float gamma = b.tau_scale;
     double e_run = t.active ? b.e_run[t.chain] : 0.0;
+    // tempering definition (oracle/ising_oracle.h): the running energy receives one partial sum per
+    // energy block of attempts (a layer of a layered model, else the sweep), summed from 0.0 in flip order
+    double e_blk = 0.0;
+    const uint32_t energy_block = t.model.energy_block;
+    uint32_t blk_left = energy_block;
     unsigned long long flips = 0;
     const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
@@ -267,9 +274,14 @@ __global__ void __launch_bounds__(kThreads) sweep_generic_kernel(DevBatch b, uin
                     }
                     if (accept) {
                         ++flips;
-                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(hsi, hti))));
+                        e_blk = __dadd_rn(e_blk, double(__fmul_rn(two_s, __fadd_rn(hsi, __fmul_rn(gamma, hti)))));
                     }
                     if (t.lane == 0) t.words[i] = word[k] ^ ballot;
+                }
+                if (--blk_left == 0u) {
+                    e_run = __dadd_rn(e_run, e_blk);
+                    e_blk = 0.0;
+                    blk_left = energy_block;
                 }
             }
         }
@@ -434,6 +446,11 @@ __device__ void split_sweep(const DevBatch& b, const TileView& t, uint32_t sweep
     const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
     const float gamma = b.tau_scale;
     double e_run = t.active ? b.e_run[t.chain] : 0.0;
+    // tempering definition (oracle/ising_oracle.h): the running energy receives one partial sum per
+    // energy block of attempts (a layer of a layered model, else the sweep), summed from 0.0 in flip order
+    double e_blk = 0.0;
+    const uint32_t energy_block = t.model.energy_block;
+    uint32_t blk_left = energy_block;
     unsigned long long flips = 0;
     const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
@@ -513,9 +530,14 @@ __device__ void split_sweep(const DevBatch& b, const TileView& t, uint32_t sweep
                     }
                     if (accept) {
                         ++flips;
-                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(hsi, hti))));
+                        e_blk = __dadd_rn(e_blk, double(__fmul_rn(two_s, __fadd_rn(hsi, __fmul_rn(gamma, hti)))));
                     }
                     if (t.lane == 0) t.words[i] = word[k] ^ ballot;
+                }
+                if (--blk_left == 0u) {
+                    e_run = __dadd_rn(e_run, e_blk);
+                    e_blk = 0.0;
+                    blk_left = energy_block;
                 }
             }
             split_arrive(&empty[st]);
@@ -588,6 +610,11 @@ __device__ void trio_sweep(const DevBatch& b, const TileView& t, uint32_t sweeps
     const float neg_beta = t.active ? -b.betas[b.slot_of_chain[t.chain]] : 0.0f;
     const float gamma = b.tau_scale;
     double e_run = t.active ? b.e_run[t.chain] : 0.0;
+    // tempering definition (oracle/ising_oracle.h): the running energy receives one partial sum per
+    // energy block of attempts (a layer of a layered model, else the sweep), summed from 0.0 in flip order
+    double e_blk = 0.0;
+    const uint32_t energy_block = t.model.energy_block;
+    uint32_t blk_left = energy_block;
     unsigned long long flips = 0;
     const bool record_wait = b.wait_counts != nullptr && b.tile_count[t.tile] == 32;  // full tiles only
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
@@ -648,9 +675,14 @@ __device__ void trio_sweep(const DevBatch& b, const TileView& t, uint32_t sweeps
                     }
                     if (accept) {
                         ++flips;
-                        e_run = __dadd_rn(e_run, double(__fmul_rn(two_s, __fadd_rn(hsi, hti))));
+                        e_blk = __dadd_rn(e_blk, double(__fmul_rn(two_s, __fadd_rn(hsi, __fmul_rn(gamma, hti)))));
                     }
                     if (t.lane == 0) t.words[i] = word[k] ^ ballot;
+                }
+                if (--blk_left == 0u) {
+                    e_run = __dadd_rn(e_run, e_blk);
+                    e_blk = 0.0;
+                    blk_left = energy_block;
                 }
             }
             split_arrive(&sh.empty[st]);
@@ -815,7 +847,7 @@ __global__ void swap_kernel(DevBatch b, unsigned long long round) {
 __global__ void __launch_bounds__(kThreads) energies_kernel(DevBatch b, double* out) {
     TileView t;
     if (!open_tile(b, t)) return;
-    const double cost = chain_cost(t.model, t.words, t.lane);  // the whole warp, see chain_cost
+    const double cost = chain_cost(t.model, t.model.cost_terms, t.words, t.lane);  // the whole warp, see chain_cost
     if (t.active) out[t.chain] = cost;
 }
 
@@ -885,7 +917,7 @@ __global__ void __launch_bounds__(kThreads) pack_results_kernel(DevBatch b, Resu
     TileView t;
     if (!open_tile(b, t)) return;
     ResultRecord r;
-    r.energy = chain_cost(t.model, t.words, t.lane);  // the whole warp, see chain_cost
+    r.energy = chain_cost(t.model, t.model.cost_terms, t.words, t.lane);  // the whole warp, see chain_cost
     if (!t.active) return;
     r.e_run = b.e_run[t.chain];
     r.flips = b.flips[t.chain];

@@ -349,7 +349,7 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
                     const uint32_t p = p0 + k;
                     const uint32_t word = w_cur[p];
                     const uint2 as = s.agree_sign[p];
-                    const uint2 tau = *reinterpret_cast<const uint2*>(g.pos + p);
+                    const uint32_t tau_g = *reinterpret_cast<const uint32_t*>(g.pos + p);  // bits of gamma * 2J_tau
                     const uint32_t spin_top = word * h.sh;  // bit 31 set <=> s = -1 (lower bits: other lanes)
                     const uint32_t sgn_up = (as.y * h.sh) & 0x80000000u;
                     const uint32_t agree = uint32_t(int32_t(as.x * h.sh) >> 31);  // ones when s_up == s_dn
@@ -359,9 +359,9 @@ __device__ void producer_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane,
                     // x = -beta*((2s)*v) == (-2*beta*s)*v: doubling is exact, one rounding either way
                     rec.y = __uint_as_float(h.nb2 ^ (spin_top & 0x80000000u));
                     signs = __funnelshift_l(spin_top, signs, 1);  // attempt k ends up at bit 7-k
-                    // tau field J*(s_up + s_dn) in {+2J, +0, -2J}: scaled by gamma, and raw
-                    rec.z = __uint_as_float((tau.x ^ sgn_up) & agree);
-                    rec.w = __uint_as_float((tau.y ^ sgn_up) & agree);
+                    // tau field J*(s_up + s_dn) in {+2J, +0, -2J}, scaled by gamma
+                    rec.z = __uint_as_float((tau_g ^ sgn_up) & agree);
+                    rec.w = 0.0f;
                     recs[k * 32] = rec;
                 }
                 s.signs[st * 32 + lane] = signs;
@@ -470,6 +470,7 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
     for (uint32_t sw = 0; sw < sweeps; ++sw) {
         for (uint32_t l = 0; l < L; ++l) {
             uint32_t* w_cur = s.words + slot_cur * P;
+            double e_blk = 0.0;  // one partial sum per layer (tempering definition, oracle/ising_oracle.h)
             layer_transition(1, tm, hs_prev, hs_g + size_t(l) * P * 32, P);
             chunk_barrier(bar_id);
             hs_prev = hs_g + size_t(l) * P * 32;
@@ -488,17 +489,19 @@ __device__ void post_warp(const DevBatch& b, uint32_t sweeps, uint32_t lane, con
                 for (int k = 0; k < int(kUnroll); ++k) {
                     const uint32_t ballot = ballots[k];
                     const float4 rec = recs[k * 32];
-                    // (2s)*(h + h_tau): doubling is exact, and rec.y = -2*beta*s carries the opposite of
-                    // the spin's sign, so the product is 2*(h + h_tau) with its sign flipped where s = -1
-                    const float twice = __fmul_rn(__fadd_rn(rec.x, rec.w), 2.0f);
+                    // (2s)*(h + gamma*h_tau), the inner factor of the flip exponent: doubling is exact, and
+                    // rec.y = -2*beta*s carries the opposite of the spin's sign, so the product is
+                    // 2*(h + gamma*h_tau) with its sign flipped where s = -1
+                    const float twice = __fmul_rn(__fadd_rn(rec.x, rec.z), 2.0f);
                     const float de = __uint_as_float(__float_as_uint(twice) ^ (~__float_as_uint(rec.y) & 0x80000000u));
                     const bool mine = int32_t(ballot * lane_top) < 0;  // bit `lane` of the ballot, moved to the sign
                     flips += mine ? 1u : 0u;
-                    e_run = __dadd_rn(e_run, double(mine ? de : -0.0f));  // -0.0: the identity for every value
+                    e_blk = __dadd_rn(e_blk, double(mine ? de : -0.0f));  // -0.0: the identity for every value
                 }
                 mbar_arrive(&empty[st]);
                 cursor.advance(stages);
             }
+            e_run = __dadd_rn(e_run, e_blk);
             chunk_barrier(bar_id);  // layer rendezvous (the sweep warp waits for the far warp here)
             slot_cur = slot_cur == 2 ? 0u : slot_cur + 1;
             if (WAIT && record_wait) {  // flushed per layer (lanes 0..7 hold partial sums of at most 64 * 32 each)
