@@ -44,7 +44,7 @@ def parse_args():
     ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--ladders", type=int, default=0, help="override ladders per GPU (0: the workload's)")
     ap.add_argument("--exp", default="fast", choices=["exact", "fast", "accurate"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "layered", "coalesced"],
+    ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "layered", "strand", "coalesced"],
                     help="coalesced: the intra-system schedule (one warp per chain; layered workloads, 1 GPU)")
     ap.add_argument("--chains", type=int, default=148, help="chains for --kernel coalesced")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -316,7 +316,8 @@ def main():
         csrs = [csrs[(rank * wl.n_ladders + l) % len(csrs)] for l in range(wl.n_ladders)]
     n = csrs[0]["n_spins"]
     dbar = float(np.mean([workloads.mean_degree(c) for c in csrs[:8]]))
-    kernel = {"auto": ib.KERNEL_AUTO, "generic": ib.KERNEL_GENERIC, "layered": ib.KERNEL_LAYERED}[args.kernel]
+    kernel = {"auto": ib.KERNEL_AUTO, "generic": ib.KERNEL_GENERIC, "layered": ib.KERNEL_LAYERED,
+              "strand": ib.KERNEL_STRAND}[args.kernel]
     first_ladder = rank * wl.n_ladders
 
     def make_state():
@@ -375,7 +376,7 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "bytes_per_attempt": bytes_per_attempt,
                 "flip_rate": flip_rate, "mean_degree": dbar,
-                "kernel": {1: "sweep_generic", 2: "sweep_layered"}[after["kernel"]],
+                "kernel": {1: "sweep_generic", 2: "sweep_layered", 3: "sweep_strand"}[after["kernel"]],
                 "kernel_ms_per_launch": sweep_ms / max(1, sweep_launches),
                 "roofline_attempts_per_sec": peak * 1e9 / bytes_per_attempt}
     info = after

@@ -91,11 +91,14 @@ ISING_B200_API ising_status ising_b200_model_cost(const ising_b200_model* model,
 
 /* ---------------------------------------------------------------- batches ---- */
 
-/* Which sweep kernel family a batch uses. AUTO picks LAYERED when every model qualifies. */
+/* Which sweep kernel family a batch uses.  All families follow the same trajectories bit for bit. */
 typedef enum ising_b200_kernel {
-    ISING_KERNEL_AUTO = 0,
+    ISING_KERNEL_AUTO = 0,    /* STRAND when every model qualifies, else GENERIC */
     ISING_KERNEL_GENERIC = 1, /* any graph: state in HBM, replica-interleaved [spin][32 chains] */
-    ISING_KERNEL_LAYERED = 2  /* identical-layer models: one layer of fields on chip per chain */
+    ISING_KERNEL_LAYERED = 2, /* identical-layer models, at most 512 positions per layer: one layer of
+                                 fields in Tensor Memory per 32 chains, one sweep warp per tile */
+    ISING_KERNEL_STRAND = 3   /* identical-layer models: the layers of a tile swept by several warps in
+                                 a wavefront (same order of decisions per chain), state in HBM/L2 */
 } ising_b200_kernel;
 
 /* The batch counterpart of EngineConfig + the per-chain SweepParams
@@ -186,7 +189,7 @@ typedef struct ising_batch_info {
     /* generic family only: 0 read-modify-write updates (some coupling or field is below 2^-100 in
      * magnitude), 1 updates as f32 reductions, 2 reductions + own-field window for every model */
     uint32_t generic_variant;
-    uint32_t reserved;
+    uint32_t strands;        /* strand family: layers of a tile swept concurrently (0 otherwise) */
 } ising_batch_info;
 /* timing = 1 brackets every sweep/swap launch with CUDA events on the batch's stream. */
 ISING_B200_API ising_status ising_batch_set_timing(ising_batch* batch, int timing);
@@ -233,7 +236,7 @@ ISING_B200_API ising_status ising_b200_run(const ising_b200_model* model, const 
 /* ref: ising_run_json, include/isingmc.h:108-112, src/capi.cpp:230-262: the same run, plus a JSON
  * document with the reference's keys (engine, exp, spins, sweeps, beta, tau_scale, seed, workers,
  * final_cost, flip_rate, flips, attempts, wait, checksum as 16 hex digits, environment).  `engine`
- * names the kernel family used ("b200-generic" / "b200-layered"); `wait` is empty for a single
+ * names the kernel family used ("b200-generic" / "b200-layered" / "b200-strand"); `wait` is empty for a single
  * chain (see ising_batch_read_wait_stats).  *out_json is freed with ising_b200_string_free;
  * out_report may be NULL. */
 ISING_B200_API ising_status ising_b200_run_json(const ising_b200_model* model, const ising_b200_run_params* params,

@@ -9,11 +9,11 @@ batch needs the built library and a CUDA device.
 from .api import (BatchState, CoalescedState, init_coalesced, ExpKind, IsingError, LayerSpec, SpinModel, SweepParams,
                   build_layered_model, init_state, run_single, run_single_json, run_sweeps, state_checksum,
                   total_cost)
-from ._lib import KERNEL_AUTO, KERNEL_GENERIC, KERNEL_LAYERED
+from ._lib import KERNEL_AUTO, KERNEL_GENERIC, KERNEL_LAYERED, KERNEL_STRAND
 
 __all__ = [
     "BatchState", "CoalescedState", "init_coalesced", "ExpKind", "IsingError", "LayerSpec", "SpinModel", "SweepParams",
     "build_layered_model", "init_state", "run_single", "run_single_json", "run_sweeps", "state_checksum",
     "total_cost",
-    "KERNEL_AUTO", "KERNEL_GENERIC", "KERNEL_LAYERED",
+    "KERNEL_AUTO", "KERNEL_GENERIC", "KERNEL_LAYERED", "KERNEL_STRAND",
 ]

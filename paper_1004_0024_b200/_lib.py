@@ -11,7 +11,7 @@ LIB_PATH = _PKG / "libisingb200.so"
 
 ISING_OK, ISING_ERR_ARGUMENT, ISING_ERR_PARSE, ISING_ERR_IO, ISING_ERR_INTERNAL = range(5)
 EXP_DEFAULT, EXP_EXACT, EXP_FAST, EXP_ACCURATE = range(4)
-KERNEL_AUTO, KERNEL_GENERIC, KERNEL_LAYERED = range(3)
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_LAYERED, KERNEL_STRAND = range(4)
 
 u8p, i8p = C.POINTER(C.c_uint8), C.POINTER(C.c_int8)
 u32p, u64p = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
@@ -33,7 +33,7 @@ class BatchInfo(C.Structure):
         ("kernel", C.c_int), ("sweeps_done", C.c_uint64), ("device_bytes", C.c_uint64),
         ("sweep_launches", C.c_uint64), ("swap_launches", C.c_uint64),
         ("other_launches", C.c_uint64), ("sweep_ms", C.c_double), ("swap_ms", C.c_double),
-        ("last_run_ms", C.c_double), ("generic_variant", C.c_uint32), ("reserved", C.c_uint32),
+        ("last_run_ms", C.c_double), ("generic_variant", C.c_uint32), ("strands", C.c_uint32),
     ]
 
 

@@ -19,7 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libisingb200.so"
 
-SOURCES = ["host_model.cpp", "model_text.cpp", "batch.cpp", "coalesced.cpp", "capi.cpp", "kernels_generic.cu", "kernels_layered.cu", "kernels_coalesced.cu"]
+SOURCES = ["host_model.cpp", "model_text.cpp", "batch.cpp", "coalesced.cpp", "capi.cpp", "kernels_generic.cu", "kernels_layered.cu", "kernels_strand.cu", "kernels_coalesced.cu"]
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo", "-fmad=false",
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -162,6 +163,89 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
     return out;
 }
 
+
+// Host-side image of DevStrandGraph (see device_batch.hpp and kernels_strand.cu).
+struct HostStrandGraph {
+    std::vector<uint4> pos, band_pm, chunks, edges;
+    std::vector<uint32_t> groups;
+};
+
+HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
+    const uint32_t P = m.per_layer;
+    HostStrandGraph out;
+    out.pos.resize(P);
+    out.band_pm.resize(2 * size_t(P));
+    out.chunks.resize(P / 8);
+    struct Edge { uint32_t k, t, j2; };
+    for (uint32_t p0 = 0; p0 < P; p0 += 8) {
+        std::vector<Edge> grouped;
+        std::vector<std::vector<Edge>> near_of(8);
+        bool careful = false;
+        for (uint32_t k = 0; k < 8; ++k) {
+            const uint32_t p = p0 + k;
+            uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
+            for (uint32_t e = m.layer_offsets[p]; e < m.layer_offsets[p + 1]; ++e) {
+                const uint32_t t = m.layer_targets[e];
+                const uint32_t doubled = bits(2.0f * m.layer_couplings[e]);  // exact
+                if (is_band(p, t)) {
+                    const int off = int(t) - int(p);               // -2, -1, +1, +2
+                    const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
+                    j2[slot] = doubled;
+                    mask[slot] = 0;
+                } else if (t > p && t <= p0 + 10) {
+                    // the column has been requested already (the chunk loads p0+3 .. p0+10 at its start):
+                    // the update must reach the copy on its way into the register window
+                    near_of[k].push_back({k, t, doubled});
+                    careful = true;
+                } else {
+                    grouped.push_back({k, t, doubled});
+                }
+            }
+            const float tau2g = tau_scale * (2.0f * m.layer_tau[p]);  // f32 product, as gamma * h_tau in the reference
+            out.pos[p] = make_uint4(bits(tau2g), 0, 0, 0);
+            // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign of -s; an
+            // empty slot adds -0.0.  Entry 2p is for s = -1, entry 2p+1 for s = +1.
+            for (uint32_t neg = 0; neg < 2; ++neg) {
+                const uint32_t flip = neg ? 0x80000000u : 0u;
+                out.band_pm[2 * size_t(p) + neg] = make_uint4((j2[0] ^ flip) | mask[0], (j2[1] ^ flip) | mask[1],
+                                                             (j2[2] ^ flip) | mask[2], (j2[3] ^ flip) | mask[3]);
+            }
+        }
+        for (uint32_t k = 0; k < 8; ++k) {
+            out.pos[p0 + k].y = uint32_t(out.edges.size()) | uint32_t(near_of[k].size()) << 16;
+            for (const Edge& e : near_of[k]) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 0u));
+        }
+        // groups of up to 8 edges with distinct targets, edges in attempt order (so that a column's
+        // updates keep the reference's order across and inside groups)
+        const uint32_t first_group = uint32_t(out.groups.size()), first_edge = uint32_t(out.edges.size());
+        std::vector<Edge> cur;
+        const auto close = [&]() {
+            if (cur.empty()) return;
+            out.groups.push_back(uint32_t(out.edges.size()) | uint32_t(cur.size()) << 16);
+            for (const Edge& e : cur) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 0u));
+            cur.clear();
+        };
+        for (const Edge& e : grouped) {
+            const bool clash = std::any_of(cur.begin(), cur.end(), [&](const Edge& o) { return o.t == e.t; });
+            if (cur.size() == 8 || clash) close();
+            cur.push_back(e);
+        }
+        close();
+        out.chunks[p0 / 8] = make_uint4(first_group | (uint32_t(out.groups.size()) - first_group) << 16,
+                                        first_edge | (uint32_t(out.edges.size()) - first_edge) << 16,
+                                        careful ? 1u : 0u, 0u);
+    }
+    return out;
+}
+
+// An unsigned value from the environment (tuning knobs of the strand family), 0 when unset or malformed.
+uint32_t env_u32(const char* name) {
+    const char* text = std::getenv(name);
+    if (text == nullptr || *text == 0) return 0;
+    char* end = nullptr;
+    const unsigned long v = std::strtoul(text, &end, 10);
+    return (end != nullptr && *end == 0 && v <= 0xfffffffful) ? uint32_t(v) : 0u;
+}
 }  // namespace
 
 // Runs fn(0) .. fn(count - 1) on up to 16 host threads (the per-model graph analysis of a batch with
@@ -250,7 +334,7 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     for (uint32_t idx : model_of_ladder) {
         if (idx >= models.size()) throw Error("init_state: model_of_ladder entry out of range");
     }
-    if (cfg.kernel < 0 || cfg.kernel > 2) throw Error("invalid kernel value " + std::to_string(cfg.kernel));
+    if (cfg.kernel < 0 || cfg.kernel > 3) throw Error("invalid kernel value " + std::to_string(cfg.kernel));
     // The layered family needs every model to qualify (HostModel::layered_uniform) and one layer
     // to fit the on-chip window: <= 512 positions (TMEM columns) and the graph within shared memory.
     uint32_t max_per_layer = 0, max_far_edges = 0, max_groups = 0;
@@ -267,8 +351,26 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             layered_ok = layered_ok && far_here < 16;  // 4-bit edge counts in DevLayerGraph::pos
         }
     }
+    // The strand family needs identical-layer models with one tau coupling per position as well, but
+    // nothing on chip: any per_layer that is a multiple of 8 (two chunks at least).
+    bool strand_ok = true;
+    uint32_t common_layers = 0;  // gcd of the models' layer counts: the strand count must divide it
+    uint32_t min_chunks = 0xffffffffu;
+    for (const HostModel* m : models) {
+        strand_ok = strand_ok && m->layered_uniform && m->per_layer % 8 == 0 && m->per_layer >= 16;
+        if (!strand_ok) break;
+        uint32_t a = common_layers, c = m->layers;
+        while (c != 0) { const uint32_t r = a % c; a = c; c = r; }
+        common_layers = a;
+        min_chunks = std::min(min_chunks, m->per_layer / 8);
+    }
+    if (cfg.kernel == int(KernelFamily::strand) && !strand_ok) {
+        throw Error("init_state: the strand kernel needs identical-layer models with equal tau couplings "
+                    "and a multiple of 8, at least 16, positions per layer");
+    }
+    const bool use_strand = cfg.kernel == int(KernelFamily::strand);
     std::vector<HostLayerGraph> host_graphs;
-    if (layered_ok && cfg.kernel != int(KernelFamily::generic)) {
+    if (layered_ok && !use_strand && cfg.kernel != int(KernelFamily::generic)) {
         host_graphs.resize(models.size());
         parallel_for(models.size(), [&](size_t k) { host_graphs[k] = build_layer_graph(*models[k], cfg.tau_scale); });
         for (const HostLayerGraph& hg : host_graphs) {
@@ -284,9 +386,10 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         throw Error("init_state: the layered kernel needs identical-layer models with equal tau couplings "
                     "and a multiple of 8, at most 512, positions per layer");
     }
-    family_ = (cfg.kernel != int(KernelFamily::generic) && layered_ok) ? KernelFamily::layered
-                                                                        : KernelFamily::generic;
-    if (family_ == KernelFamily::layered) any_tau = false;  // the tau field is rebuilt, never stored
+    family_ = use_strand ? KernelFamily::strand
+              : (cfg.kernel != int(KernelFamily::generic) && layered_ok) ? KernelFamily::layered
+                                                                         : KernelFamily::generic;
+    if (family_ != KernelFamily::generic) any_tau = false;  // the tau field is rebuilt, never stored
 
     // ---- device
     int count = 0;
@@ -430,6 +533,63 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         cuda_check(prepare_layered_kernels(layered_smem), "cudaFuncSetAttribute");
     }
 
+    if (family_ == KernelFamily::strand) {
+        cudaDeviceProp prop{};
+        cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+        sm_count_ = prop.multiProcessorCount;
+        std::vector<HostStrandGraph> strand_host(models.size());
+        parallel_for(models.size(), [&](size_t k) { strand_host[k] = build_strand_graph(*models[k], cfg.tau_scale); });
+        std::vector<DevStrandGraph> graphs;
+        for (size_t k = 0; k < models.size(); ++k) {
+            HostStrandGraph& hg = strand_host[k];
+            if (hg.edges.size() > 0xffffu || hg.groups.size() > 0xffffu) {
+                throw Error("init_state: layer graph too large for the strand kernel");
+            }
+            DevStrandGraph g{};
+            g.per_layer = models[k]->per_layer;
+            g.layers = models[k]->layers;
+            if (hg.edges.empty()) hg.edges.push_back(make_uint4(0, 0, 0, 0));
+            if (hg.groups.empty()) hg.groups.push_back(0);
+            g.pos = keep(hg.pos)->as<uint4>();
+            g.band_pm = keep(hg.band_pm)->as<uint4>();
+            g.chunks = keep(hg.chunks)->as<uint4>();
+            g.groups = keep(hg.groups)->as<uint32_t>();
+            g.edges = keep(hg.edges)->as<uint4>();
+            graphs.push_back(g);
+        }
+        cuda_check(cudaStreamSynchronize(stream_), "upload strand graphs");  // strand_host dies with this block
+        upload(strand_graphs_, graphs, device_bytes_, stream_);
+        cuda_check(cudaStreamSynchronize(stream_), "upload strand graphs");
+        dev_.strand_graphs = strand_graphs_.as<DevStrandGraph>();
+        // How many layers of a tile are swept at once.  Every strand and producer of a round must be
+        // resident, sm_count * warps of them; more strands hide more latency, fewer keep the tape ring
+        // (S * per_layer rows per tile) small.  ISING_B200_STRANDS / ISING_B200_STRAND_WARPS override.
+        const uint32_t tiles = uint32_t(tile_first.size());
+        strand_warps_ = env_u32("ISING_B200_STRAND_WARPS");
+        if (strand_warps_ == 0 || strand_warps_ > strand_max_warps()) strand_warps_ = 18;
+        const uint32_t capacity = uint32_t(sm_count_) * strand_warps_;
+        const uint32_t limit = std::min<uint32_t>({common_layers, 32u, std::max(1u, min_chunks / 2)});
+        uint32_t strands = env_u32("ISING_B200_STRANDS");
+        if (strands == 0) {
+            strands = 1;
+            for (uint32_t s = 2; s <= limit; ++s) {
+                if (common_layers % s == 0 && uint64_t(tiles) * (s + 1) <= capacity && s <= 8) strands = s;
+            }
+        }
+        if (strands > limit || common_layers % strands != 0 || strands + 1 > capacity) {
+            throw Error("init_state: invalid strand count " + std::to_string(strands));
+        }
+        dev_.strands = strands;
+        dev_.strand_pub = std::max(1u, std::min(4u, min_chunks / strands > 2 ? min_chunks / strands - 2 : 1u));
+        dev_.tape_rows = (strands * max_per_layer + 1024 + 31) / 32 * 32;
+        tape_.allocate(size_t(tiles) * dev_.tape_rows * 32 * sizeof(uint32_t), device_bytes_);
+        spin_bytes_.allocate(std::max<size_t>(1, size_t(tiles) * (n / 8) * 32), device_bytes_);
+        strand_flags_.allocate(size_t(strand_flag_words(tiles, strands)) * sizeof(uint32_t), device_bytes_);
+        dev_.tape = tape_.as<uint32_t>();
+        dev_.spin_bytes = spin_bytes_.as<uint8_t>();
+        dev_.strand_flags = strand_flags_.as<uint32_t>();
+    }
+
     // ---- batch description
     dev_.n_spins = n;
     dev_.n_tiles = uint32_t(tile_first.size());
@@ -503,13 +663,20 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     // The MT19937 states (2,496 B per chain) are re-read and re-written every 624 attempts while
     // 8 B per attempt of field data stream past them.  Ask for them to persist in L2 so they stop
     // costing HBM traffic; this is a hint, so failure (older driver, MIG, ...) is not an error.
-    {
+    // The set-aside is a device-wide limit: it is only ever raised here (a smaller batch must not shrink
+    // it under a live larger one), and the stream's window goes away with the batch (see ~Batch).  The
+    // strand family reads the states once per launch and needs no window.
+    if (family_ != KernelFamily::strand) {
         cudaDeviceProp prop{};
         if (cudaGetDeviceProperties(&prop, device_) == cudaSuccess && prop.persistingL2CacheMaxSize > 0 &&
             prop.accessPolicyMaxWindowSize > 0) {
             const size_t want = std::min<size_t>(mt_.bytes(), size_t(prop.persistingL2CacheMaxSize));
             const size_t window = std::min<size_t>(mt_.bytes(), size_t(prop.accessPolicyMaxWindowSize));
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess && window > 0) {
+            size_t have = 0;
+            if (cudaDeviceGetLimit(&have, cudaLimitPersistingL2CacheSize) != cudaSuccess) have = 0;
+            const bool limit_ok = have >= want || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess;
+            if (limit_ok && window > 0) {
+                l2_window_set_ = true;
                 cudaStreamAttrValue attr{};
                 attr.accessPolicyWindow.base_ptr = mt_.as<void>();
                 attr.accessPolicyWindow.num_bytes = window;
@@ -526,6 +693,14 @@ Batch::Batch(const std::vector<const HostModel*>& models,
 Batch::~Batch() {
     cudaSetDevice(device_);
     if (stream_ != nullptr) cudaStreamSynchronize(stream_);
+    if (l2_window_set_ && stream_ != nullptr) {
+        // drop the access-policy window and let the lines it pinned go back to normal use
+        cudaStreamAttrValue attr{};
+        attr.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr);
+        cudaCtxResetPersistingL2Cache();
+        cudaGetLastError();
+    }
     for (TimedLaunch& t : pending_) {
         cudaEventDestroy(t.start);
         cudaEventDestroy(t.stop);
@@ -565,7 +740,10 @@ void Batch::drain_timings() {
 void Batch::launch_sweeps(uint32_t sweeps) {
     if (sweeps == 0) return;
     begin_timed(false);
-    if (family_ == KernelFamily::layered) {
+    if (family_ == KernelFamily::strand) {
+        cuda_check(launch_sweep_strand(dev_, sweeps, sm_count_, strand_warps_, stream_), "strand sweep kernel");
+        other_launches += 2;  // spin words <-> spin bytes around the sweep kernel
+    } else if (family_ == KernelFamily::layered) {
         cuda_check(launch_sweep_layered(dev_, sweeps, sm_count_, stream_), "layered sweep kernel");
     } else {
         cuda_check(launch_sweep_generic(dev_, sweeps, stream_), "sweep kernel");
@@ -594,6 +772,10 @@ void Batch::run(uint64_t sweeps, uint32_t swap_interval) {
         // the kernels count a launch's flips in 32 bits: keep sweeps * n_spins below 2^32
         step = std::min<uint64_t>(step, std::max<uint64_t>(1, 0xFFFFFFFFull / std::max<uint32_t>(1, dev_.n_spins)));
         step = std::min<uint64_t>(step, 1u << 20);
+        // the strand family indexes a launch's draws (sweeps * n_spins + 624 tape rows) in 32 bits
+        if (family_ == KernelFamily::strand) {
+            step = std::min<uint64_t>(step, std::max<uint64_t>(1, 0x7FFFFFFFull / std::max<uint32_t>(1, dev_.n_spins)));
+        }
         launch_sweeps(uint32_t(step));
         left -= step;
         if (swapping && sweeps_done_ % swap_interval == 0) launch_swap_round();

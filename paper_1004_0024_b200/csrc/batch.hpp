@@ -40,7 +40,7 @@ class DeviceBuffer {
     size_t bytes_ = 0;
 };
 
-enum class KernelFamily : int { generic = 1, layered = 2 };
+enum class KernelFamily : int { generic = 1, layered = 2, strand = 3 };
 
 struct BatchConfig {
     uint32_t n_ladders = 0;
@@ -51,7 +51,7 @@ struct BatchConfig {
     float tau_scale = 1.0f;
     int exp_kind = 2;  // ising_exp_kind: fast
     int device = 0;
-    int kernel = 0;  // 0 auto, 1 generic, 2 layered
+    int kernel = 0;  // 0 auto, 1 generic, 2 layered, 3 strand
 };
 
 class Batch {
@@ -91,6 +91,9 @@ class Batch {
     KernelFamily family() const { return family_; }
     // generic family: 0 read-modify-write, 1 reductions, 2 reductions + own-field window in every model
     uint32_t generic_variant() const { return generic_variant_; }
+    // strand family: concurrent layers per tile and warps per persistent CTA (0 for the other families)
+    uint32_t strands() const { return dev_.strands; }
+    uint32_t strand_warps() const { return strand_warps_; }
     uint64_t sweeps_done() const { return sweeps_done_; }
     uint64_t device_bytes() const { return device_bytes_; }
     uint64_t sweep_launches = 0, swap_launches = 0, other_launches = 0;
@@ -125,6 +128,9 @@ class Batch {
     DeviceBuffer slot_of_chain_, chain_at_slot_, hs_, ht_, spin_bits_, mt_, mt_pos_, e_run_, flips_;
     DeviceBuffer swap_seeds_, swap_mt_, swap_pos_, swap_acc_, swap_att_;
     DeviceBuffer layer_graphs_, wait_counts_;
+    DeviceBuffer strand_graphs_, tape_, spin_bytes_, strand_flags_;
+    uint32_t strand_warps_ = 0;
+    bool l2_window_set_ = false;
     DeviceBuffer scratch_;  // readout staging
     int sm_count_ = 0;
 

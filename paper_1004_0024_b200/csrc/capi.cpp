@@ -414,7 +414,7 @@ ising_status ising_batch_get_info(ising_batch* batch, ising_batch_info* out) {
         out->swap_ms = b.swap_ms();
         out->last_run_ms = b.last_run_ms();
         out->generic_variant = b.generic_variant();
-        out->reserved = 0;
+        out->strands = b.strands();
         return ISING_OK;
     });
 }
@@ -455,7 +455,7 @@ ising_status ising_b200_run_json(const ising_b200_model* model, const ising_b200
         j += "  \"attempts\": " + std::to_string(run.report.attempts) + ",\n";
         j += "  \"beta\": " + json_number(double(params->beta)) + ",\n";
         j += std::string("  \"checksum\": \"") + checksum + "\",\n";
-        j += std::string("  \"engine\": \"") + (run.family == 2 ? "b200-layered" : "b200-generic") + "\",\n";
+        j += std::string("  \"engine\": \"") + (run.family == 3 ? "b200-strand" : run.family == 2 ? "b200-layered" : "b200-generic") + "\",\n";
         j += "  \"environment\": \"" + env + "\",\n";
         j += std::string("  \"exp\": \"") + exp_names[run.exp_kind] + "\",\n";
         j += "  \"final_cost\": " + json_number(run.report.final_cost) + ",\n";

@@ -79,6 +79,21 @@ struct DevLayerGraph {
     const uint4* far;  // {target position, 7 - attempt index in its chunk, bits of 2J, 0}
 };
 
+// One layer of an identical-layer model as the strand (layer-wavefront) kernel reads it, from global
+// memory through the read-only cache.  Band slots as in DevLayerGraph; every other in-layer edge of
+// position p (chunk c = p / 8) is either NEAR — its target lies among the columns the chunk has
+// already requested, p+3 .. 8c+10, which makes the chunk CAREFUL — or goes into the chunk's GROUPS,
+// applied in global memory after the chunk's last attempt.
+struct DevStrandGraph {
+    uint32_t per_layer;
+    uint32_t layers;
+    const uint4* pos;        // per position: {bits of gamma*2J_tau, near edges begin | count << 16, 0, 0}
+    const uint4* band_pm;    // as DevLayerGraph::band_pm
+    const uint4* chunks;     // per chunk: {groups begin | count << 16, group edges begin | count << 16, flags (1 careful), 0}
+    const uint32_t* groups;  // up to 8 edges with distinct targets, in attempt order: edge begin | count << 16
+    const uint4* edges;      // {target position, attempt index in its chunk, bits of 2J, 0}
+};
+
 struct DevBatch {
     const DevLayerGraph* layer_graphs;  // per model; nullptr unless the layered family is used
     uint32_t max_far_edges;             // largest n_far over the batch's models
@@ -116,6 +131,14 @@ struct DevBatch {
     unsigned long long* wait_counts;  // [tile][kWaitSlots]
     uint32_t generic_reduce;          // every model is reduction_safe: the generic family uses sweep_split_kernel
     uint32_t generic_windows;         // ... and every model has an own-field window: sweep_trio_kernel
+    // strand (layer-wavefront) family: kernels_strand.cu
+    const DevStrandGraph* strand_graphs;  // per model
+    uint32_t strands;       // S: concurrent layers per tile (divides every model's layer count)
+    uint32_t strand_pub;    // a strand publishes its progress every strand_pub chunks
+    uint32_t tape_rows;     // R: rows of a tile's MT19937 tape ring (a multiple of 32)
+    uint32_t* tape;         // u32 [tile][R][32]: raw MT19937 words in draw order
+    uint8_t* spin_bytes;    // u8 [tile][spin / 8][32]: bit k of a lane's byte <=> its spin 8c+k is -1
+    uint32_t* strand_flags; // per tile S + 1 progress counters (strand chunks done, tape head), one line each
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]
@@ -133,6 +156,11 @@ cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_coun
 size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared);
 uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared);
 cudaError_t prepare_layered_kernels(size_t smem_bytes);
+// Strand family: needs b.strand_graphs, tape, spin_bytes, strand_flags; `warps_per_cta` <= strand_max_warps().
+cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count, uint32_t warps_per_cta,
+                                cudaStream_t stream);
+uint32_t strand_max_warps();
+uint32_t strand_flag_words(uint32_t n_tiles, uint32_t strands);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);
 cudaError_t launch_checksums(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);

@@ -405,7 +405,12 @@ size_t coalesced_window_smem_bytes(uint32_t lanes, uint32_t per_layer, uint32_t 
     return bytes <= 227 * 1024 ? bytes : 0;
 }
 
+// The attribute is per function and context, shared by every live batch: it is always set to the
+// largest size any batch can ask for (227 KB, the opt-in maximum), never to one batch's own need,
+// so creating a small batch cannot take shared memory away from a large one.
 cudaError_t prepare_coalesced_kernels(size_t smem_bytes) {
+    if (smem_bytes > 227 * 1024) return cudaErrorInvalidValue;
+    smem_bytes = 227 * 1024;
     cudaError_t e = prepare_exp<kExpExact>(smem_bytes);
     if (e == cudaSuccess) e = prepare_exp<kExpFast>(smem_bytes);
     if (e == cudaSuccess) e = prepare_exp<kExpAccurate>(smem_bytes);

@@ -1065,7 +1065,12 @@ void launch_either(const DevBatch& b, uint32_t sweeps, dim3 grid, size_t smem, c
 }
 }  // namespace
 
+// The attribute is per function and context, shared by every live batch: it is always set to the
+// largest size any batch can ask for (227 KB, the opt-in maximum), never to one batch's own need,
+// so creating a batch with a small layer graph cannot take shared memory away from a large one.
 cudaError_t prepare_layered_kernels(size_t smem_bytes) {
+    if (smem_bytes > 227 * 1024) return cudaErrorInvalidValue;
+    smem_bytes = 227 * 1024;
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = prepare_one<kExpExact, false>(smem_bytes);
     if (e == cudaSuccess) e = prepare_one<kExpExact, true>(smem_bytes);

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 REL_ENERGY = 1e-5  # north_star tolerance for energies
 KERNELS = [ib.KERNEL_GENERIC]                       # any graph
-LAYERED_KERNELS = [ib.KERNEL_GENERIC, ib.KERNEL_LAYERED]  # identical-layer models: both families
+LAYERED_KERNELS = [ib.KERNEL_GENERIC, ib.KERNEL_LAYERED, ib.KERNEL_STRAND]  # identical-layer models: all families
 
 
 def run_both(port, csrs, n_ladders, betas, sweeps, swap_interval, *, seed0=ins.CHAIN_SEED_BASE, tau_scale=1.0,
