@@ -167,7 +167,7 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
 // Host-side image of DevStrandGraph (see device_batch.hpp and kernels_strand.cu).
 struct HostStrandGraph {
     std::vector<uint4> pos, band_pm, chunks, edges;
-    std::vector<uint32_t> groups;
+    std::vector<uint32_t> groups, tau;
 };
 
 HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
@@ -180,7 +180,7 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
     for (uint32_t p0 = 0; p0 < P; p0 += 8) {
         std::vector<Edge> grouped;
         std::vector<std::vector<Edge>> near_of(8);
-        bool careful = false;
+        bool careful = false, late_columns = false;
         for (uint32_t k = 0; k < 8; ++k) {
             const uint32_t p = p0 + k;
             uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
@@ -199,10 +199,14 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
                     careful = true;
                 } else {
                     grouped.push_back({k, t, doubled});
+                    // the next chunk requests columns p0+11 .. p0+18 while this one is swept, unless
+                    // this one updates them
+                    late_columns = late_columns || (t >= p0 + 11 && t <= p0 + 18);
                 }
             }
             const float tau2g = tau_scale * (2.0f * m.layer_tau[p]);  // f32 product, as gamma * h_tau in the reference
             out.pos[p] = make_uint4(bits(tau2g), 0, 0, 0);
+            out.tau.push_back(bits(tau2g));
             // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign of -s; an
             // empty slot adds -0.0.  Entry 2p is for s = -1, entry 2p+1 for s = +1.
             for (uint32_t neg = 0; neg < 2; ++neg) {
@@ -213,7 +217,7 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
         }
         for (uint32_t k = 0; k < 8; ++k) {
             out.pos[p0 + k].y = uint32_t(out.edges.size()) | uint32_t(near_of[k].size()) << 16;
-            for (const Edge& e : near_of[k]) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 0u));
+            for (const Edge& e : near_of[k]) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 31u - e.k));
         }
         // groups of up to 8 edges with distinct targets, edges in attempt order (so that a column's
         // updates keep the reference's order across and inside groups)
@@ -222,7 +226,7 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
         const auto close = [&]() {
             if (cur.empty()) return;
             out.groups.push_back(uint32_t(out.edges.size()) | uint32_t(cur.size()) << 16);
-            for (const Edge& e : cur) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 0u));
+            for (const Edge& e : cur) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 31u - e.k));
             cur.clear();
         };
         for (const Edge& e : grouped) {
@@ -233,7 +237,7 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
         close();
         out.chunks[p0 / 8] = make_uint4(first_group | (uint32_t(out.groups.size()) - first_group) << 16,
                                         first_edge | (uint32_t(out.edges.size()) - first_edge) << 16,
-                                        careful ? 1u : 0u, 0u);
+                                        (careful ? 1u : 0u) | (late_columns ? 2u : 0u), 0u);
     }
     return out;
 }
@@ -548,10 +552,13 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             DevStrandGraph g{};
             g.per_layer = models[k]->per_layer;
             g.layers = models[k]->layers;
+            g.n_edges = uint32_t(hg.edges.size());
+            g.n_groups = uint32_t(hg.groups.size());
             if (hg.edges.empty()) hg.edges.push_back(make_uint4(0, 0, 0, 0));
             if (hg.groups.empty()) hg.groups.push_back(0);
             g.pos = keep(hg.pos)->as<uint4>();
             g.band_pm = keep(hg.band_pm)->as<uint4>();
+            g.tau = keep(hg.tau)->as<uint4>();
             g.chunks = keep(hg.chunks)->as<uint4>();
             g.groups = keep(hg.groups)->as<uint32_t>();
             g.edges = keep(hg.edges)->as<uint4>();
@@ -561,12 +568,18 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         upload(strand_graphs_, graphs, device_bytes_, stream_);
         cuda_check(cudaStreamSynchronize(stream_), "upload strand graphs");
         dev_.strand_graphs = strand_graphs_.as<DevStrandGraph>();
+        // one model: its graph is staged in every CTA's shared memory (next to the warps' landing stages)
+        dev_.strand_graph_smem = 0;
+        if (graphs.size() == 1) {
+            const size_t bytes = strand_graph_bytes(graphs[0].per_layer, graphs[0].n_edges, graphs[0].n_groups);
+            if (bytes + size_t(strand_max_warps()) * strand_warp_smem() <= 200 * 1024) dev_.strand_graph_smem = uint32_t(bytes);
+        }
         // How many layers of a tile are swept at once.  Every strand and producer of a round must be
         // resident, sm_count * warps of them; more strands hide more latency, fewer keep the tape ring
         // (S * per_layer rows per tile) small.  ISING_B200_STRANDS / ISING_B200_STRAND_WARPS override.
         const uint32_t tiles = uint32_t(tile_first.size());
         strand_warps_ = env_u32("ISING_B200_STRAND_WARPS");
-        if (strand_warps_ == 0 || strand_warps_ > strand_max_warps()) strand_warps_ = 18;
+        if (strand_warps_ == 0 || strand_warps_ > strand_max_warps()) strand_warps_ = strand_max_warps();
         const uint32_t capacity = uint32_t(sm_count_) * strand_warps_;
         const uint32_t limit = std::min<uint32_t>({common_layers, 32u, std::max(1u, min_chunks / 2)});
         uint32_t strands = env_u32("ISING_B200_STRANDS");
@@ -580,7 +593,10 @@ Batch::Batch(const std::vector<const HostModel*>& models,
             throw Error("init_state: invalid strand count " + std::to_string(strands));
         }
         dev_.strands = strands;
-        dev_.strand_pub = std::max(1u, std::min(4u, min_chunks / strands > 2 ? min_chunks / strands - 2 : 1u));
+        // a publication costs a device-scope fence (~4000 cycles): as rarely as the wavefront allows — the
+        // strands of a tile may trail each other by min_chunks / strands chunks
+        dev_.strand_pub = std::max(1u, std::min(16u, min_chunks / (2 * strands)));
+        if (env_u32("ISING_B200_STRAND_PUB") != 0) dev_.strand_pub = env_u32("ISING_B200_STRAND_PUB");
         dev_.tape_rows = (strands * max_per_layer + 1024 + 31) / 32 * 32;
         tape_.allocate(size_t(tiles) * dev_.tape_rows * 32 * sizeof(uint32_t), device_bytes_);
         spin_bytes_.allocate(std::max<size_t>(1, size_t(tiles) * (n / 8) * 32), device_bytes_);

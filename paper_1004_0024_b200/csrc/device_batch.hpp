@@ -89,9 +89,13 @@ struct DevStrandGraph {
     uint32_t layers;
     const uint4* pos;        // per position: {bits of gamma*2J_tau, near edges begin | count << 16, 0, 0}
     const uint4* band_pm;    // as DevLayerGraph::band_pm
-    const uint4* chunks;     // per chunk: {groups begin | count << 16, group edges begin | count << 16, flags (1 careful), 0}
+    const uint4* tau;        // per position the bits of gamma*2J_tau (u32 [per_layer], read 8 at a time)
+    const uint4* chunks;     // per chunk: {groups begin | count << 16, group edges begin | count << 16,
+                             //             flags (1 careful, 2 updates columns the next chunk loads), 0}
     const uint32_t* groups;  // up to 8 edges with distinct targets, in attempt order: edge begin | count << 16
-    const uint4* edges;      // {target position, attempt index in its chunk, bits of 2J, 0}
+    const uint4* edges;      // {target position, attempt index k in its chunk, bits of 2J, 31 - k}
+    uint32_t n_groups;
+    uint32_t n_edges;
 };
 
 struct DevBatch {
@@ -139,6 +143,7 @@ struct DevBatch {
     uint32_t* tape;         // u32 [tile][R][32]: raw MT19937 words in draw order
     uint8_t* spin_bytes;    // u8 [tile][spin / 8][32]: bit k of a lane's byte <=> its spin 8c+k is -1
     uint32_t* strand_flags; // per tile S + 1 progress counters (strand chunks done, tape head), one line each
+    uint32_t strand_graph_smem;  // bytes of model 0's graph staged in shared memory (0: tables read from global)
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]
@@ -160,7 +165,9 @@ cudaError_t prepare_layered_kernels(size_t smem_bytes);
 cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count, uint32_t warps_per_cta,
                                 cudaStream_t stream);
 uint32_t strand_max_warps();
+uint32_t strand_warp_smem();  // shared-memory bytes per warp (landing stages, scratch)
 uint32_t strand_flag_words(uint32_t n_tiles, uint32_t strands);
+size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges, uint32_t n_groups);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);
 cudaError_t launch_checksums(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);

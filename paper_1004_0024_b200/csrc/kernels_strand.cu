@@ -33,11 +33,27 @@
 #include "device_batch.hpp"
 #include "device_math.cuh"
 
+// -DISING_STRAND_PROFILE: per-segment cycle counters of a few strands, printed at the end of the
+// launch (profiles/r02_strand_segments.md was made with it); never in the product build.
+#ifdef ISING_STRAND_PROFILE
+#include <cstdio>
+#define ISING_TICK(acc)             \
+    do {                            \
+        const long long now_ = clock64(); \
+        acc += now_ - t0;           \
+        t0 = now_;                  \
+    } while (0)
+#else
+#define ISING_TICK(acc) \
+    do {                \
+    } while (0)
+#endif
+
 namespace isingb200 {
 
 namespace {
 
-constexpr uint32_t kStrandMaxWarps = 20;
+constexpr uint32_t kStrandMaxWarps = 20;  // registers are granted 32 per thread at a time: 20 warps x 96
 constexpr uint32_t kFlagStride = 32;  // one 128-byte line per progress counter
 
 // ---- memory access helpers -----------------------------------------------------------------
@@ -82,16 +98,19 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 }
 
 // Blocks until the counter at `p` has reached `need` (counters only grow; compared modulo 2^32).
-// Every lane polls — one broadcast transaction — so every lane's later loads are ordered after
-// the value it saw.
+// Every lane polls — one broadcast transaction.  The polls are relaxed loads; the value that ends the
+// wait is read once more with acquire semantics (ptxas turns every ld.acquire.gpu into a load plus an
+// invalidation of the SM's whole L1, CCTL.IVALL: one per wait, not one per poll), so every lane's
+// later loads are ordered after a value >= need.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t need, uint32_t& cached) {
     if (int32_t(need - cached) > 0) {
-        uint32_t v = ld_acquire(p);
-        while (int32_t(need - v) > 0) {
-            __nanosleep(100);
-            v = ld_acquire(p);
-        }
-        cached = __reduce_min_sync(0xffffffffu, v);
+        while (int32_t(need - ld_relaxed(p)) > 0) __nanosleep(64);
+        cached = __reduce_min_sync(0xffffffffu, ld_acquire(p));
     }
 }
 // The whole warp's earlier writes, then the counter (the release is cumulative over what lane 0
@@ -101,42 +120,96 @@ __device__ __forceinline__ void publish(uint32_t* p, uint32_t value, uint32_t la
     if (lane == 0) st_release(p, value);
 }
 
+// ---- bulk (TMA) copies into a warp's landing buffers, completion on an mbarrier ------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (done == 0u);
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned (SASS: UBLKCP.S.G)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 // ---- one attempt ----------------------------------------------------------------------------
 // Everything an attempt needs that does not depend on the fields, per chunk of eight attempts.
 struct ChunkBits {
     uint32_t cur8;    // bit k: the spin of attempt k is -1 (before the attempt)
     uint32_t up8;     // bit k: the spin above (next layer, not yet visited) is -1
-    uint32_t agree8;  // bit k: the spins above and below are equal
+    uint32_t agree8;  // bit k: the spins above and below are equal (set by finish(), from dn8)
+    uint32_t dn8;     // bit k: the spin below (previous layer, already visited) is -1
+    // (kept apart from the loads, so that requesting the bytes does not wait for them)
+    __device__ __forceinline__ void finish() { agree8 = ~(up8 ^ dn8); }
 };
 
+// The part of a chunk's eight attempts that does not depend on the fields — eight independent
+// strings of integer work, computed together ahead of the attempts so that they overlap each other
+// instead of lengthening the loop-carried chain: the uniform draws (MT19937 tempering, u32_to_unit),
+// -2*beta*s, and gamma * h_tau.
+struct Prepared {
+    float u[8];
+    uint32_t ny[8];  // bits of -2*beta*s
+    float hz[8];     // gamma * h_tau, h_tau = J*(s_up + s_dn) in {+2J, +0, -2J}
+};
+__device__ __forceinline__ void prepare_chunk(Prepared& pr, const uint32_t (&raw)[8], const ChunkBits& cb, uint32_t nb2,
+                                              float u_offset, const uint4 tau_lo, const uint4 tau_hi) {
+    const uint32_t tau_g[8] = {tau_lo.x, tau_lo.y, tau_lo.z, tau_lo.w, tau_hi.x, tau_hi.y, tau_hi.z, tau_hi.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        // u32_to_unit (x * 2^-32 is exact, so is adding +0); padding lanes get u + 2 and never accept
+        pr.u[k] = __fmaf_rn(__uint2float_rz(mt_temper(raw[k])), 0x1p-32f, u_offset);
+        const uint32_t sgn = (cb.cur8 << (31 - k)) & 0x80000000u;  // set <=> s = -1
+        const uint32_t sgn_up = (cb.up8 << (31 - k)) & 0x80000000u;
+        const uint32_t agree = uint32_t(int32_t(cb.agree8 << (31 - k)) >> 31);
+        pr.ny[k] = nb2 ^ sgn;
+        pr.hz[k] = __uint_as_float((tau_g[k] ^ sgn_up) & agree);
+    }
+}
+// The band_pm entry of attempt K's flip: the pair's first entry is for s = -1, the second (16 bytes
+// on) for s = +1.
+template <int K>
+__device__ __forceinline__ uint4 band_entry(const uint4* pair0, uint32_t cur8) {
+    const uint32_t off = ((K <= 4 ? cur8 << (4 - K) : cur8 >> (K - 4)) & 16u) ^ 16u;
+    return *reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(pair0 + 2 * K) + off);
+}
+
 // Attempt K (compile-time index in the unrolled chunk; the register window r[] is indexed by
-// position & 7) of position p = p0 + K.  `tau_g` holds the bits of gamma * 2J_tau(p), `band` points
-// at the band_pm pair of p.  ref: sweep_kernels.hpp:14-16, sweep_basic.cpp:36-48.
+// position & 7) of position p = p0 + K: the loop-carried part.  `op` is the band_pm entry of the
+// flip.  ref: sweep_kernels.hpp:14-16, sweep_basic.cpp:36-48.
 template <int EXP, int K>
-__device__ __forceinline__ void strand_attempt(float (&r)[8], uint32_t raw, const ChunkBits& cb,
-                                               uint32_t nb2, float u_offset, uint32_t tau_g, const uint4* band,
+__device__ __forceinline__ void strand_attempt(float (&r)[8], const Prepared& pr, uint32_t nb2, const uint4 op,
                                                uint32_t& acc8, double& e_blk) {
-    // u32_to_unit (x * 2^-32 is exact, so is adding +0); padding lanes get u + 2 and never accept
-    const float u = __fmaf_rn(__uint2float_rz(mt_temper(raw)), 0x1p-32f, u_offset);
-    const uint32_t sgn = (cb.cur8 << (31 - K)) & 0x80000000u;     // set <=> s = -1
-    const uint32_t sgn_up = (cb.up8 << (31 - K)) & 0x80000000u;
-    const uint32_t agree = uint32_t(int32_t(cb.agree8 << (31 - K)) >> 31);
-    // gamma * h_tau, h_tau = J*(s_up + s_dn) in {+2J, +0, -2J}
-    const float hz = __uint_as_float((tau_g ^ sgn_up) & agree);
     // x = -beta*((2s)*v) == (-2*beta*s)*v: doubling is exact, one rounding either way
-    const float v = __fadd_rn(r[K], hz);
-    const float x = __fmul_rn(__uint_as_float(nb2 ^ sgn), v);
-    const bool accept = u < exp_kind<EXP>(x);
-    // band neighbours p-2, p-1, p+1, p+2: h -= (2s)*J == h + (-(2s)*J); entry 2p+1 is for s = +1; an
-    // empty slot holds -0.0
-    const uint4 op = __ldg(band + ((sgn >> 31) ^ 1u));
+    const float v = __fadd_rn(r[K], pr.hz[K]);
+    const float x = __fmul_rn(__uint_as_float(pr.ny[K]), v);
+    const bool accept = pr.u[K] < exp_kind<EXP>(x);
+    // band neighbours p-2, p-1, p+1, p+2: h -= (2s)*J == h + (-(2s)*J); an empty slot holds -0.0
     if (accept) {
         r[(K + 6) & 7] = __fadd_rn(r[(K + 6) & 7], __uint_as_float(op.x));
         r[(K + 7) & 7] = __fadd_rn(r[(K + 7) & 7], __uint_as_float(op.y));
         r[(K + 1) & 7] = __fadd_rn(r[(K + 1) & 7], __uint_as_float(op.z));
         r[(K + 2) & 7] = __fadd_rn(r[(K + 2) & 7], __uint_as_float(op.w));
-        // running energy of the tempering swap: (2s)*(h + gamma*h_tau), the inner factor of x
-        e_blk = __dadd_rn(e_blk, double(__uint_as_float(__float_as_uint(__fmul_rn(v, 2.0f)) ^ sgn)));
+        // running energy of the tempering swap: (2s)*(h + gamma*h_tau), the inner factor of x — 2v with
+        // its sign flipped where s = -1 (ny ^ nb2 is that sign bit)
+        e_blk = __dadd_rn(e_blk, double(__uint_as_float(__float_as_uint(__fmul_rn(v, 2.0f)) ^ pr.ny[K] ^ nb2)));
         acc8 |= 1u << K;
     }
 }
@@ -146,23 +219,49 @@ __device__ __forceinline__ float edge_addend(const uint4 e, uint32_t cur8) {
     return __uint_as_float(e.z ^ ((((cur8 >> e.y) & 1u) ^ 1u) << 31));
 }
 
-// Far neighbours of the chunk's flips, after its last attempt: read-modify-writes in global memory,
-// in groups of up to 8 edges with distinct targets (loads together, then adds and stores).  Groups
-// and edges are in attempt order, so every column receives its updates in the reference's order.
-__device__ __forceinline__ void apply_groups(float* hs_l, const DevStrandGraph& g, uint32_t ginfo, uint32_t acc8,
-                                             uint32_t cur8) {
-    const uint32_t* grp = g.groups + (ginfo & 0xffffu);
+// Far neighbours of the chunk's flips, after its last attempt (edges in attempt order, so every
+// column receives its updates in the reference's order).
+//
+// RED: h[t] -= (2s)*J goes out as a global f32 reduction of -(2s)*J — it rounds exactly like the
+// subtraction, reductions and loads of one thread to one address keep program order, and nothing
+// comes back, so the chunk pays no round trip.  Every lane takes part (a lane that did not accept
+// adds -0.0, the identity for every bit pattern): one full 128-byte reduction per edge.  Global f32
+// reductions flush subnormals (REDG.ADD.F32.FTZ.RN), so this path is only used when no field can be
+// subnormal (DevModel::reduction_safe for every model of the batch).
+__device__ __forceinline__ void reduce_field(float* p, float addend) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(addend) : "memory");
+}
+__device__ __forceinline__ void apply_edges_red(float* hs_l, const uint4* edges, uint32_t einfo, uint32_t acc8,
+                                                uint32_t cur8) {
+    const uint4* fe = edges + (einfo & 0xffffu);
+    const uint32_t n = einfo >> 16;
+    // bit k of `flip`: the addend of attempt k's edges is -2J (s = +1); of `acc8`: this lane accepted it
+    const uint32_t flip = ~cur8;
+#pragma unroll 4
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint4 e = fe[i];  // {target position, attempt, bits of 2J, 31 - attempt}
+        const uint32_t addend = e.z ^ ((flip << e.w) & 0x80000000u);
+        // every lane takes part, a lane that did not accept adds -0.0 (reductions of accepting lanes
+        // only were measured slower: 1180 against 890 cycles per chunk)
+        reduce_field(hs_l + size_t(e.x) * 32, __uint_as_float(int32_t(acc8 << e.w) < 0 ? addend : 0x80000000u));
+    }
+}
+// Otherwise: read-modify-writes in groups of up to 8 edges with distinct targets (loads together,
+// then adds and stores).
+__device__ __noinline__ void apply_groups_rmw(float* hs_l, const uint32_t* groups, const uint4* edges, uint32_t ginfo,
+                                              uint32_t acc8, uint32_t cur8) {
+    const uint32_t* grp = groups + (ginfo & 0xffffu);
     const uint32_t n_groups = ginfo >> 16;
 #pragma unroll 1
     for (uint32_t q = 0; q < n_groups; ++q) {
-        const uint32_t info = __ldg(grp + q);
-        const uint4* fe = g.edges + (info & 0xffffu);
+        const uint32_t info = grp[q];
+        const uint4* fe = edges + (info & 0xffffu);
         const uint32_t n = info >> 16;
         uint4 e[8];
         float v[8];
 #pragma unroll
         for (uint32_t i = 0; i < 8; ++i) {
-            if (i < n) e[i] = __ldg(fe + i);
+            if (i < n) e[i] = fe[i];
         }
 #pragma unroll
         for (uint32_t i = 0; i < 8; ++i) {
@@ -195,32 +294,34 @@ struct CarefulResult {
 };
 
 template <int EXP, int K>
-__device__ __forceinline__ void careful_attempt(float (&r)[8], float* scratch, uint32_t raw, const ChunkBits& cb,
-                                                uint32_t nb2, float u_offset, const uint4 posrec, const uint4* band,
-                                                uint32_t& acc8, double& e_blk, const uint4* edges, uint32_t p0) {
+__device__ __forceinline__ void careful_attempt(float (&r)[8], float* scratch, const Prepared& pr, uint32_t nb2,
+                                                uint32_t cur8, const uint4 posrec, const uint4* band, uint32_t& acc8,
+                                                double& e_blk, const uint4* edges, uint32_t p0) {
     const uint32_t before = acc8;
-    strand_attempt<EXP, K>(r, raw, cb, nb2, u_offset, posrec.x, band, acc8, e_blk);
+    strand_attempt<EXP, K>(r, pr, nb2, band_entry<K>(band, cur8), acc8, e_blk);
     const uint32_t near = posrec.y;
     if ((near >> 16) != 0u && acc8 != before) {
         const uint4* ne = edges + (near & 0xffffu);
         for (uint32_t i = 0; i < (near >> 16); ++i) {
-            const uint4 e = __ldg(ne + i);
+            const uint4 e = ne[i];
             float* cell = scratch + (e.x - (p0 + 3)) * 32;
-            *cell = __fadd_rn(*cell, edge_addend(e, cb.cur8));
+            *cell = __fadd_rn(*cell, edge_addend(e, cur8));
         }
     }
 }
 
 template <int EXP>
 __device__ __noinline__ CarefulResult careful_chunk(Window w, RawWords raw, ChunkBits cb, uint32_t nb2, float u_offset,
-                                                    const uint4* pos, const uint4* band, const uint4* edges,
-                                                    uint32_t p0, float* hs_l, float* scratch, double e_blk) {
+                                                    const uint4* pos, const uint4* band, const uint4* tau,
+                                                    const uint4* edges, uint32_t p0, float* hs_l, float* scratch,
+                                                    double e_blk) {
     float (&r)[8] = w.r;
     uint32_t acc8 = 0;
-#define ISING_CAREFUL(K)                                                                                              \
-    careful_attempt<EXP, K>(r, scratch, raw.v[K], cb, nb2, u_offset, __ldg(pos + K), band + 2 * K, acc8, e_blk, edges, \
-                            p0);                                                                                      \
-    if (p0 != 0 || K >= 2) st_f32(hs_l + (size_t(p0) + K - 2) * 32, r[(K + 6) & 7]);                                  \
+    Prepared pr;
+    prepare_chunk(pr, raw.v, cb, nb2, u_offset, tau[0], tau[1]);
+#define ISING_CAREFUL(K)                                                                                   \
+    careful_attempt<EXP, K>(r, scratch, pr, nb2, cb.cur8, pos[K], band, acc8, e_blk, edges, p0);            \
+    if (p0 != 0 || K >= 2) st_f32(hs_l + (size_t(p0) + K - 2) * 32, r[(K + 6) & 7]);                        \
     r[(K + 3) & 7] = scratch[K * 32];
     ISING_CAREFUL(0)
     ISING_CAREFUL(1)
@@ -239,9 +340,32 @@ __device__ __noinline__ CarefulResult careful_chunk(Window w, RawWords raw, Chun
 }
 
 // ---- a strand ---------------------------------------------------------------------------------
-template <int EXP, bool WAIT>
+// Per-warp shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB and
+// the three spin-byte rows of a chunk), their mbarriers, and the scratch of the careful chunks.
+constexpr uint32_t kStageBytes = 1024 + 128;
+constexpr uint32_t kWarpSmem = 2 * kStageBytes + 16 + 1024;
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// Everything a chunk reads from global memory is requested one chunk ahead: the tape rows and the
+// spin bytes by bulk (TMA) copies of one elected lane into the warp's landing stage (no registers
+// held meanwhile), the eight columns entering the window by plain loads (they must stay in program
+// order with this thread's own stores and reductions to the same addresses); the columns three
+// chunks ahead are prefetched into L2.  So the loop-carried chain of the attempts is all a strand
+// waits for.  The one exception: when a far edge of chunk c targets the columns chunk c+1 loads
+// (chunk flag 2), those are requested after chunk c's updates.
+template <int EXP, bool WAIT, bool RED>
 __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t tile, uint32_t j, uint32_t sweeps,
-                           uint32_t lane, float* scratch) {
+                           uint32_t lane, unsigned char* warp_smem) {
     const uint32_t P = g.per_layer, L = g.layers, C = P / 8, S = b.strands, n = b.n_spins;
     const uint32_t blocks_per_sweep = L / S;
     const uint32_t total_blocks = blocks_per_sweep * sweeps;
@@ -250,9 +374,9 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
     const uint32_t nb2 = __float_as_uint(active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
     const float u_offset = active ? 0.0f : 2.0f;
     float* hs_tile = b.hs + size_t(tile) * n * 32 + lane;
-    uint8_t* bytes_tile = b.spin_bytes + size_t(tile) * (n / 8) * 32 + lane;
+    uint8_t* bytes_tile = b.spin_bytes + size_t(tile) * (n / 8) * 32;  // (no lane offset: rows are copied whole)
     const uint32_t R = b.tape_rows;
-    const uint32_t* tape = b.tape + size_t(tile) * R * 32 + lane;
+    const uint32_t* tape = b.tape + size_t(tile) * R * 32;             // (likewise)
     uint32_t* flags = b.strand_flags + size_t(tile) * (S + 1) * kFlagStride;
     uint32_t* my_flag = flags + j * kFlagStride;
     const uint32_t* pred_flag = flags + ((j + S - 1) % S) * kFlagStride;
@@ -261,100 +385,159 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
     uint32_t pred_cached = 0, head_cached = 0;
     uint32_t flips = 0;
     uint32_t seq = 0;  // chunks finished
+    // landing stages: stage s at wsm + s * kStageBytes (tape rows, then the cur / up / dn byte rows)
+    const uint32_t wsm = smem_u32(warp_smem);
+    const uint32_t bar0 = wsm + 2 * kStageBytes;
+    float* scratch = reinterpret_cast<float*>(warp_smem + 2 * kStageBytes + 16) + lane;
+    uint32_t stage = 0, phases = 0;  // current stage; bit s of phases = parity the next wait on stage s sees
+    if (lane == 0) {
+        mbar_init(bar0, 1);
+        mbar_init(bar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     // wait statistics (ref: FlipStats::group_wait): lane k folds the ballot of attempt k of every chunk
     const bool record_wait = WAIT && b.wait_counts != nullptr && b.tile_count[tile] == 32;
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
 
+    // one elected lane requests a chunk's tape rows and spin bytes into stage `st`
+    const auto request = [&](uint32_t st, uint32_t slot, const uint8_t* cur, const uint8_t* up, const uint8_t* dn) {
+        if (lane == 0) {
+            const uint32_t dst = wsm + st * kStageBytes, bar = bar0 + st * 8;
+            // the rows were written through the generic proxy (by other warps, acquired above): order
+            // the async-proxy reads after what this lane has observed
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_expect(bar, 1024 + 96);
+            bulk_load(dst, tape + size_t(slot) * 32, 1024, bar);
+            bulk_load(dst + 1024, cur, 32, bar);
+            bulk_load(dst + 1056, up, 32, bar);
+            bulk_load(dst + 1088, dn, 32, bar);
+        }
+    };
+
+#ifdef ISING_STRAND_PROFILE
+    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0;
+#endif
     for (uint32_t blk = 0; blk < total_blocks; ++blk) {
         const uint32_t sw = blk / blocks_per_sweep, m = blk - sw * blocks_per_sweep;
         const uint32_t l = j + S * m;
         const uint32_t l_up = l + 1 == L ? 0u : l + 1, l_dn = l == 0 ? L - 1 : l - 1;
         float* hs_l = hs_tile + size_t(l) * P * 32;
-        uint8_t* by_cur = bytes_tile + size_t(l) * C * 32;
-        const uint8_t* by_up = bytes_tile + size_t(l_up) * C * 32;
-        const uint8_t* by_dn = bytes_tile + size_t(l_dn) * C * 32;
         // The strand of the layer below: its chunk c of the matching block must be finished before
         // this strand reads that layer's new spins.  For j > 0 the matching block has this block's
         // index, for j == 0 it is the block before (layer L-1 of the previous sweep when m == 0).
         const bool has_pred = S > 1 && !(j == 0 && blk == 0);
-        const uint32_t pred_base = (j == 0 ? blk - 1 : blk) * C;
+        uint32_t pred_need = (j == 0 ? blk - 1 : blk) * C + 1;  // the predecessor's count once it has finished chunk c
         // this block's draws: tape rows 624 + (sw*L + l)*P + p
         const uint32_t row0 = kMtN + (sw * L + l) * P;
-        uint32_t slot = row0 % R;  // (R and row0 are multiples of 8: a chunk's rows never wrap)
+        uint32_t head_need = row0 + 8;  // the head once chunk c's rows exist
+        uint32_t slot = row0 % R;       // (R and row0 are multiples of 8: a chunk's rows never wrap)
         double e_blk = 0.0;
 
-        RawWords raw_words;
-        uint32_t (&raw)[8] = raw_words.v;
-        wait_counter(head_flag, row0 + 8, head_cached);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) raw[k] = ld_cg_u32(tape + size_t(slot + k) * 32);
+        // running pointers: the chunk being swept (…_c) is at p0 = 8c
+        float* hs_c = hs_l;
+        uint8_t* cur_c = bytes_tile + size_t(l) * C * 32;
+        const uint8_t* up_c = bytes_tile + size_t(l_up) * C * 32;
+        const uint8_t* dn_c = bytes_tile + size_t(l_dn) * C * 32;
+        const uint4* chunk_c = g.chunks;
+        const uint4* pos_c = g.pos;
+        const uint4* band_c = g.band_pm;
+        const uint4* tau_c = g.tau;
 
+        // ---- the first chunk's operands (the only exposed round trip of the block)
+        wait_counter(head_flag, head_need, head_cached);
+        if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
+        __syncwarp();  // every lane has left the stage's previous contents
+        request(stage, slot, cur_c, up_c, dn_c);
         // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
         Window w;
         float (&r)[8] = w.r;
 #pragma unroll
         for (int k = 0; k < 8; ++k) r[k] = 0.0f;
-        r[0] = ld_cg_f32(hs_l);
-        r[1] = ld_cg_f32(hs_l + 32);
-        r[2] = ld_cg_f32(hs_l + 64);
+        r[0] = ld_cg_f32(hs_c);
+        r[1] = ld_cg_f32(hs_c + 32);
+        r[2] = ld_cg_f32(hs_c + 64);
+        float nx[8];  // the columns entering the window during the chunk: p0+3 .. p0+10
+#pragma unroll
+        for (int k = 0; k < 8; ++k) nx[k] = ld_cg_f32(hs_c + (3 + k) * 32);  // (a layer has 16 positions at least)
 
         for (uint32_t c = 0; c < C; ++c) {
-            const uint32_t p0 = c * 8;
-            const uint4 chunk_info = __ldg(g.chunks + c);
-            if (has_pred) wait_counter(pred_flag, pred_base + c + 1, pred_cached);
-            // ---- requests: the columns entering the window (p0+3 .. p0+10; the last chunk has five),
-            // the spin bytes, the next chunk's tape rows; L2 prefetches one chunk ahead
-            float nx[8];
-            const float* enter = hs_l + (size_t(p0) + 3) * 32;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) nx[k] = (k < 5 || c + 1 < C) ? ld_cg_f32(enter + k * 32) : 0.0f;
-            ChunkBits cb;
-            cb.cur8 = ld_cg_u8(by_cur + c * 32);
-            cb.up8 = ld_cg_u8(by_up + c * 32);
-            cb.agree8 = ~(cb.up8 ^ ld_cg_u8(by_dn + c * 32));
-            uint32_t raw_next[8];
-            if (c + 1 < C) {
+#ifdef ISING_STRAND_PROFILE
+            t0 = clock64();
+#endif
+            const uint4 chunk_info = *chunk_c;
+            const bool more = c + 1 < C;
+            const bool late_columns = (chunk_info.z & 2u) != 0u;  // this chunk updates columns the next one loads
+            // ---- requests for the next chunk
+            float nx_next[8];
+            if (more) {
                 slot = slot + 8 == R ? 0u : slot + 8;
-                wait_counter(head_flag, row0 + p0 + 16, head_cached);
+                head_need += 8;
+                ++pred_need;
+                wait_counter(head_flag, head_need, head_cached);
+                if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
+                __syncwarp();  // every lane has left the other stage's previous contents
+                request(stage ^ 1u, slot, cur_c + 32, up_c + 32, dn_c + 32);
+                if (!late_columns) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) raw_next[k] = ld_cg_u32(tape + size_t(slot + k) * 32);
-                if (lane < 8 && p0 + 11 + lane < P) prefetch_l2(enter + (8 + lane) * 32);
+                    for (int k = 0; k < 8; ++k) nx_next[k] = (k < 5 || c + 2 < C) ? ld_cg_f32(hs_c + (11 + k) * 32) : 0.0f;
+                }
+                // the columns three chunks ahead, into L2
+                if (lane < 8 && c + 4 < C) prefetch_l2(hs_c + (27 + lane) * 32);
             }
-            {
-                const uint32_t n_edges = chunk_info.y >> 16;
-                if (lane < n_edges) prefetch_l2(hs_l + size_t(__ldg(g.edges + (chunk_info.y & 0xffffu) + lane).x) * 32);
-            }
+            // ---- this chunk's tape words and spin bytes have landed
+            const uint32_t st_addr = wsm + stage * kStageBytes;
+            ISING_TICK(tA);
+            mbar_wait(bar0 + stage * 8, (phases >> stage) & 1u);
+            ISING_TICK(tB);
+            phases ^= 1u << stage;
+            RawWords raw_words;
+            uint32_t (&raw)[8] = raw_words.v;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) raw[k] = lds_u32(st_addr + k * 128 + lane * 4);
+            ChunkBits cb;
+            cb.cur8 = lds_u8(st_addr + 1024 + lane);
+            cb.up8 = lds_u8(st_addr + 1056 + lane);
+            cb.dn8 = lds_u8(st_addr + 1088 + lane);
+            cb.finish();
 
             // ---- eight attempts
             uint32_t acc8 = 0;
             if (__builtin_expect((chunk_info.z & 1u) == 0u, 1)) {
-                const uint4* band = g.band_pm + 2 * size_t(p0);
-                const uint4* pos = g.pos + p0;
-#define ISING_STRAND_ATTEMPT(K)                                                                                   \
-    strand_attempt<EXP, K>(r, raw[K], cb, nb2, u_offset, __ldg(&pos[K].x), band + 2 * K, acc8, e_blk);           \
-    if (c != 0 || K >= 2) st_f32(hs_l + (size_t(p0) + K - 2) * 32, r[(K + 6) & 7]);                               \
-    r[(K + 3) & 7] = nx[K];
-                ISING_STRAND_ATTEMPT(0)
-                ISING_STRAND_ATTEMPT(1)
-                ISING_STRAND_ATTEMPT(2)
-                ISING_STRAND_ATTEMPT(3)
-                ISING_STRAND_ATTEMPT(4)
-                ISING_STRAND_ATTEMPT(5)
-                ISING_STRAND_ATTEMPT(6)
-                ISING_STRAND_ATTEMPT(7)
+                Prepared pr;
+                prepare_chunk(pr, raw, cb, nb2, u_offset, tau_c[0], tau_c[1]);
+                // the band entry of an attempt is requested during the attempt before it
+                uint4 op = band_entry<0>(band_c, cb.cur8);
+#define ISING_STRAND_ATTEMPT(K, NEXT)                                                \
+    {                                                                                \
+        const uint4 op_next = band_entry<NEXT>(band_c, cb.cur8);                     \
+        strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
+        if (c != 0 || K >= 2) st_f32(hs_c + (K - 2) * 32, r[(K + 6) & 7]);           \
+        r[(K + 3) & 7] = nx[K];                                                      \
+        op = op_next;                                                                \
+    }
+                ISING_STRAND_ATTEMPT(0, 1)
+                ISING_STRAND_ATTEMPT(1, 2)
+                ISING_STRAND_ATTEMPT(2, 3)
+                ISING_STRAND_ATTEMPT(3, 4)
+                ISING_STRAND_ATTEMPT(4, 5)
+                ISING_STRAND_ATTEMPT(5, 6)
+                ISING_STRAND_ATTEMPT(6, 7)
+                ISING_STRAND_ATTEMPT(7, 7)
 #undef ISING_STRAND_ATTEMPT
             } else {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) scratch[k * 32] = nx[k];
-                const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, g.pos + p0,
-                                                             g.band_pm + 2 * size_t(p0), g.edges, p0, hs_l, scratch, e_blk);
+                const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, pos_c, band_c, tau_c,
+                                                             g.edges, c * 8, hs_l, scratch, e_blk);
                 w = res.w;
                 acc8 = res.acc8;
                 e_blk = res.e_blk;
             }
 
             // ---- after the chunk: spins, far neighbours, progress
-            st_u8(by_cur + c * 32, cb.cur8 ^ acc8);
+            ISING_TICK(tC);
+            st_u8(cur_c + lane, cb.cur8 ^ acc8);
             flips += __popc(acc8);
             if (WAIT && record_wait) {
 #pragma unroll
@@ -363,28 +546,49 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
                     if (lane == uint32_t(k)) wait_fold(ballot, wait);
                 }
             }
-            if ((chunk_info.x >> 16) != 0u && __any_sync(0xffffffffu, acc8 != 0u)) {
-                apply_groups(hs_l, g, chunk_info.x, acc8, cb.cur8);
+            if ((chunk_info.y >> 16) != 0u && __any_sync(0xffffffffu, acc8 != 0u)) {
+                if (RED) apply_edges_red(hs_l, g.edges, chunk_info.y, acc8, cb.cur8);
+                else apply_groups_rmw(hs_l, g.groups, g.edges, chunk_info.x, acc8, cb.cur8);
             }
             ++seq;
-            if (c + 1 < C) {
+            ISING_TICK(tD);
+            if (more) {
+                if (late_columns) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) raw[k] = raw_next[k];
+                    for (int k = 0; k < 8; ++k) nx_next[k] = (k < 5 || c + 2 < C) ? ld_cg_f32(hs_c + (11 + k) * 32) : 0.0f;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) nx[k] = nx_next[k];
+                stage ^= 1u;
+                hs_c += 8 * 32;
+                cur_c += 32;
+                up_c += 32;
+                dn_c += 32;
+                chunk_c += 1;
+                pos_c += 8;
+                band_c += 16;
+                tau_c += 2;
                 if (seq % pub == 0u) publish(my_flag, seq, lane);
             }
+            ISING_TICK(tE);
         }
+#ifdef ISING_STRAND_PROFILE
+        t0 = clock64();
+#endif
+        stage ^= 1u;
         // ---- end of the layer: the last two columns leave the window; the block's partial sum joins
         // the running energy after the partial sums of all earlier blocks (tempering definition,
         // oracle/ising_oracle.h), which the strand of the layer below has published with its block
-        st_f32(hs_l + (size_t(P) - 2) * 32, r[6]);
-        st_f32(hs_l + (size_t(P) - 1) * 32, r[7]);
-        if (has_pred) wait_counter(pred_flag, pred_base + C, pred_cached);
+        st_f32(hs_c + 6 * 32, r[6]);
+        st_f32(hs_c + 7 * 32, r[7]);
+        if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
         if (active) {
             double* e_run = b.e_run + chain;
             const double e = ld_cg_f64(e_run);
             asm volatile("st.global.f64 [%0], %1;" ::"l"(e_run), "d"(__dadd_rn(e, e_blk)) : "memory");
         }
         publish(my_flag, seq, lane);
+        ISING_TICK(tF);
         if (WAIT && record_wait) {  // flushed per layer (lanes 0..7 hold partial sums of at most 64 * 32 each)
             unsigned long long* out = b.wait_counts + size_t(tile) * kWaitSlots;
 #pragma unroll
@@ -398,6 +602,9 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
         }
     }
     if (active && flips != 0u) atomicAdd(b.flips + chain, static_cast<unsigned long long>(flips));
+#ifdef ISING_STRAND_PROFILE
+    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld edges %lld rotate %lld; block end %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tF / total_blocks);
+#endif
 }
 
 // ---- the producer -------------------------------------------------------------------------------
@@ -437,37 +644,65 @@ __device__ void producer_run(const DevBatch& b, const DevStrandGraph& g, uint32_
     uint32_t a = kMtN;      // next row to generate
     uint32_t tail = 0;      // draws known to be consumed by every strand
     uint32_t so = kMtN % R, sa = 0, sf = kMtM % R;  // slots of rows a, a-624, a-227 (624 - 227 = 397)
-    uint32_t cur = ld_cg_u32(tape);                         // x[a-624]
+    uint32_t cur = ld_cg_u32(tape);                 // x[a-624]
+    // A producer feeds S strands and is one in-order warp: what bounds it is the round trip of its
+    // operand loads.  So rows are generated 32 at a time with all 64 operand loads in flight together
+    // (x[a-623+k] and x[a-227+k], k < 32: every one of them lies behind row a).
     while (a < end) {
-        const uint32_t batch = min(32u, end - a);
+        const uint32_t batch = min(64u, end - a);  // (a multiple of 8)
         // rows a .. a+batch-1 overwrite rows a-R .. : they must be consumed draws (row < 624 + tail)
         while (int32_t(a + batch - R - kMtN - tail) > 0) {
             uint32_t d = 0xffffffffu;
-            if (lane < S) d = strand_draw_index(ld_acquire(flags + lane * kFlagStride), lane, S, C, L, P, total_blocks);
+            // (relaxed: a strand's count is published after its last read of the rows it stands for, and
+            // the rows written next are published with a release of their own)
+            if (lane < S) d = strand_draw_index(ld_relaxed(flags + lane * kFlagStride), lane, S, C, L, P, total_blocks);
             d = __reduce_min_sync(0xffffffffu, d);
             if (d == 0xffffffffu) d = total;
-            if (d == tail) __nanosleep(200);
+            if (d == tail) __nanosleep(2000);
             tail = d;
         }
-        for (uint32_t g8 = 0; g8 < batch; g8 += 8) {
-            uint32_t nxt[8], far[8];
+        for (uint32_t done = 0; done < batch;) {
+            const uint32_t rows = min(32u, batch - done);
+            if (rows == 32u && sa + 32 < R && sf + 32 <= R && so + 32 <= R) {  // no run crosses the end of the ring
+                const uint32_t* pa = tape + size_t(sa) * 32;
+                const uint32_t* pf = tape + size_t(sf) * 32;
+                uint32_t* po = tape + size_t(so) * 32;
+                uint32_t nxt[32], far[32];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                uint32_t s1 = sa + k + 1;  // (sa is a multiple of 8: only sa + 8 can wrap)
-                s1 = s1 == R ? 0u : s1;
-                uint32_t s2 = sf + k;
-                s2 = s2 >= R ? s2 - R : s2;
-                nxt[k] = ld_cg_u32(tape + size_t(s1) * 32);
-                far[k] = ld_cg_u32(tape + size_t(s2) * 32);
-            }
+                for (int k = 0; k < 32; ++k) {
+                    nxt[k] = ld_cg_u32(pa + (k + 1) * 32);
+                    far[k] = ld_cg_u32(pf + k * 32);
+                }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                st_u32(tape + size_t(so + k) * 32, mt_recurrence(cur, nxt[k], far[k]));
-                cur = nxt[k];
+                for (int k = 0; k < 32; ++k) {
+                    st_u32(po + k * 32, mt_recurrence(cur, nxt[k], far[k]));
+                    cur = nxt[k];
+                }
+                sa += 32;
+                sf = sf + 32 == R ? 0u : sf + 32;
+                so = so + 32 == R ? 0u : so + 32;
+                done += 32;
+            } else {  // near the end of the ring, or a short tail: 8 rows at a time, every slot wrapped
+                uint32_t nxt[8], far[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    uint32_t s1 = sa + k + 1;
+                    s1 = s1 >= R ? s1 - R : s1;
+                    uint32_t s2 = sf + k;
+                    s2 = s2 >= R ? s2 - R : s2;
+                    nxt[k] = ld_cg_u32(tape + size_t(s1) * 32);
+                    far[k] = ld_cg_u32(tape + size_t(s2) * 32);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    st_u32(tape + size_t(so + k) * 32, mt_recurrence(cur, nxt[k], far[k]));  // (so is a multiple of 8)
+                    cur = nxt[k];
+                }
+                sa = sa + 8 >= R ? sa + 8 - R : sa + 8;
+                sf = sf + 8 >= R ? sf + 8 - R : sf + 8;
+                so = so + 8 >= R ? so + 8 - R : so + 8;
+                done += 8;
             }
-            so = so + 8 == R ? 0u : so + 8;
-            sa = sa + 8 == R ? 0u : sa + 8;
-            sf = sf + 8 >= R ? sf + 8 - R : sf + 8;
         }
         a += batch;
         publish(head_flag, a, lane);
@@ -485,12 +720,41 @@ __device__ void producer_run(const DevBatch& b, const DevStrandGraph& g, uint32_
 
 // Persistent grid of independent warps.  Work items of a round: for each of `tiles_per_round` tiles
 // its S strands and its producer; every item of a round is resident at once (the launcher sizes the
-// rounds), so the waits above always end.
-template <int EXP, bool WAIT>
+// rounds), so the waits above always end.  Dynamic shared memory: kWarpSmem bytes per warp (landing
+// stages, scratch), then — for single-model batches — a copy of the layer graph, which every strand
+// of the CTA reads (b.strand_graph_smem bytes; otherwise the tables are read from global memory).
+template <int EXP, bool WAIT, bool RED>
 __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(DevBatch b, uint32_t sweeps,
                                                                                  uint32_t tiles_per_round) {
-    __shared__ float scratch_all[kStrandMaxWarps][8][32];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    extern __shared__ __align__(16) unsigned char strand_smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, warps = blockDim.x >> 5;
+    unsigned char* warp_smem = strand_smem + size_t(warp) * kWarpSmem;
+    DevStrandGraph staged{};
+    const bool use_staged = b.strand_graph_smem != 0u;
+    if (use_staged) {
+        const DevStrandGraph g0 = b.strand_graphs[0];
+        const uint32_t P = g0.per_layer;
+        uint4* pos = reinterpret_cast<uint4*>(strand_smem + size_t(warps) * kWarpSmem);
+        uint4* band = pos + P;
+        uint4* chunks = band + 2 * size_t(P);
+        uint4* tau = chunks + P / 8;
+        uint4* edges = tau + P / 4;
+        uint32_t* groups = reinterpret_cast<uint32_t*>(edges + g0.n_edges);
+        for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) pos[k] = g0.pos[k];
+        for (uint32_t k = threadIdx.x; k < 2 * P; k += blockDim.x) band[k] = g0.band_pm[k];
+        for (uint32_t k = threadIdx.x; k < P / 8; k += blockDim.x) chunks[k] = g0.chunks[k];
+        for (uint32_t k = threadIdx.x; k < P / 4; k += blockDim.x) tau[k] = g0.tau[k];
+        for (uint32_t k = threadIdx.x; k < g0.n_edges; k += blockDim.x) edges[k] = g0.edges[k];
+        for (uint32_t k = threadIdx.x; k < g0.n_groups; k += blockDim.x) groups[k] = g0.groups[k];
+        staged = g0;
+        staged.pos = pos;
+        staged.band_pm = band;
+        staged.chunks = chunks;
+        staged.tau = tau;
+        staged.edges = edges;
+        staged.groups = groups;
+        __syncthreads();
+    }
     const uint32_t item = warp * gridDim.x + blockIdx.x;
     const uint32_t S = b.strands;
     for (uint32_t base = 0; base < b.n_tiles; base += tiles_per_round) {
@@ -498,9 +762,9 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
         if (item >= tiles * (S + 1)) continue;
         // consecutive items are the same role of consecutive tiles: an SM hosts a mix of tiles
         const uint32_t role = item / tiles, tile = base + item - role * tiles;
-        const DevStrandGraph& g = b.strand_graphs[b.tile_model[tile]];
+        const DevStrandGraph g = use_staged ? staged : b.strand_graphs[b.tile_model[tile]];
         if (role == S) producer_run(b, g, tile, sweeps, lane);
-        else strand_run<EXP, WAIT>(b, g, tile, role, sweeps, lane, &scratch_all[warp][0][lane]);
+        else strand_run<EXP, WAIT, RED>(b, g, tile, role, sweeps, lane, warp_smem);
     }
 }
 
@@ -539,7 +803,43 @@ __global__ void __launch_bounds__(256) bytes_to_words_kernel(DevBatch b) {
 }  // namespace
 
 uint32_t strand_max_warps() { return kStrandMaxWarps; }
+uint32_t strand_warp_smem() { return kWarpSmem; }
 uint32_t strand_flag_words(uint32_t n_tiles, uint32_t strands) { return n_tiles * (strands + 1) * kFlagStride; }
+// Shared-memory bytes of a staged layer graph (see sweep_strand_kernel).
+size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges, uint32_t n_groups) {
+    return (size_t(per_layer) * 3 + per_layer / 8 + per_layer / 4 + n_edges) * sizeof(uint4) +
+           size_t(n_groups) * sizeof(uint32_t);
+}
+
+namespace {
+template <int EXP, bool WAIT, bool RED>
+cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t smem, uint32_t round,
+                                  cudaStream_t stream) {
+    // the attribute is per function and context: always the opt-in maximum, never one batch's own need
+    static bool prepared = false;
+    if (!prepared) {
+        const cudaError_t e = cudaFuncSetAttribute(sweep_strand_kernel<EXP, WAIT, RED>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        prepared = true;
+    }
+    sweep_strand_kernel<EXP, WAIT, RED><<<grid, block, smem, stream>>>(b, sweeps, round);
+    return cudaGetLastError();
+}
+template <int EXP>
+cudaError_t launch_strand_exp(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t smem, uint32_t round,
+                              cudaStream_t stream) {
+    // separate instantiations: the default kernel carries no wait statistics; reductions need every
+    // model to be reduction-safe (no subnormal field possible)
+    const bool wait = b.wait_counts != nullptr, red = b.generic_reduce != 0u;
+    if (wait) {
+        return red ? launch_strand_variant<EXP, true, true>(b, sweeps, grid, block, smem, round, stream)
+                   : launch_strand_variant<EXP, true, false>(b, sweeps, grid, block, smem, round, stream);
+    }
+    return red ? launch_strand_variant<EXP, false, true>(b, sweeps, grid, block, smem, round, stream)
+               : launch_strand_variant<EXP, false, false>(b, sweeps, grid, block, smem, round, stream);
+}
+}  // namespace
 
 cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count, uint32_t warps_per_cta,
                                 cudaStream_t stream) {
@@ -559,17 +859,13 @@ cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count
     const dim3 grid(ctas), block(warps_per_cta * 32);
     // items are dealt warp-major over the launched CTAs: recompute the round size for this grid
     const uint32_t round = min(b.n_tiles, ctas * warps_per_cta / per_tile);
-    // the wait-statistics variant is a separate instantiation: the default kernel carries none of it
-    const bool wait = b.wait_counts != nullptr;
-#define ISING_LAUNCH_STRAND(EXP)                                                              \
-    if (wait) sweep_strand_kernel<EXP, true><<<grid, block, 0, stream>>>(b, sweeps, round);   \
-    else sweep_strand_kernel<EXP, false><<<grid, block, 0, stream>>>(b, sweeps, round);
+    const size_t smem = size_t(warps_per_cta) * kWarpSmem + b.strand_graph_smem;
     switch (b.exp_kind) {
-        case kExpExact: ISING_LAUNCH_STRAND(kExpExact) break;
-        case kExpFast: ISING_LAUNCH_STRAND(kExpFast) break;
-        default: ISING_LAUNCH_STRAND(kExpAccurate) break;
+        case kExpExact: e = launch_strand_exp<kExpExact>(b, sweeps, grid, block, smem, round, stream); break;
+        case kExpFast: e = launch_strand_exp<kExpFast>(b, sweeps, grid, block, smem, round, stream); break;
+        default: e = launch_strand_exp<kExpAccurate>(b, sweeps, grid, block, smem, round, stream); break;
     }
-#undef ISING_LAUNCH_STRAND
+    if (e != cudaSuccess) return e;
     bytes_to_words_kernel<<<convert_blocks, 256, 0, stream>>>(b);
     return cudaGetLastError();
 }

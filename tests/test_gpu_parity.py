@@ -342,6 +342,8 @@ def test_layered_chord_graphs_every_edge_class(lib, port, positions, layers, off
     sweeps = 12 if positions < 512 else 6
     out = {}
     for kernel in LAYERED_KERNELS:
+        if kernel == ib.KERNEL_STRAND and positions < 16:
+            continue  # the strand family wants two chunks of 8 positions at least
         state, want = run_both(port, [csr], ladders, betas, sweeps, 3, tau_scale=1.25, exp_kind=exp_kind,
                                kernel=kernel, chunks=[sweeps // 2, sweeps - sweeps // 2])
         assert state.info()["kernel"] == kernel
@@ -350,9 +352,10 @@ def test_layered_chord_graphs_every_edge_class(lib, port, positions, layers, off
             hs, ht = state.fields(c)
             out.setdefault(c, []).append((hs.copy(), ht.copy()))
         state.close()
-    for c, (a, b) in out.items():  # both families leave identical fields behind, bit for bit
-        np.testing.assert_array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
-        np.testing.assert_array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+    for c, per_family in out.items():  # all families leave identical fields behind, bit for bit
+        for other in per_family[1:]:
+            np.testing.assert_array_equal(per_family[0][0].view(np.uint32), other[0].view(np.uint32))
+            np.testing.assert_array_equal(per_family[0][1].view(np.uint32), other[1].view(np.uint32))
 
 
 @pytest.mark.parametrize("kernel", LAYERED_KERNELS)
