@@ -217,7 +217,7 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
         }
         for (uint32_t k = 0; k < 8; ++k) {
             out.pos[p0 + k].y = uint32_t(out.edges.size()) | uint32_t(near_of[k].size()) << 16;
-            for (const Edge& e : near_of[k]) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 31u - e.k));
+            for (const Edge& e : near_of[k]) out.edges.push_back(make_uint4(e.t, e.k, e.j2, (31u - e.k) | (e.t * 128u) << 8));
         }
         // groups of up to 8 edges with distinct targets, edges in attempt order (so that a column's
         // updates keep the reference's order across and inside groups)
@@ -226,7 +226,7 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
         const auto close = [&]() {
             if (cur.empty()) return;
             out.groups.push_back(uint32_t(out.edges.size()) | uint32_t(cur.size()) << 16);
-            for (const Edge& e : cur) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 31u - e.k));
+            for (const Edge& e : cur) out.edges.push_back(make_uint4(e.t, e.k, e.j2, (31u - e.k) | (e.t * 128u) << 8));
             cur.clear();
         };
         for (const Edge& e : grouped) {

@@ -93,7 +93,7 @@ struct DevStrandGraph {
     const uint4* chunks;     // per chunk: {groups begin | count << 16, group edges begin | count << 16,
                              //             flags (1 careful, 2 updates columns the next chunk loads), 0}
     const uint32_t* groups;  // up to 8 edges with distinct targets, in attempt order: edge begin | count << 16
-    const uint4* edges;      // {target position, attempt index k in its chunk, bits of 2J, 31 - k}
+    const uint4* edges;      // {target position, attempt index k in its chunk, bits of 2J, (31 - k) | target * 128 << 8}
     uint32_t n_groups;
     uint32_t n_edges;
 };

@@ -119,6 +119,15 @@ __device__ __forceinline__ void publish(uint32_t* p, uint32_t value, uint32_t la
     __syncwarp();
     if (lane == 0) st_release(p, value);
 }
+// A strand's progress line: word 0 its finished chunks (what the strand of the next layer waits on),
+// word 1 the draw index it will need next (what the producer may not overwrite yet; 0xffffffff: done).
+__device__ __forceinline__ void publish_strand(uint32_t* line, uint32_t chunks, uint32_t next_draw, uint32_t lane) {
+    __syncwarp();
+    if (lane == 0) {
+        st_u32(line + 1, next_draw);
+        st_release(line, chunks);
+    }
+}
 
 // ---- bulk (TMA) copies into a warp's landing buffers, completion on an mbarrier ------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -224,26 +233,30 @@ __device__ __forceinline__ float edge_addend(const uint4 e, uint32_t cur8) {
 //
 // RED: h[t] -= (2s)*J goes out as a global f32 reduction of -(2s)*J — it rounds exactly like the
 // subtraction, reductions and loads of one thread to one address keep program order, and nothing
-// comes back, so the chunk pays no round trip.  Every lane takes part (a lane that did not accept
-// adds -0.0, the identity for every bit pattern): one full 128-byte reduction per edge.  Global f32
+// comes back, so the chunk pays no round trip.  Global f32
 // reductions flush subnormals (REDG.ADD.F32.FTZ.RN), so this path is only used when no field can be
 // subnormal (DevModel::reduction_safe for every model of the batch).
-__device__ __forceinline__ void reduce_field(float* p, float addend) {
-    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(addend) : "memory");
-}
 __device__ __forceinline__ void apply_edges_red(float* hs_l, const uint4* edges, uint32_t einfo, uint32_t acc8,
                                                 uint32_t cur8) {
     const uint4* fe = edges + (einfo & 0xffffu);
     const uint32_t n = einfo >> 16;
     // bit k of `flip`: the addend of attempt k's edges is -2J (s = +1); of `acc8`: this lane accepted it
     const uint32_t flip = ~cur8;
-#pragma unroll 4
+    unsigned char* base = reinterpret_cast<unsigned char*>(hs_l);
+#pragma unroll 2
     for (uint32_t i = 0; i < n; ++i) {
-        const uint4 e = fe[i];  // {target position, attempt, bits of 2J, 31 - attempt}
-        const uint32_t addend = e.z ^ ((flip << e.w) & 0x80000000u);
-        // every lane takes part, a lane that did not accept adds -0.0 (reductions of accepting lanes
-        // only were measured slower: 1180 against 890 cycles per chunk)
-        reduce_field(hs_l + size_t(e.x) * 32, __uint_as_float(int32_t(acc8 << e.w) < 0 ? addend : 0x80000000u));
+        const uint4 e = fe[i];  // {target position, attempt, bits of 2J, (31 - attempt) | target byte offset << 8}
+        const uint32_t addend = e.z ^ (__funnelshift_l(0u, flip, e.w) & 0x80000000u);  // (the shift wraps at 32)
+        // only the lanes that accepted take part: with 18 warps per SM the load/store unit is the limit
+        // of full 32-lane reductions (~40 cycles each), and its cost follows the active lanes (c5: +4 %)
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.lt.s32 p, %2, 0;\n"
+            "@p red.global.add.f32 [%0], %1;\n"
+            "}\n" ::"l"(base + (e.w >> 8)),
+            "f"(__uint_as_float(addend)), "r"(int32_t(__funnelshift_l(0u, acc8, e.w)))
+            : "memory");
     }
 }
 // Otherwise: read-modify-writes in groups of up to 8 edges with distinct targets (loads together,
@@ -340,21 +353,11 @@ __device__ __noinline__ CarefulResult careful_chunk(Window w, RawWords raw, Chun
 }
 
 // ---- a strand ---------------------------------------------------------------------------------
-// Per-warp shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB and
-// the three spin-byte rows of a chunk), their mbarriers, and the scratch of the careful chunks.
-constexpr uint32_t kStageBytes = 1024 + 128;
+// Per-warp shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB),
+// their mbarriers, and the scratch of the careful chunks.
+constexpr uint32_t kStageBytes = 1024;
 constexpr uint32_t kWarpSmem = 2 * kStageBytes + 16 + 1024;
 
-__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
 
 // Everything a chunk reads from global memory is requested one chunk ahead: the tape rows and the
 // spin bytes by bulk (TMA) copies of one elected lane into the warp's landing stage (no registers
@@ -374,9 +377,9 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
     const uint32_t nb2 = __float_as_uint(active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
     const float u_offset = active ? 0.0f : 2.0f;
     float* hs_tile = b.hs + size_t(tile) * n * 32 + lane;
-    uint8_t* bytes_tile = b.spin_bytes + size_t(tile) * (n / 8) * 32;  // (no lane offset: rows are copied whole)
+    uint8_t* bytes_tile = b.spin_bytes + size_t(tile) * (n / 8) * 32 + lane;
     const uint32_t R = b.tape_rows;
-    const uint32_t* tape = b.tape + size_t(tile) * R * 32;             // (likewise)
+    const uint32_t* tape = b.tape + size_t(tile) * R * 32;  // (no lane offset: rows are copied whole)
     uint32_t* flags = b.strand_flags + size_t(tile) * (S + 1) * kFlagStride;
     uint32_t* my_flag = flags + j * kFlagStride;
     const uint32_t* pred_flag = flags + ((j + S - 1) % S) * kFlagStride;
@@ -400,24 +403,18 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
     const bool record_wait = WAIT && b.wait_counts != nullptr && b.tile_count[tile] == 32;
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
 
-    // one elected lane requests a chunk's tape rows and spin bytes into stage `st`
-    const auto request = [&](uint32_t st, uint32_t slot, const uint8_t* cur, const uint8_t* up, const uint8_t* dn) {
+    // one elected lane requests a chunk's tape rows into stage `st`
+    const auto request = [&](uint32_t st, uint32_t slot) {
         if (lane == 0) {
             const uint32_t dst = wsm + st * kStageBytes, bar = bar0 + st * 8;
-            // the rows were written through the generic proxy (by other warps, acquired above): order
-            // the async-proxy reads after what this lane has observed
+            // the rows were written through the generic proxy (by the producer, acquired above): order
+            // the async-proxy read after what this lane has observed
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            mbar_expect(bar, 1024 + 96);
+            mbar_expect(bar, 1024);
             bulk_load(dst, tape + size_t(slot) * 32, 1024, bar);
-            bulk_load(dst + 1024, cur, 32, bar);
-            bulk_load(dst + 1056, up, 32, bar);
-            bulk_load(dst + 1088, dn, 32, bar);
         }
     };
 
-#ifdef ISING_STRAND_PROFILE
-    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0;
-#endif
     for (uint32_t blk = 0; blk < total_blocks; ++blk) {
         const uint32_t sw = blk / blocks_per_sweep, m = blk - sw * blocks_per_sweep;
         const uint32_t l = j + S * m;
@@ -446,9 +443,8 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
 
         // ---- the first chunk's operands (the only exposed round trip of the block)
         wait_counter(head_flag, head_need, head_cached);
-        if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
         __syncwarp();  // every lane has left the stage's previous contents
-        request(stage, slot, cur_c, up_c, dn_c);
+        request(stage, slot);
         // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
         Window w;
         float (&r)[8] = w.r;
@@ -457,9 +453,6 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
         r[0] = ld_cg_f32(hs_c);
         r[1] = ld_cg_f32(hs_c + 32);
         r[2] = ld_cg_f32(hs_c + 64);
-        float nx[8];  // the columns entering the window during the chunk: p0+3 .. p0+10
-#pragma unroll
-        for (int k = 0; k < 8; ++k) nx[k] = ld_cg_f32(hs_c + (3 + k) * 32);  // (a layer has 16 positions at least)
 
         for (uint32_t c = 0; c < C; ++c) {
 #ifdef ISING_STRAND_PROFILE
@@ -467,38 +460,39 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
 #endif
             const uint4 chunk_info = *chunk_c;
             const bool more = c + 1 < C;
-            const bool late_columns = (chunk_info.z & 2u) != 0u;  // this chunk updates columns the next one loads
-            // ---- requests for the next chunk
-            float nx_next[8];
+            // ---- the columns entering the window during this chunk, p0+3 .. p0+10 (the last chunk has five):
+            // requested after every update the chunks before could send them, L2 hits (prefetched below)
+            float nx[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) nx[k] = (k < 5 || more) ? ld_cg_f32(hs_c + (3 + k) * 32) : 0.0f;
+            // ... and its spin bytes: the layer below must have finished the chunk
+            if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
+            ChunkBits cb;
+            cb.cur8 = ld_cg_u8(cur_c);
+            cb.up8 = ld_cg_u8(up_c);
+            cb.dn8 = ld_cg_u8(dn_c);
+            // ---- the next chunk's tape rows, by bulk copy
             if (more) {
                 slot = slot + 8 == R ? 0u : slot + 8;
                 head_need += 8;
                 ++pred_need;
                 wait_counter(head_flag, head_need, head_cached);
-                if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
                 __syncwarp();  // every lane has left the other stage's previous contents
-                request(stage ^ 1u, slot, cur_c + 32, up_c + 32, dn_c + 32);
-                if (!late_columns) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) nx_next[k] = (k < 5 || c + 2 < C) ? ld_cg_f32(hs_c + (11 + k) * 32) : 0.0f;
-                }
+                request(stage ^ 1u, slot);
                 // the columns three chunks ahead, into L2
                 if (lane < 8 && c + 4 < C) prefetch_l2(hs_c + (27 + lane) * 32);
             }
             // ---- this chunk's tape words and spin bytes have landed
-            const uint32_t st_addr = wsm + stage * kStageBytes;
             ISING_TICK(tA);
             mbar_wait(bar0 + stage * 8, (phases >> stage) & 1u);
             ISING_TICK(tB);
             phases ^= 1u << stage;
+            // (plain loads: the compiler may put each one next to its use; the wait above keeps them behind it)
+            const uint32_t* landed = reinterpret_cast<const uint32_t*>(warp_smem + stage * kStageBytes) + lane;
             RawWords raw_words;
             uint32_t (&raw)[8] = raw_words.v;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) raw[k] = lds_u32(st_addr + k * 128 + lane * 4);
-            ChunkBits cb;
-            cb.cur8 = lds_u8(st_addr + 1024 + lane);
-            cb.up8 = lds_u8(st_addr + 1056 + lane);
-            cb.dn8 = lds_u8(st_addr + 1088 + lane);
+            for (int k = 0; k < 8; ++k) raw[k] = landed[k * 32];
             cb.finish();
 
             // ---- eight attempts
@@ -537,7 +531,7 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
 
             // ---- after the chunk: spins, far neighbours, progress
             ISING_TICK(tC);
-            st_u8(cur_c + lane, cb.cur8 ^ acc8);
+            st_u8(cur_c, cb.cur8 ^ acc8);
             flips += __popc(acc8);
             if (WAIT && record_wait) {
 #pragma unroll
@@ -553,12 +547,6 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
             ++seq;
             ISING_TICK(tD);
             if (more) {
-                if (late_columns) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) nx_next[k] = (k < 5 || c + 2 < C) ? ld_cg_f32(hs_c + (11 + k) * 32) : 0.0f;
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) nx[k] = nx_next[k];
                 stage ^= 1u;
                 hs_c += 8 * 32;
                 cur_c += 32;
@@ -568,7 +556,7 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
                 pos_c += 8;
                 band_c += 16;
                 tau_c += 2;
-                if (seq % pub == 0u) publish(my_flag, seq, lane);
+                if (seq % pub == 0u) publish_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
             }
             ISING_TICK(tE);
         }
@@ -587,7 +575,7 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
             const double e = ld_cg_f64(e_run);
             asm volatile("st.global.f64 [%0], %1;" ::"l"(e_run), "d"(__dadd_rn(e, e_blk)) : "memory");
         }
-        publish(my_flag, seq, lane);
+        publish_strand(my_flag, seq, blk + 1 == total_blocks ? 0xffffffffu : row0 - kMtN + P, lane);
         ISING_TICK(tF);
         if (WAIT && record_wait) {  // flushed per layer (lanes 0..7 hold partial sums of at most 64 * 32 each)
             unsigned long long* out = b.wait_counts + size_t(tile) * kWaitSlots;
@@ -608,31 +596,19 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
 }
 
 // ---- the producer -------------------------------------------------------------------------------
-// Stream position of strand `s` after `seq` finished chunks: the draw index of its next attempt
-// (0xffffffff when it has finished).
-__device__ __forceinline__ uint32_t strand_draw_index(uint32_t seq, uint32_t s, uint32_t S, uint32_t C, uint32_t L,
-                                                      uint32_t P, uint32_t total_blocks) {
-    const uint32_t blocks_per_sweep = L / S;
-    const uint32_t blk = seq / C, c = seq - blk * C;
-    if (blk >= total_blocks) return 0xffffffffu;
-    const uint32_t sw = blk / blocks_per_sweep, m = blk - sw * blocks_per_sweep;
-    return (sw * L + s + S * m) * P + c * 8;
-}
-
 // MT19937 as a tape: row a of the ring holds word x[a] of all 32 chains, x[0..623] being the state
 // at launch in draw order, and draw q of the launch is temper(x[624 + q]).  Rows are generated in
 // order, 32 at a time, never overwriting a row a strand has yet to read or the 624 rows behind the
 // head; the head is published after every batch.  At the end the last 624 rows go back to the
 // in-place state array the other kernel families use.
 __device__ void producer_run(const DevBatch& b, const DevStrandGraph& g, uint32_t tile, uint32_t sweeps, uint32_t lane) {
-    const uint32_t P = g.per_layer, L = g.layers, C = P / 8, S = b.strands, R = b.tape_rows;
+    const uint32_t S = b.strands, R = b.tape_rows;
     uint32_t* tape = b.tape + size_t(tile) * R * 32 + lane;
     uint32_t* state = b.mt + size_t(tile) * kMtN * 32 + lane;
     uint32_t* flags = b.strand_flags + size_t(tile) * (S + 1) * kFlagStride;
     uint32_t* head_flag = flags + S * kFlagStride;
     const uint32_t pos = b.mt_pos[tile];
     const uint32_t total = sweeps * b.n_spins;  // draws of this launch (a multiple of 8)
-    const uint32_t total_blocks = (L / S) * sweeps;
 
     for (uint32_t i = 0; i < kMtN; ++i) {
         uint32_t w = pos + i;
@@ -652,13 +628,12 @@ __device__ void producer_run(const DevBatch& b, const DevStrandGraph& g, uint32_
         const uint32_t batch = min(64u, end - a);  // (a multiple of 8)
         // rows a .. a+batch-1 overwrite rows a-R .. : they must be consumed draws (row < 624 + tail)
         while (int32_t(a + batch - R - kMtN - tail) > 0) {
-            uint32_t d = 0xffffffffu;
-            // (relaxed: a strand's count is published after its last read of the rows it stands for, and
+            // (relaxed: a strand's draw index is published after its last read of the rows before it, and
             // the rows written next are published with a release of their own)
-            if (lane < S) d = strand_draw_index(ld_relaxed(flags + lane * kFlagStride), lane, S, C, L, P, total_blocks);
+            uint32_t d = lane < S ? ld_relaxed(flags + lane * kFlagStride + 1) : 0xffffffffu;
             d = __reduce_min_sync(0xffffffffu, d);
             if (d == 0xffffffffu) d = total;
-            if (d == tail) __nanosleep(2000);
+            if (d == tail) __nanosleep(8000);  // (normally far ahead of the strands: the ring is full)
             tail = d;
         }
         for (uint32_t done = 0; done < batch;) {
