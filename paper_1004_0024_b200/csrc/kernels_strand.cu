@@ -192,12 +192,53 @@ __device__ __forceinline__ void prepare_chunk(Prepared& pr, const uint32_t (&raw
         pr.hz[k] = __uint_as_float((tau_g[k] ^ sgn_up) & agree);
     }
 }
-// The band_pm entry of attempt K's flip: the pair's first entry is for s = -1, the second (16 bytes
-// on) for s = +1.
-template <int K>
-__device__ __forceinline__ uint4 band_entry(const uint4* pair0, uint32_t cur8) {
+// The layer graph's tables (DevStrandGraph), read either from the CTA's staged copy in shared
+// memory (STAGED: explicit ld.shared on 32-bit addresses — generic loads that resolve to shared
+// memory cost several times the latency) or from global memory through the read-only cache.
+template <bool STAGED>
+struct Tables;
+template <>
+struct Tables<false> {
+    const uint4 *chunks, *pos, *band, *tau, *edges;
+    const uint32_t* groups;
+    __device__ __forceinline__ uint4 chunk(uint32_t c) const { return __ldg(chunks + c); }
+    __device__ __forceinline__ uint4 tau4(uint32_t i) const { return __ldg(tau + i); }
+    __device__ __forceinline__ uint4 posrec(uint32_t p) const { return __ldg(pos + p); }
+    __device__ __forceinline__ uint4 edge(uint32_t i) const { return __ldg(edges + i); }
+    __device__ __forceinline__ uint32_t group(uint32_t i) const { return __ldg(groups + i); }
+    __device__ __forceinline__ uint4 band_at(uint32_t p, uint32_t byte_off) const {
+        return __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(band + 2 * size_t(p)) + byte_off));
+    }
+};
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 v;
+    // not volatile: the tables are constant while the kernel runs
+    asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_b32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+template <>
+struct Tables<true> {
+    uint32_t chunks, pos, band, tau, edges, groups;  // shared-window addresses
+    __device__ __forceinline__ uint4 chunk(uint32_t c) const { return lds_v4(chunks + c * 16); }
+    __device__ __forceinline__ uint4 tau4(uint32_t i) const { return lds_v4(tau + i * 16); }
+    __device__ __forceinline__ uint4 posrec(uint32_t p) const { return lds_v4(pos + p * 16); }
+    __device__ __forceinline__ uint4 edge(uint32_t i) const { return lds_v4(edges + i * 16); }
+    __device__ __forceinline__ uint32_t group(uint32_t i) const { return lds_b32(groups + i * 4); }
+    __device__ __forceinline__ uint4 band_at(uint32_t p, uint32_t byte_off) const {
+        return lds_v4(band + p * 32 + byte_off);
+    }
+};
+// The band_pm entry of the flip of position p, attempt K of its chunk: the pair's first entry is for
+// s = -1, the second (16 bytes on) for s = +1.
+template <int K, bool STAGED>
+__device__ __forceinline__ uint4 band_entry(const Tables<STAGED>& t, uint32_t p, uint32_t cur8) {
     const uint32_t off = ((K <= 4 ? cur8 << (4 - K) : cur8 >> (K - 4)) & 16u) ^ 16u;
-    return *reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(pair0 + 2 * K) + off);
+    return t.band_at(p, off);
 }
 
 // Attempt K (compile-time index in the unrolled chunk; the register window r[] is indexed by
@@ -236,16 +277,17 @@ __device__ __forceinline__ float edge_addend(const uint4 e, uint32_t cur8) {
 // comes back, so the chunk pays no round trip.  Global f32
 // reductions flush subnormals (REDG.ADD.F32.FTZ.RN), so this path is only used when no field can be
 // subnormal (DevModel::reduction_safe for every model of the batch).
-__device__ __forceinline__ void apply_edges_red(float* hs_l, const uint4* edges, uint32_t einfo, uint32_t acc8,
+template <bool STAGED>
+__device__ __forceinline__ void apply_edges_red(float* hs_l, const Tables<STAGED>& t, uint32_t einfo, uint32_t acc8,
                                                 uint32_t cur8) {
-    const uint4* fe = edges + (einfo & 0xffffu);
+    const uint32_t first = einfo & 0xffffu;
     const uint32_t n = einfo >> 16;
     // bit k of `flip`: the addend of attempt k's edges is -2J (s = +1); of `acc8`: this lane accepted it
     const uint32_t flip = ~cur8;
     unsigned char* base = reinterpret_cast<unsigned char*>(hs_l);
 #pragma unroll 2
     for (uint32_t i = 0; i < n; ++i) {
-        const uint4 e = fe[i];  // {target position, attempt, bits of 2J, (31 - attempt) | target byte offset << 8}
+        const uint4 e = t.edge(first + i);  // {target position, attempt, bits of 2J, (31 - attempt) | target byte offset << 8}
         const uint32_t addend = e.z ^ (__funnelshift_l(0u, flip, e.w) & 0x80000000u);  // (the shift wraps at 32)
         // only the lanes that accepted take part: with 18 warps per SM the load/store unit is the limit
         // of full 32-lane reductions (~40 cycles each), and its cost follows the active lanes (c5: +4 %)
@@ -261,20 +303,21 @@ __device__ __forceinline__ void apply_edges_red(float* hs_l, const uint4* edges,
 }
 // Otherwise: read-modify-writes in groups of up to 8 edges with distinct targets (loads together,
 // then adds and stores).
-__device__ __noinline__ void apply_groups_rmw(float* hs_l, const uint32_t* groups, const uint4* edges, uint32_t ginfo,
-                                              uint32_t acc8, uint32_t cur8) {
-    const uint32_t* grp = groups + (ginfo & 0xffffu);
+template <bool STAGED>
+__device__ __noinline__ void apply_groups_rmw(float* hs_l, const Tables<STAGED> t, uint32_t ginfo, uint32_t acc8,
+                                              uint32_t cur8) {
+    const uint32_t first_group = ginfo & 0xffffu;
     const uint32_t n_groups = ginfo >> 16;
 #pragma unroll 1
     for (uint32_t q = 0; q < n_groups; ++q) {
-        const uint32_t info = grp[q];
-        const uint4* fe = edges + (info & 0xffffu);
+        const uint32_t info = t.group(first_group + q);
+        const uint32_t first = info & 0xffffu;
         const uint32_t n = info >> 16;
         uint4 e[8];
         float v[8];
 #pragma unroll
         for (uint32_t i = 0; i < 8; ++i) {
-            if (i < n) e[i] = fe[i];
+            if (i < n) e[i] = t.edge(first + i);
         }
 #pragma unroll
         for (uint32_t i = 0; i < 8; ++i) {
@@ -306,35 +349,33 @@ struct CarefulResult {
     double e_blk;
 };
 
-template <int EXP, int K>
+template <int EXP, int K, bool STAGED>
 __device__ __forceinline__ void careful_attempt(float (&r)[8], float* scratch, const Prepared& pr, uint32_t nb2,
-                                                uint32_t cur8, const uint4 posrec, const uint4* band, uint32_t& acc8,
-                                                double& e_blk, const uint4* edges, uint32_t p0) {
+                                                uint32_t cur8, const Tables<STAGED>& t, uint32_t& acc8, double& e_blk,
+                                                uint32_t p0) {
     const uint32_t before = acc8;
-    strand_attempt<EXP, K>(r, pr, nb2, band_entry<K>(band, cur8), acc8, e_blk);
-    const uint32_t near = posrec.y;
+    strand_attempt<EXP, K>(r, pr, nb2, band_entry<K>(t, p0 + K, cur8), acc8, e_blk);
+    const uint32_t near = t.posrec(p0 + K).y;
     if ((near >> 16) != 0u && acc8 != before) {
-        const uint4* ne = edges + (near & 0xffffu);
         for (uint32_t i = 0; i < (near >> 16); ++i) {
-            const uint4 e = ne[i];
+            const uint4 e = t.edge((near & 0xffffu) + i);
             float* cell = scratch + (e.x - (p0 + 3)) * 32;
             *cell = __fadd_rn(*cell, edge_addend(e, cur8));
         }
     }
 }
 
-template <int EXP>
+template <int EXP, bool STAGED>
 __device__ __noinline__ CarefulResult careful_chunk(Window w, RawWords raw, ChunkBits cb, uint32_t nb2, float u_offset,
-                                                    const uint4* pos, const uint4* band, const uint4* tau,
-                                                    const uint4* edges, uint32_t p0, float* hs_l, float* scratch,
+                                                    const Tables<STAGED> t, uint32_t p0, float* hs_l, float* scratch,
                                                     double e_blk) {
     float (&r)[8] = w.r;
     uint32_t acc8 = 0;
     Prepared pr;
-    prepare_chunk(pr, raw.v, cb, nb2, u_offset, tau[0], tau[1]);
-#define ISING_CAREFUL(K)                                                                                   \
-    careful_attempt<EXP, K>(r, scratch, pr, nb2, cb.cur8, pos[K], band, acc8, e_blk, edges, p0);            \
-    if (p0 != 0 || K >= 2) st_f32(hs_l + (size_t(p0) + K - 2) * 32, r[(K + 6) & 7]);                        \
+    prepare_chunk(pr, raw.v, cb, nb2, u_offset, t.tau4(p0 / 4), t.tau4(p0 / 4 + 1));
+#define ISING_CAREFUL(K)                                                                  \
+    careful_attempt<EXP, K>(r, scratch, pr, nb2, cb.cur8, t, acc8, e_blk, p0);             \
+    if (p0 != 0 || K >= 2) st_f32(hs_l + (size_t(p0) + K - 2) * 32, r[(K + 6) & 7]);       \
     r[(K + 3) & 7] = scratch[K * 32];
     ISING_CAREFUL(0)
     ISING_CAREFUL(1)
@@ -366,10 +407,10 @@ constexpr uint32_t kWarpSmem = 2 * kStageBytes + 16 + 1024;
 // chunks ahead are prefetched into L2.  So the loop-carried chain of the attempts is all a strand
 // waits for.  The one exception: when a far edge of chunk c targets the columns chunk c+1 loads
 // (chunk flag 2), those are requested after chunk c's updates.
-template <int EXP, bool WAIT, bool RED>
-__device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t tile, uint32_t j, uint32_t sweeps,
-                           uint32_t lane, unsigned char* warp_smem) {
-    const uint32_t P = g.per_layer, L = g.layers, C = P / 8, S = b.strands, n = b.n_spins;
+template <int EXP, bool WAIT, bool RED, bool STAGED>
+__device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t P, uint32_t L, uint32_t tile, uint32_t j,
+                           uint32_t sweeps, uint32_t lane, unsigned char* warp_smem) {
+    const uint32_t C = P / 8, S = b.strands, n = b.n_spins;
     const uint32_t blocks_per_sweep = L / S;
     const uint32_t total_blocks = blocks_per_sweep * sweeps;
     const uint32_t chain = b.tile_first[tile] + lane;
@@ -415,6 +456,9 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
         }
     };
 
+#ifdef ISING_STRAND_PROFILE
+    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0;
+#endif
     for (uint32_t blk = 0; blk < total_blocks; ++blk) {
         const uint32_t sw = blk / blocks_per_sweep, m = blk - sw * blocks_per_sweep;
         const uint32_t l = j + S * m;
@@ -436,10 +480,6 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
         uint8_t* cur_c = bytes_tile + size_t(l) * C * 32;
         const uint8_t* up_c = bytes_tile + size_t(l_up) * C * 32;
         const uint8_t* dn_c = bytes_tile + size_t(l_dn) * C * 32;
-        const uint4* chunk_c = g.chunks;
-        const uint4* pos_c = g.pos;
-        const uint4* band_c = g.band_pm;
-        const uint4* tau_c = g.tau;
 
         // ---- the first chunk's operands (the only exposed round trip of the block)
         wait_counter(head_flag, head_need, head_cached);
@@ -458,7 +498,8 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
 #ifdef ISING_STRAND_PROFILE
             t0 = clock64();
 #endif
-            const uint4 chunk_info = *chunk_c;
+            const uint32_t p0 = c * 8;
+            const uint4 chunk_info = t.chunk(c);
             const bool more = c + 1 < C;
             // ---- the columns entering the window during this chunk, p0+3 .. p0+10 (the last chunk has five):
             // requested after every update the chunks before could send them, L2 hits (prefetched below)
@@ -499,12 +540,12 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
             uint32_t acc8 = 0;
             if (__builtin_expect((chunk_info.z & 1u) == 0u, 1)) {
                 Prepared pr;
-                prepare_chunk(pr, raw, cb, nb2, u_offset, tau_c[0], tau_c[1]);
+                prepare_chunk(pr, raw, cb, nb2, u_offset, t.tau4(2 * c), t.tau4(2 * c + 1));
                 // the band entry of an attempt is requested during the attempt before it
-                uint4 op = band_entry<0>(band_c, cb.cur8);
+                uint4 op = band_entry<0>(t, p0, cb.cur8);
 #define ISING_STRAND_ATTEMPT(K, NEXT)                                                \
     {                                                                                \
-        const uint4 op_next = band_entry<NEXT>(band_c, cb.cur8);                     \
+        const uint4 op_next = band_entry<NEXT>(t, p0 + NEXT, cb.cur8);               \
         strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
         if (c != 0 || K >= 2) st_f32(hs_c + (K - 2) * 32, r[(K + 6) & 7]);           \
         r[(K + 3) & 7] = nx[K];                                                      \
@@ -522,8 +563,7 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
             } else {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) scratch[k * 32] = nx[k];
-                const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, pos_c, band_c, tau_c,
-                                                             g.edges, c * 8, hs_l, scratch, e_blk);
+                const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, t, p0, hs_l, scratch, e_blk);
                 w = res.w;
                 acc8 = res.acc8;
                 e_blk = res.e_blk;
@@ -541,8 +581,8 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
                 }
             }
             if ((chunk_info.y >> 16) != 0u && __any_sync(0xffffffffu, acc8 != 0u)) {
-                if (RED) apply_edges_red(hs_l, g.edges, chunk_info.y, acc8, cb.cur8);
-                else apply_groups_rmw(hs_l, g.groups, g.edges, chunk_info.x, acc8, cb.cur8);
+                if (RED) apply_edges_red(hs_l, t, chunk_info.y, acc8, cb.cur8);
+                else apply_groups_rmw(hs_l, t, chunk_info.x, acc8, cb.cur8);
             }
             ++seq;
             ISING_TICK(tD);
@@ -552,10 +592,6 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
                 cur_c += 32;
                 up_c += 32;
                 dn_c += 32;
-                chunk_c += 1;
-                pos_c += 8;
-                band_c += 16;
-                tau_c += 2;
                 if (seq % pub == 0u) publish_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
             }
             ISING_TICK(tE);
@@ -601,7 +637,7 @@ __device__ void strand_run(const DevBatch& b, const DevStrandGraph& g, uint32_t 
 // order, 32 at a time, never overwriting a row a strand has yet to read or the 624 rows behind the
 // head; the head is published after every batch.  At the end the last 624 rows go back to the
 // in-place state array the other kernel families use.
-__device__ void producer_run(const DevBatch& b, const DevStrandGraph& g, uint32_t tile, uint32_t sweeps, uint32_t lane) {
+__device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, uint32_t lane) {
     const uint32_t S = b.strands, R = b.tape_rows;
     uint32_t* tape = b.tape + size_t(tile) * R * 32 + lane;
     uint32_t* state = b.mt + size_t(tile) * kMtN * 32 + lane;
@@ -698,15 +734,14 @@ __device__ void producer_run(const DevBatch& b, const DevStrandGraph& g, uint32_
 // rounds), so the waits above always end.  Dynamic shared memory: kWarpSmem bytes per warp (landing
 // stages, scratch), then — for single-model batches — a copy of the layer graph, which every strand
 // of the CTA reads (b.strand_graph_smem bytes; otherwise the tables are read from global memory).
-template <int EXP, bool WAIT, bool RED>
+template <int EXP, bool WAIT, bool RED, bool STAGED>
 __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(DevBatch b, uint32_t sweeps,
                                                                                  uint32_t tiles_per_round) {
     extern __shared__ __align__(16) unsigned char strand_smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, warps = blockDim.x >> 5;
     unsigned char* warp_smem = strand_smem + size_t(warp) * kWarpSmem;
-    DevStrandGraph staged{};
-    const bool use_staged = b.strand_graph_smem != 0u;
-    if (use_staged) {
+    Tables<STAGED> staged{};
+    if constexpr (STAGED) {
         const DevStrandGraph g0 = b.strand_graphs[0];
         const uint32_t P = g0.per_layer;
         uint4* pos = reinterpret_cast<uint4*>(strand_smem + size_t(warps) * kWarpSmem);
@@ -721,13 +756,12 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
         for (uint32_t k = threadIdx.x; k < P / 4; k += blockDim.x) tau[k] = g0.tau[k];
         for (uint32_t k = threadIdx.x; k < g0.n_edges; k += blockDim.x) edges[k] = g0.edges[k];
         for (uint32_t k = threadIdx.x; k < g0.n_groups; k += blockDim.x) groups[k] = g0.groups[k];
-        staged = g0;
-        staged.pos = pos;
-        staged.band_pm = band;
-        staged.chunks = chunks;
-        staged.tau = tau;
-        staged.edges = edges;
-        staged.groups = groups;
+        staged.pos = smem_u32(pos);
+        staged.band = smem_u32(band);
+        staged.chunks = smem_u32(chunks);
+        staged.tau = smem_u32(tau);
+        staged.edges = smem_u32(edges);
+        staged.groups = smem_u32(groups);
         __syncthreads();
     }
     const uint32_t item = warp * gridDim.x + blockIdx.x;
@@ -737,9 +771,23 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
         if (item >= tiles * (S + 1)) continue;
         // consecutive items are the same role of consecutive tiles: an SM hosts a mix of tiles
         const uint32_t role = item / tiles, tile = base + item - role * tiles;
-        const DevStrandGraph g = use_staged ? staged : b.strand_graphs[b.tile_model[tile]];
-        if (role == S) producer_run(b, g, tile, sweeps, lane);
-        else strand_run<EXP, WAIT, RED>(b, g, tile, role, sweeps, lane, warp_smem);
+        if (role == S) {
+            producer_run(b, tile, sweeps, lane);
+            continue;
+        }
+        const DevStrandGraph& g = b.strand_graphs[STAGED ? 0u : b.tile_model[tile]];
+        if constexpr (STAGED) {
+            strand_run<EXP, WAIT, RED, true>(b, staged, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
+        } else {
+            Tables<false> t;
+            t.chunks = g.chunks;
+            t.pos = g.pos;
+            t.band = g.band_pm;
+            t.tau = g.tau;
+            t.edges = g.edges;
+            t.groups = g.groups;
+            strand_run<EXP, WAIT, RED, false>(b, t, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
+        }
     }
 }
 
@@ -787,32 +835,39 @@ size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges, uint32_t n_group
 }
 
 namespace {
-template <int EXP, bool WAIT, bool RED>
+template <int EXP, bool WAIT, bool RED, bool STAGED>
 cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t smem, uint32_t round,
                                   cudaStream_t stream) {
     // the attribute is per function and context: always the opt-in maximum, never one batch's own need
     static bool prepared = false;
     if (!prepared) {
-        const cudaError_t e = cudaFuncSetAttribute(sweep_strand_kernel<EXP, WAIT, RED>,
+        const cudaError_t e = cudaFuncSetAttribute(sweep_strand_kernel<EXP, WAIT, RED, STAGED>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         prepared = true;
     }
-    sweep_strand_kernel<EXP, WAIT, RED><<<grid, block, smem, stream>>>(b, sweeps, round);
+    sweep_strand_kernel<EXP, WAIT, RED, STAGED><<<grid, block, smem, stream>>>(b, sweeps, round);
     return cudaGetLastError();
 }
 template <int EXP>
-cudaError_t launch_strand_exp(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t smem, uint32_t round,
-                              cudaStream_t stream) {
-    // separate instantiations: the default kernel carries no wait statistics; reductions need every
-    // model to be reduction-safe (no subnormal field possible)
+cudaError_t launch_strand_exp(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t warp_smem,
+                              uint32_t round, cudaStream_t stream) {
+    // Separate instantiations: reductions need every model to be reduction-safe (no subnormal field
+    // possible); the wait-statistics variant is the only one that carries them (and reads the graph
+    // from global memory); the default reads the staged graph when the batch has one model.
     const bool wait = b.wait_counts != nullptr, red = b.generic_reduce != 0u;
+    const bool staged = !wait && b.strand_graph_smem != 0u;
+    const size_t smem = warp_smem + (staged ? b.strand_graph_smem : 0u);
     if (wait) {
-        return red ? launch_strand_variant<EXP, true, true>(b, sweeps, grid, block, smem, round, stream)
-                   : launch_strand_variant<EXP, true, false>(b, sweeps, grid, block, smem, round, stream);
+        return red ? launch_strand_variant<EXP, true, true, false>(b, sweeps, grid, block, smem, round, stream)
+                   : launch_strand_variant<EXP, true, false, false>(b, sweeps, grid, block, smem, round, stream);
     }
-    return red ? launch_strand_variant<EXP, false, true>(b, sweeps, grid, block, smem, round, stream)
-               : launch_strand_variant<EXP, false, false>(b, sweeps, grid, block, smem, round, stream);
+    if (staged) {
+        return red ? launch_strand_variant<EXP, false, true, true>(b, sweeps, grid, block, smem, round, stream)
+                   : launch_strand_variant<EXP, false, false, true>(b, sweeps, grid, block, smem, round, stream);
+    }
+    return red ? launch_strand_variant<EXP, false, true, false>(b, sweeps, grid, block, smem, round, stream)
+               : launch_strand_variant<EXP, false, false, false>(b, sweeps, grid, block, smem, round, stream);
 }
 }  // namespace
 
@@ -834,7 +889,7 @@ cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count
     const dim3 grid(ctas), block(warps_per_cta * 32);
     // items are dealt warp-major over the launched CTAs: recompute the round size for this grid
     const uint32_t round = min(b.n_tiles, ctas * warps_per_cta / per_tile);
-    const size_t smem = size_t(warps_per_cta) * kWarpSmem + b.strand_graph_smem;
+    const size_t smem = size_t(warps_per_cta) * kWarpSmem;  // (+ the staged graph, see launch_strand_exp)
     switch (b.exp_kind) {
         case kExpExact: e = launch_strand_exp<kExpExact>(b, sweeps, grid, block, smem, round, stream); break;
         case kExpFast: e = launch_strand_exp<kExpFast>(b, sweeps, grid, block, smem, round, stream); break;
