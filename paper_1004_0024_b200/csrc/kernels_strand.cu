@@ -637,7 +637,12 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
 // order, 32 at a time, never overwriting a row a strand has yet to read or the 624 rows behind the
 // head; the head is published after every batch.  At the end the last 624 rows go back to the
 // in-place state array the other kernel families use.
-__device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, uint32_t lane) {
+// `landing`: 2 stages of 8 KB (32 rows x[a-623..] and 32 rows x[a-227..]) plus two mbarriers, in shared
+// memory, or nullptr: then the operands of a group are loaded into registers, one round trip per
+// 32 rows (about a third of the rate).
+constexpr uint32_t kProducerStage = 8192;
+constexpr uint32_t kProducerSmem = 2 * kProducerStage + 16;
+__device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, uint32_t lane, unsigned char* landing) {
     const uint32_t S = b.strands, R = b.tape_rows;
     uint32_t* tape = b.tape + size_t(tile) * R * 32 + lane;
     uint32_t* state = b.mt + size_t(tile) * kMtN * 32 + lane;
@@ -651,6 +656,33 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
         w = w >= kMtN ? w - kMtN : w;
         st_u32(tape + size_t(i) * 32, state[size_t(w) * 32]);
     }
+    // Bulk copies read the ring through the async proxy: every row they fetch must be globally
+    // performed first.  The rows above are made so here; later ones by the fence of a publication —
+    // a group's operands are at least 132 rows (two publications) behind the row being written.
+    const uint32_t lsm = landing != nullptr ? smem_u32(landing) : 0u;
+    const uint32_t lbar = lsm + 2 * kProducerStage;
+    uint32_t lstage = 0, lphases = 0;
+    bool in_flight = false;  // the operands of the group at (sa, sf) have been requested into stage lstage
+    if (landing != nullptr) {
+        __threadfence();
+        if (lane == 0) {
+            mbar_init(lbar, 1);
+            mbar_init(lbar + 8, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    const uint32_t* tape_rows = b.tape + size_t(tile) * R * 32;  // (no lane offset: rows are copied whole)
+    const auto request_group = [&](uint32_t st, uint32_t slot_a, uint32_t slot_f) {
+        __syncwarp();  // every lane has left the stage's previous contents
+        if (lane == 0) {
+            const uint32_t dst = lsm + st * kProducerStage, bar = lbar + st * 8;
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_expect(bar, kProducerStage);
+            bulk_load(dst, tape_rows + size_t(slot_a + 1) * 32, 4096, bar);
+            bulk_load(dst + 4096, tape_rows + size_t(slot_f) * 32, 4096, bar);
+        }
+    };
 
     const uint32_t end = kMtN + total;
     uint32_t a = kMtN;      // next row to generate
@@ -674,7 +706,30 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
         }
         for (uint32_t done = 0; done < batch;) {
             const uint32_t rows = min(32u, batch - done);
-            if (rows == 32u && sa + 32 < R && sf + 32 <= R && so + 32 <= R) {  // no run crosses the end of the ring
+            const bool whole = rows == 32u && sa + 32 < R && sf + 32 <= R && so + 32 <= R;  // no run crosses the end of the ring
+            if (whole && landing != nullptr) {
+                if (!in_flight) request_group(lstage, sa, sf);
+                // the group after this one, while this one is generated (its operands lie behind row a too)
+                const uint32_t sa2 = sa + 32, sf2 = sf + 32 == R ? 0u : sf + 32, so2 = so + 32 == R ? 0u : so + 32;
+                const bool next_whole = a + done + 64 <= end && sa2 + 32 < R && sf2 + 32 <= R && so2 + 32 <= R;
+                if (next_whole) request_group(lstage ^ 1u, sa2, sf2);
+                mbar_wait(lbar + lstage * 8, (lphases >> lstage) & 1u);
+                lphases ^= 1u << lstage;
+                const uint32_t* in = reinterpret_cast<const uint32_t*>(landing + lstage * kProducerStage) + lane;
+                uint32_t* po = tape + size_t(so) * 32;
+#pragma unroll 8
+                for (int k = 0; k < 32; ++k) {
+                    const uint32_t nx = in[k * 32];
+                    st_u32(po + k * 32, mt_recurrence(cur, nx, in[1024 + k * 32]));
+                    cur = nx;
+                }
+                sa = sa2;
+                sf = sf2;
+                so = so2;
+                done += 32;
+                lstage ^= 1u;
+                in_flight = next_whole;
+            } else if (whole) {
                 const uint32_t* pa = tape + size_t(sa) * 32;
                 const uint32_t* pf = tape + size_t(sf) * 32;
                 uint32_t* po = tape + size_t(so) * 32;
@@ -694,6 +749,11 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
                 so = so + 32 == R ? 0u : so + 32;
                 done += 32;
             } else {  // near the end of the ring, or a short tail: 8 rows at a time, every slot wrapped
+                if (in_flight) {  // operands requested for a whole group that is not to be: let them land, unused
+                    mbar_wait(lbar + lstage * 8, (lphases >> lstage) & 1u);
+                    lphases ^= 1u << lstage;
+                    in_flight = false;
+                }
                 uint32_t nxt[8], far[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -713,6 +773,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
                 sf = sf + 8 >= R ? sf + 8 - R : sf + 8;
                 so = so + 8 >= R ? so + 8 - R : so + 8;
                 done += 8;
+                in_flight = false;
             }
         }
         a += batch;
@@ -736,10 +797,13 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
 // of the CTA reads (b.strand_graph_smem bytes; otherwise the tables are read from global memory).
 template <int EXP, bool WAIT, bool RED, bool STAGED>
 __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(DevBatch b, uint32_t sweeps,
-                                                                                 uint32_t tiles_per_round) {
+                                                                                 uint32_t tiles_per_round,
+                                                                                 uint32_t producer_slots) {
     extern __shared__ __align__(16) unsigned char strand_smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, warps = blockDim.x >> 5;
     unsigned char* warp_smem = strand_smem + size_t(warp) * kWarpSmem;
+    // after the warps' regions and the staged graph: the producers' landing buffers
+    unsigned char* producer_smem = strand_smem + (size_t(warps) * kWarpSmem + (STAGED ? b.strand_graph_smem : 0u) + 15) / 16 * 16;
     Tables<STAGED> staged{};
     if constexpr (STAGED) {
         const DevStrandGraph g0 = b.strand_graphs[0];
@@ -772,7 +836,12 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
         // consecutive items are the same role of consecutive tiles: an SM hosts a mix of tiles
         const uint32_t role = item / tiles, tile = base + item - role * tiles;
         if (role == S) {
-            producer_run(b, tile, sweeps, lane);
+            // producers are the last items of a round, hence the CTA's highest warps: landing buffer
+            // number warp - (first warp that can be a producer), when the launcher has provided them
+            const uint32_t first_producer_warp = tiles * S / gridDim.x;
+            const uint32_t slot = warp - first_producer_warp;
+            unsigned char* landing = slot < producer_slots ? producer_smem + size_t(slot) * kProducerSmem : nullptr;
+            producer_run(b, tile, sweeps, lane, landing);
             continue;
         }
         const DevStrandGraph& g = b.strand_graphs[STAGED ? 0u : b.tile_model[tile]];
@@ -846,7 +915,13 @@ cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, dim3 grid,
         if (e != cudaSuccess) return e;
         prepared = true;
     }
-    sweep_strand_kernel<EXP, WAIT, RED, STAGED><<<grid, block, smem, stream>>>(b, sweeps, round);
+    // landing buffers for the producers a CTA can host (ceil(tiles of a round / CTAs) + 1 warp indices),
+    // when they fit; else the producers load their operands into registers
+    uint32_t slots = (round + grid.x - 1) / grid.x + 1;
+    const size_t base = (smem + 15) / 16 * 16;
+    if (base + size_t(slots) * kProducerSmem > 227 * 1024) slots = 0;
+    const size_t total_smem = slots != 0 ? base + size_t(slots) * kProducerSmem : smem;
+    sweep_strand_kernel<EXP, WAIT, RED, STAGED><<<grid, block, total_smem, stream>>>(b, sweeps, round, slots);
     return cudaGetLastError();
 }
 template <int EXP>
