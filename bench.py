@@ -41,7 +41,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=100)  # 100 steps x 10 sweeps = the 1000 sweeps of c5
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "all"],
+                    help="all: c1..c5 one after the other, one JSON line each (see --save)")
+    ap.add_argument("--save", default="", help="with --workload all: also write the lines to this JSON file")
     ap.add_argument("--ladders", type=int, default=0, help="override ladders per GPU (0: the workload's)")
     ap.add_argument("--exp", default="fast", choices=["exact", "fast", "accurate"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "layered", "strand", "coalesced"],
@@ -112,6 +114,47 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+
+def config_of(wl, exp_name, sweeps_per_step, world):
+    """The `config` object of the JSON line — the same keys and values in both arms."""
+    return {"workload": f"{wl.name}: {wl.description}", "chains_per_gpu": int(wl.n_ladders * len(wl.betas)),
+            "sweeps_per_step": int(sweeps_per_step), "swap_interval": int(wl.swap_interval), "exp_kind": exp_name,
+            "l2": "per-GPU state streamed every sweep (far larger than the 126 MB L2 at full size), no explicit flush",
+            "parallelism": f"ladders sharded over {world} GPU(s), no data-path collective"}
+
+
+def kernel_source_hash() -> str:
+    """Identifies the kernel sources a DRAM-traffic profile was taken with (profiles/sweep_traffic.json)."""
+    import hashlib
+    h = hashlib.sha256()
+    for name in ("kernels_strand.cu", "kernels_layered.cu", "kernels_generic.cu", "device_math.cuh", "device_mt.cuh"):
+        h.update((ROOT / "paper_1004_0024_b200" / "csrc" / name).read_bytes())
+    return h.hexdigest()[:16]
+
+
+def profiled_traffic(workload: str, kernel: int, attempts_per_launch: float):
+    """DRAM bytes per launch from the committed ncu capture of this workload and kernel family, or
+    (None, why): a capture taken with other kernel sources is refused."""
+    prof = ROOT / "profiles" / "sweep_traffic.json"
+    if not prof.exists():
+        return None, "no ncu capture committed"
+    try:
+        entry = json.loads(prof.read_text()).get(f"{workload}:{kernel}")
+    except Exception as exc:  # malformed file: say so, do not guess
+        return None, f"unreadable profile: {exc}"
+    if entry is None:
+        return None, "no ncu capture of this workload and kernel family"
+    if entry.get("kernel_source_hash") != kernel_source_hash():
+        return None, f"stale: capture {entry.get('source')} was taken with other kernel sources"
+    return entry["dram_bytes_per_attempt"] * attempts_per_launch, entry.get("source")
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
 def build_models(wl, csrs):
     """One product model per instance (validation and layer analysis run in C++ with the GIL released, so
     workloads with many distinct instances build them on a few host threads)."""
@@ -132,9 +175,11 @@ def model_bytes(csrs) -> int:
                    (0 if c["tau_counts"] is None else c["tau_counts"].nbytes) for c in csrs))
 
 
-def cpu_baseline(wl, csrs, exp_kind, sample_ladders, sweeps_per_step, steps, warmup):
+def cpu_baseline(wl, csrs, exp_kind, sample_ladders, sweeps_per_step, steps, warmup, engine=1):
     """Times the reference's CPU path (oracle/_ref when built, else the C port) on a bounded sample
-    of the same workload, all host cores.  Returns (dict, seconds_per_step)."""
+    of the same workload, all host cores.  engine 1: `basic`, the tier the GPU path is bit-exact
+    with; engine 2: `vector4` on the reference's own permuted model (its fastest tier: another
+    trajectory, timing only, reference library only).  Returns (dict, seconds_per_step)."""
     from oracle import pyoracle
     from paper_1004_0024_b200 import instances as ins
     cores = os.cpu_count() or 1
@@ -147,12 +192,16 @@ def cpu_baseline(wl, csrs, exp_kind, sample_ladders, sweeps_per_step, steps, war
     if pyoracle.Reference.available():
         ref = pyoracle.Reference()
         models = [ref.model(c) for c in csrs]
+        if engine == 2:
+            models = [m.prepared_for(2)[0] for m in models]
         lad = ref.ladders([models[pick(l)] for l in range(ladders)], ladders, wl.betas, seeds, swap_seeds, 1.0,
-                          exp_kind)
+                          exp_kind, engine)
         for _ in range(warmup):
             lad.run(sweeps_per_step, wl.swap_interval, cores)
         secs = sum(lad.run(sweeps_per_step, wl.swap_interval, cores) for _ in range(steps))
         kind = "reference"
+    elif engine != 1:
+        return None, None
     else:
         port = pyoracle.Port()
         models = [port.model(c) for c in csrs]
@@ -164,8 +213,10 @@ def cpu_baseline(wl, csrs, exp_kind, sample_ladders, sweeps_per_step, steps, war
         secs = (time.perf_counter() - t0) * steps / (steps + warmup)  # includes state setup
         kind = "port"
     attempts = ladders * nb * csrs[0]["n_spins"] * sweeps_per_step * steps
+    tier = "basic" if engine == 1 else "vector4 (another trajectory: timing only)"
     sample = (f"{ladders} ladders x {nb} betas = {ladders * nb} chains of {csrs[0]['n_spins']} spins, "
-              f"{sweeps_per_step * steps} sweeps (swap every {wl.swap_interval}), basic engine / {exp_kind_name(exp_kind)} exp")
+              f"{sweeps_per_step * steps} sweeps (swap every {wl.swap_interval}), {tier} engine / "
+              f"{exp_kind_name(exp_kind)} exp")
     return {"value": attempts / secs, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}, secs / steps
 
 
@@ -256,19 +307,52 @@ def bench_coalesced(args, wl, exp_kind):
     print(json.dumps(line), flush=True)
 
 
+def respawn_ranks(args) -> int:
+    """`python bench.py --gpus N` with N > 1 and no launcher around it: start N ranks of this very
+    command under torch.distributed.run (one per GPU, NCCL over 127.0.0.1) and wait for them."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} asked, {have} CUDA device(s) visible",
+                          "n_gpus": args.gpus}), flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.kernel != "coalesced":
+        raise SystemExit(respawn_ranks(args))
+    names = ["c1", "c2", "c3", "c4", "c5"] if args.workload == "all" else [args.workload]
+    lines = []
+    for name in names:
+        line = run_workload(args, name)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+            lines.append(line)
+    if args.save and lines:
+        Path(args.save).write_text(json.dumps(lines, indent=1) + "\n")
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def run_workload(args, name):
+    """One workload, this rank; returns the JSON line on rank 0 (None elsewhere)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     exp_kind = {"exact": 1, "fast": 2, "accurate": 3}[args.exp]
 
     from paper_1004_0024_b200 import workloads
-    wl = workloads.get(args.workload)
+    wl = workloads.get(name)
     if args.kernel == "coalesced":
         if rank == 0 and args.impl == "ours":
             bench_coalesced(args, wl, exp_kind)
-        return
+        return None
     if args.ladders:
         wl.n_ladders = args.ladders
     sweeps_per_step = wl.swap_interval if wl.swap_interval else 10
@@ -277,23 +361,22 @@ def main():
     # ------------------------------------------------------------------ reference arm (CPU)
     if args.impl == "reference":
         if rank != 0:
-            return
+            return None
         csrs = wl.make_csrs() if wl.shared_graph else wl.make_csrs()[: max(1, min(wl.n_ladders, 8))]
         n = csrs[0]["n_spins"]
         sample = args.cpu_ladders or max(1, min(wl.n_ladders, int(4.0e8 // (nb * n * sweeps_per_step)) or 1))
         base, per_step = cpu_baseline(wl, csrs, exp_kind, sample, sweeps_per_step, args.steps, args.warmup)
-        line = {
+        config = config_of(wl, args.exp, sweeps_per_step, max(world, args.gpus))
+        config["n_spins"] = int(n)
+        return {
             "impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": f"{wl.name}: {wl.description}", "exp_kind": args.exp,
-                                            "sweeps_per_step": sweeps_per_step},
+            "data": "synthetic", "config": config,
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0,
         }
-        print(json.dumps(line), flush=True)
-        return
 
     # ------------------------------------------------------------------ our arm (GPU)
     import torch
@@ -303,7 +386,7 @@ def main():
     libbuild.build()
 
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    if world > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     def barrier():
@@ -357,6 +440,7 @@ def main():
     value = total_attempts / (ms_max * 1e-3)
     sweep_launches = after["sweep_launches"] - before["sweep_launches"]
     swap_launches = after["swap_launches"] - before["swap_launches"]
+    other_launches = after["other_launches"] - before["other_launches"]
     sweep_ms = after["sweep_ms"] - before["sweep_ms"]
 
     # ---- roofline of the sweep kernel (this rank): algorithmic bytes B = S + f*(1 + 8*dbar)
@@ -364,19 +448,13 @@ def main():
     bytes_per_attempt = wl.state_bytes_per_spin + flip_rate * (1.0 + 8.0 * dbar)
     peak, peak_src = peak_hbm()
     achieved = bytes_per_attempt * attempts_per_step * args.steps / (sweep_ms * 1e-3) / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "sweep_traffic.json"
-    if prof.exists():
-        try:
-            entry = json.loads(prof.read_text()).get(f"{wl.name}:{after['kernel']}")
-            # per launch, like `achieved`: the profiled bytes per attempt x the attempts of one launch here
-            traffic = entry["dram_bytes_per_attempt"] * attempts_per_step * args.steps / max(1, sweep_launches)
-        except Exception:
-            traffic = None
+    traffic, traffic_src = profiled_traffic(wl.name, after["kernel"],
+                                            attempts_per_step * args.steps / max(1, sweep_launches))
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "bytes_per_attempt": bytes_per_attempt,
-                "flip_rate": flip_rate, "mean_degree": dbar,
+                "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                "bytes_per_attempt": bytes_per_attempt, "flip_rate": flip_rate, "mean_degree": dbar,
                 "kernel": {1: "sweep_generic", 2: "sweep_layered", 3: "sweep_strand"}[after["kernel"]],
+                "strands_per_tile": after.get("strands", 0),
                 "kernel_ms_per_launch": sweep_ms / max(1, sweep_launches),
                 "roofline_attempts_per_sec": peak * 1e9 / bytes_per_attempt}
     info = after
@@ -399,7 +477,7 @@ def main():
             rec = torch.empty((chains, sharding.RECORD_WORDS), dtype=torch.int64, device="cuda")
             st.pack_results(rec.data_ptr())
             allrec = sharding.all_gather_records(rec, [chains] * world)
-            host = allrec.cpu() if rank == 0 else None
+            host = allrec.cpu() if rank == 0 else None  # noqa: F841 (the read-back is the point)
             d2h_final = world * chains * 32 if rank == 0 else 0
         else:
             en, cs = st.energies(), st.checksums()
@@ -420,32 +498,33 @@ def main():
                            "counts and running energies, final energies+checksums" +
                            (" via NCCL all-gather" if world > 1 else "") + ", 16-chain spin readout"}
 
-    # ---- CPU baseline beside it (rank 0, N = 1 only)
-    base = None
+    # ---- CPU baselines beside it (rank 0, N = 1 only): the tier the GPU path is bit-exact with, and
+    # for layered workloads the reference's fastest tier (vector4 on its own permuted model)
+    base = best = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = args.cpu_ladders or max(1, min(wl.n_ladders, int(2.0e9 // (nb * n * sweeps_per_step * 4)) or 1))
-        base, _ = cpu_baseline(wl, csrs[:8] if not wl.shared_graph else csrs, exp_kind, sample, sweeps_per_step,
-                               4, 1)
+        some = csrs[:8] if not wl.shared_graph else csrs
+        base, _ = cpu_baseline(wl, some, exp_kind, sample, sweeps_per_step, 4, 1)
+        if csrs[0]["layers"]:
+            best, _ = cpu_baseline(wl, some, exp_kind, sample, sweeps_per_step, 4, 1, engine=2)
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{wl.name}: {wl.description}", "chains_per_gpu": chains, "n_spins": n,
-                       "sweeps_per_step": sweeps_per_step, "swap_interval": wl.swap_interval,
-                       "exp_kind": args.exp, "kernel_family": roofline["kernel"],
-                       "l2": f"per-GPU state {info['device_bytes'] / 1e9:.2f} GB streamed every sweep "
-                             "(>> 126 MB L2), no explicit flush",
-                       "parallelism": f"ladders sharded over {world} GPU(s), no data-path collective"},
-            "roofline": roofline, "cpu_baseline": base, "e2e": e2e,
-            "gpu_launches": int(sweep_launches + swap_launches),
-            "launch_breakdown": {"sweep": int(sweep_launches), "swap": int(swap_launches)},
-            "clocks": clocks,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    config = config_of(wl, args.exp, sweeps_per_step, world)
+    config["n_spins"] = int(n)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config, "first_ladder_of_rank": [r * wl.n_ladders for r in range(world)],
+        "device_bytes_per_gpu": int(info["device_bytes"]),
+        "roofline": roofline, "cpu_baseline": base, "cpu_baseline_best": best, "e2e": e2e,
+        # the strand family brackets its sweep kernel with two small conversion kernels (spin words <-> bytes)
+        "gpu_launches": int(sweep_launches + swap_launches + other_launches),
+        "launch_breakdown": {"sweep": int(sweep_launches), "swap": int(swap_launches),
+                             "spin_format_conversions": int(other_launches)},
+        "clocks": clocks,
+    }
 
 
 if __name__ == "__main__":

@@ -372,7 +372,9 @@ Batch::Batch(const std::vector<const HostModel*>& models,
         throw Error("init_state: the strand kernel needs identical-layer models with equal tau couplings "
                     "and a multiple of 8, at least 16, positions per layer");
     }
-    const bool use_strand = cfg.kernel == int(KernelFamily::strand);
+    // AUTO: the strand family whenever the batch qualifies (the fastest on every layered workload
+    // measured); the Tensor Memory family only on request.
+    const bool use_strand = cfg.kernel == int(KernelFamily::strand) || (cfg.kernel == 0 && strand_ok);
     std::vector<HostLayerGraph> host_graphs;
     if (layered_ok && !use_strand && cfg.kernel != int(KernelFamily::generic)) {
         host_graphs.resize(models.size());

@@ -36,7 +36,7 @@ def test_c5_full_batch_properties_and_subsample_parity(lib, port, c5):
     with ib.init_state(model, wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE,
                        swap_base_seed=ins.SWAP_SEED_BASE) as st:
         info = st.info()
-        assert info["kernel"] == ib.KERNEL_LAYERED and info["n_chains"] == 16384 and info["n_tiles"] == 512
+        assert info["kernel"] == ib.KERNEL_STRAND and info["n_chains"] == 16384 and info["n_tiles"] == 512
         e0 = st.energies()
         np.testing.assert_array_equal(st.running_energies(), e0)  # initial running energy == total_cost
         st.run(sweeps, wl.swap_interval)

@@ -261,11 +261,18 @@ def test_pack_results_matches_host_readouts(lib):
 
 
 def test_layered_family_selection_and_rejection(lib):
-    """AUTO picks the on-chip family exactly when every model qualifies; asking for it otherwise
-    is an argument error (no silent fallback)."""
+    """AUTO picks the strand family exactly when every model qualifies (identical layers, one tau
+    coupling per position, a multiple of 8 and at least 16 positions per layer), else the Tensor Memory
+    family when that one does, else the generic one; asking for a family that does not apply is an
+    argument error (no silent fallback)."""
     layered = product_model(ins.build_layered_csr(*ins.layered_spec(16, 3), 4, 1.5))
-    generic = product_model(ins.cubic_pm1(4, 1, 0.0))  # 64 spins like the layered one
+    short_layers = product_model(ins.build_layered_csr(*ins.layered_spec(8, 3), 8, 1.5))  # 8 positions per layer
+    generic = product_model(ins.cubic_pm1(4, 1, 0.0))  # 64 spins like the layered ones
     with ib.init_state(layered, [1.0], 2) as st:
+        assert st.info()["kernel"] == ib.KERNEL_STRAND and st.info()["strands"] >= 1
+    with ib.init_state(layered, [1.0], 2, kernel=ib.KERNEL_LAYERED) as st:
+        assert st.info()["kernel"] == ib.KERNEL_LAYERED and st.info()["strands"] == 0
+    with ib.init_state(short_layers, [1.0], 2) as st:
         assert st.info()["kernel"] == ib.KERNEL_LAYERED
     with ib.init_state(generic, [1.0], 2) as st:
         assert st.info()["kernel"] == ib.KERNEL_GENERIC
@@ -274,6 +281,10 @@ def test_layered_family_selection_and_rejection(lib):
     with pytest.raises(ib.IsingError) as err:
         ib.init_state(generic, [1.0], 2, kernel=ib.KERNEL_LAYERED)
     assert err.value.status == _lib.ISING_ERR_ARGUMENT and "layered kernel needs" in str(err.value)
+    for bad in (generic, short_layers):
+        with pytest.raises(ib.IsingError) as err:
+            ib.init_state(bad, [1.0], 2, kernel=ib.KERNEL_STRAND)
+        assert err.value.status == _lib.ISING_ERR_ARGUMENT and "strand kernel needs" in str(err.value)
     # unequal tau couplings per spin: still a valid layered model, but the tau field must be stored
     csr = ins.build_layered_csr(*ins.layered_spec(8, 5), 4, 1.5)
     csr["couplings"] = csr["couplings"].copy()
@@ -423,7 +434,7 @@ def test_one_shot_run_json_has_the_reference_report_keys(lib, port, tmp_path):
     assert doc["final_cost"] == pytest.approx(port.total_cost(port.model(csr), chain.spins), rel=REL_ENERGY)
     assert doc["flip_rate"] == report["flips"] / report["attempts"]
     head = (doc["engine"], doc["exp"], doc["spins"], doc["sweeps"], doc["seed"], doc["workers"])
-    assert head == ("b200-layered", "fast", 64, 25, 4321, 1)
+    assert head == ("b200-strand", "fast", 64, 25, 4321, 1)
     assert doc["beta"] == float(np.float32(0.7)) and doc["tau_scale"] == 1.25 and doc["wait"] == {}
     assert "device=" in doc["environment"]
 
