@@ -1,7 +1,9 @@
 """BASELINE.json's full-size configurations on the GPU, checked through size-independent
-properties (the oracle cannot finish them): agreement of the two kernel families, the running
+properties (the oracle cannot finish them): agreement of the kernel families, the running
 energy against the recomputed energy, determinism (a checksum of checksums), shard invariance,
-and bit parity with the oracle on a subsample of ladders inside the full batch."""
+bit parity with the oracle on a subsample of ladders inside the full batch for the FULL run
+length of every configuration, and all 16,384 chains of config 5 against a record the reference
+itself produced (tests/golden/make_golden_c5.py)."""
 import os
 
 import numpy as np
@@ -12,6 +14,9 @@ from paper_1004_0024_b200 import sharding, workloads
 from helpers import assert_batch_matches, ins, oracle_batch, product_model, random_graph
 
 pytestmark = pytest.mark.gpu
+
+
+FAMILIES = (ib.KERNEL_STRAND, ib.KERNEL_LAYERED, ib.KERNEL_GENERIC)  # identical-layer models: all three
 
 
 def fold(values) -> int:
@@ -91,13 +96,14 @@ def test_c4_kernel_families_agree_on_distinct_instances(lib):
     csrs = [ins.build_layered_csr(*ins.layered_spec(512, ins.INSTANCE_SEED + k, 0.5, 6), 64, 1.5) for k in range(3)]
     models = [product_model(c) for c in csrs]
     out = {}
-    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC):
+    for family in FAMILIES:
         with ib.init_state(models, wl.betas, 3, base_seed=11, swap_base_seed=12, kernel=family) as st:
             assert st.info()["kernel"] == family
             st.run(6, 1)
             out[family] = (st.checksums(), st.stats()[0], st.slots(), st.running_energies(), st.energies())
-    for a, b in zip(out[ib.KERNEL_LAYERED], out[ib.KERNEL_GENERIC]):
-        np.testing.assert_array_equal(a, b)
+    for family in FAMILIES[1:]:
+        for a, b in zip(out[FAMILIES[0]], out[family]):
+            np.testing.assert_array_equal(a, b)
     assert out[ib.KERNEL_LAYERED][1].sum() > 0
 
 
@@ -138,7 +144,7 @@ def test_more_tiles_than_warp_slots_each_pair_sweeps_several_tiles(lib, port):
     betas = ins.geometric_betas(0.3, 2.5, 4)
     ladders = 700 * 8  # 22,400 chains = 700 tiles
     out = {}
-    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC):
+    for family in FAMILIES:
         with ib.init_state(model, betas, ladders, base_seed=31, swap_base_seed=32, kernel=family) as st:
             assert st.info()["n_tiles"] == 700 and st.info()["kernel"] == family
             st.run(7, 3)
@@ -146,18 +152,19 @@ def test_more_tiles_than_warp_slots_each_pair_sweeps_several_tiles(lib, port):
             out[family] = (st.checksums(), st.stats()[0], st.slots(), st.running_energies())
             if family == ib.KERNEL_LAYERED:
                 sample = st.spins(4 * 5000, 8)  # ladders 5000, 5001: tile 625, in the second round of its pair
-    for a, b in zip(out[ib.KERNEL_LAYERED], out[ib.KERNEL_GENERIC]):
-        np.testing.assert_array_equal(a, b)
+    for family in FAMILIES[1:]:
+        for a, b in zip(out[FAMILIES[0]], out[family]):
+            np.testing.assert_array_equal(a, b)
     want = oracle_batch(port, [csr], 2, betas, sharding.chain_seeds(31, 5000, 2, 4),
                         sharding.ladder_seeds(32, 5000, 2), 12, 3)
     np.testing.assert_array_equal(sample, want["spins"])
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("ISING_FUZZ_SEEDS", "12"))))
-def test_random_layer_graphs_both_families_bit_identical(lib, seed):
-    """Seeded fuzz of the layered kernel's edge classification (band / near in the loaded columns /
-    near in the next chunk's / far warp, group splitting on repeated targets, padding): random layer
-    graphs with chords at random distances, both kernel families must leave identical spins, flip
+def test_random_layer_graphs_all_families_bit_identical(lib, seed):
+    """Seeded fuzz of the layered and strand kernels' edge classification (band / near in the loaded
+    columns / near in the next chunk's / far, group splitting on repeated targets, padding): random
+    layer graphs with chords at random distances, all kernel families must leave identical spins, flip
     counts, slots, running energies and FIELDS (bit for bit) behind."""
     rng = np.random.default_rng(1000 + seed)
     positions = int(rng.choice([8, 16, 24, 40, 64, 104, 160, 256, 512]))
@@ -193,22 +200,24 @@ def test_random_layer_graphs_both_families_bit_identical(lib, seed):
     ladders = int(rng.integers(3, 20))
     sweeps, interval = int(rng.integers(4, 12)), int(rng.integers(1, 4))
     gamma = float(rng.choice([1.0, 1.25]))
-    out = {}
-    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC):
+    chain = int(rng.integers(0, ladders * betas.size))
+    first = None
+    for family in (ib.KERNEL_LAYERED, ib.KERNEL_GENERIC, ib.KERNEL_STRAND):
+        if family == ib.KERNEL_STRAND and positions < 16:
+            continue  # the strand family wants two chunks of 8 positions at least
         with ib.init_state(model, betas, ladders, base_seed=7 + seed, swap_base_seed=99 + seed, kernel=family,
                            params=ib.SweepParams(gamma, 2)) as st:
             assert st.info()["kernel"] == family
             st.run(sweeps, interval)
             st.run(3, interval)
-            chain = int(rng.integers(0, ladders * betas.size)) if family == ib.KERNEL_LAYERED else out["chain"]
             hs, ht = st.fields(chain)
             got = (st.spins(), st.stats()[0], st.slots(), st.running_energies().view(np.uint64),
                    hs.view(np.uint32), ht.view(np.uint32))
-            if family == ib.KERNEL_LAYERED:
-                out["chain"], out["layered"] = chain, got
-            else:
-                for a, b in zip(out["layered"], got):
-                    np.testing.assert_array_equal(a, b)
+        if first is None:
+            first = got
+        else:
+            for a, b in zip(first, got):
+                np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("ISING_FUZZ_SEEDS", "12"))))
@@ -259,3 +268,114 @@ def test_random_multigraphs_generic_family_matches_the_oracle(lib, port, seed):
         st.run(split, interval)
         st.run(sweeps - split, interval)
         assert_batch_matches(st, want, 1e-5)
+
+
+# ---- full-length runs ("bit parity on a subset for the full run") -----------------
+
+def test_c5_full_length_two_ladders_inside_the_batch_and_family_soak(lib, port, c5):
+    """Config 5 for its full 1,000 sweeps (swap every 10) on all 16,384 chains: ladders 1000 and 1001,
+    deep inside the batch, bit for bit against the oracle; and every chain of the batch identical
+    under the strand and the Tensor Memory families (checksum, accept count, slot, running energy,
+    swap counts) — the long run crosses every MT19937 wrap, careful chunk and tape-ring wrap."""
+    wl, csr = c5
+    model = product_model(csr)
+    out = {}
+    for family in (ib.KERNEL_STRAND, ib.KERNEL_LAYERED):
+        with ib.init_state(model, wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE,
+                           swap_base_seed=ins.SWAP_SEED_BASE, kernel=family) as st:
+            st.run(wl.sweeps, wl.swap_interval)
+            out[family] = (st.checksums(), st.stats()[0], st.slots(), st.running_energies().view(np.uint64),
+                           st.swap_stats()[0])
+            if family == ib.KERNEL_STRAND:
+                sample, energies = st.spins(16 * 1000, 32), st.energies()
+                e_run = st.running_energies()
+    for a, b in zip(out[ib.KERNEL_STRAND], out[ib.KERNEL_LAYERED]):
+        np.testing.assert_array_equal(a, b)
+    # the running energy stays within f32-rounding distance of the exact energy over ~2e9 flips a chain
+    np.testing.assert_allclose(e_run, energies, rtol=1e-5)
+    seeds = sharding.chain_seeds(ins.CHAIN_SEED_BASE, 1000, 2, 16)
+    swap_seeds = sharding.ladder_seeds(ins.SWAP_SEED_BASE, 1000, 2)
+    want = oracle_batch(port, [csr], 2, wl.betas, seeds, swap_seeds, wl.sweeps, wl.swap_interval, threads=2)
+    checks, flips, slots, e_bits, _ = out[ib.KERNEL_STRAND]
+    np.testing.assert_array_equal(sample, want["spins"])
+    np.testing.assert_array_equal(flips[16000:16032], want["flips"])
+    np.testing.assert_array_equal(slots[16000:16032], want["slot"])
+    np.testing.assert_array_equal(e_bits[16000:16032], want["e_run"].view(np.uint64))
+
+
+def test_c5_all_chains_first_100_sweeps_against_the_reference_record(lib, golden):
+    """Every one of the 16,384 chains of config 5, 100 sweeps without swaps, against accept counts and
+    final total_cost the REFERENCE produced (tests/golden/make_golden_c5.py -> oracle/_ref): a checksum
+    of checksums over the batch, one per tile to localise a failure, and 64 chains verbatim."""
+    g = golden("c5_first100")
+    wl = workloads.get("c5")
+    csr = wl.make_csrs()[0]
+    with ib.init_state(product_model(csr), wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as st:
+        assert st.info()["n_chains"] == int(g["chains"])
+        st.run(int(g["sweeps"]), 0)
+        flips, energy = st.stats()[0], st.energies()
+    np.testing.assert_array_equal(flips[:64], g["flips_head"])
+    np.testing.assert_array_equal(energy[:64].view(np.uint64), g["energy_head"].view(np.uint64))
+    tiles = flips.size // 32
+    got_f = np.array([fold(flips[32 * t:32 * t + 32]) for t in range(tiles)], np.uint64)
+    got_e = np.array([fold(energy[32 * t:32 * t + 32].view(np.uint64)) for t in range(tiles)], np.uint64)
+    bad = np.nonzero((got_f != g["tile_flips_fold"]) | (got_e != g["tile_energy_fold"]))[0]
+    assert bad.size == 0, f"tiles differing from the reference record: {bad[:10].tolist()}"
+    assert fold(flips) == int(g["flips_fold"]) and fold(energy.view(np.uint64)) == int(g["energy_fold"])
+
+
+def test_c2_full_length_replicas_inside_the_batch(lib, port):
+    """Config 2: 1,024 replicas of the 16^3 lattice with Gaussian fields for the full 10,000 sweeps;
+    replicas 480..511 (one tile in the middle) bit for bit against the oracle."""
+    wl = workloads.get("c2")
+    csr = wl.make_csrs()[0]
+    with ib.init_state(product_model(csr), wl.betas, wl.n_ladders, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as st:
+        st.run(wl.sweeps, 0)
+        sample, flips, energies = st.spins(480, 32), st.stats()[0], st.energies()
+    seeds = sharding.chain_seeds(ins.CHAIN_SEED_BASE, 480, 32, 1)
+    want = oracle_batch(port, [csr], 32, wl.betas, seeds, sharding.ladder_seeds(ins.SWAP_SEED_BASE, 480, 32),
+                        wl.sweeps, 0, threads=16)
+    np.testing.assert_array_equal(sample, want["spins"])
+    np.testing.assert_array_equal(flips[480:512], want["flips"])
+    np.testing.assert_allclose(energies[480:512], want["energy"], rtol=1e-5)
+
+
+def test_c3_full_length_one_ladder_inside_distinct_graphs(lib, port):
+    """Config 3: 32 betas, swap every sweep, distinct mixed-degree graphs, the full 10,000 sweeps; ladder
+    5 of a 12-system batch bit for bit against the oracle (spins, accept counts, slots, running energies)."""
+    wl = workloads.get("c3")
+    systems = 12
+    csrs = [ins.cubic_mixed_degree(16, ins.INSTANCE_SEED + k) for k in range(systems)]
+    with ib.init_state([product_model(c) for c in csrs], wl.betas, systems, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as st:
+        st.run(wl.sweeps, wl.swap_interval)
+        sample = st.spins(5 * 32, 32)
+        flips, slots, e_run = st.stats()[0], st.slots(), st.running_energies()
+    want = oracle_batch(port, [csrs[5]], 1, wl.betas, sharding.chain_seeds(ins.CHAIN_SEED_BASE, 5, 1, 32),
+                        sharding.ladder_seeds(ins.SWAP_SEED_BASE, 5, 1), wl.sweeps, wl.swap_interval)
+    np.testing.assert_array_equal(sample, want["spins"])
+    np.testing.assert_array_equal(flips[160:192], want["flips"])
+    np.testing.assert_array_equal(slots[160:192], want["slot"])
+    np.testing.assert_array_equal(e_run[160:192].view(np.uint64), want["e_run"].view(np.uint64))
+
+
+def test_c4_full_length_one_system_inside_distinct_instances(lib, port):
+    """Config 4: 512x64 layered instances, 32 betas, swap every sweep, the full 5,000 sweeps; system 2
+    of a 4-system batch bit for bit against the oracle."""
+    wl = workloads.get("c4")
+    systems = 4
+    csrs = [ins.build_layered_csr(*ins.layered_spec(512, ins.INSTANCE_SEED + k, 0.5, 6), 64, 1.5) for k in range(systems)]
+    with ib.init_state([product_model(c) for c in csrs], wl.betas, systems, base_seed=ins.CHAIN_SEED_BASE,
+                       swap_base_seed=ins.SWAP_SEED_BASE) as st:
+        assert st.info()["kernel"] == ib.KERNEL_STRAND
+        st.run(wl.sweeps, wl.swap_interval)
+        sample = st.spins(2 * 32, 32)
+        flips, slots, e_run = st.stats()[0], st.slots(), st.running_energies()
+    want = oracle_batch(port, [csrs[2]], 1, wl.betas, sharding.chain_seeds(ins.CHAIN_SEED_BASE, 2, 1, 32),
+                        sharding.ladder_seeds(ins.SWAP_SEED_BASE, 2, 1), wl.sweeps, wl.swap_interval)
+    np.testing.assert_array_equal(sample, want["spins"])
+    np.testing.assert_array_equal(flips[64:96], want["flips"])
+    np.testing.assert_array_equal(slots[64:96], want["slot"])
+    np.testing.assert_array_equal(e_run[64:96].view(np.uint64), want["e_run"].view(np.uint64))
