@@ -340,6 +340,12 @@ class Reference:
         lib.ref_model_from_string.argtypes = [C.c_char_p]
         lib.ref_total_cost.restype = C.c_double
         lib.ref_total_cost.argtypes = [C.c_void_p, f32p]
+        if hasattr(lib, "ref_enumerate_boltzmann"):  # (absent from a library built before round 2)
+            lib.ref_enumerate_boltzmann.restype = C.c_int
+            lib.ref_enumerate_boltzmann.argtypes = [C.c_void_p, C.c_double, f64p, f64p]
+            lib.ref_chain_statistics.restype = C.c_int
+            lib.ref_chain_statistics.argtypes = [C.c_void_p, C.c_int, C.c_float, C.c_float, C.c_int, C.c_uint64,
+                                                 C.c_uint64, C.c_uint32, C.c_uint32, C.c_double, f64p]
         lib.ref_checksum.restype = C.c_uint64
         lib.ref_checksum.argtypes = [f32p, C.c_uint32]
         lib.ref_chain_create.restype = C.c_void_p
@@ -406,6 +412,26 @@ class Reference:
     def checksum(self, spins):
         s = np.ascontiguousarray(spins, np.float32)
         return self.lib.ref_checksum(_p(s, C.c_float), s.size)
+
+    def enumerate_boltzmann(self, model, beta: float) -> dict:
+        """ref: enumerate_boltzmann, src/oracle.cpp:64-109.  probabilities[state], bit i set <=> s_i = +1."""
+        prob = np.empty(1 << model.n_spins, np.float64)
+        mom = np.empty(3, np.float64)
+        if self.lib.ref_enumerate_boltzmann(model.handle, float(beta), _p(prob, C.c_double), _p(mom, C.c_double)):
+            raise ValueError(self.error())
+        return dict(probabilities=prob, mean_cost=float(mom[0]), mean_magnetization=float(mom[1]),
+                    log_partition=float(mom[2]))
+
+    def chain_statistics(self, model, beta, *, engine=1, tau_scale=1.0, exp_kind=EXP_EXACT, sweeps=20000,
+                         burn_in=2000, replicates=12, base_seed=1, z_threshold=4.0) -> dict:
+        """ref: chain_statistics_test, src/oracle.cpp:111-174."""
+        out = np.empty(9, np.float64)
+        if self.lib.ref_chain_statistics(model.handle, engine, beta, tau_scale, exp_kind, sweeps, burn_in, replicates,
+                                         base_seed, z_threshold, _p(out, C.c_double)):
+            raise ValueError(self.error())
+        keys = ("exact_cost", "exact_magnetization", "est_cost", "est_magnetization", "se_cost", "se_magnetization",
+                "z_cost", "z_magnetization", "pass")
+        return dict(zip(keys, out.tolist()))
 
     def chain(self, model, seed, beta, tau_scale=1.0, exp_kind=EXP_FAST, initial=None, engine=1):
         return RefChain(self, model, seed, beta, tau_scale, exp_kind, initial, engine)

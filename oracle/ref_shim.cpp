@@ -17,6 +17,7 @@
 #include "isingmc/model.hpp"
 #include "isingmc/model_io.hpp"
 #include "isingmc/rng.hpp"
+#include "isingmc/oracle.hpp"
 #include "isingmc/sweep.hpp"
 
 using namespace isingmc;
@@ -320,6 +321,50 @@ void ref_ladders_read(const void* p, uint64_t* flips_out, double* energy_out) {
             if (energy_out) energy_out[c] = total_cost(*lad.model, std::span<const float>(s.spins));
             ++c;
         }
+    }
+}
+
+// ---- the reference's own validators (src/oracle.cpp:64-174): exact enumeration and the
+// replicate-means z-test, for pinning what can be pinned of the tempering sampler.
+// probabilities: 2^n entries, state index bit i set <=> s_i = +1 (oracle.hpp:13); moments[3] =
+// {mean_cost, mean_magnetization, log_partition}.  Returns 0, or -1 with ref_last_error().
+int ref_enumerate_boltzmann(const void* m, double beta, double* probabilities, double* moments) {
+    try {
+        const ExactDistribution d = enumerate_boltzmann(*static_cast<const SpinModel*>(m), beta);
+        if (probabilities) std::copy(d.probabilities.begin(), d.probabilities.end(), probabilities);
+        if (moments) {
+            moments[0] = d.mean_cost;
+            moments[1] = d.mean_magnetization;
+            moments[2] = d.log_partition;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// out[9] = {exact_cost, exact_magnetization, est_cost, est_magnetization, se_cost, se_magnetization,
+// z_cost, z_magnetization, pass}
+int ref_chain_statistics(const void* m, int engine, float beta, float tau_scale, int exp_kind, uint64_t sweeps,
+                         uint64_t burn_in, uint32_t replicates, uint32_t base_seed, double z_threshold, double* out) {
+    try {
+        ChainStatsConfig cfg;
+        cfg.engine = engine_of(engine);
+        cfg.params = {beta, tau_scale, exp_of(exp_kind)};
+        cfg.sweeps = sweeps;
+        cfg.burn_in = burn_in;
+        cfg.replicates = replicates;
+        cfg.base_seed = base_seed;
+        cfg.z_threshold = z_threshold;
+        const ChainStatsReport r = chain_statistics_test(*static_cast<const SpinModel*>(m), cfg);
+        const double v[9] = {r.exact_cost, r.exact_magnetization, r.est_cost, r.est_magnetization, r.se_cost,
+                             r.se_magnetization, r.z_cost, r.z_magnetization, r.pass ? 1.0 : 0.0};
+        std::copy(v, v + 9, out);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
     }
 }
 

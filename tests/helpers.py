@@ -71,4 +71,48 @@ def random_graph(n, mean_degree, seed, repeats=0):
     return ins.csr_from_adjacency(h, ins._adjacency(n, np.array(edges, np.int64), coup))
 
 
-__all__ = ["random_graph", "csr_from_npz", "product_model", "bits", "oracle_batch", "assert_batch_matches", "ins", "ib"]
+# ---- a 12-spin model small enough to enumerate (statistical validation of the tempering sampler)
+SMALL_N = 12
+N = SMALL_N
+
+
+def small_model(seed):
+    """12 spins, ~degree 4, Gaussian couplings and fields (f32 values, exact in f64)."""
+    rng = ins.MT19937(seed)
+    edges = {}
+    for i in range(N):
+        edges[(i, (i + 1) % N)] = 0.0
+    while len(edges) < 24:
+        a, b = rng.below(N), rng.below(N)
+        if a != b:
+            edges.setdefault((min(a, b), max(a, b)), 0.0)
+    js = rng.normals(len(edges), 0.8)
+    h = rng.normals(N, 0.4).astype(np.float32)
+    pairs = [(a, b, np.float32(j)) for (a, b), j in zip(sorted(edges), js)]
+    adj = [[] for _ in range(N)]
+    for a, b, j in pairs:
+        adj[a].append((b, j))
+        adj[b].append((a, j))
+    offsets, targets, couplings = [0], [], []
+    for i in range(N):
+        for t, j in sorted(adj[i]):
+            targets.append(t)
+            couplings.append(j)
+        offsets.append(len(targets))
+    csr = dict(n_spins=N, h=h, offsets=np.array(offsets, np.uint32), targets=np.array(targets, np.uint32),
+               couplings=np.array(couplings, np.float32), tau_counts=np.zeros(N, np.uint8), layers=0, per_layer=0)
+    return csr, pairs, h
+
+
+def enumerate_energies(pairs, h):
+    """E(s) = -sum h_i s_i - sum_{i<j} J_ij s_i s_j for all 4096 states; bit i of the state index set
+    <=> s_i = -1 (ref sign convention: total_cost, src/model.cpp:108-126)."""
+    idx = np.arange(1 << N)
+    s = 1.0 - 2.0 * ((idx[:, None] >> np.arange(N)[None, :]) & 1)
+    e = -(s @ h.astype(np.float64))
+    for a, b, j in pairs:
+        e -= float(j) * s[:, a] * s[:, b]
+    return e
+
+
+__all__ = ["random_graph", "csr_from_npz", "product_model", "bits", "oracle_batch", "assert_batch_matches", "ins", "ib", "SMALL_N", "small_model", "enumerate_energies"]

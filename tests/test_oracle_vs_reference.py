@@ -82,3 +82,35 @@ def test_layered_builder_agrees(ref):
     theirs = ref.build_layered(positions, h, edges, 7, 1.25).csr()
     for key in ("h", "offsets", "targets", "couplings", "tau_counts"):
         np.testing.assert_array_equal(mine[key], theirs[key])
+
+
+def test_numpy_enumeration_equals_the_reference_enumerate_boltzmann(ref):
+    """The exact distributions the GPU statistics tests compare against (tests/helpers.py:
+    enumerate_energies, restated with numpy) against the reference's own validator
+    (ref: enumerate_boltzmann, proj/src/oracle.cpp:64-109) on the same 12-spin model: every state
+    probability, the mean cost and the mean magnetization.  The reference indexes states with bit i
+    set for s_i = +1, the tests with bit i set for s_i = -1: complementary indices."""
+    from helpers import SMALL_N, enumerate_energies, small_model
+    csr, pairs, h = small_model(2024)
+    energies = enumerate_energies(pairs, h)
+    model = ref.model(csr)
+    full = (1 << SMALL_N) - 1
+    for beta in (0.15, 0.5, 1.7):
+        exact = ref.enumerate_boltzmann(model, beta)
+        w = np.exp(-beta * (energies - energies.min()))
+        prob = w / w.sum()
+        np.testing.assert_allclose(prob[full - np.arange(full + 1)], exact["probabilities"], rtol=1e-10, atol=1e-300)
+        assert abs((prob * energies).sum() - exact["mean_cost"]) < 1e-10
+        spins = 1.0 - 2.0 * ((np.arange(full + 1)[:, None] >> np.arange(SMALL_N)[None, :]) & 1)
+        assert abs((prob * spins.mean(axis=1)).sum() - exact["mean_magnetization"]) < 1e-12
+
+
+def test_reference_chain_statistics_accepts_the_oracle_model(ref):
+    """The reference's replicate-means z-test (ref: chain_statistics_test, proj/src/oracle.cpp:111-174)
+    runs on the small model through the shim and passes for its own basic engine: the same bounds
+    are applied to the device ladder in tests/test_gpu_statistics.py."""
+    from helpers import small_model
+    csr, _, _ = small_model(2024)
+    rep = ref.chain_statistics(ref.model(csr), 0.5, sweeps=20000, burn_in=2000, replicates=12, base_seed=7)
+    assert rep["pass"] == 1.0 and rep["z_cost"] <= 4.0 and rep["z_magnetization"] <= 4.0
+    assert abs(rep["est_cost"] - rep["exact_cost"]) < 0.05 * abs(rep["exact_cost"])
