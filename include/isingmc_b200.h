@@ -171,6 +171,15 @@ ISING_B200_API ising_status ising_batch_read_swap_stats(ising_batch* batch, uint
  * into a DEVICE buffer (e.g. a torch CUDA tensor) so a multi-GPU caller can gather results
  * with one NCCL all-gather and no host round trip.  device_out: n_chains * 32 bytes. */
 ISING_B200_API ising_status ising_batch_pack_results(ising_batch* batch, void* device_out);
+/* The same records of EVERY rank's shard, gathered over NCCL (NVLink / NVSwitch) on the batch's own
+ * stream: packs this rank's records and calls ncclAllGather on `nccl_comm` (an ncclComm_t of the
+ * caller, every rank holding the same number of chains — the weak-scaling layout of the bench).
+ * device_out_all: n_ranks * n_chains * 32 bytes of DEVICE memory, rank-major.  This is the data
+ * path's only collective; it replaces the shared-memory result vectors of the reference's chain
+ * pool (ref: src/bench.cpp:51-84: one RepetitionResult per chain, filled by the workers).  NCCL is
+ * looked up at run time (the libnccl.so.2 the process has loaded, else the system's): the library
+ * has no link-time dependency on it.  ISING_ERR_INTERNAL when NCCL is missing or reports an error. */
+ISING_B200_API ising_status ising_batch_all_gather_results(ising_batch* batch, void* nccl_comm, void* device_out_all);
 
 /* --- introspection / measurement --- */
 typedef struct ising_batch_info {

@@ -32,6 +32,9 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", str(HERE), "oracle"], check=True)
     if ref and REFERENCE_ROOT.exists():
         subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+        # the reference-side binding of INTEGRATION.md, against the product library when that is built
+        if (HERE.parent / "paper_1004_0024_b200" / "libisingb200.so").exists():
+            subprocess.run(["make", "-s", "-C", str(HERE), "binding"], check=True)
 
 
 def _p(a, ctype):

@@ -87,6 +87,7 @@ SIGNATURES = {
     "ising_batch_read_slots": (C.c_int, [C.c_void_p, u32p]),
     "ising_batch_read_swap_stats": (C.c_int, [C.c_void_p, u64p, u64p]),
     "ising_batch_pack_results": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ising_batch_all_gather_results": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ising_batch_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "ising_batch_record_wait": (C.c_int, [C.c_void_p, C.c_int]),
     "ising_batch_read_wait_stats": (C.c_int, [C.c_void_p, C.c_uint32, u32p, f64p, u64p, u64p]),

@@ -256,6 +256,11 @@ class BatchState:
     def pack_results(self, device_ptr: int) -> None:
         _check(L.load().ising_batch_pack_results(self._h, C.c_void_p(device_ptr)))
 
+    def all_gather_results(self, nccl_comm: int, device_ptr: int) -> None:
+        """Packs this shard's records and all-gathers every rank's over `nccl_comm` (an ncclComm_t as an
+        integer) into device memory at `device_ptr` (n_ranks * n_chains * 32 bytes)."""
+        _check(L.load().ising_batch_all_gather_results(self._h, C.c_void_p(nccl_comm), C.c_void_p(device_ptr)))
+
     def record_wait(self, on: bool = True) -> None:
         """Starts (counters zeroed) or stops recording wait statistics (ref: EngineConfig::stats_widths)."""
         _check(L.load().ising_batch_record_wait(self._h, int(on)))

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <atomic>
 #include <cstdlib>
+#include <dlfcn.h>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -972,6 +973,40 @@ void Batch::pack_results(void* device_out) {
     cuda_check(launch_pack_results(dev_, device_out, stream_), "pack kernel");
     ++other_launches;
     cuda_check(cudaStreamSynchronize(stream_), "pack");
+}
+
+}  // namespace isingb200
+
+namespace isingb200 {
+
+// NCCL, found at run time: the copy the process has loaded already (the caller's communicator belongs
+// to it), else the system's.  ncclAllGather(send, recv, count, datatype, comm, stream); ncclInt64 == 4.
+void Batch::all_gather_results(void* nccl_comm, void* device_out_all) {
+    bind_device();
+    if (nccl_comm == nullptr || device_out_all == nullptr) throw Error("null argument");
+    using AllGather = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
+    using ErrorString = const char* (*)(int);
+    static void* handle = nullptr;
+    static AllGather all_gather = nullptr;
+    static ErrorString error_string = nullptr;
+    if (all_gather == nullptr) {
+        handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (handle == nullptr) handle = dlopen("libnccl.so.2", RTLD_NOW);
+        if (handle == nullptr) handle = dlopen("libnccl.so", RTLD_NOW);
+        if (handle == nullptr) throw CudaError("NCCL not found (libnccl.so.2): " + std::string(dlerror() ? dlerror() : ""));
+        all_gather = reinterpret_cast<AllGather>(dlsym(handle, "ncclAllGather"));
+        error_string = reinterpret_cast<ErrorString>(dlsym(handle, "ncclGetErrorString"));
+        if (all_gather == nullptr) throw CudaError("NCCL has no ncclAllGather");
+    }
+    const size_t bytes = size_t(dev_.n_chains) * 32;
+    size_t ignored = 0;
+    if (gather_send_.bytes() < bytes) gather_send_.allocate(std::max<size_t>(bytes, 32), ignored);
+    cuda_check(launch_pack_results(dev_, gather_send_.as<void>(), stream_), "pack kernel");
+    ++other_launches;
+    const int rc = all_gather(gather_send_.as<void>(), device_out_all, size_t(dev_.n_chains) * 4, /*ncclInt64*/ 4, nccl_comm,
+                              stream_);
+    if (rc != 0) throw CudaError(std::string("ncclAllGather: ") + (error_string ? error_string(rc) : "error"));
+    cuda_check(cudaStreamSynchronize(stream_), "all-gather");
 }
 
 }  // namespace isingb200

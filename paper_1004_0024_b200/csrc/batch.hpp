@@ -76,6 +76,7 @@ class Batch {
     void read_slots(uint32_t* out);
     void read_swap_stats(uint64_t* acc, uint64_t* att);
     void pack_results(void* device_out);
+    void all_gather_results(void* nccl_comm, void* device_out_all);
 
     void set_timing(bool on) { timing_ = on; }
     // wait statistics (ref: FlipStats::group_wait): recording starts (counters zeroed) or stops
@@ -132,6 +133,7 @@ class Batch {
     uint32_t strand_warps_ = 0;
     bool l2_window_set_ = false;
     DeviceBuffer scratch_;  // readout staging
+    DeviceBuffer gather_send_;  // this rank's packed records on their way into the all-gather
     int sm_count_ = 0;
 
     // timing

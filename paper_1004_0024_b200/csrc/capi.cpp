@@ -369,6 +369,13 @@ ising_status ising_batch_pack_results(ising_batch* batch, void* device_out) {
     });
 }
 
+ising_status ising_batch_all_gather_results(ising_batch* batch, void* nccl_comm, void* device_out_all) {
+    return guarded([&]() {
+        impl_of(batch).all_gather_results(nccl_comm, device_out_all);
+        return ISING_OK;
+    });
+}
+
 ising_status ising_batch_set_timing(ising_batch* batch, int timing) {
     return guarded([&]() {
         impl_of(batch).set_timing(timing != 0);

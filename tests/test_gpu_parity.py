@@ -490,3 +490,40 @@ def test_generic_family_high_degree_ragged_and_repeated_edges(lib, port, exp_kin
     state, want = run_both(port, [plain], 3, betas, 150, 2, exp_kind=exp_kind, kernel=ib.KERNEL_GENERIC)
     assert state.info()["generic_variant"] == 2
     assert_batch_matches(state, want, REL_ENERGY)
+
+
+def test_results_all_gather_through_the_c_entry(lib):
+    """ising_batch_all_gather_results: the data path's only collective behind the C ABI, for callers
+    without torch.  One rank here (the run has one GPU): a 1-rank NCCL communicator made with NCCL's own
+    C API, the gathered records against ising_batch_pack_results and the host readouts."""
+    import ctypes as C
+    import torch
+    torch.cuda.set_device(0)
+    nccl = C.CDLL("libnccl.so.2")  # the copy torch has loaded: the library looks it up the same way
+
+    class UniqueId(C.Structure):
+        _fields_ = [("internal", C.c_char * 128)]
+
+    nccl.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, UniqueId, C.c_int]
+    nccl.ncclCommDestroy.argtypes = [C.c_void_p]
+    uid, comm = UniqueId(), C.c_void_p()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        csr = ins.build_layered_csr(*ins.layered_spec(32, 3), 8, 1.5)
+        betas = ins.geometric_betas(0.3, 2.0, 4)
+        with ib.init_state(product_model(csr), betas, 10, base_seed=5, swap_base_seed=6) as st:
+            st.run(12, 3)
+            chains = st.n_chains
+            gathered = torch.zeros((chains, 4), dtype=torch.int64, device="cuda")
+            packed = torch.zeros((chains, 4), dtype=torch.int64, device="cuda")
+            st.all_gather_results(comm.value, gathered.data_ptr())
+            st.pack_results(packed.data_ptr())
+            torch.cuda.synchronize()
+            rec = gathered.cpu().numpy()
+            np.testing.assert_array_equal(rec, packed.cpu().numpy())
+            np.testing.assert_array_equal(rec[:, 0].view(np.float64), st.energies())
+            np.testing.assert_array_equal(rec[:, 2].view(np.uint64), st.stats()[0])
+            np.testing.assert_array_equal(rec[:, 3].view(np.uint64), st.checksums())
+    finally:
+        nccl.ncclCommDestroy(comm)
