@@ -156,6 +156,12 @@ ISING_B200_API ising_status ising_batch_read_fields(ising_batch* batch, uint64_t
 ISING_B200_API ising_status ising_batch_read_energies(ising_batch* batch, double* out);
 /* Running energy used by the swap rule (initial cost + sum of flip energies). */
 ISING_B200_API ising_status ising_batch_read_running_energies(ising_batch* batch, double* out);
+/* Recomputes every chain's running energy from its spins (the tempering cost: total_cost with the
+ * tau couplings scaled by tau_scale, oracle: orc_tempering_cost), discarding the rounding the flip
+ * energies have accumulated.  New: the reference has no running energy.  Optional — a long
+ * tempering run may call it every few thousand sweeps; a parity run sets the oracle chain's e_run to
+ * orc_tempering_cost at the same sweep counts. */
+ISING_B200_API ising_status ising_batch_resync_energies(ising_batch* batch);
 /* ref: FlipStats::flips / attempts (sweep.hpp:38-44). Either pointer may be NULL. */
 ISING_B200_API ising_status ising_batch_read_stats(ising_batch* batch, uint64_t* flips, uint64_t* attempts);
 /* ref: state_checksum (sweep_state.cpp:325-336): FNV-1a over the sign sequence. */

@@ -81,6 +81,7 @@ SIGNATURES = {
     "ising_batch_read_fields": (C.c_int, [C.c_void_p, C.c_uint64, f32p, f32p]),
     "ising_batch_read_energies": (C.c_int, [C.c_void_p, f64p]),
     "ising_batch_read_running_energies": (C.c_int, [C.c_void_p, f64p]),
+    "ising_batch_resync_energies": (C.c_int, [C.c_void_p]),
     "ising_batch_read_stats": (C.c_int, [C.c_void_p, u64p, u64p]),
     "ising_batch_checksums": (C.c_int, [C.c_void_p, u64p]),
     "ising_batch_field_coherence": (C.c_int, [C.c_void_p, u64p]),

@@ -231,6 +231,10 @@ class BatchState:
     def running_energies(self) -> np.ndarray:
         return self._f64(L.load().ising_batch_read_running_energies)
 
+    def resync_energies(self) -> None:
+        """Running energies := tempering cost of the current spins (drops accumulated rounding)."""
+        _check(L.load().ising_batch_resync_energies(self._h))
+
     def stats(self):
         flips, attempts = np.empty(self.n_chains, np.uint64), np.empty(self.n_chains, np.uint64)
         _check(L.load().ising_batch_read_stats(self._h, _p(flips, C.c_uint64), _p(attempts, C.c_uint64)))

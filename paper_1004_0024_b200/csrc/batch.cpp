@@ -27,9 +27,10 @@ void DeviceBuffer::allocate(size_t bytes, size_t& tally) {
         cudaFree(ptr_);
         ptr_ = nullptr;
     }
-    bytes_ = bytes;
+    bytes_ = 0;
     if (bytes == 0) return;
     cuda_check(cudaMalloc(&ptr_, bytes), "cudaMalloc");
+    bytes_ = bytes;  // (only once the memory exists: a failed allocation leaves an empty buffer)
     tally += bytes;
 }
 
@@ -314,6 +315,32 @@ static std::vector<uint4> build_cost_terms(const HostModel& m, float tau_scale =
 Batch::Batch(const std::vector<const HostModel*>& models,
              const std::vector<uint32_t>& model_of_ladder, const BatchConfig& cfg,
              const int8_t* initial_spins) {
+    // The destructor does not run for an object whose constructor throws: release what the body had
+    // created by then (stream, events; the DeviceBuffer members clean up after themselves).
+    try {
+        construct(models, model_of_ladder, cfg, initial_spins);
+    } catch (...) {
+        release_cuda_objects();
+        throw;
+    }
+}
+
+void Batch::release_cuda_objects() {
+    for (TimedLaunch& t : pending_) {
+        cudaEventDestroy(t.start);
+        cudaEventDestroy(t.stop);
+    }
+    pending_.clear();
+    if (run_start_ != nullptr) cudaEventDestroy(run_start_);
+    if (run_stop_ != nullptr) cudaEventDestroy(run_stop_);
+    if (stream_ != nullptr) cudaStreamDestroy(stream_);
+    run_start_ = run_stop_ = nullptr;
+    stream_ = nullptr;
+}
+
+void Batch::construct(const std::vector<const HostModel*>& models,
+                      const std::vector<uint32_t>& model_of_ladder, const BatchConfig& cfg,
+                      const int8_t* initial_spins) {
     // ---- argument checks (ref: check_engine_model, sweep_state.cpp:108-158)
     if (models.empty()) throw Error("init_state: no model given");
     if (cfg.n_ladders == 0 || cfg.n_betas == 0) throw Error("init_state: batch needs at least one chain");
@@ -397,6 +424,13 @@ Batch::Batch(const std::vector<const HostModel*>& models,
               : (cfg.kernel != int(KernelFamily::generic) && layered_ok) ? KernelFamily::layered
                                                                          : KernelFamily::generic;
     if (family_ != KernelFamily::generic) any_tau = false;  // the tau field is rebuilt, never stored
+
+    if (initial_spins != nullptr) {  // (host-side validation first: nothing to release on failure)
+        const size_t total = size_t(chains64) * n;
+        for (size_t k = 0; k < total; ++k) {
+            if (initial_spins[k] != 1 && initial_spins[k] != -1) throw Error("init_state: spins must be +/-1");
+        }
+    }
 
     // ---- device
     int count = 0;
@@ -667,9 +701,6 @@ Batch::Batch(const std::vector<const HostModel*>& models,
     size_t ignored = 0;
     if (initial_spins != nullptr) {
         const size_t total = chains * n;
-        for (size_t k = 0; k < total; ++k) {
-            if (initial_spins[k] != 1 && initial_spins[k] != -1) throw Error("init_state: spins must be +/-1");
-        }
         initial_dev.allocate(std::max<size_t>(1, total), ignored);
         cuda_check(cudaMemcpyAsync(initial_dev.as<void>(), initial_spins, total, cudaMemcpyHostToDevice,
                                    stream_),
@@ -720,13 +751,7 @@ Batch::~Batch() {
         cudaCtxResetPersistingL2Cache();
         cudaGetLastError();
     }
-    for (TimedLaunch& t : pending_) {
-        cudaEventDestroy(t.start);
-        cudaEventDestroy(t.stop);
-    }
-    if (run_start_ != nullptr) cudaEventDestroy(run_start_);
-    if (run_stop_ != nullptr) cudaEventDestroy(run_stop_);
-    if (stream_ != nullptr) cudaStreamDestroy(stream_);
+    release_cuda_objects();
 }
 
 void Batch::begin_timed(bool is_swap) {
@@ -884,6 +909,12 @@ void Batch::read_energies(double* out) {
     cuda_check(launch_energies(dev_, scratch_.as<double>(), stream_), "energy kernel");
     ++other_launches;
     download(out, scratch_.as<void>(), dev_.n_chains, stream_);
+}
+
+void Batch::resync_energies() {
+    bind_device();
+    cuda_check(launch_resync_energies(dev_, stream_), "energy resync kernel");
+    ++other_launches;
 }
 
 void Batch::read_running_energies(double* out) {

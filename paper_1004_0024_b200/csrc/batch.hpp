@@ -70,6 +70,7 @@ class Batch {
     void read_fields(uint64_t chain, float* hs, float* ht);
     void read_energies(double* out);
     void read_running_energies(double* out);
+    void resync_energies();
     void read_stats(uint64_t* flips, uint64_t* attempts);
     void read_checksums(uint64_t* out);
     void read_coherence(uint64_t* out);
@@ -107,6 +108,9 @@ class Batch {
         cudaEvent_t start, stop;
         bool is_swap;
     };
+    void construct(const std::vector<const HostModel*>& models, const std::vector<uint32_t>& model_of_ladder,
+                   const BatchConfig& cfg, const int8_t* initial_spins);
+    void release_cuda_objects();
     void bind_device() const;
     void launch_sweeps(uint32_t sweeps);
     void launch_swap_round();

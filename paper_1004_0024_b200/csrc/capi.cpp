@@ -327,6 +327,13 @@ ising_status ising_batch_read_running_energies(ising_batch* batch, double* out) 
     });
 }
 
+ising_status ising_batch_resync_energies(ising_batch* batch) {
+    return guarded([&]() {
+        impl_of(batch).resync_energies();
+        return ISING_OK;
+    });
+}
+
 ising_status ising_batch_read_stats(ising_batch* batch, uint64_t* flips, uint64_t* attempts) {
     return guarded([&]() {
         impl_of(batch).read_stats(flips, attempts);

@@ -170,6 +170,7 @@ uint32_t strand_flag_words(uint32_t n_tiles, uint32_t strands);
 size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges, uint32_t n_groups);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);
+cudaError_t launch_resync_energies(const DevBatch& b, cudaStream_t stream);  // e_run := tempering cost of the spins
 cudaError_t launch_checksums(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);
 cudaError_t launch_coherence(const DevBatch& b, unsigned long long* out_dev, cudaStream_t stream);
 cudaError_t launch_unpack_spins(const DevBatch& b, uint32_t first_chain, uint32_t n_chains,

@@ -851,6 +851,13 @@ __global__ void __launch_bounds__(kThreads) energies_kernel(DevBatch b, double* 
     if (t.active) out[t.chain] = cost;
 }
 
+__global__ void __launch_bounds__(kThreads) resync_energies_kernel(DevBatch b) {
+    TileView t;
+    if (!open_tile(b, t)) return;
+    const double cost = chain_cost(t.model, t.model.tempering_terms, t.words, t.lane);  // as init_kernel does
+    if (t.active) b.e_run[t.chain] = cost;
+}
+
 __global__ void __launch_bounds__(kThreads) checksums_kernel(DevBatch b, unsigned long long* out) {
     TileView t;
     if (!open_tile(b, t) || !t.active) return;
@@ -963,6 +970,11 @@ cudaError_t launch_sweep_generic(const DevBatch& b, uint32_t sweeps, cudaStream_
 
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t s) {
     swap_kernel<<<(b.n_ladders + 127) / 128, 128, 0, s>>>(b, round);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resync_energies(const DevBatch& b, cudaStream_t s) {
+    resync_energies_kernel<<<tile_grid(b), kThreads, 0, s>>>(b);
     return cudaGetLastError();
 }
 

@@ -527,3 +527,30 @@ def test_results_all_gather_through_the_c_entry(lib):
             np.testing.assert_array_equal(rec[:, 3].view(np.uint64), st.checksums())
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.parametrize("gamma", [1.0, 0.7])
+def test_resync_energies_sets_the_tempering_cost(lib, port, gamma):
+    """ising_batch_resync_energies: running energy := orc_tempering_cost of the current spins, in every
+    family."""
+    positions, h, edges = ins.layered_spec(16, 31)
+    csr = ins.build_layered_csr(positions, h, edges, 8, 0.75)
+    omodel = port.model(csr)
+    betas = ins.geometric_betas(0.3, 1.2, 3)
+    for family in LAYERED_KERNELS:
+        with ib.init_state(product_model(csr), betas, 11, base_seed=77, params=ib.SweepParams(gamma, 2),
+                           kernel=family) as st:
+            st.run(40, 4)
+            drifted = st.running_energies()
+            st.resync_energies()
+            fresh = st.running_energies()
+            spins = st.spins(0, st.n_chains)
+            want = np.array([port.tempering_cost(omodel, s, gamma) for s in spins])
+            np.testing.assert_array_equal(fresh, want)
+            np.testing.assert_allclose(drifted, want, rtol=REL_ENERGY, atol=1e-4)
+            if gamma == 1.0:
+                np.testing.assert_array_equal(fresh, st.energies())
+            # the next sweeps add their flip energies to the resynchronised value
+            st.run(3, 0)
+            after = np.array([port.tempering_cost(omodel, s, gamma) for s in st.spins(0, st.n_chains)])
+            np.testing.assert_allclose(st.running_energies(), after, rtol=REL_ENERGY, atol=1e-4)
