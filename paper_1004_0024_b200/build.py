@@ -20,7 +20,9 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libisingb200.so"
 
 SOURCES = ["host_model.cpp", "model_text.cpp", "batch.cpp", "coalesced.cpp", "capi.cpp", "kernels_generic.cu", "kernels_layered.cu", "kernels_strand.cu", "kernels_coalesced.cu"]
+# ISING_NVCC_DEFINES: extra -D flags for timing experiments (profiles/), never set for the product build
 NVCC_FLAGS = [*(["-DISING_STRAND_PROFILE"] if os.environ.get("ISING_STRAND_PROFILE") else []),
+    *os.environ.get("ISING_NVCC_DEFINES", "").split(),
     "-std=c++17", "-O3", "-lineinfo", "-fmad=false",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-Wall,-Wextra,-fvisibility=hidden",

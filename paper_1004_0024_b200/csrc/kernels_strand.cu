@@ -580,10 +580,12 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                     if (lane == uint32_t(k)) wait_fold(ballot, wait);
                 }
             }
+#ifndef ISING_X_NO_FAR  // (timing experiment: wrong trajectories)
             if ((chunk_info.y >> 16) != 0u && __any_sync(0xffffffffu, acc8 != 0u)) {
                 if (RED) apply_edges_red(hs_l, t, chunk_info.y, acc8, cb.cur8);
                 else apply_groups_rmw(hs_l, t, chunk_info.x, acc8, cb.cur8);
             }
+#endif
             ++seq;
             ISING_TICK(tD);
             if (more) {
@@ -951,19 +953,22 @@ cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count
     if (b.n_tiles == 0 || sweeps == 0) return cudaSuccess;
     const uint32_t capacity = uint32_t(sm_count) * warps_per_cta;
     const uint32_t per_tile = b.strands + 1;
-    const uint32_t tiles_per_round = min(b.n_tiles, capacity / per_tile);
-    if (tiles_per_round == 0) return cudaErrorInvalidConfiguration;
+    const uint32_t most_tiles = min(b.n_tiles, capacity / per_tile);
+    if (most_tiles == 0) return cudaErrorInvalidConfiguration;
+    // rounds of equal size, and every SM in use: the items of a round (S + 1 warps per tile) are dealt
+    // over all `sm_count` CTAs, each just wide enough (c5: 2560 items = 148 CTAs of 18 warps, not 128 of 20)
+    const uint32_t rounds = (b.n_tiles + most_tiles - 1) / most_tiles;
+    const uint32_t tiles_per_round = (b.n_tiles + rounds - 1) / rounds;
     cudaError_t e = cudaMemsetAsync(b.strand_flags, 0, size_t(strand_flag_words(b.n_tiles, b.strands)) * 4, stream);
     if (e != cudaSuccess) return e;
     const size_t cells = size_t(b.n_tiles) * (b.n_spins / 8) * 32;
     const unsigned convert_blocks = unsigned((cells + 255) / 256);
     words_to_bytes_kernel<<<convert_blocks, 256, 0, stream>>>(b);
-    // no more CTAs than the first round's items need
     const uint32_t items = tiles_per_round * per_tile;
-    const uint32_t ctas = min(uint32_t(sm_count), (items + warps_per_cta - 1) / warps_per_cta);
+    const uint32_t ctas = min(uint32_t(sm_count), items);
+    warps_per_cta = (items + ctas - 1) / ctas;  // <= the caller's bound, since items <= capacity
     const dim3 grid(ctas), block(warps_per_cta * 32);
-    // items are dealt warp-major over the launched CTAs: recompute the round size for this grid
-    const uint32_t round = min(b.n_tiles, ctas * warps_per_cta / per_tile);
+    const uint32_t round = tiles_per_round;
     const size_t smem = size_t(warps_per_cta) * kWarpSmem;  // (+ the staged graph, see launch_strand_exp)
     switch (b.exp_kind) {
         case kExpExact: e = launch_strand_exp<kExpExact>(b, sweeps, grid, block, smem, round, stream); break;
