@@ -168,8 +168,8 @@ HostLayerGraph build_layer_graph(const HostModel& m, float tau_scale) {
 
 // Host-side image of DevStrandGraph (see device_batch.hpp and kernels_strand.cu).
 struct HostStrandGraph {
-    std::vector<uint4> pos, band_pm, chunks, edges;
-    std::vector<uint32_t> groups, tau;
+    std::vector<uint4> pos, band_pm, chunks, edges, inslots;
+    std::vector<uint32_t> tau;
 };
 
 HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
@@ -178,68 +178,79 @@ HostStrandGraph build_strand_graph(const HostModel& m, float tau_scale) {
     out.pos.resize(P);
     out.band_pm.resize(2 * size_t(P));
     out.chunks.resize(P / 8);
-    struct Edge { uint32_t k, t, j2; };
+    struct NearEdge { uint32_t k, t, j2; };
+    // A far edge q -> t is PULLED by its target: {q, index in q's list, 2J} per target, in the order the
+    // reference applies them to h[t] between two attempts of t — sources after t (the sweep before),
+    // then sources before t (this sweep), each group in attempt order.
+    struct InEdge { uint32_t q, e, j2; };
+    std::vector<std::vector<InEdge>> incoming(P);
+    std::vector<std::vector<NearEdge>> near_of(P);
+    for (uint32_t p = 0; p < P; ++p) {
+        const uint32_t p0 = p / 8 * 8;
+        uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
+        for (uint32_t e = m.layer_offsets[p]; e < m.layer_offsets[p + 1]; ++e) {
+            const uint32_t t = m.layer_targets[e];
+            const uint32_t doubled = bits(2.0f * m.layer_couplings[e]);  // exact
+            if (is_band(p, t)) {
+                const int off = int(t) - int(p);               // -2, -1, +1, +2
+                const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
+                j2[slot] = doubled;
+                mask[slot] = 0;
+            } else if (t > p && t <= p0 + 10) {
+                // the target column is on its way into the register window already (the chunk loads
+                // p0+3 .. p0+10 at its start and pulls their far updates then): pushed, through the scratch
+                near_of[p].push_back({p - p0, t, doubled});
+            } else {
+                incoming[t].push_back({p, e, doubled});
+            }
+        }
+        const float tau2g = tau_scale * (2.0f * m.layer_tau[p]);  // f32 product, as gamma * h_tau in the reference
+        out.pos[p] = make_uint4(bits(tau2g), 0, 0, 0);
+        out.tau.push_back(bits(tau2g));
+        // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign of -s; an
+        // empty slot adds -0.0.  Entry 2p is for s = -1, entry 2p+1 for s = +1.
+        for (uint32_t neg = 0; neg < 2; ++neg) {
+            const uint32_t flip = neg ? 0x80000000u : 0u;
+            out.band_pm[2 * size_t(p) + neg] = make_uint4((j2[0] ^ flip) | mask[0], (j2[1] ^ flip) | mask[1],
+                                                         (j2[2] ^ flip) | mask[2], (j2[3] ^ flip) | mask[3]);
+        }
+    }
+    // slot: {bits of 2J, meta}; meta = shift | byte offset of the source chunk's cell row << 8, the shift
+    // (23 - bit) moving the source's spin bit (8 + bit of its cell) to bit 31 and its flip bit to bit 23.
+    // The null slot shifts by 31 (bit 23 ends up clear: never flipped) and adds -0.0.
+    const uint32_t null_j2 = 0x80000000u, null_meta = 31u;
+    const auto slot_of = [](const InEdge& in) { return (23u - (in.q & 7u)) | ((in.q / 8u) * 64u) << 8; };
+    std::vector<bool> extra_in(P, false);
+    out.inslots.assign(size_t(P) + 8, make_uint4(null_j2, null_meta, null_j2, null_meta));
+    for (uint32_t t = 0; t < P; ++t) {
+        std::vector<InEdge>& in = incoming[t];
+        std::stable_sort(in.begin(), in.end(), [t](const InEdge& a, const InEdge& b) {
+            const bool a_after = a.q > t, b_after = b.q > t;  // sources after t come first (older sweep)
+            if (a_after != b_after) return a_after;
+            return a.q != b.q ? a.q < b.q : a.e < b.e;
+        });
+        uint4 s = make_uint4(null_j2, null_meta, null_j2, null_meta);
+        if (in.size() > 0) { s.x = in[0].j2; s.y = slot_of(in[0]); }
+        if (in.size() > 1) { s.z = in[1].j2; s.w = slot_of(in[1]); }
+        out.inslots[t] = s;
+        // further far edges into t: a list in `edges`, applied by the careful path
+        const uint32_t more = in.size() > 2 ? uint32_t(in.size() - 2) : 0u;
+        out.pos[t].z = uint32_t(out.edges.size()) | more << 16;
+        for (size_t i = 2; i < in.size(); ++i) out.edges.push_back(make_uint4(in[i].j2, slot_of(in[i]), 0u, 0u));
+        extra_in[t] = more != 0;
+    }
     for (uint32_t p0 = 0; p0 < P; p0 += 8) {
-        std::vector<Edge> grouped;
-        std::vector<std::vector<Edge>> near_of(8);
-        bool careful = false, late_columns = false;
+        bool careful = false;
         for (uint32_t k = 0; k < 8; ++k) {
-            const uint32_t p = p0 + k;
-            uint32_t j2[4] = {0, 0, 0, 0}, mask[4] = {0x80000000u, 0x80000000u, 0x80000000u, 0x80000000u};
-            for (uint32_t e = m.layer_offsets[p]; e < m.layer_offsets[p + 1]; ++e) {
-                const uint32_t t = m.layer_targets[e];
-                const uint32_t doubled = bits(2.0f * m.layer_couplings[e]);  // exact
-                if (is_band(p, t)) {
-                    const int off = int(t) - int(p);               // -2, -1, +1, +2
-                    const int slot = off < 0 ? off + 2 : off + 1;  //  0,  1,  2,  3
-                    j2[slot] = doubled;
-                    mask[slot] = 0;
-                } else if (t > p && t <= p0 + 10) {
-                    // the column has been requested already (the chunk loads p0+3 .. p0+10 at its start):
-                    // the update must reach the copy on its way into the register window
-                    near_of[k].push_back({k, t, doubled});
-                    careful = true;
-                } else {
-                    grouped.push_back({k, t, doubled});
-                    // the next chunk requests columns p0+11 .. p0+18 while this one is swept, unless
-                    // this one updates them
-                    late_columns = late_columns || (t >= p0 + 11 && t <= p0 + 18);
-                }
-            }
-            const float tau2g = tau_scale * (2.0f * m.layer_tau[p]);  // f32 product, as gamma * h_tau in the reference
-            out.pos[p] = make_uint4(bits(tau2g), 0, 0, 0);
-            out.tau.push_back(bits(tau2g));
-            // what a flip of s adds to the four band neighbours: -(2s)*J, i.e. 2J with the sign of -s; an
-            // empty slot adds -0.0.  Entry 2p is for s = -1, entry 2p+1 for s = +1.
-            for (uint32_t neg = 0; neg < 2; ++neg) {
-                const uint32_t flip = neg ? 0x80000000u : 0u;
-                out.band_pm[2 * size_t(p) + neg] = make_uint4((j2[0] ^ flip) | mask[0], (j2[1] ^ flip) | mask[1],
-                                                             (j2[2] ^ flip) | mask[2], (j2[3] ^ flip) | mask[3]);
-            }
+            const std::vector<NearEdge>& near = near_of[p0 + k];
+            out.pos[p0 + k].y = uint32_t(out.edges.size()) | uint32_t(near.size()) << 16;
+            for (const NearEdge& e : near) out.edges.push_back(make_uint4(e.t, e.k, e.j2, 0u));
+            careful = careful || !near.empty();
+            // the columns entering the window during this chunk
+            const uint32_t entering = p0 + 3 + k;
+            careful = careful || (entering < P && extra_in[entering]);
         }
-        for (uint32_t k = 0; k < 8; ++k) {
-            out.pos[p0 + k].y = uint32_t(out.edges.size()) | uint32_t(near_of[k].size()) << 16;
-            for (const Edge& e : near_of[k]) out.edges.push_back(make_uint4(e.t, e.k, e.j2, (31u - e.k) | (e.t * 128u) << 8));
-        }
-        // groups of up to 8 edges with distinct targets, edges in attempt order (so that a column's
-        // updates keep the reference's order across and inside groups)
-        const uint32_t first_group = uint32_t(out.groups.size()), first_edge = uint32_t(out.edges.size());
-        std::vector<Edge> cur;
-        const auto close = [&]() {
-            if (cur.empty()) return;
-            out.groups.push_back(uint32_t(out.edges.size()) | uint32_t(cur.size()) << 16);
-            for (const Edge& e : cur) out.edges.push_back(make_uint4(e.t, e.k, e.j2, (31u - e.k) | (e.t * 128u) << 8));
-            cur.clear();
-        };
-        for (const Edge& e : grouped) {
-            const bool clash = std::any_of(cur.begin(), cur.end(), [&](const Edge& o) { return o.t == e.t; });
-            if (cur.size() == 8 || clash) close();
-            cur.push_back(e);
-        }
-        close();
-        out.chunks[p0 / 8] = make_uint4(first_group | (uint32_t(out.groups.size()) - first_group) << 16,
-                                        first_edge | (uint32_t(out.edges.size()) - first_edge) << 16,
-                                        (careful ? 1u : 0u) | (late_columns ? 2u : 0u), 0u);
+        out.chunks[p0 / 8] = make_uint4(0u, 0u, careful ? 1u : 0u, 0u);
     }
     return out;
 }
@@ -583,21 +594,17 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         std::vector<DevStrandGraph> graphs;
         for (size_t k = 0; k < models.size(); ++k) {
             HostStrandGraph& hg = strand_host[k];
-            if (hg.edges.size() > 0xffffu || hg.groups.size() > 0xffffu) {
-                throw Error("init_state: layer graph too large for the strand kernel");
-            }
+            if (hg.edges.size() > 0xffffu) throw Error("init_state: layer graph too large for the strand kernel");
             DevStrandGraph g{};
             g.per_layer = models[k]->per_layer;
             g.layers = models[k]->layers;
             g.n_edges = uint32_t(hg.edges.size());
-            g.n_groups = uint32_t(hg.groups.size());
             if (hg.edges.empty()) hg.edges.push_back(make_uint4(0, 0, 0, 0));
-            if (hg.groups.empty()) hg.groups.push_back(0);
             g.pos = keep(hg.pos)->as<uint4>();
             g.band_pm = keep(hg.band_pm)->as<uint4>();
             g.tau = keep(hg.tau)->as<uint4>();
             g.chunks = keep(hg.chunks)->as<uint4>();
-            g.groups = keep(hg.groups)->as<uint32_t>();
+            g.inslots = keep(hg.inslots)->as<uint4>();
             g.edges = keep(hg.edges)->as<uint4>();
             graphs.push_back(g);
         }
@@ -605,12 +612,9 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         upload(strand_graphs_, graphs, device_bytes_, stream_);
         cuda_check(cudaStreamSynchronize(stream_), "upload strand graphs");
         dev_.strand_graphs = strand_graphs_.as<DevStrandGraph>();
-        // one model: its graph is staged in every CTA's shared memory (next to the warps' landing stages)
-        dev_.strand_graph_smem = 0;
-        if (graphs.size() == 1) {
-            const size_t bytes = strand_graph_bytes(graphs[0].per_layer, graphs[0].n_edges, graphs[0].n_groups);
-            if (bytes + size_t(strand_max_warps()) * strand_warp_smem() <= 200 * 1024) dev_.strand_graph_smem = uint32_t(bytes);
-        }
+        // one model: its graph is staged in every CTA's shared memory, next to the strands' landing stages
+        // and cell rows, when the launcher finds room (launch_sweep_strand)
+        dev_.strand_graph_smem = graphs.size() == 1 ? uint32_t(strand_graph_bytes(graphs[0].per_layer, graphs[0].n_edges)) : 0u;
         // How many layers of a tile are swept at once.  Every strand and producer of a round must be
         // resident, sm_count * warps of them; more strands hide more latency, fewer keep the tape ring
         // (S * per_layer rows per tile) small.  ISING_B200_STRANDS / ISING_B200_STRAND_WARPS override.
@@ -634,12 +638,15 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         // strands of a tile may trail each other by min_chunks / strands chunks
         dev_.strand_pub = std::max(1u, std::min(16u, min_chunks / (2 * strands)));
         if (env_u32("ISING_B200_STRAND_PUB") != 0) dev_.strand_pub = env_u32("ISING_B200_STRAND_PUB");
+        dev_.max_per_layer = max_per_layer;
+        dev_.max_layers = 0;
+        for (const HostModel* m : models) dev_.max_layers = std::max(dev_.max_layers, m->layers);
         dev_.tape_rows = (strands * max_per_layer + 1024 + 31) / 32 * 32;
         tape_.allocate(size_t(tiles) * dev_.tape_rows * 32 * sizeof(uint32_t), device_bytes_);
-        spin_bytes_.allocate(std::max<size_t>(1, size_t(tiles) * (n / 8) * 32), device_bytes_);
+        spin_cells_.allocate(std::max<size_t>(1, size_t(tiles) * (n / 8) * 32 * sizeof(uint16_t)), device_bytes_);
         strand_flags_.allocate(size_t(strand_flag_words(tiles, strands)) * sizeof(uint32_t), device_bytes_);
         dev_.tape = tape_.as<uint32_t>();
-        dev_.spin_bytes = spin_bytes_.as<uint8_t>();
+        dev_.spin_cells = spin_cells_.as<uint16_t>();
         dev_.strand_flags = strand_flags_.as<uint32_t>();
     }
 
@@ -785,8 +792,11 @@ void Batch::launch_sweeps(uint32_t sweeps) {
     if (sweeps == 0) return;
     begin_timed(false);
     if (family_ == KernelFamily::strand) {
-        cuda_check(launch_sweep_strand(dev_, sweeps, sm_count_, strand_warps_, stream_), "strand sweep kernel");
-        other_launches += 2;  // spin words <-> spin bytes around the sweep kernel
+        // the cells stay authoritative between strand launches (settle() restores the canonical state)
+        cuda_check(launch_sweep_strand(dev_, sweeps, sm_count_, strand_warps_, !strand_live_, stream_),
+                   "strand sweep kernel");
+        if (!strand_live_) ++other_launches;  // spin words -> cells
+        strand_live_ = true;
     } else if (family_ == KernelFamily::layered) {
         cuda_check(launch_sweep_layered(dev_, sweeps, sm_count_, stream_), "layered sweep kernel");
     } else {
@@ -795,6 +805,13 @@ void Batch::launch_sweeps(uint32_t sweeps) {
     end_timed();
     ++sweep_launches;
     sweeps_done_ += sweeps;
+}
+
+void Batch::settle() {
+    if (!strand_live_) return;
+    cuda_check(launch_strand_settle(dev_, stream_), "strand settle kernels");
+    other_launches += 2;  // pending far updates into the fields, cells -> spin words
+    strand_live_ = false;
 }
 
 void Batch::launch_swap_round() {
@@ -868,6 +885,7 @@ void download(T* host, const void* dev, size_t count, cudaStream_t stream) {
 
 void Batch::read_spins(uint64_t first_chain, uint64_t n_chains, int8_t* out) {
     bind_device();
+    settle();
     if (first_chain > dev_.n_chains || n_chains > dev_.n_chains - first_chain) {
         throw Error("read_spins: chain range out of bounds");
     }
@@ -889,6 +907,7 @@ void Batch::read_spins(uint64_t first_chain, uint64_t n_chains, int8_t* out) {
 
 void Batch::read_fields(uint64_t chain, float* hs, float* ht) {
     bind_device();
+    settle();
     if (chain >= dev_.n_chains) throw Error("read_fields: chain out of range");
     if (hs == nullptr || ht == nullptr) throw Error("null argument");
     const size_t n = dev_.n_spins;
@@ -903,6 +922,7 @@ void Batch::read_fields(uint64_t chain, float* hs, float* ht) {
 
 void Batch::read_energies(double* out) {
     bind_device();
+    settle();
     if (out == nullptr) throw Error("null argument");
     size_t ignored = 0;
     if (scratch_.bytes() < dev_.n_chains * sizeof(double)) scratch_.allocate(dev_.n_chains * sizeof(double), ignored);
@@ -913,6 +933,7 @@ void Batch::read_energies(double* out) {
 
 void Batch::resync_energies() {
     bind_device();
+    settle();
     cuda_check(launch_resync_energies(dev_, stream_), "energy resync kernel");
     ++other_launches;
 }
@@ -968,6 +989,7 @@ void Batch::read_wait(uint32_t n_widths, const uint32_t* widths, uint64_t* group
 
 void Batch::read_checksums(uint64_t* out) {
     bind_device();
+    settle();
     if (out == nullptr) throw Error("null argument");
     size_t ignored = 0;
     if (scratch_.bytes() < dev_.n_chains * sizeof(uint64_t)) scratch_.allocate(dev_.n_chains * sizeof(uint64_t), ignored);
@@ -978,6 +1000,7 @@ void Batch::read_checksums(uint64_t* out) {
 
 void Batch::read_coherence(uint64_t* out) {
     bind_device();
+    settle();
     if (out == nullptr) throw Error("null argument");
     size_t ignored = 0;
     if (scratch_.bytes() < dev_.n_chains * sizeof(uint64_t)) scratch_.allocate(dev_.n_chains * sizeof(uint64_t), ignored);
@@ -1000,6 +1023,7 @@ void Batch::read_swap_stats(uint64_t* acc, uint64_t* att) {
 
 void Batch::pack_results(void* device_out) {
     bind_device();
+    settle();
     if (device_out == nullptr) throw Error("null argument");
     cuda_check(launch_pack_results(dev_, device_out, stream_), "pack kernel");
     ++other_launches;
@@ -1032,6 +1056,7 @@ void Batch::all_gather_results(void* nccl_comm, void* device_out_all) {
     const size_t bytes = size_t(dev_.n_chains) * 32;
     size_t ignored = 0;
     if (gather_send_.bytes() < bytes) gather_send_.allocate(std::max<size_t>(bytes, 32), ignored);
+    settle();
     cuda_check(launch_pack_results(dev_, gather_send_.as<void>(), stream_), "pack kernel");
     ++other_launches;
     const int rc = all_gather(gather_send_.as<void>(), device_out_all, size_t(dev_.n_chains) * 4, /*ncclInt64*/ 4, nccl_comm,

@@ -79,22 +79,27 @@ struct DevLayerGraph {
     const uint4* far;  // {target position, 7 - attempt index in its chunk, bits of 2J, 0}
 };
 
-// One layer of an identical-layer model as the strand (layer-wavefront) kernel reads it, from global
-// memory through the read-only cache.  Band slots as in DevLayerGraph; every other in-layer edge of
-// position p (chunk c = p / 8) is either NEAR — its target lies among the columns the chunk has
-// already requested, p+3 .. 8c+10, which makes the chunk CAREFUL — or goes into the chunk's GROUPS,
-// applied in global memory after the chunk's last attempt.
+// One layer of an identical-layer model as the strand (layer-wavefront) kernel reads it.  Band slots
+// as in DevLayerGraph.  Every other in-layer edge q -> t is either NEAR — t lies among the columns
+// q's chunk has already requested, q+3 .. 8*(q/8)+10, pushed through a scratch, which makes the chunk
+// CAREFUL — or FAR: the target PULLS it when column t enters the register window, from the source
+// chunk's CELL (u16 per chain and chunk of 8 spins: bit k = spin k flipped in the chunk's latest
+// sweep, bit 8+k = spin k is -1).  Two far edges per column are fixed slots of the lean path; a column
+// with more makes the chunk it enters in careful.
 struct DevStrandGraph {
     uint32_t per_layer;
     uint32_t layers;
-    const uint4* pos;        // per position: {bits of gamma*2J_tau, near edges begin | count << 16, 0, 0}
-    const uint4* band_pm;    // as DevLayerGraph::band_pm
-    const uint4* tau;        // per position the bits of gamma*2J_tau (u32 [per_layer], read 8 at a time)
-    const uint4* chunks;     // per chunk: {groups begin | count << 16, group edges begin | count << 16,
-                             //             flags (1 careful, 2 updates columns the next chunk loads), 0}
-    const uint32_t* groups;  // up to 8 edges with distinct targets, in attempt order: edge begin | count << 16
-    const uint4* edges;      // {target position, attempt index k in its chunk, bits of 2J, (31 - k) | target * 128 << 8}
-    uint32_t n_groups;
+    const uint4* pos;      // per position: {bits of gamma*2J_tau, near edges begin | count << 16,
+                           //                far in-edges beyond the two slots begin | count << 16, 0} (into `edges`)
+    const uint4* band_pm;  // as DevLayerGraph::band_pm
+    const uint4* tau;      // per position the bits of gamma*2J_tau (u32 [per_layer], read 8 at a time)
+    const uint4* chunks;   // per chunk: {0, 0, flags (1 careful), 0}
+    // per position, per_layer + 8 entries (the last 8 null): the first two far in-edges in application
+    // order (sources after the column — flips of the sweep before — then sources before it), each
+    // {bits of 2J, (23 - source bit) | byte offset of the source chunk's cell row << 8}; a null slot is
+    // {-0.0, 31}
+    const uint4* inslots;
+    const uint4* edges;    // near: {target position, attempt index k in its chunk, bits of 2J, 0}; far: {bits of 2J, meta, 0, 0}
     uint32_t n_edges;
 };
 
@@ -138,10 +143,12 @@ struct DevBatch {
     // strand (layer-wavefront) family: kernels_strand.cu
     const DevStrandGraph* strand_graphs;  // per model
     uint32_t strands;       // S: concurrent layers per tile (divides every model's layer count)
+    uint32_t max_layers;    // largest layer count over the batch's models
     uint32_t strand_pub;    // a strand publishes its progress every strand_pub chunks
     uint32_t tape_rows;     // R: rows of a tile's MT19937 tape ring (a multiple of 32)
     uint32_t* tape;         // u32 [tile][R][32]: raw MT19937 words in draw order
-    uint8_t* spin_bytes;    // u8 [tile][spin / 8][32]: bit k of a lane's byte <=> its spin 8c+k is -1
+    uint16_t* spin_cells;   // u16 [tile][spin / 8][32]: bit 8+k of a lane's cell <=> its spin 8c+k is -1, bit k <=> it
+                            // flipped in the chunk's latest sweep (DevStrandGraph)
     uint32_t* strand_flags; // per tile S + 1 progress counters (strand chunks done, tape head), one line each
     uint32_t strand_graph_smem;  // bytes of model 0's graph staged in shared memory (0: tables read from global)
     // tempering
@@ -161,13 +168,17 @@ cudaError_t launch_sweep_layered(const DevBatch& b, uint32_t sweeps, int sm_coun
 size_t layered_smem_bytes(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared);
 uint32_t layered_stage_count(uint32_t per_layer, uint32_t max_far_edges, uint32_t max_groups, bool graph_shared);
 cudaError_t prepare_layered_kernels(size_t smem_bytes);
-// Strand family: needs b.strand_graphs, tape, spin_bytes, strand_flags; `warps_per_cta` <= strand_max_warps().
+// Strand family: needs b.strand_graphs, tape, spin_cells, strand_flags; `warps_per_cta` <= strand_max_warps().
+// While the family runs, the cells hold the spins and the fields lack the far updates of each layer's
+// latest sweep (they are pulled during the next one): `from_words` builds the cells from spin_bits
+// first; launch_strand_settle applies what is pending and writes spin_bits back.
 cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count, uint32_t warps_per_cta,
-                                cudaStream_t stream);
+                                bool from_words, cudaStream_t stream);
+cudaError_t launch_strand_settle(const DevBatch& b, cudaStream_t stream);
 uint32_t strand_max_warps();
 uint32_t strand_warp_smem();  // shared-memory bytes per warp (landing stages, scratch)
 uint32_t strand_flag_words(uint32_t n_tiles, uint32_t strands);
-size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges, uint32_t n_groups);
+size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges);
 cudaError_t launch_swap(const DevBatch& b, uint64_t round, cudaStream_t stream);
 cudaError_t launch_energies(const DevBatch& b, double* out_dev, cudaStream_t stream);
 cudaError_t launch_resync_energies(const DevBatch& b, cudaStream_t stream);  // e_run := tempering cost of the spins

@@ -25,11 +25,19 @@
 //
 // Per strand, fields move in chunks of 8 positions: the window of positions p-2..p+2 lives in
 // registers (band neighbours are predicated register adds, as in kernels_layered.cu); eight columns
-// enter it from HBM and eight leave it per chunk (full 128-byte lines); far neighbours are
-// read-modify-written in global memory after the chunk, in groups of distinct targets whose loads go
-// out together.  All field traffic of a layer comes from one thread per chain, so program order is
-// the only ordering it needs.  HBM traffic per attempt: 4 B field in, 4 B out, 1/4 B spin bytes, plus
-// the tape (4 B written, 4 B read, both L2 hits while the ring fits).
+// enter it from HBM and eight leave it per chunk (full 128-byte lines), each exactly once per sweep.
+// A FAR neighbour's update is not sent to the field in memory (a scattered read-modify-write of a
+// 32-byte sector per flip: 6 B of HBM traffic per attempt on c5, a quarter of the total, and a
+// reduction instruction per edge): the TARGET pulls it when its column enters the window, from the
+// source chunk's CELL — 16 bits per chain and chunk, the chunk's spins and which of them flipped in the
+// chunk's latest sweep — kept in shared memory for the layer being swept (8 bytes per position and
+// strand; in global memory when that does not fit).  A column's far sources after it flipped in the
+// sweep before, those before it in this sweep: pulled in that order they reproduce the reference's
+// order of subtractions from h[t] exactly.  Between sweeps the fields in memory therefore lack the far
+// updates of the latest sweep ("pending"); settle_fields_kernel applies them when anything else wants
+// the fields (Batch::settle).  All field traffic of a layer comes from one thread per chain, so
+// program order is the only ordering it needs.  HBM traffic per attempt: 4 B field in, 4 B out, 1/2 B
+// cells, plus the tape (4 B written, 4 B read).
 #include "device_batch.hpp"
 #include "device_math.cuh"
 
@@ -72,6 +80,22 @@ __device__ __forceinline__ uint32_t ld_cg_u8(const uint8_t* p) {
     asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint32_t ld_cg_u16(const uint16_t* p) {
+    uint32_t v;
+    asm volatile("{\n.reg .b16 t;\nld.global.cg.u16 t, [%1];\ncvt.u32.u16 %0, t;\n}" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_u16(uint16_t* p, uint32_t v) {
+    asm volatile("{\n.reg .b16 t;\ncvt.u16.u32 t, %1;\nst.global.u16 [%0], t;\n}" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint32_t v;
+    asm volatile("{\n.reg .b16 t;\nld.shared.u16 t, [%1];\ncvt.u32.u16 %0, t;\n}" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+    asm volatile("{\n.reg .b16 t;\ncvt.u16.u32 t, %1;\nst.shared.u16 [%0], t;\n}" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ double ld_cg_f64(const double* p) {
     double v;
     asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
@@ -82,9 +106,6 @@ __device__ __forceinline__ void st_f32(float* p, float v) {
 }
 __device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
-    asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
@@ -199,13 +220,12 @@ template <bool STAGED>
 struct Tables;
 template <>
 struct Tables<false> {
-    const uint4 *chunks, *pos, *band, *tau, *edges;
-    const uint32_t* groups;
+    const uint4 *chunks, *pos, *band, *tau, *edges, *inslots;
     __device__ __forceinline__ uint4 chunk(uint32_t c) const { return __ldg(chunks + c); }
     __device__ __forceinline__ uint4 tau4(uint32_t i) const { return __ldg(tau + i); }
     __device__ __forceinline__ uint4 posrec(uint32_t p) const { return __ldg(pos + p); }
     __device__ __forceinline__ uint4 edge(uint32_t i) const { return __ldg(edges + i); }
-    __device__ __forceinline__ uint32_t group(uint32_t i) const { return __ldg(groups + i); }
+    __device__ __forceinline__ uint4 inslot(uint32_t p) const { return __ldg(inslots + p); }
     __device__ __forceinline__ uint4 band_at(uint32_t p, uint32_t byte_off) const {
         return __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(band + 2 * size_t(p)) + byte_off));
     }
@@ -216,23 +236,61 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
     asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
-__device__ __forceinline__ uint32_t lds_b32(uint32_t addr) {
-    uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
 template <>
 struct Tables<true> {
-    uint32_t chunks, pos, band, tau, edges, groups;  // shared-window addresses
+    uint32_t chunks, pos, band, tau, edges, inslots;  // shared-window addresses
     __device__ __forceinline__ uint4 chunk(uint32_t c) const { return lds_v4(chunks + c * 16); }
     __device__ __forceinline__ uint4 tau4(uint32_t i) const { return lds_v4(tau + i * 16); }
     __device__ __forceinline__ uint4 posrec(uint32_t p) const { return lds_v4(pos + p * 16); }
     __device__ __forceinline__ uint4 edge(uint32_t i) const { return lds_v4(edges + i * 16); }
-    __device__ __forceinline__ uint32_t group(uint32_t i) const { return lds_b32(groups + i * 4); }
+    __device__ __forceinline__ uint4 inslot(uint32_t p) const { return lds_v4(inslots + p * 16); }
     __device__ __forceinline__ uint4 band_at(uint32_t p, uint32_t byte_off) const {
         return lds_v4(band + p * 32 + byte_off);
     }
 };
+
+// The cells of the layer a strand is sweeping, as this lane sees them: `at(off)` is the lane's cell of
+// the chunk whose row starts `off` bytes into the layer (64 bytes per chunk).  STAGED: the warp's copy
+// in shared memory, which the strand keeps current itself; otherwise global memory, past L1 (the
+// lane's own earlier stores, in program order).
+template <bool STAGED>
+struct Cells;
+template <>
+struct Cells<false> {
+    const unsigned char* layer;
+    __device__ __forceinline__ uint32_t at(uint32_t off) const { return ld_cg_u16(reinterpret_cast<const uint16_t*>(layer + off)); }
+    __device__ __forceinline__ void keep(uint32_t, uint32_t) const {}
+};
+template <>
+struct Cells<true> {
+    uint32_t layer;  // shared-window address
+    __device__ __forceinline__ uint32_t at(uint32_t off) const { return lds_u16(layer + off); }
+    __device__ __forceinline__ void keep(uint32_t off, uint32_t cell) const { sts_u16(layer + off, cell); }
+};
+
+// One far in-edge of a column (DevStrandGraph::inslots): `cell` is the source chunk's cell, `meta`'s
+// low five bits the shift that brings the source's spin bit to bit 31 and its flip bit to bit 23.
+// A flip of the source from s to -s subtracted (2s)*J from h: adds 2J with the sign of the NEW spin.
+// Not flipped (or a null slot): adds -0.0, the identity for every bit pattern.
+__device__ __forceinline__ float pull_slot(float h, uint32_t j2, uint32_t meta, uint32_t cell) {
+    const uint32_t x = __funnelshift_l(0u, cell, meta);  // (the shift wraps at 32)
+    const uint32_t addend = (x & 0x00800000u) != 0u ? (j2 ^ (x & 0x80000000u)) : 0x80000000u;
+    return __fadd_rn(h, __uint_as_float(addend));
+}
+// Every far in-edge of column `col`, in application order (the two slots, then the list).
+template <bool STAGED>
+__device__ __forceinline__ float pull_column(float h, uint32_t col, const Tables<STAGED>& t, const Cells<STAGED>& cells) {
+    const uint4 in = t.inslot(col);
+    h = pull_slot(h, in.x, in.y, cells.at(in.y >> 8));
+    h = pull_slot(h, in.z, in.w, cells.at(in.w >> 8));
+    const uint32_t more = t.posrec(col).z;
+    for (uint32_t i = 0; i < (more >> 16); ++i) {
+        const uint4 e = t.edge((more & 0xffffu) + i);
+        h = pull_slot(h, e.x, e.y, cells.at(e.y >> 8));
+    }
+    return h;
+}
+
 // The band_pm entry of the flip of position p, attempt K of its chunk: the pair's first entry is for
 // s = -1, the second (16 bytes on) for s = +1.
 template <int K, bool STAGED>
@@ -269,73 +327,11 @@ __device__ __forceinline__ float edge_addend(const uint4 e, uint32_t cur8) {
     return __uint_as_float(e.z ^ ((((cur8 >> e.y) & 1u) ^ 1u) << 31));
 }
 
-// Far neighbours of the chunk's flips, after its last attempt (edges in attempt order, so every
-// column receives its updates in the reference's order).
-//
-// RED: h[t] -= (2s)*J goes out as a global f32 reduction of -(2s)*J — it rounds exactly like the
-// subtraction, reductions and loads of one thread to one address keep program order, and nothing
-// comes back, so the chunk pays no round trip.  Global f32
-// reductions flush subnormals (REDG.ADD.F32.FTZ.RN), so this path is only used when no field can be
-// subnormal (DevModel::reduction_safe for every model of the batch).
-template <bool STAGED>
-__device__ __forceinline__ void apply_edges_red(float* hs_l, const Tables<STAGED>& t, uint32_t einfo, uint32_t acc8,
-                                                uint32_t cur8) {
-    const uint32_t first = einfo & 0xffffu;
-    const uint32_t n = einfo >> 16;
-    // bit k of `flip`: the addend of attempt k's edges is -2J (s = +1); of `acc8`: this lane accepted it
-    const uint32_t flip = ~cur8;
-    unsigned char* base = reinterpret_cast<unsigned char*>(hs_l);
-#pragma unroll 2
-    for (uint32_t i = 0; i < n; ++i) {
-        const uint4 e = t.edge(first + i);  // {target position, attempt, bits of 2J, (31 - attempt) | target byte offset << 8}
-        const uint32_t addend = e.z ^ (__funnelshift_l(0u, flip, e.w) & 0x80000000u);  // (the shift wraps at 32)
-        // only the lanes that accepted take part: with 18 warps per SM the load/store unit is the limit
-        // of full 32-lane reductions (~40 cycles each), and its cost follows the active lanes (c5: +4 %)
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "setp.lt.s32 p, %2, 0;\n"
-            "@p red.global.add.f32 [%0], %1;\n"
-            "}\n" ::"l"(base + (e.w >> 8)),
-            "f"(__uint_as_float(addend)), "r"(int32_t(__funnelshift_l(0u, acc8, e.w)))
-            : "memory");
-    }
-}
-// Otherwise: read-modify-writes in groups of up to 8 edges with distinct targets (loads together,
-// then adds and stores).
-template <bool STAGED>
-__device__ __noinline__ void apply_groups_rmw(float* hs_l, const Tables<STAGED> t, uint32_t ginfo, uint32_t acc8,
-                                              uint32_t cur8) {
-    const uint32_t first_group = ginfo & 0xffffu;
-    const uint32_t n_groups = ginfo >> 16;
-#pragma unroll 1
-    for (uint32_t q = 0; q < n_groups; ++q) {
-        const uint32_t info = t.group(first_group + q);
-        const uint32_t first = info & 0xffffu;
-        const uint32_t n = info >> 16;
-        uint4 e[8];
-        float v[8];
-#pragma unroll
-        for (uint32_t i = 0; i < 8; ++i) {
-            if (i < n) e[i] = t.edge(first + i);
-        }
-#pragma unroll
-        for (uint32_t i = 0; i < 8; ++i) {
-            if (i < n) v[i] = ld_cg_f32(hs_l + size_t(e[i].x) * 32);
-        }
-#pragma unroll
-        for (uint32_t i = 0; i < 8; ++i) {
-            if (i < n && ((acc8 >> e[i].y) & 1u)) {
-                st_f32(hs_l + size_t(e[i].x) * 32, __fadd_rn(v[i], edge_addend(e[i], cur8)));
-            }
-        }
-    }
-}
-
 // A CAREFUL chunk: some attempt has a far neighbour among the columns that have already been
-// requested (p+3 .. p0+10).  The entering columns go through a per-warp shared-memory scratch
-// ([8][32] floats, a lane only touches its own entries; the caller has stored them there), where
-// such updates are applied before the column enters the register window.  Out of line and by value:
+// requested (p+3 .. p0+10), or a column entering has more far in-edges than the two slots.  The
+// entering columns go through a per-warp shared-memory scratch ([8][32] floats, a lane only touches
+// its own entries; the caller has stored them there with everything pulled), where the near updates
+// are applied before the column enters the register window.  Out of line and by value:
 // the hot loop keeps its window in registers.
 struct Window {
     float r[8];
@@ -394,20 +390,19 @@ __device__ __noinline__ CarefulResult careful_chunk(Window w, RawWords raw, Chun
 }
 
 // ---- a strand ---------------------------------------------------------------------------------
-// Per-warp shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB),
-// their mbarriers, and the scratch of the careful chunks.
+// Per-strand shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB),
+// three mbarriers, the scratch of the careful chunks and — STAGED — the cells of the layer being swept
+// (64 bytes per chunk).
 constexpr uint32_t kStageBytes = 1024;
-constexpr uint32_t kWarpSmem = 2 * kStageBytes + 16 + 1024;
+constexpr uint32_t kWarpSmem = 2 * kStageBytes + 32 + 1024;
 
-
-// Everything a chunk reads from global memory is requested one chunk ahead: the tape rows and the
-// spin bytes by bulk (TMA) copies of one elected lane into the warp's landing stage (no registers
-// held meanwhile), the eight columns entering the window by plain loads (they must stay in program
-// order with this thread's own stores and reductions to the same addresses); the columns three
-// chunks ahead are prefetched into L2.  So the loop-carried chain of the attempts is all a strand
-// waits for.  The one exception: when a far edge of chunk c targets the columns chunk c+1 loads
-// (chunk flag 2), those are requested after chunk c's updates.
-template <int EXP, bool WAIT, bool RED, bool STAGED>
+// Everything a chunk reads from global memory is requested one chunk ahead or more: the tape rows by
+// a bulk (TMA) copy of one elected lane into the warp's landing stage (no registers held meanwhile),
+// the eight columns entering the window by plain loads at the chunk's start (consumed three attempts
+// later at the earliest); the columns three chunks ahead are prefetched into L2; the layer's cells
+// arrive by one bulk copy per layer.  So the loop-carried chain of the attempts is all a strand waits
+// for.
+template <int EXP, bool WAIT, bool STAGED>
 __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t P, uint32_t L, uint32_t tile, uint32_t j,
                            uint32_t sweeps, uint32_t lane, unsigned char* warp_smem) {
     const uint32_t C = P / 8, S = b.strands, n = b.n_spins;
@@ -418,7 +413,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     const uint32_t nb2 = __float_as_uint(active ? -2.0f * b.betas[b.slot_of_chain[chain]] : 0.0f);
     const float u_offset = active ? 0.0f : 2.0f;
     float* hs_tile = b.hs + size_t(tile) * n * 32 + lane;
-    uint8_t* bytes_tile = b.spin_bytes + size_t(tile) * (n / 8) * 32 + lane;
+    uint16_t* cells_tile = b.spin_cells + size_t(tile) * (n / 8) * 32 + lane;
     const uint32_t R = b.tape_rows;
     const uint32_t* tape = b.tape + size_t(tile) * R * 32;  // (no lane offset: rows are copied whole)
     uint32_t* flags = b.strand_flags + size_t(tile) * (S + 1) * kFlagStride;
@@ -429,14 +424,16 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     uint32_t pred_cached = 0, head_cached = 0;
     uint32_t flips = 0;
     uint32_t seq = 0;  // chunks finished
-    // landing stages: stage s at wsm + s * kStageBytes (tape rows, then the cur / up / dn byte rows)
+    // landing stages: stage s at wsm + s * kStageBytes; then the barriers, the scratch, the cells
     const uint32_t wsm = smem_u32(warp_smem);
-    const uint32_t bar0 = wsm + 2 * kStageBytes;
-    float* scratch = reinterpret_cast<float*>(warp_smem + 2 * kStageBytes + 16) + lane;
-    uint32_t stage = 0, phases = 0;  // current stage; bit s of phases = parity the next wait on stage s sees
+    const uint32_t bar0 = wsm + 2 * kStageBytes, bar_cells = bar0 + 16;
+    float* scratch = reinterpret_cast<float*>(warp_smem + 2 * kStageBytes + 32) + lane;
+    const uint32_t cells_smem = wsm + kWarpSmem;
+    uint32_t stage = 0, phases = 0;  // current stage; bit s of phases = parity the next wait on stage s sees (bit 2: the cells)
     if (lane == 0) {
         mbar_init(bar0, 1);
         mbar_init(bar0 + 8, 1);
+        mbar_init(bar_cells, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -475,13 +472,29 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         uint32_t slot = row0 % R;       // (R and row0 are multiples of 8: a chunk's rows never wrap)
         double e_blk = 0.0;
 
-        // running pointers: the chunk being swept (…_c) is at p0 = 8c
+        // running pointers: the chunk being swept (…_c) is at p0 = 8c; the neighbours' spins are the
+        // high bytes of their cells
         float* hs_c = hs_l;
-        uint8_t* cur_c = bytes_tile + size_t(l) * C * 32;
-        const uint8_t* up_c = bytes_tile + size_t(l_up) * C * 32;
-        const uint8_t* dn_c = bytes_tile + size_t(l_dn) * C * 32;
+        uint16_t* cur_c = cells_tile + size_t(l) * C * 32;
+        const uint8_t* up_c = reinterpret_cast<const uint8_t*>(cells_tile + size_t(l_up) * C * 32) + 1;
+        const uint8_t* dn_c = reinterpret_cast<const uint8_t*>(cells_tile + size_t(l_dn) * C * 32) + 1;
+        Cells<STAGED> cells;
+        if constexpr (STAGED) {
+            // The layer's cells as this warp left them a sweep ago (or as the launch found them), by one
+            // bulk copy: every lane's stores to them, and every lane's reads of the copy it replaces,
+            // come before it.
+            asm volatile("fence.proxy.async.global;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_expect(bar_cells, C * 64);
+                bulk_load(cells_smem, cur_c - lane, C * 64, bar_cells);
+            }
+            cells.layer = cells_smem + lane * 2;
+        } else {
+            cells.layer = reinterpret_cast<const unsigned char*>(cur_c);
+        }
 
-        // ---- the first chunk's operands (the only exposed round trip of the block)
+        // ---- the first chunk's operands (the only exposed round trips of the block)
         wait_counter(head_flag, head_need, head_cached);
         __syncwarp();  // every lane has left the stage's previous contents
         request(stage, slot);
@@ -493,6 +506,13 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         r[0] = ld_cg_f32(hs_c);
         r[1] = ld_cg_f32(hs_c + 32);
         r[2] = ld_cg_f32(hs_c + 64);
+        if constexpr (STAGED) {
+            mbar_wait(bar_cells, (phases >> 2) & 1u);
+            phases ^= 4u;
+        }
+        r[0] = pull_column(r[0], 0u, t, cells);
+        r[1] = pull_column(r[1], 1u, t, cells);
+        r[2] = pull_column(r[2], 2u, t, cells);
 
         for (uint32_t c = 0; c < C; ++c) {
 #ifdef ISING_STRAND_PROFILE
@@ -501,15 +521,14 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             const uint32_t p0 = c * 8;
             const uint4 chunk_info = t.chunk(c);
             const bool more = c + 1 < C;
-            // ---- the columns entering the window during this chunk, p0+3 .. p0+10 (the last chunk has five):
-            // requested after every update the chunks before could send them, L2 hits (prefetched below)
+            // ---- the columns entering the window during this chunk, p0+3 .. p0+10 (the last chunk has five)
             float nx[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) nx[k] = (k < 5 || more) ? ld_cg_f32(hs_c + (3 + k) * 32) : 0.0f;
-            // ... and its spin bytes: the layer below must have finished the chunk
+            // ... and its spins: the layer below must have finished the chunk
             if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
             ChunkBits cb;
-            cb.cur8 = ld_cg_u8(cur_c);
+            cb.cur8 = (STAGED ? cells.at(c * 64) : ld_cg_u16(cur_c)) >> 8;
             cb.up8 = ld_cg_u8(up_c);
             cb.dn8 = ld_cg_u8(dn_c);
             // ---- the next chunk's tape rows, by bulk copy
@@ -523,7 +542,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                 // the columns three chunks ahead, into L2
                 if (lane < 8 && c + 4 < C) prefetch_l2(hs_c + (27 + lane) * 32);
             }
-            // ---- this chunk's tape words and spin bytes have landed
+            // ---- this chunk's tape words have landed
             ISING_TICK(tA);
             mbar_wait(bar0 + stage * 8, (phases >> stage) & 1u);
             ISING_TICK(tB);
@@ -541,14 +560,18 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             if (__builtin_expect((chunk_info.z & 1u) == 0u, 1)) {
                 Prepared pr;
                 prepare_chunk(pr, raw, cb, nb2, u_offset, t.tau4(2 * c), t.tau4(2 * c + 1));
-                // the band entry of an attempt is requested during the attempt before it
+                // the band entry of an attempt is requested during the attempt before it; the far in-edges
+                // of the column that enters after the attempt, and their cells, before it (their sources
+                // lie in earlier chunks or later positions: nothing this chunk decides)
                 uint4 op = band_entry<0>(t, p0, cb.cur8);
 #define ISING_STRAND_ATTEMPT(K, NEXT)                                                \
     {                                                                                \
         const uint4 op_next = band_entry<NEXT>(t, p0 + NEXT, cb.cur8);               \
+        const uint4 in = t.inslot(p0 + 3 + K);                                       \
+        const uint32_t cell_a = cells.at(in.y >> 8), cell_b = cells.at(in.w >> 8);   \
         strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
         if (c != 0 || K >= 2) st_f32(hs_c + (K - 2) * 32, r[(K + 6) & 7]);           \
-        r[(K + 3) & 7] = nx[K];                                                      \
+        r[(K + 3) & 7] = pull_slot(pull_slot(nx[K], in.x, in.y, cell_a), in.z, in.w, cell_b); \
         op = op_next;                                                                \
     }
                 ISING_STRAND_ATTEMPT(0, 1)
@@ -562,16 +585,18 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
 #undef ISING_STRAND_ATTEMPT
             } else {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) scratch[k * 32] = nx[k];
+                for (int k = 0; k < 8; ++k) scratch[k * 32] = (k < 5 || more) ? pull_column(nx[k], p0 + 3 + k, t, cells) : 0.0f;
                 const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, t, p0, hs_l, scratch, e_blk);
                 w = res.w;
                 acc8 = res.acc8;
                 e_blk = res.e_blk;
             }
 
-            // ---- after the chunk: spins, far neighbours, progress
+            // ---- after the chunk: the cell (new spins, what flipped), progress
             ISING_TICK(tC);
-            st_u8(cur_c, cb.cur8 ^ acc8);
+            const uint32_t cell = acc8 | (cb.cur8 ^ acc8) << 8;
+            st_u16(cur_c, cell);
+            cells.keep(c * 64, cell);
             flips += __popc(acc8);
             if (WAIT && record_wait) {
 #pragma unroll
@@ -580,20 +605,14 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                     if (lane == uint32_t(k)) wait_fold(ballot, wait);
                 }
             }
-#ifndef ISING_X_NO_FAR  // (timing experiment: wrong trajectories)
-            if ((chunk_info.y >> 16) != 0u && __any_sync(0xffffffffu, acc8 != 0u)) {
-                if (RED) apply_edges_red(hs_l, t, chunk_info.y, acc8, cb.cur8);
-                else apply_groups_rmw(hs_l, t, chunk_info.x, acc8, cb.cur8);
-            }
-#endif
             ++seq;
             ISING_TICK(tD);
             if (more) {
                 stage ^= 1u;
                 hs_c += 8 * 32;
                 cur_c += 32;
-                up_c += 32;
-                dn_c += 32;
+                up_c += 64;
+                dn_c += 64;
                 if (seq % pub == 0u) publish_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
             }
             ISING_TICK(tE);
@@ -629,7 +648,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     }
     if (active && flips != 0u) atomicAdd(b.flips + chain, static_cast<unsigned long long>(flips));
 #ifdef ISING_STRAND_PROFILE
-    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld edges %lld rotate %lld; block end %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tF / total_blocks);
+    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld cell %lld rotate %lld; block end %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tF / total_blocks);
 #endif
 }
 
@@ -794,40 +813,44 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
 
 // Persistent grid of independent warps.  Work items of a round: for each of `tiles_per_round` tiles
 // its S strands and its producer; every item of a round is resident at once (the launcher sizes the
-// rounds), so the waits above always end.  Dynamic shared memory: kWarpSmem bytes per warp (landing
-// stages, scratch), then — for single-model batches — a copy of the layer graph, which every strand
-// of the CTA reads (b.strand_graph_smem bytes; otherwise the tables are read from global memory).
-template <int EXP, bool WAIT, bool RED, bool STAGED>
+// rounds), so the waits above always end.  Items are dealt warp-major, so a CTA's low warps are
+// strands and its high warps producers.  Dynamic shared memory: `strand_regions` regions of kWarpSmem
+// bytes (landing stages, scratch) plus — STAGED, single-model batches — the cells of the strand's
+// layer; then a copy of the layer graph, which every strand of the CTA reads; then `producer_slots`
+// landing buffers for the producers.
+template <int EXP, bool WAIT, bool STAGED>
 __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(DevBatch b, uint32_t sweeps,
                                                                                  uint32_t tiles_per_round,
+                                                                                 uint32_t strand_regions,
                                                                                  uint32_t producer_slots) {
-    extern __shared__ __align__(16) unsigned char strand_smem[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u, warps = blockDim.x >> 5;
-    unsigned char* warp_smem = strand_smem + size_t(warp) * kWarpSmem;
-    // after the warps' regions and the staged graph: the producers' landing buffers
-    unsigned char* producer_smem = strand_smem + (size_t(warps) * kWarpSmem + (STAGED ? b.strand_graph_smem : 0u) + 15) / 16 * 16;
+    extern __shared__ __align__(128) unsigned char strand_smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t region_bytes = kWarpSmem + (STAGED ? b.max_per_layer * 8u : 0u);
+    unsigned char* warp_smem = strand_smem + size_t(warp) * region_bytes;  // (strands only: warp < strand_regions)
+    unsigned char* graph_smem = strand_smem + size_t(strand_regions) * region_bytes;
+    unsigned char* producer_smem = graph_smem + ((STAGED ? b.strand_graph_smem : 0u) + 15u) / 16u * 16u;
     Tables<STAGED> staged{};
     if constexpr (STAGED) {
         const DevStrandGraph g0 = b.strand_graphs[0];
         const uint32_t P = g0.per_layer;
-        uint4* pos = reinterpret_cast<uint4*>(strand_smem + size_t(warps) * kWarpSmem);
+        uint4* pos = reinterpret_cast<uint4*>(graph_smem);
         uint4* band = pos + P;
         uint4* chunks = band + 2 * size_t(P);
         uint4* tau = chunks + P / 8;
-        uint4* edges = tau + P / 4;
-        uint32_t* groups = reinterpret_cast<uint32_t*>(edges + g0.n_edges);
+        uint4* inslots = tau + P / 4;
+        uint4* edges = inslots + P + 8;
         for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) pos[k] = g0.pos[k];
         for (uint32_t k = threadIdx.x; k < 2 * P; k += blockDim.x) band[k] = g0.band_pm[k];
         for (uint32_t k = threadIdx.x; k < P / 8; k += blockDim.x) chunks[k] = g0.chunks[k];
         for (uint32_t k = threadIdx.x; k < P / 4; k += blockDim.x) tau[k] = g0.tau[k];
+        for (uint32_t k = threadIdx.x; k < P + 8; k += blockDim.x) inslots[k] = g0.inslots[k];
         for (uint32_t k = threadIdx.x; k < g0.n_edges; k += blockDim.x) edges[k] = g0.edges[k];
-        for (uint32_t k = threadIdx.x; k < g0.n_groups; k += blockDim.x) groups[k] = g0.groups[k];
         staged.pos = smem_u32(pos);
         staged.band = smem_u32(band);
         staged.chunks = smem_u32(chunks);
         staged.tau = smem_u32(tau);
+        staged.inslots = smem_u32(inslots);
         staged.edges = smem_u32(edges);
-        staged.groups = smem_u32(groups);
         __syncthreads();
     }
     const uint32_t item = warp * gridDim.x + blockIdx.x;
@@ -838,17 +861,18 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
         // consecutive items are the same role of consecutive tiles: an SM hosts a mix of tiles
         const uint32_t role = item / tiles, tile = base + item - role * tiles;
         if (role == S) {
-            // producers are the last items of a round, hence the CTA's highest warps: landing buffer
-            // number warp - (first warp that can be a producer), when the launcher has provided them
+            // a CTA's producers are consecutive warps, at most `producer_slots` of them: landing buffer
+            // number (warp - first warp that can be a producer) mod producer_slots, when the launcher has
+            // provided them
             const uint32_t first_producer_warp = tiles * S / gridDim.x;
-            const uint32_t slot = warp - first_producer_warp;
-            unsigned char* landing = slot < producer_slots ? producer_smem + size_t(slot) * kProducerSmem : nullptr;
+            unsigned char* landing =
+                producer_slots != 0u ? producer_smem + size_t((warp - first_producer_warp) % producer_slots) * kProducerSmem : nullptr;
             producer_run(b, tile, sweeps, lane, landing);
             continue;
         }
         const DevStrandGraph& g = b.strand_graphs[STAGED ? 0u : b.tile_model[tile]];
         if constexpr (STAGED) {
-            strand_run<EXP, WAIT, RED, true>(b, staged, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
+            strand_run<EXP, WAIT, true>(b, staged, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
         } else {
             Tables<false> t;
             t.chunks = g.chunks;
@@ -856,14 +880,14 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
             t.band = g.band_pm;
             t.tau = g.tau;
             t.edges = g.edges;
-            t.groups = g.groups;
-            strand_run<EXP, WAIT, RED, false>(b, t, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
+            t.inslots = g.inslots;
+            strand_run<EXP, WAIT, false>(b, t, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
         }
     }
 }
 
-// spin words [tile][spin] (bit = lane) -> spin bytes [tile][spin/8][lane] (bit = position in the chunk)
-__global__ void __launch_bounds__(256) words_to_bytes_kernel(DevBatch b) {
+// spin words [tile][spin] (bit = lane) -> cells [tile][spin/8][lane] (bit 8+k = spin 8c+k is -1; nothing flipped)
+__global__ void __launch_bounds__(256) words_to_cells_kernel(DevBatch b) {
     const size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t chunks = size_t(b.n_tiles) * (b.n_spins / 8);
     if (idx >= chunks * 32) return;
@@ -875,16 +899,16 @@ __global__ void __launch_bounds__(256) words_to_bytes_kernel(DevBatch b) {
     uint32_t byte = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) byte |= ((word[k] >> lane) & 1u) << k;
-    b.spin_bytes[idx] = uint8_t(byte);
+    b.spin_cells[idx] = uint16_t(byte << 8);
 }
 
-__global__ void __launch_bounds__(256) bytes_to_words_kernel(DevBatch b) {
+__global__ void __launch_bounds__(256) cells_to_words_kernel(DevBatch b) {
     const size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t chunks = size_t(b.n_tiles) * (b.n_spins / 8);
     if (idx >= chunks * 32) return;  // (whole warps: the total is a multiple of 32)
     const size_t chunk = idx >> 5;
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t byte = b.spin_bytes[idx];
+    const uint32_t byte = uint32_t(b.spin_cells[idx]) >> 8;
     uint32_t mine = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -894,61 +918,94 @@ __global__ void __launch_bounds__(256) bytes_to_words_kernel(DevBatch b) {
     if (lane < 8) b.spin_bits[chunk * 8 + lane] = mine;
 }
 
+// What the strands leave pending: the far updates of every layer's latest sweep that their targets
+// have not pulled yet — for column t, its far sources AFTER t (those before it were pulled when t
+// entered the window in that same sweep), in position order.  One warp per (tile, layer), lane = chain.
+__global__ void __launch_bounds__(256) settle_fields_kernel(DevBatch b) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const size_t unit = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    // (layer counts differ between models: units are dealt per tile with the largest count)
+    const uint32_t tile = uint32_t(unit / b.max_layers), l = uint32_t(unit % b.max_layers);
+    if (tile >= b.n_tiles) return;
+    const DevStrandGraph g = b.strand_graphs[b.tile_model[tile]];
+    if (l >= g.layers) return;
+    const uint32_t P = g.per_layer, C = P / 8;
+    float* hs_l = b.hs + (size_t(tile) * b.n_spins + size_t(l) * P) * 32 + lane;
+    const uint16_t* cells_l = b.spin_cells + (size_t(tile) * (b.n_spins / 8) + size_t(l) * C) * 32 + lane;
+    const auto pending = [&](float h, uint32_t t, uint32_t j2, uint32_t meta) {
+        const int q = int(meta >> 8) / 64 * 8 + 23 - int(meta & 31u);  // (a null slot gives -8)
+        if (q <= int(t)) return h;
+        return pull_slot(h, j2, meta, cells_l[(meta >> 8) / 2]);
+    };
+    for (uint32_t t = 0; t < P; ++t) {
+        const uint4 in = __ldg(g.inslots + t);
+        const uint32_t more = __ldg(g.pos + t).z;
+        const int q0 = int(in.y >> 8) / 64 * 8 + 23 - int(in.y & 31u);
+        if (q0 <= int(t)) continue;  // in application order the sources after t come first: none
+        float h = hs_l[size_t(t) * 32];
+        h = pending(h, t, in.x, in.y);
+        h = pending(h, t, in.z, in.w);
+        for (uint32_t i = 0; i < (more >> 16); ++i) {
+            const uint4 e = __ldg(g.edges + (more & 0xffffu) + i);
+            h = pending(h, t, e.x, e.y);
+        }
+        hs_l[size_t(t) * 32] = h;
+    }
+}
+
 }  // namespace
 
 uint32_t strand_max_warps() { return kStrandMaxWarps; }
 uint32_t strand_warp_smem() { return kWarpSmem; }
 uint32_t strand_flag_words(uint32_t n_tiles, uint32_t strands) { return n_tiles * (strands + 1) * kFlagStride; }
 // Shared-memory bytes of a staged layer graph (see sweep_strand_kernel).
-size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges, uint32_t n_groups) {
-    return (size_t(per_layer) * 3 + per_layer / 8 + per_layer / 4 + n_edges) * sizeof(uint4) +
-           size_t(n_groups) * sizeof(uint32_t);
+size_t strand_graph_bytes(uint32_t per_layer, uint32_t n_edges) {
+    return (size_t(per_layer) * 4 + 8 + per_layer / 8 + per_layer / 4 + n_edges) * sizeof(uint4);
 }
 
 namespace {
-template <int EXP, bool WAIT, bool RED, bool STAGED>
-cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t smem, uint32_t round,
-                                  cudaStream_t stream) {
+constexpr size_t kStrandSmemLimit = 227 * 1024;
+
+struct StrandLaunch {
+    dim3 grid, block;
+    uint32_t round, regions, tiles_over_ctas;
+};
+
+template <int EXP, bool WAIT, bool STAGED>
+cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, const StrandLaunch& geo, cudaStream_t stream) {
     // the attribute is per function and context: always the opt-in maximum, never one batch's own need
     static bool prepared = false;
     if (!prepared) {
-        const cudaError_t e = cudaFuncSetAttribute(sweep_strand_kernel<EXP, WAIT, RED, STAGED>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        const cudaError_t e = cudaFuncSetAttribute(sweep_strand_kernel<EXP, WAIT, STAGED>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(kStrandSmemLimit));
         if (e != cudaSuccess) return e;
         prepared = true;
     }
-    // landing buffers for the producers a CTA can host (ceil(tiles of a round / CTAs) + 1 warp indices),
-    // when they fit; else the producers load their operands into registers
-    uint32_t slots = (round + grid.x - 1) / grid.x + 1;
-    const size_t base = (smem + 15) / 16 * 16;
-    if (base + size_t(slots) * kProducerSmem > 227 * 1024) slots = 0;
-    const size_t total_smem = slots != 0 ? base + size_t(slots) * kProducerSmem : smem;
-    sweep_strand_kernel<EXP, WAIT, RED, STAGED><<<grid, block, total_smem, stream>>>(b, sweeps, round, slots);
+    const size_t region = kWarpSmem + (STAGED ? size_t(b.max_per_layer) * 8 : 0);
+    const size_t base = (size_t(geo.regions) * region + (STAGED ? b.strand_graph_smem : 0u) + 15) / 16 * 16;
+    // landing buffers for the producers a CTA can host, when they fit; else the producers load their
+    // operands into registers
+    uint32_t slots = geo.tiles_over_ctas;
+    if (base + size_t(slots) * kProducerSmem > kStrandSmemLimit) slots = 0;
+    const size_t total_smem = base + size_t(slots) * kProducerSmem;
+    sweep_strand_kernel<EXP, WAIT, STAGED><<<geo.grid, geo.block, total_smem, stream>>>(b, sweeps, geo.round, geo.regions, slots);
     return cudaGetLastError();
 }
 template <int EXP>
-cudaError_t launch_strand_exp(const DevBatch& b, uint32_t sweeps, dim3 grid, dim3 block, size_t warp_smem,
-                              uint32_t round, cudaStream_t stream) {
-    // Separate instantiations: reductions need every model to be reduction-safe (no subnormal field
-    // possible); the wait-statistics variant is the only one that carries them (and reads the graph
-    // from global memory); the default reads the staged graph when the batch has one model.
-    const bool wait = b.wait_counts != nullptr, red = b.generic_reduce != 0u;
-    const bool staged = !wait && b.strand_graph_smem != 0u;
-    const size_t smem = warp_smem + (staged ? b.strand_graph_smem : 0u);
-    if (wait) {
-        return red ? launch_strand_variant<EXP, true, true, false>(b, sweeps, grid, block, smem, round, stream)
-                   : launch_strand_variant<EXP, true, false, false>(b, sweeps, grid, block, smem, round, stream);
-    }
-    if (staged) {
-        return red ? launch_strand_variant<EXP, false, true, true>(b, sweeps, grid, block, smem, round, stream)
-                   : launch_strand_variant<EXP, false, false, true>(b, sweeps, grid, block, smem, round, stream);
-    }
-    return red ? launch_strand_variant<EXP, false, true, false>(b, sweeps, grid, block, smem, round, stream)
-               : launch_strand_variant<EXP, false, false, false>(b, sweeps, grid, block, smem, round, stream);
+cudaError_t launch_strand_exp(const DevBatch& b, uint32_t sweeps, const StrandLaunch& geo, cudaStream_t stream) {
+    // Separate instantiations: the wait-statistics variant is the only one that carries them (and reads
+    // the graph and the cells from global memory); the default stages the graph and the strands' cells
+    // in shared memory when the batch has one model and they fit.
+    const bool wait = b.wait_counts != nullptr;
+    const size_t staged_bytes = size_t(geo.regions) * (kWarpSmem + size_t(b.max_per_layer) * 8) + b.strand_graph_smem;
+    const bool staged = !wait && b.strand_graph_smem != 0u && staged_bytes <= kStrandSmemLimit;
+    if (wait) return launch_strand_variant<EXP, true, false>(b, sweeps, geo, stream);
+    if (staged) return launch_strand_variant<EXP, false, true>(b, sweeps, geo, stream);
+    return launch_strand_variant<EXP, false, false>(b, sweeps, geo, stream);
 }
 }  // namespace
 
-cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count, uint32_t warps_per_cta,
+cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count, uint32_t warps_per_cta, bool from_words,
                                 cudaStream_t stream) {
     if (b.n_tiles == 0 || sweeps == 0) return cudaSuccess;
     const uint32_t capacity = uint32_t(sm_count) * warps_per_cta;
@@ -961,22 +1018,33 @@ cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count
     const uint32_t tiles_per_round = (b.n_tiles + rounds - 1) / rounds;
     cudaError_t e = cudaMemsetAsync(b.strand_flags, 0, size_t(strand_flag_words(b.n_tiles, b.strands)) * 4, stream);
     if (e != cudaSuccess) return e;
-    const size_t cells = size_t(b.n_tiles) * (b.n_spins / 8) * 32;
-    const unsigned convert_blocks = unsigned((cells + 255) / 256);
-    words_to_bytes_kernel<<<convert_blocks, 256, 0, stream>>>(b);
+    if (from_words) {
+        const size_t cells = size_t(b.n_tiles) * (b.n_spins / 8) * 32;
+        words_to_cells_kernel<<<unsigned((cells + 255) / 256), 256, 0, stream>>>(b);
+    }
     const uint32_t items = tiles_per_round * per_tile;
     const uint32_t ctas = min(uint32_t(sm_count), items);
     warps_per_cta = (items + ctas - 1) / ctas;  // <= the caller's bound, since items <= capacity
-    const dim3 grid(ctas), block(warps_per_cta * 32);
-    const uint32_t round = tiles_per_round;
-    const size_t smem = size_t(warps_per_cta) * kWarpSmem;  // (+ the staged graph, see launch_strand_exp)
+    StrandLaunch geo;
+    geo.grid = dim3(ctas);
+    geo.block = dim3(warps_per_cta * 32);
+    geo.round = tiles_per_round;
+    geo.regions = min(warps_per_cta, (tiles_per_round * b.strands + ctas - 1) / ctas);  // warps that can be strands
+    geo.tiles_over_ctas = (tiles_per_round + ctas - 1) / ctas;                          // producers a CTA can host
     switch (b.exp_kind) {
-        case kExpExact: e = launch_strand_exp<kExpExact>(b, sweeps, grid, block, smem, round, stream); break;
-        case kExpFast: e = launch_strand_exp<kExpFast>(b, sweeps, grid, block, smem, round, stream); break;
-        default: e = launch_strand_exp<kExpAccurate>(b, sweeps, grid, block, smem, round, stream); break;
+        case kExpExact: return launch_strand_exp<kExpExact>(b, sweeps, geo, stream);
+        case kExpFast: return launch_strand_exp<kExpFast>(b, sweeps, geo, stream);
+        default: return launch_strand_exp<kExpAccurate>(b, sweeps, geo, stream);
     }
-    if (e != cudaSuccess) return e;
-    bytes_to_words_kernel<<<convert_blocks, 256, 0, stream>>>(b);
+}
+
+cudaError_t launch_strand_settle(const DevBatch& b, cudaStream_t stream) {
+    if (b.n_tiles == 0) return cudaSuccess;
+    // one warp per (tile, layer), then the spin words from the cells
+    const size_t threads = size_t(b.n_tiles) * b.max_layers * 32;
+    settle_fields_kernel<<<unsigned((threads + 255) / 256), 256, 0, stream>>>(b);
+    const size_t cells = size_t(b.n_tiles) * (b.n_spins / 8) * 32;
+    cells_to_words_kernel<<<unsigned((cells + 255) / 256), 256, 0, stream>>>(b);
     return cudaGetLastError();
 }
 
