@@ -37,8 +37,13 @@ def _nvcc() -> str:
     return exe
 
 
+FLAGS_STAMP = PKG / "build" / "flags.txt"  # the flags of the last build: other flags, other library
+
+
 def needs_build() -> bool:
     if not LIB.exists():
+        return True
+    if not FLAGS_STAMP.exists() or FLAGS_STAMP.read_text() != " ".join(NVCC_FLAGS):
         return True
     newest = max(p.stat().st_mtime for p in list(CSRC.iterdir()) + [ROOT / "include" / "isingmc_b200.h"])
     return newest > LIB.stat().st_mtime
@@ -69,6 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("link failed")
+    FLAGS_STAMP.write_text(" ".join(NVCC_FLAGS))
     return LIB
 
 

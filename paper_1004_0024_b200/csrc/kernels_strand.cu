@@ -108,6 +108,31 @@ __device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// L2 eviction policies (folded into the access descriptor, a uniform register pair)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float ld_cg_f32(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_f32(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
+}
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
@@ -453,6 +478,14 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         }
     };
 
+#ifdef ISING_X_HS_EF
+    const uint64_t pol_hs = policy_evict_first();
+#define ISING_HS_LD(p) ld_cg_f32(p, pol_hs)
+#define ISING_HS_ST(p, v) st_f32(p, v, pol_hs)
+#else
+#define ISING_HS_LD(p) ld_cg_f32(p)
+#define ISING_HS_ST(p, v) st_f32(p, v)
+#endif
 #ifdef ISING_STRAND_PROFILE
     long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0;
 #endif
@@ -503,9 +536,9 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         float (&r)[8] = w.r;
 #pragma unroll
         for (int k = 0; k < 8; ++k) r[k] = 0.0f;
-        r[0] = ld_cg_f32(hs_c);
-        r[1] = ld_cg_f32(hs_c + 32);
-        r[2] = ld_cg_f32(hs_c + 64);
+        r[0] = ISING_HS_LD(hs_c);
+        r[1] = ISING_HS_LD(hs_c + 32);
+        r[2] = ISING_HS_LD(hs_c + 64);
         if constexpr (STAGED) {
             mbar_wait(bar_cells, (phases >> 2) & 1u);
             phases ^= 4u;
@@ -524,7 +557,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             // ---- the columns entering the window during this chunk, p0+3 .. p0+10 (the last chunk has five)
             float nx[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) nx[k] = (k < 5 || more) ? ld_cg_f32(hs_c + (3 + k) * 32) : 0.0f;
+            for (int k = 0; k < 8; ++k) nx[k] = (k < 5 || more) ? ISING_HS_LD(hs_c + (3 + k) * 32) : 0.0f;
             // ... and its spins: the layer below must have finished the chunk
             if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
             ChunkBits cb;
@@ -540,7 +573,11 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                 __syncwarp();  // every lane has left the other stage's previous contents
                 request(stage ^ 1u, slot);
                 // the columns three chunks ahead, into L2
+#ifdef ISING_X_PF_BULK
+                if (lane == 0 && c + 4 < C) bulk_prefetch_l2(hs_c + 24 * 32, 1024, pol_hs);
+#else
                 if (lane < 8 && c + 4 < C) prefetch_l2(hs_c + (27 + lane) * 32);
+#endif
             }
             // ---- this chunk's tape words have landed
             ISING_TICK(tA);
@@ -570,7 +607,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         const uint4 in = t.inslot(p0 + 3 + K);                                       \
         const uint32_t cell_a = cells.at(in.y >> 8), cell_b = cells.at(in.w >> 8);   \
         strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
-        if (c != 0 || K >= 2) st_f32(hs_c + (K - 2) * 32, r[(K + 6) & 7]);           \
+        if (c != 0 || K >= 2) ISING_HS_ST(hs_c + (K - 2) * 32, r[(K + 6) & 7]);      \
         r[(K + 3) & 7] = pull_slot(pull_slot(nx[K], in.x, in.y, cell_a), in.z, in.w, cell_b); \
         op = op_next;                                                                \
     }
@@ -624,8 +661,8 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         // ---- end of the layer: the last two columns leave the window; the block's partial sum joins
         // the running energy after the partial sums of all earlier blocks (tempering definition,
         // oracle/ising_oracle.h), which the strand of the layer below has published with its block
-        st_f32(hs_c + 6 * 32, r[6]);
-        st_f32(hs_c + 7 * 32, r[7]);
+        ISING_HS_ST(hs_c + 6 * 32, r[6]);
+        ISING_HS_ST(hs_c + 7 * 32, r[7]);
         if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
         if (active) {
             double* e_run = b.e_run + chain;
@@ -671,6 +708,12 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     uint32_t* head_flag = flags + S * kFlagStride;
     const uint32_t pos = b.mt_pos[tile];
     const uint32_t total = sweeps * b.n_spins;  // draws of this launch (a multiple of 8)
+#ifdef ISING_X_TAPE_EL
+    const uint64_t pol_tape = policy_evict_last();
+#define ISING_TAPE_ST(p, v) st_u32(p, v, pol_tape)
+#else
+#define ISING_TAPE_ST(p, v) st_u32(p, v)
+#endif
 
     for (uint32_t i = 0; i < kMtN; ++i) {
         uint32_t w = pos + i;
@@ -741,7 +784,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
 #pragma unroll 8
                 for (int k = 0; k < 32; ++k) {
                     const uint32_t nx = in[k * 32];
-                    st_u32(po + k * 32, mt_recurrence(cur, nx, in[1024 + k * 32]));
+                    ISING_TAPE_ST(po + k * 32, mt_recurrence(cur, nx, in[1024 + k * 32]));
                     cur = nx;
                 }
                 sa = sa2;
@@ -762,7 +805,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
                 }
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    st_u32(po + k * 32, mt_recurrence(cur, nxt[k], far[k]));
+                    ISING_TAPE_ST(po + k * 32, mt_recurrence(cur, nxt[k], far[k]));
                     cur = nxt[k];
                 }
                 sa += 32;
@@ -787,7 +830,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
                 }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    st_u32(tape + size_t(so + k) * 32, mt_recurrence(cur, nxt[k], far[k]));  // (so is a multiple of 8)
+                    ISING_TAPE_ST(tape + size_t(so + k) * 32, mt_recurrence(cur, nxt[k], far[k]));  // (so is a multiple of 8)
                     cur = nxt[k];
                 }
                 sa = sa + 8 >= R ? sa + 8 - R : sa + 8;
@@ -811,6 +854,16 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     if (lane == 0) b.mt_pos[tile] = (pos + total % kMtN) % kMtN;
 }
 
+// Which logical warp (work item dealer below) each hardware warp of a CTA is.  The four schedulers of
+// an SM take the hardware warps round-robin (warp % 4), a tile advances at the pace of its slowest
+// warp, and a producer costs about half a strand's issue slots: so the strands take the low
+// hardware warps and each producer the next free warp of the least loaded scheduler, leaving gaps
+// (c5: 14 strands + 4 producers per CTA as 4 | 4 | 3 + 2 | 3 + 2 instead of 4 + 1 | 4 + 1 | 3 + 1 | 3 + 1).
+constexpr uint32_t kIdleWarp = 0xffu;
+struct StrandWarpMap {
+    uint8_t logical[32];
+};
+
 // Persistent grid of independent warps.  Work items of a round: for each of `tiles_per_round` tiles
 // its S strands and its producer; every item of a round is resident at once (the launcher sizes the
 // rounds), so the waits above always end.  Items are dealt warp-major, so a CTA's low warps are
@@ -822,9 +875,10 @@ template <int EXP, bool WAIT, bool STAGED>
 __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(DevBatch b, uint32_t sweeps,
                                                                                  uint32_t tiles_per_round,
                                                                                  uint32_t strand_regions,
-                                                                                 uint32_t producer_slots) {
+                                                                                 uint32_t producer_slots, StrandWarpMap map) {
     extern __shared__ __align__(128) unsigned char strand_smem[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    // `warp` is the LOGICAL warp index (see StrandWarpMap); kIdleWarp: a padding warp
+    const uint32_t warp = map.logical[threadIdx.x >> 5], lane = threadIdx.x & 31u;
     const uint32_t region_bytes = kWarpSmem + (STAGED ? b.max_per_layer * 8u : 0u);
     unsigned char* warp_smem = strand_smem + size_t(warp) * region_bytes;  // (strands only: warp < strand_regions)
     unsigned char* graph_smem = strand_smem + size_t(strand_regions) * region_bytes;
@@ -853,6 +907,7 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
         staged.edges = smem_u32(edges);
         __syncthreads();
     }
+    if (warp == kIdleWarp) return;
     const uint32_t item = warp * gridDim.x + blockIdx.x;
     const uint32_t S = b.strands;
     for (uint32_t base = 0; base < b.n_tiles; base += tiles_per_round) {
@@ -969,7 +1024,37 @@ constexpr size_t kStrandSmemLimit = 227 * 1024;
 struct StrandLaunch {
     dim3 grid, block;
     uint32_t round, regions, tiles_over_ctas;
+    StrandWarpMap map;
 };
+
+// Hardware warps for `logical_warps` logical ones, the first `strands` of them strands (see
+// StrandWarpMap); returns the hardware warps per CTA.
+uint32_t place_warps(uint32_t logical_warps, uint32_t strands, StrandWarpMap& map) {
+    for (uint8_t& w : map.logical) w = uint8_t(kIdleWarp);
+    float load[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    uint32_t used = 0;
+    for (uint32_t w = 0; w < strands; ++w) {
+        map.logical[w] = uint8_t(w);
+        load[w % 4] += 1.0f;
+        used = w + 1;
+    }
+    for (uint32_t w = strands; w < logical_warps; ++w) {
+        uint32_t best = 0;
+        for (uint32_t sch = 1; sch < 4; ++sch) {
+            if (load[sch] < load[best]) best = sch;
+        }
+        uint32_t hw = strands;
+        while (hw < kStrandMaxWarps && (map.logical[hw] != kIdleWarp || hw % 4 != best)) ++hw;
+        if (hw >= kStrandMaxWarps) {  // no room on that scheduler: the first free warp
+            hw = strands;
+            while (map.logical[hw] != kIdleWarp) ++hw;
+        }
+        map.logical[hw] = uint8_t(w);
+        load[hw % 4] += 0.55f;
+        used = max(used, hw + 1);
+    }
+    return used;
+}
 
 template <int EXP, bool WAIT, bool STAGED>
 cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, const StrandLaunch& geo, cudaStream_t stream) {
@@ -988,7 +1073,8 @@ cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, const Stra
     uint32_t slots = geo.tiles_over_ctas;
     if (base + size_t(slots) * kProducerSmem > kStrandSmemLimit) slots = 0;
     const size_t total_smem = base + size_t(slots) * kProducerSmem;
-    sweep_strand_kernel<EXP, WAIT, STAGED><<<geo.grid, geo.block, total_smem, stream>>>(b, sweeps, geo.round, geo.regions, slots);
+    sweep_strand_kernel<EXP, WAIT, STAGED><<<geo.grid, geo.block, total_smem, stream>>>(b, sweeps, geo.round, geo.regions, slots,
+                                                                                        geo.map);
     return cudaGetLastError();
 }
 template <int EXP>
@@ -1027,9 +1113,9 @@ cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count
     warps_per_cta = (items + ctas - 1) / ctas;  // <= the caller's bound, since items <= capacity
     StrandLaunch geo;
     geo.grid = dim3(ctas);
-    geo.block = dim3(warps_per_cta * 32);
     geo.round = tiles_per_round;
     geo.regions = min(warps_per_cta, (tiles_per_round * b.strands + ctas - 1) / ctas);  // warps that can be strands
+    geo.block = dim3(place_warps(warps_per_cta, geo.regions, geo.map) * 32);
     geo.tiles_over_ctas = (tiles_per_round + ctas - 1) / ctas;                          // producers a CTA can host
     switch (b.exp_kind) {
         case kExpExact: return launch_strand_exp<kExpExact>(b, sweeps, geo, stream);
