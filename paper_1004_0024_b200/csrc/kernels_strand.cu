@@ -415,16 +415,17 @@ __device__ __noinline__ CarefulResult careful_chunk(Window w, RawWords raw, Chun
 }
 
 // ---- a strand ---------------------------------------------------------------------------------
-// Per-strand shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB),
-// three mbarriers, the scratch of the careful chunks and — STAGED — the cells of the layer being swept
-// (64 bytes per chunk).
-constexpr uint32_t kStageBytes = 1024;
-constexpr uint32_t kWarpSmem = 2 * kStageBytes + 32 + 1024;
+// Per-strand shared memory: two landing stages for what the bulk copies bring (8 tape rows = 1 KB and
+// the 8 field columns entering the window = 1 KB; the latter doubles as the scratch of a careful
+// chunk), three mbarriers and — STAGED — the cells of the layer being swept (64 bytes per chunk).
+constexpr uint32_t kStageBytes = 2048;
+constexpr uint32_t kWarpSmem = 2 * kStageBytes + 32;
 
-// Everything a chunk reads from global memory is requested one chunk ahead or more: the tape rows by
-// a bulk (TMA) copy of one elected lane into the warp's landing stage (no registers held meanwhile),
-// the eight columns entering the window by plain loads at the chunk's start (consumed three attempts
-// later at the earliest); the columns three chunks ahead are prefetched into L2; the layer's cells
+// Everything a chunk reads from global memory is requested one chunk ahead or more: the tape rows and
+// the eight field columns entering the window by bulk (TMA) copies of one elected lane into the warp's
+// landing stage (no registers held meanwhile; nobody but this strand writes those columns, and it last
+// did a sweep ago), the spin bytes of the two neighbouring layers by plain loads into a register each
+// (the layer below's only once its strand is known to have finished that chunk); the layer's cells
 // arrive by one bulk copy per layer.  So the loop-carried chain of the attempts is all a strand waits
 // for.
 template <int EXP, bool WAIT, bool STAGED>
@@ -449,10 +450,10 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     uint32_t pred_cached = 0, head_cached = 0;
     uint32_t flips = 0;
     uint32_t seq = 0;  // chunks finished
-    // landing stages: stage s at wsm + s * kStageBytes; then the barriers, the scratch, the cells
+    uint32_t until_pub = pub;
+    // landing stages: stage s at wsm + s * kStageBytes (tape rows, then columns); then the barriers, the cells
     const uint32_t wsm = smem_u32(warp_smem);
     const uint32_t bar0 = wsm + 2 * kStageBytes, bar_cells = bar0 + 16;
-    float* scratch = reinterpret_cast<float*>(warp_smem + 2 * kStageBytes + 32) + lane;
     const uint32_t cells_smem = wsm + kWarpSmem;
     uint32_t stage = 0, phases = 0;  // current stage; bit s of phases = parity the next wait on stage s sees (bit 2: the cells)
     if (lane == 0) {
@@ -466,15 +467,18 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     const bool record_wait = WAIT && b.wait_counts != nullptr && b.tile_count[tile] == 32;
     uint32_t wait[6] = {0, 0, 0, 0, 0, 0};
 
-    // one elected lane requests a chunk's tape rows into stage `st`
-    const auto request = [&](uint32_t st, uint32_t slot) {
+    // one elected lane requests a chunk's tape rows and entering columns (`columns` points at lane 0's
+    // entry of the first one) into stage `st`
+    const auto request = [&](uint32_t st, uint32_t slot, const float* columns, uint32_t column_bytes) {
         if (lane == 0) {
             const uint32_t dst = wsm + st * kStageBytes, bar = bar0 + st * 8;
-            // the rows were written through the generic proxy (by the producer, acquired above): order
-            // the async-proxy read after what this lane has observed
+            // the rows were written through the generic proxy (by the producer, acquired above; the
+            // columns by this warp before the block began, fenced there): order the async-proxy reads
+            // after what this lane has observed
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            mbar_expect(bar, 1024);
+            mbar_expect(bar, 1024 + column_bytes);
             bulk_load(dst, tape + size_t(slot) * 32, 1024, bar);
+            bulk_load(dst + 1024, columns, column_bytes, bar);
         }
     };
 
@@ -512,12 +516,12 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         const uint8_t* up_c = reinterpret_cast<const uint8_t*>(cells_tile + size_t(l_up) * C * 32) + 1;
         const uint8_t* dn_c = reinterpret_cast<const uint8_t*>(cells_tile + size_t(l_dn) * C * 32) + 1;
         Cells<STAGED> cells;
+        // What the bulk copies of this block read — the layer's columns and cells as this warp left
+        // them a sweep ago (or as the launch found them) — was stored through the generic proxy by every
+        // lane, and every lane has read the shared-memory copies they replace: both come before them.
+        asm volatile("fence.proxy.async.global;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
         if constexpr (STAGED) {
-            // The layer's cells as this warp left them a sweep ago (or as the launch found them), by one
-            // bulk copy: every lane's stores to them, and every lane's reads of the copy it replaces,
-            // come before it.
-            asm volatile("fence.proxy.async.global;\n\tfence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
             if (lane == 0) {
                 mbar_expect(bar_cells, C * 64);
                 bulk_load(cells_smem, cur_c - lane, C * 64, bar_cells);
@@ -530,7 +534,13 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         // ---- the first chunk's operands (the only exposed round trips of the block)
         wait_counter(head_flag, head_need, head_cached);
         __syncwarp();  // every lane has left the stage's previous contents
-        request(stage, slot);
+        request(stage, slot, hs_c - lane + 3 * 32, 1024);  // (a layer has two chunks at least)
+        // The neighbour spins of a chunk are requested a chunk ahead when the layer below is already known
+        // to have finished it.  (The spins above wait for the same condition: above the last layer lies
+        // layer 0, swept earlier in this sweep by the strand S - 1 hops ahead in the ring of waits, whose
+        // chunk c is only known to be finished once the layer below's is.)
+        uint32_t up_next = 0, dn_next = 0;
+        bool dn_ready = false;
         // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
         Window w;
         float (&r)[8] = w.r;
@@ -554,30 +564,32 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             const uint32_t p0 = c * 8;
             const uint4 chunk_info = t.chunk(c);
             const bool more = c + 1 < C;
-            // ---- the columns entering the window during this chunk, p0+3 .. p0+10 (the last chunk has five)
-            float nx[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) nx[k] = (k < 5 || more) ? ISING_HS_LD(hs_c + (3 + k) * 32) : 0.0f;
-            // ... and its spins: the layer below must have finished the chunk
-            if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
+            // ---- the chunk's spins: the layer below must have finished it (normally known from an earlier
+            // wait, and the byte requested a chunk ago)
+            if (!dn_ready) {
+                if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
+                dn_next = ld_cg_u8(dn_c);
+                up_next = ld_cg_u8(up_c);
+            }
             ChunkBits cb;
             cb.cur8 = (STAGED ? cells.at(c * 64) : ld_cg_u16(cur_c)) >> 8;
-            cb.up8 = ld_cg_u8(up_c);
-            cb.dn8 = ld_cg_u8(dn_c);
-            // ---- the next chunk's tape rows, by bulk copy
+            cb.up8 = up_next;
+            cb.dn8 = dn_next;
+            dn_ready = false;
+            // ---- the next chunk's tape rows and entering columns (p0+11 .. p0+18; the last chunk has five),
+            // by bulk copy; its neighbour spins
             if (more) {
                 slot = slot + 8 == R ? 0u : slot + 8;
                 head_need += 8;
                 ++pred_need;
+                if (!has_pred || int32_t(pred_cached - pred_need) >= 0) {
+                    dn_next = ld_cg_u8(dn_c + 64);
+                    up_next = ld_cg_u8(up_c + 64);
+                    dn_ready = true;
+                }
                 wait_counter(head_flag, head_need, head_cached);
                 __syncwarp();  // every lane has left the other stage's previous contents
-                request(stage ^ 1u, slot);
-                // the columns three chunks ahead, into L2
-#ifdef ISING_X_PF_BULK
-                if (lane == 0 && c + 4 < C) bulk_prefetch_l2(hs_c + 24 * 32, 1024, pol_hs);
-#else
-                if (lane < 8 && c + 4 < C) prefetch_l2(hs_c + (27 + lane) * 32);
-#endif
+                request(stage ^ 1u, slot, hs_c - lane + 11 * 32, c + 2 < C ? 1024u : 640u);
             }
             // ---- this chunk's tape words have landed
             ISING_TICK(tA);
@@ -586,6 +598,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             phases ^= 1u << stage;
             // (plain loads: the compiler may put each one next to its use; the wait above keeps them behind it)
             const uint32_t* landed = reinterpret_cast<const uint32_t*>(warp_smem + stage * kStageBytes) + lane;
+            float* nx = reinterpret_cast<float*>(warp_smem + stage * kStageBytes + 1024) + lane;  // column p0+3+k at nx[k * 32]
             RawWords raw_words;
             uint32_t (&raw)[8] = raw_words.v;
 #pragma unroll
@@ -608,7 +621,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         const uint32_t cell_a = cells.at(in.y >> 8), cell_b = cells.at(in.w >> 8);   \
         strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
         if (c != 0 || K >= 2) ISING_HS_ST(hs_c + (K - 2) * 32, r[(K + 6) & 7]);      \
-        r[(K + 3) & 7] = pull_slot(pull_slot(nx[K], in.x, in.y, cell_a), in.z, in.w, cell_b); \
+        r[(K + 3) & 7] = pull_slot(pull_slot(nx[K * 32], in.x, in.y, cell_a), in.z, in.w, cell_b); \
         op = op_next;                                                                \
     }
                 ISING_STRAND_ATTEMPT(0, 1)
@@ -621,12 +634,17 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                 ISING_STRAND_ATTEMPT(7, 7)
 #undef ISING_STRAND_ATTEMPT
             } else {
+                // the landed columns are the scratch: everything pulled first, in place
 #pragma unroll
-                for (int k = 0; k < 8; ++k) scratch[k * 32] = (k < 5 || more) ? pull_column(nx[k], p0 + 3 + k, t, cells) : 0.0f;
-                const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, t, p0, hs_l, scratch, e_blk);
+                for (int k = 0; k < 8; ++k) {
+                    if (k < 5 || more) nx[k * 32] = pull_column(nx[k * 32], p0 + 3 + k, t, cells);
+                }
+                const CarefulResult res = careful_chunk<EXP>(w, raw_words, cb, nb2, u_offset, t, p0, hs_l, nx, e_blk);
                 w = res.w;
                 acc8 = res.acc8;
                 e_blk = res.e_blk;
+                // (this stage's next bulk copy comes after these generic writes)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
 
             // ---- after the chunk: the cell (new spins, what flipped), progress
@@ -650,7 +668,10 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                 cur_c += 32;
                 up_c += 64;
                 dn_c += 64;
-                if (seq % pub == 0u) publish_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
+                if (--until_pub == 0u) {
+                    publish_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
+                    until_pub = pub;
+                }
             }
             ISING_TICK(tE);
         }
