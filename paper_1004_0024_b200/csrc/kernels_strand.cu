@@ -474,7 +474,8 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             const uint32_t dst = wsm + st * kStageBytes, bar = bar0 + st * 8;
             // the rows were written through the generic proxy (by the producer, acquired above; the
             // columns by this warp before the block began, fenced there): order the async-proxy reads
-            // after what this lane has observed
+            // after what this lane has observed (measured: the fence is not what a request costs — issuing
+            // the two copies is, about 300 cycles)
             asm volatile("fence.proxy.async.global;" ::: "memory");
             mbar_expect(bar, 1024 + column_bytes);
             bulk_load(dst, tape + size_t(slot) * 32, 1024, bar);
@@ -491,7 +492,15 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
 #define ISING_HS_ST(p, v) st_f32(p, v)
 #endif
 #ifdef ISING_STRAND_PROFILE
-    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0;
+    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0, tPred = 0, tHead = 0, tReq = 0;
+#define ISING_TIMED(acc, stmt)                  \
+    {                                           \
+        const long long before_ = clock64();    \
+        stmt;                                   \
+        acc += clock64() - before_;             \
+    }
+#else
+#define ISING_TIMED(acc, stmt) stmt;
 #endif
     for (uint32_t blk = 0; blk < total_blocks; ++blk) {
         const uint32_t sw = blk / blocks_per_sweep, m = blk - sw * blocks_per_sweep;
@@ -567,7 +576,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             // ---- the chunk's spins: the layer below must have finished it (normally known from an earlier
             // wait, and the byte requested a chunk ago)
             if (!dn_ready) {
-                if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
+                if (has_pred) ISING_TIMED(tPred, wait_counter(pred_flag, pred_need, pred_cached))
                 dn_next = ld_cg_u8(dn_c);
                 up_next = ld_cg_u8(up_c);
             }
@@ -587,9 +596,9 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                     up_next = ld_cg_u8(up_c + 64);
                     dn_ready = true;
                 }
-                wait_counter(head_flag, head_need, head_cached);
+                ISING_TIMED(tHead, wait_counter(head_flag, head_need, head_cached))
                 __syncwarp();  // every lane has left the other stage's previous contents
-                request(stage ^ 1u, slot, hs_c - lane + 11 * 32, c + 2 < C ? 1024u : 640u);
+                ISING_TIMED(tReq, request(stage ^ 1u, slot, hs_c - lane + 11 * 32, c + 2 < C ? 1024u : 640u); __syncwarp())
             }
             // ---- this chunk's tape words have landed
             ISING_TICK(tA);
@@ -706,7 +715,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     }
     if (active && flips != 0u) atomicAdd(b.flips + chain, static_cast<unsigned long long>(flips));
 #ifdef ISING_STRAND_PROFILE
-    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld cell %lld rotate %lld; block end %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tF / total_blocks);
+    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld cell %lld rotate %lld (in request: pred wait %lld head wait %lld bulk requests %lld); block end %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tPred / seq, tHead / seq, tReq / seq, tF / total_blocks);
 #endif
 }
 
