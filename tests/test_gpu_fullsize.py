@@ -379,3 +379,22 @@ def test_c4_full_length_one_system_inside_distinct_instances(lib, port):
     np.testing.assert_array_equal(flips[64:96], want["flips"])
     np.testing.assert_array_equal(slots[64:96], want["slot"])
     np.testing.assert_array_equal(e_run[64:96].view(np.uint64), want["e_run"].view(np.uint64))
+
+
+def test_bench_two_gpus_when_the_box_has_them():
+    """`bench.py --gpus 2` started plainly spawns its two ranks (torch.distributed.run, NCCL) and prints one
+    line for the whole job.  The GPU boxes of this project have one device: skipped there."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+                          "--ladders", "64", "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["first_ladder_of_rank"] == [0, 64]
+    assert line["gpu_launches"] > 0 and line["value"] > 0
