@@ -155,7 +155,7 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 }
 __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t need, uint32_t& cached) {
     if (int32_t(need - cached) > 0) {
-        while (int32_t(need - ld_relaxed(p)) > 0) __nanosleep(64);
+        while (int32_t(need - ld_relaxed(p)) > 0) __nanosleep(128);
         cached = __reduce_min_sync(0xffffffffu, ld_acquire(p));
     }
 }
@@ -296,7 +296,8 @@ struct Cells<true> {
 // One far in-edge of a column (DevStrandGraph::inslots): `cell` is the source chunk's cell, `meta`'s
 // low five bits the shift that brings the source's spin bit to bit 31 and its flip bit to bit 23.
 // A flip of the source from s to -s subtracted (2s)*J from h: adds 2J with the sign of the NEW spin.
-// Not flipped (or a null slot): adds -0.0, the identity for every bit pattern.
+// Not flipped (or a null slot, meta == kNullSlot): adds -0.0, the identity for every bit pattern.
+constexpr uint32_t kNullSlot = 31u;
 __device__ __forceinline__ float pull_slot(float h, uint32_t j2, uint32_t meta, uint32_t cell) {
     const uint32_t x = __funnelshift_l(0u, cell, meta);  // (the shift wraps at 32)
     const uint32_t addend = (x & 0x00800000u) != 0u ? (j2 ^ (x & 0x80000000u)) : 0x80000000u;
@@ -627,10 +628,13 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     {                                                                                \
         const uint4 op_next = band_entry<NEXT>(t, p0 + NEXT, cb.cur8);               \
         const uint4 in = t.inslot(p0 + 3 + K);                                       \
-        const uint32_t cell_a = cells.at(in.y >> 8), cell_b = cells.at(in.w >> 8);   \
+        const uint32_t cell_a = cells.at(in.y >> 8);                                 \
+        float entering = pull_slot(nx[K * 32], in.x, in.y, cell_a);                  \
+        /* (warp-uniform: most columns of a sparse layer have one far in-edge or none) */ \
+        if (in.w != kNullSlot) entering = pull_slot(entering, in.z, in.w, cells.at(in.w >> 8)); \
         strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
         if (c != 0 || K >= 2) ISING_HS_ST(hs_c + (K - 2) * 32, r[(K + 6) & 7]);      \
-        r[(K + 3) & 7] = pull_slot(pull_slot(nx[K * 32], in.x, in.y, cell_a), in.z, in.w, cell_b); \
+        r[(K + 3) & 7] = entering;                                                   \
         op = op_next;                                                                \
     }
                 ISING_STRAND_ATTEMPT(0, 1)
