@@ -61,7 +61,11 @@ namespace isingb200 {
 
 namespace {
 
+#ifdef ISING_X_MAXWARPS  // (timing experiment: more, thinner warps)
+constexpr uint32_t kStrandMaxWarps = ISING_X_MAXWARPS;
+#else
 constexpr uint32_t kStrandMaxWarps = 20;  // registers are granted 32 per thread at a time: 20 warps x 96
+#endif
 constexpr uint32_t kFlagStride = 32;  // one 128-byte line per progress counter
 
 // ---- memory access helpers -----------------------------------------------------------------
