@@ -647,7 +647,9 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         spin_cells_.allocate(std::max<size_t>(1, size_t(tiles) * (n / 8) * 32 * sizeof(uint16_t)), device_bytes_);
         strand_flags_.allocate(size_t(strand_flag_words(tiles, strands)) * sizeof(uint32_t), device_bytes_);
         dev_.tape = tape_.as<uint32_t>();
+        spin_nbr_.allocate(std::max<size_t>(1, size_t(tiles) * (n / 8) * 32 * sizeof(uint16_t)), device_bytes_);
         dev_.spin_cells = spin_cells_.as<uint16_t>();
+        dev_.spin_nbr = spin_nbr_.as<uint16_t>();
         dev_.strand_flags = strand_flags_.as<uint32_t>();
     }
 
@@ -794,6 +796,7 @@ void Batch::launch_sweeps(uint32_t sweeps) {
     begin_timed(false);
     if (family_ == KernelFamily::strand) {
         // the cells stay authoritative between strand launches (settle() restores the canonical state)
+        dev_.strand_epoch = uint32_t(sweeps_done_ & 0xffu);
         cuda_check(launch_sweep_strand(dev_, sweeps, sm_count_, strand_warps_, !strand_live_, stream_),
                    "strand sweep kernel");
         if (!strand_live_) ++other_launches;  // spin words -> cells

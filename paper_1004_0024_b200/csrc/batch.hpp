@@ -133,7 +133,7 @@ class Batch {
     DeviceBuffer slot_of_chain_, chain_at_slot_, hs_, ht_, spin_bits_, mt_, mt_pos_, e_run_, flips_;
     DeviceBuffer swap_seeds_, swap_mt_, swap_pos_, swap_acc_, swap_att_;
     DeviceBuffer layer_graphs_, wait_counts_;
-    DeviceBuffer strand_graphs_, tape_, spin_cells_, strand_flags_;
+    DeviceBuffer strand_graphs_, tape_, spin_cells_, spin_nbr_, strand_flags_;
     bool strand_live_ = false;  // the strand family has run since the last settle(): cells hold the spins, far updates pending
     void settle();              // back to the canonical state (fields complete, spin_bits current); no-op otherwise
     uint32_t strand_warps_ = 0;

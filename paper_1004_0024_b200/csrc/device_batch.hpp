@@ -149,6 +149,11 @@ struct DevBatch {
     uint32_t* tape;         // u32 [tile][R][32]: raw MT19937 words in draw order
     uint16_t* spin_cells;   // u16 [tile][spin / 8][32]: bit 8+k of a lane's cell <=> its spin 8c+k is -1, bit k <=> it
                             // flipped in the chunk's latest sweep (DevStrandGraph)
+    // u16 [tile][spin / 8][32], what the strands of the neighbouring layers read: bit k <=> spin 8c+k is
+    // -1, high byte = low byte of the number of sweeps the chunk has seen (batch lifetime) — spins and
+    // their version in one word, so a reader needs no fence between a progress counter and the data
+    uint16_t* spin_nbr;
+    uint32_t strand_epoch;  // sweeps done before this launch: the version every chunk carries at its start
     uint32_t* strand_flags; // per tile S + 1 progress counters (strand chunks done, tape head), one line each
     uint32_t strand_graph_smem;  // bytes of model 0's graph staged in shared memory (0: tables read from global)
     // tempering

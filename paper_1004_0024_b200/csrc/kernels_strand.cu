@@ -61,11 +61,9 @@ namespace isingb200 {
 
 namespace {
 
-#ifdef ISING_X_MAXWARPS  // (timing experiment: more, thinner warps)
-constexpr uint32_t kStrandMaxWarps = ISING_X_MAXWARPS;
-#else
-constexpr uint32_t kStrandMaxWarps = 20;  // registers are granted 32 per thread at a time: 20 warps x 96
-#endif
+// registers are granted 32 per thread at a time: 20 warps x 96.  (Measured with 32 warps x 64 registers:
+// the strand spills, c5 1.36e11 at 4 strands per tile and 1.22e11 at 8.)
+constexpr uint32_t kStrandMaxWarps = 20;
 constexpr uint32_t kFlagStride = 32;  // one 128-byte line per progress counter
 
 // ---- memory access helpers -----------------------------------------------------------------
@@ -77,11 +75,6 @@ __device__ __forceinline__ float ld_cg_f32(const float* p) {
 __device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_cg_u8(const uint8_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ uint32_t ld_cg_u16(const uint16_t* p) {
@@ -111,33 +104,6 @@ __device__ __forceinline__ void st_f32(float* p, float v) {
 __device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-// L2 eviction policies (folded into the access descriptor, a uniform register pair)
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ float ld_cg_f32(const float* p, uint64_t pol) {
-    float v;
-    asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_f32(float* p, float v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
-    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
-}
-
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -157,6 +123,25 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_u16(const uint16_t* p) {
+    uint32_t v;
+    asm volatile("{\n.reg .b16 t;\nld.relaxed.gpu.global.u16 t, [%1];\ncvt.u32.u16 %0, t;\n}" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u16(uint16_t* p, uint32_t v) {
+    asm volatile("{\n.reg .b16 t;\ncvt.u16.u32 t, %1;\nst.relaxed.gpu.global.u16 [%0], t;\n}" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// The same wait without the acquire: a HINT that what the counter announces is probably visible — for
+// data that carries its own version (DevBatch::spin_nbr), checked by the reader.
+__device__ __forceinline__ void wait_hint(const uint32_t* p, uint32_t need, uint32_t& cached) {
+    if (int32_t(need - cached) > 0) {
+        while (int32_t(need - ld_relaxed(p)) > 0) __nanosleep(128);
+        cached = __reduce_min_sync(0xffffffffu, ld_relaxed(p));
+    }
+}
 __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t need, uint32_t& cached) {
     if (int32_t(need - cached) > 0) {
         while (int32_t(need - ld_relaxed(p)) > 0) __nanosleep(128);
@@ -171,6 +156,14 @@ __device__ __forceinline__ void publish(uint32_t* p, uint32_t value, uint32_t la
 }
 // A strand's progress line: word 0 its finished chunks (what the strand of the next layer waits on),
 // word 1 the draw index it will need next (what the producer may not overwrite yet; 0xffffffff: done).
+// Inside a layer the same line is only a hint (no fence: MEMBAR.ALL.GPU costs ~3,500 cycles): the spins
+// the next strand reads carry their own version.
+__device__ __forceinline__ void hint_strand(uint32_t* line, uint32_t chunks, uint32_t next_draw, uint32_t lane) {
+    if (lane == 0) {
+        st_relaxed(line + 1, next_draw);
+        st_relaxed(line, chunks);
+    }
+}
 __device__ __forceinline__ void publish_strand(uint32_t* line, uint32_t chunks, uint32_t next_draw, uint32_t lane) {
     __syncwarp();
     if (lane == 0) {
@@ -445,6 +438,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     const float u_offset = active ? 0.0f : 2.0f;
     float* hs_tile = b.hs + size_t(tile) * n * 32 + lane;
     uint16_t* cells_tile = b.spin_cells + size_t(tile) * (n / 8) * 32 + lane;
+    uint16_t* nbr_tile = b.spin_nbr + size_t(tile) * (n / 8) * 32 + lane;
     const uint32_t R = b.tape_rows;
     const uint32_t* tape = b.tape + size_t(tile) * R * 32;  // (no lane offset: rows are copied whole)
     uint32_t* flags = b.strand_flags + size_t(tile) * (S + 1) * kFlagStride;
@@ -452,7 +446,8 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     const uint32_t* pred_flag = flags + ((j + S - 1) % S) * kFlagStride;
     const uint32_t* head_flag = flags + S * kFlagStride;
     const uint32_t pub = b.strand_pub;
-    uint32_t pred_cached = 0, head_cached = 0;
+    uint32_t pred_cached = 0, head_cached = 0;  // last values read WITH acquire
+    uint32_t pred_hint = 0;                     // last value of the layer below's counter read without (wait_hint)
     uint32_t flips = 0;
     uint32_t seq = 0;  // chunks finished
     uint32_t until_pub = pub;
@@ -488,14 +483,6 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         }
     };
 
-#ifdef ISING_X_HS_EF
-    const uint64_t pol_hs = policy_evict_first();
-#define ISING_HS_LD(p) ld_cg_f32(p, pol_hs)
-#define ISING_HS_ST(p, v) st_f32(p, v, pol_hs)
-#else
-#define ISING_HS_LD(p) ld_cg_f32(p)
-#define ISING_HS_ST(p, v) st_f32(p, v)
-#endif
 #ifdef ISING_STRAND_PROFILE
     long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0, tPred = 0, tHead = 0, tReq = 0;
 #define ISING_TIMED(acc, stmt)                  \
@@ -527,8 +514,14 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         // high bytes of their cells
         float* hs_c = hs_l;
         uint16_t* cur_c = cells_tile + size_t(l) * C * 32;
-        const uint8_t* up_c = reinterpret_cast<const uint8_t*>(cells_tile + size_t(l_up) * C * 32) + 1;
-        const uint8_t* dn_c = reinterpret_cast<const uint8_t*>(cells_tile + size_t(l_dn) * C * 32) + 1;
+        uint16_t* out_c = nbr_tile + size_t(l) * C * 32;
+        const uint16_t* up_c = nbr_tile + size_t(l_up) * C * 32;
+        const uint16_t* dn_c = nbr_tile + size_t(l_dn) * C * 32;
+        // Versions (DevBatch::spin_nbr): this sweep leaves `version` behind.  The layer below was swept in
+        // this sweep — except below layer 0, which is the last layer of the sweep before; the layer above
+        // will be swept later in this sweep — except above the last layer, which is layer 0, swept already.
+        const uint32_t version = (b.strand_epoch + sw + 1u) & 0xffu, before = (b.strand_epoch + sw) & 0xffu;
+        const uint32_t dn_version = l == 0u ? before : version, up_version = l_up == 0u ? version : before;
         Cells<STAGED> cells;
         // What the bulk copies of this block read — the layer's columns and cells as this warp left
         // them a sweep ago (or as the launch found them) — was stored through the generic proxy by every
@@ -549,20 +542,24 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         wait_counter(head_flag, head_need, head_cached);
         __syncwarp();  // every lane has left the stage's previous contents
         request(stage, slot, hs_c - lane + 3 * 32, 1024);  // (a layer has two chunks at least)
-        // The neighbour spins of a chunk are requested a chunk ahead when the layer below is already known
-        // to have finished it.  (The spins above wait for the same condition: above the last layer lies
-        // layer 0, swept earlier in this sweep by the strand S - 1 hops ahead in the ring of waits, whose
-        // chunk c is only known to be finished once the layer below's is.)
+        // The neighbour spins of a chunk are requested a chunk ahead when the layer below's counter says it
+        // has probably finished it; whether they are this sweep's is read off their versions when they
+        // are used (the counter is a hint: no fence orders it after the spins).  The spins above need no
+        // wait — their strand is behind this one — except above the last layer: layer 0 was swept earlier
+        // in this sweep, by the strand S - 1 hops ahead in the ring of waits.
         uint32_t up_next = 0, dn_next = 0;
         bool dn_ready = false;
+        const auto versions_ok = [&]() {
+            return __all_sync(0xffffffffu, (dn_next >> 8) == dn_version && (up_next >> 8) == up_version);
+        };
         // register window: positions 0..2 (entries for -2, -1 stay unused: their band slots are empty)
         Window w;
         float (&r)[8] = w.r;
 #pragma unroll
         for (int k = 0; k < 8; ++k) r[k] = 0.0f;
-        r[0] = ISING_HS_LD(hs_c);
-        r[1] = ISING_HS_LD(hs_c + 32);
-        r[2] = ISING_HS_LD(hs_c + 64);
+        r[0] = ld_cg_f32(hs_c);
+        r[1] = ld_cg_f32(hs_c + 32);
+        r[2] = ld_cg_f32(hs_c + 64);
         if constexpr (STAGED) {
             mbar_wait(bar_cells, (phases >> 2) & 1u);
             phases ^= 4u;
@@ -580,15 +577,22 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             const bool more = c + 1 < C;
             // ---- the chunk's spins: the layer below must have finished it (normally known from an earlier
             // wait, and the byte requested a chunk ago)
-            if (!dn_ready) {
-                if (has_pred) ISING_TIMED(tPred, wait_counter(pred_flag, pred_need, pred_cached))
-                dn_next = ld_cg_u8(dn_c);
-                up_next = ld_cg_u8(up_c);
+            if (!dn_ready || !versions_ok()) {
+                if (has_pred) ISING_TIMED(tPred, wait_hint(pred_flag, pred_need, pred_hint))
+                for (uint32_t polls = 0;; ++polls) {
+                    dn_next = ld_relaxed_u16(dn_c);
+                    up_next = ld_relaxed_u16(up_c);
+                    if (versions_ok()) break;
+                    // (the layer below finishes the chunk within microseconds of its counter saying so: ten
+                    // seconds of polling mean the versions are inconsistent — fail loudly instead of hanging)
+                    if (polls > (1u << 26)) __trap();
+                    __nanosleep(128);
+                }
             }
             ChunkBits cb;
             cb.cur8 = (STAGED ? cells.at(c * 64) : ld_cg_u16(cur_c)) >> 8;
-            cb.up8 = up_next;
-            cb.dn8 = dn_next;
+            cb.up8 = up_next & 0xffu;
+            cb.dn8 = dn_next & 0xffu;
             dn_ready = false;
             // ---- the next chunk's tape rows and entering columns (p0+11 .. p0+18; the last chunk has five),
             // by bulk copy; its neighbour spins
@@ -596,9 +600,9 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                 slot = slot + 8 == R ? 0u : slot + 8;
                 head_need += 8;
                 ++pred_need;
-                if (!has_pred || int32_t(pred_cached - pred_need) >= 0) {
-                    dn_next = ld_cg_u8(dn_c + 64);
-                    up_next = ld_cg_u8(up_c + 64);
+                if (!has_pred || int32_t(pred_hint - pred_need) >= 0) {
+                    dn_next = ld_relaxed_u16(dn_c + 32);
+                    up_next = ld_relaxed_u16(up_c + 32);
                     dn_ready = true;
                 }
                 ISING_TIMED(tHead, wait_counter(head_flag, head_need, head_cached))
@@ -637,7 +641,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         /* (warp-uniform: most columns of a sparse layer have one far in-edge or none) */ \
         if (in.w != kNullSlot) entering = pull_slot(entering, in.z, in.w, cells.at(in.w >> 8)); \
         strand_attempt<EXP, K>(r, pr, nb2, op, acc8, e_blk);                         \
-        if (c != 0 || K >= 2) ISING_HS_ST(hs_c + (K - 2) * 32, r[(K + 6) & 7]);      \
+        if (c != 0 || K >= 2) st_f32(hs_c + (K - 2) * 32, r[(K + 6) & 7]);      \
         r[(K + 3) & 7] = entering;                                                   \
         op = op_next;                                                                \
     }
@@ -669,6 +673,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             const uint32_t cell = acc8 | (cb.cur8 ^ acc8) << 8;
             st_u16(cur_c, cell);
             cells.keep(c * 64, cell);
+            st_relaxed_u16(out_c, (cb.cur8 ^ acc8) | version << 8);
             flips += __popc(acc8);
             if (WAIT && record_wait) {
 #pragma unroll
@@ -683,10 +688,11 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
                 stage ^= 1u;
                 hs_c += 8 * 32;
                 cur_c += 32;
-                up_c += 64;
-                dn_c += 64;
+                out_c += 32;
+                up_c += 32;
+                dn_c += 32;
                 if (--until_pub == 0u) {
-                    publish_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
+                    hint_strand(my_flag, seq, row0 - kMtN + (c + 1) * 8, lane);
                     until_pub = pub;
                 }
             }
@@ -699,8 +705,8 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         // ---- end of the layer: the last two columns leave the window; the block's partial sum joins
         // the running energy after the partial sums of all earlier blocks (tempering definition,
         // oracle/ising_oracle.h), which the strand of the layer below has published with its block
-        ISING_HS_ST(hs_c + 6 * 32, r[6]);
-        ISING_HS_ST(hs_c + 7 * 32, r[7]);
+        st_f32(hs_c + 6 * 32, r[6]);
+        st_f32(hs_c + 7 * 32, r[7]);
         if (has_pred) wait_counter(pred_flag, pred_need, pred_cached);
         if (active) {
             double* e_run = b.e_run + chain;
@@ -746,12 +752,6 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     uint32_t* head_flag = flags + S * kFlagStride;
     const uint32_t pos = b.mt_pos[tile];
     const uint32_t total = sweeps * b.n_spins;  // draws of this launch (a multiple of 8)
-#ifdef ISING_X_TAPE_EL
-    const uint64_t pol_tape = policy_evict_last();
-#define ISING_TAPE_ST(p, v) st_u32(p, v, pol_tape)
-#else
-#define ISING_TAPE_ST(p, v) st_u32(p, v)
-#endif
 
     for (uint32_t i = 0; i < kMtN; ++i) {
         uint32_t w = pos + i;
@@ -822,7 +822,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
 #pragma unroll 8
                 for (int k = 0; k < 32; ++k) {
                     const uint32_t nx = in[k * 32];
-                    ISING_TAPE_ST(po + k * 32, mt_recurrence(cur, nx, in[1024 + k * 32]));
+                    st_u32(po + k * 32, mt_recurrence(cur, nx, in[1024 + k * 32]));
                     cur = nx;
                 }
                 sa = sa2;
@@ -843,7 +843,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
                 }
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    ISING_TAPE_ST(po + k * 32, mt_recurrence(cur, nxt[k], far[k]));
+                    st_u32(po + k * 32, mt_recurrence(cur, nxt[k], far[k]));
                     cur = nxt[k];
                 }
                 sa += 32;
@@ -868,7 +868,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
                 }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    ISING_TAPE_ST(tape + size_t(so + k) * 32, mt_recurrence(cur, nxt[k], far[k]));  // (so is a multiple of 8)
+                    st_u32(tape + size_t(so + k) * 32, mt_recurrence(cur, nxt[k], far[k]));  // (so is a multiple of 8)
                     cur = nxt[k];
                 }
                 sa = sa + 8 >= R ? sa + 8 - R : sa + 8;
@@ -993,6 +993,7 @@ __global__ void __launch_bounds__(256) words_to_cells_kernel(DevBatch b) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) byte |= ((word[k] >> lane) & 1u) << k;
     b.spin_cells[idx] = uint16_t(byte << 8);
+    b.spin_nbr[idx] = uint16_t(byte | (b.strand_epoch & 0xffu) << 8);
 }
 
 __global__ void __launch_bounds__(256) cells_to_words_kernel(DevBatch b) {
