@@ -484,7 +484,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     };
 
 #ifdef ISING_STRAND_PROFILE
-    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0, tPred = 0, tHead = 0, tReq = 0;
+    long long tA = 0, tB = 0, tC = 0, tD = 0, tE = 0, tF = 0, t0 = 0, tPred = 0, tHead = 0, tReq = 0, tStart = 0;
 #define ISING_TIMED(acc, stmt)                  \
     {                                           \
         const long long before_ = clock64();    \
@@ -539,7 +539,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
         }
 
         // ---- the first chunk's operands (the only exposed round trips of the block)
-        wait_counter(head_flag, head_need, head_cached);
+        ISING_TIMED(tStart, wait_counter(head_flag, head_need, head_cached))
         __syncwarp();  // every lane has left the stage's previous contents
         request(stage, slot, hs_c - lane + 3 * 32, 1024);  // (a layer has two chunks at least)
         // The neighbour spins of a chunk are requested a chunk ahead when the layer below's counter says it
@@ -729,7 +729,7 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
     }
     if (active && flips != 0u) atomicAdd(b.flips + chain, static_cast<unsigned long long>(flips));
 #ifdef ISING_STRAND_PROFILE
-    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld cell %lld rotate %lld (in request: pred wait %lld head wait %lld bulk requests %lld); block end %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tPred / seq, tHead / seq, tReq / seq, tF / total_blocks);
+    if (lane == 0 && (tile % 97) == 0) printf("tile %u strand %u chunks %u: per chunk request %lld wait %lld attempts %lld cell %lld rotate %lld (in request: pred wait %lld head wait %lld bulk requests %lld); block end %lld, head wait at the start %lld per block\n", tile, j, seq, tA / seq, tB / seq, tC / seq, tD / seq, tE / seq, tPred / seq, tHead / seq, tReq / seq, tF / total_blocks, tStart / total_blocks);
 #endif
 }
 
@@ -743,6 +743,13 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
 // memory, or nullptr: then the operands of a group are loaded into registers, one round trip per
 // 32 rows (about a third of the rate).
 constexpr uint32_t kProducerStage = 8192;
+// Rows between two publications of the head (each costs a device-scope fence, ~3,500 cycles, a third of
+// the producer's time at 64 rows — and the producer sets the pace of its tile); at most 192, see below.
+#ifndef ISING_X_PRODUCER_BATCH
+#define ISING_X_PRODUCER_BATCH 128
+#endif
+constexpr uint32_t kProducerBatch = ISING_X_PRODUCER_BATCH;
+static_assert(kProducerBatch % 32 == 0 && kProducerBatch <= 192, "operands of a group must lie before its batch");
 constexpr uint32_t kProducerSmem = 2 * kProducerStage + 16;
 __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, uint32_t lane, unsigned char* landing) {
     const uint32_t S = b.strands, R = b.tape_rows;
@@ -760,7 +767,8 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     }
     // Bulk copies read the ring through the async proxy: every row they fetch must be globally
     // performed first.  The rows above are made so here; later ones by the fence of a publication —
-    // a group's operands are at least 132 rows (two publications) behind the row being written.
+    // a group's nearest operand is 227 rows behind the row being written, the last group of a batch starts
+    // kProducerBatch - 32 rows into it: the operands of every group lie before the batch, i.e. published.
     const uint32_t lsm = landing != nullptr ? smem_u32(landing) : 0u;
     const uint32_t lbar = lsm + 2 * kProducerStage;
     uint32_t lstage = 0, lphases = 0;
@@ -795,7 +803,7 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     // operand loads.  So rows are generated 32 at a time with all 64 operand loads in flight together
     // (x[a-623+k] and x[a-227+k], k < 32: every one of them lies behind row a).
     while (a < end) {
-        const uint32_t batch = min(64u, end - a);  // (a multiple of 8)
+        const uint32_t batch = min(kProducerBatch, end - a);  // (a multiple of 8)
         // rows a .. a+batch-1 overwrite rows a-R .. : they must be consumed draws (row < 624 + tail)
         while (int32_t(a + batch - R - kMtN - tail) > 0) {
             // (relaxed: a strand's draw index is published after its last read of the rows before it, and
