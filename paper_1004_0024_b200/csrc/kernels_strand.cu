@@ -713,7 +713,10 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
             const double e = ld_cg_f64(e_run);
             asm volatile("st.global.f64 [%0], %1;" ::"l"(e_run), "d"(__dadd_rn(e, e_blk)) : "memory");
         }
-        publish_strand(my_flag, seq, blk + 1 == total_blocks ? 0xffffffffu : row0 - kMtN + P, lane);
+        // (the draw this strand needs next is the first of its next layer, S layers on — or of layer j of
+        // the next sweep: the rows in between belong to the other strands)
+        const uint32_t nb = blk + 1, nsw = nb / blocks_per_sweep;
+        publish_strand(my_flag, seq, nb == total_blocks ? 0xffffffffu : (nsw * L + j + S * (nb - nsw * blocks_per_sweep)) * P, lane);
         ISING_TICK(tF);
         if (WAIT && record_wait) {  // flushed per layer (lanes 0..7 hold partial sums of at most 64 * 32 each)
             unsigned long long* out = b.wait_counts + size_t(tile) * kWaitSlots;
@@ -749,6 +752,12 @@ constexpr uint32_t kProducerStage = 8192;
 #define ISING_X_PRODUCER_BATCH 128
 #endif
 constexpr uint32_t kProducerBatch = ISING_X_PRODUCER_BATCH;
+// How far the head may run ahead of the most advanced strand's published need, in rows: 256 + 64 S.
+// A strand publishes its need every strand_pub (<= 16) chunks and needs 8 rows at a time — anything
+// above 136 rows cannot deadlock — and a strand starting a layer is S - 1 strand lags ahead of the most
+// advanced one (measured: c5, S = 4, 512 rows 2.35e11 against 2.32e11 unbounded, DRAM reads -18 %;
+// c4, S = 16, 512 rows 4.0e10, 1280 rows as unbounded).
+constexpr uint32_t kProducerLeadBase = 256, kProducerLeadPerStrand = 64;
 static_assert(kProducerBatch % 32 == 0 && kProducerBatch <= 192, "operands of a group must lie before its batch");
 constexpr uint32_t kProducerSmem = 2 * kProducerStage + 16;
 __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, uint32_t lane, unsigned char* landing) {
@@ -797,6 +806,8 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     const uint32_t end = kMtN + total;
     uint32_t a = kMtN;      // next row to generate
     uint32_t tail = 0;      // draws known to be consumed by every strand
+    uint32_t front = 0;     // the largest draw index a strand has said it needs next
+    const uint32_t lead = kProducerLeadBase + kProducerLeadPerStrand * S;
     uint32_t so = kMtN % R, sa = 0, sf = kMtM % R;  // slots of rows a, a-624, a-227 (624 - 227 = 397)
     uint32_t cur = ld_cg_u32(tape);                 // x[a-624]
     // A producer feeds S strands and is one in-order warp: what bounds it is the round trip of its
@@ -804,15 +815,20 @@ __device__ void producer_run(const DevBatch& b, uint32_t tile, uint32_t sweeps, 
     // (x[a-623+k] and x[a-227+k], k < 32: every one of them lies behind row a).
     while (a < end) {
         const uint32_t batch = min(kProducerBatch, end - a);  // (a multiple of 8)
-        // rows a .. a+batch-1 overwrite rows a-R .. : they must be consumed draws (row < 624 + tail)
-        while (int32_t(a + batch - R - kMtN - tail) > 0) {
+        // Rows a .. a+batch-1 overwrite rows a-R .. : they must be consumed draws (row < 624 + tail).  And
+        // they should not be far ahead of the most advanced strand (draw `front`): rows nobody needs yet
+        // only push the rows the strands are about to read out of L2 (`lead` rows per tile in flight
+        // instead of up to R).  Both bounds are monotonic, so stale values only delay.
+        while (int32_t(a + batch - R - kMtN - tail) > 0 || int32_t(a - kMtN - front - lead) > 0) {
             // (relaxed: a strand's draw index is published after its last read of the rows before it, and
             // the rows written next are published with a release of their own)
-            uint32_t d = lane < S ? ld_relaxed(flags + lane * kFlagStride + 1) : 0xffffffffu;
-            d = __reduce_min_sync(0xffffffffu, d);
-            if (d == 0xffffffffu) d = total;
-            if (d == tail) __nanosleep(8000);  // (normally far ahead of the strands: the ring is full)
-            tail = d;
+            const uint32_t d = lane < S ? ld_relaxed(flags + lane * kFlagStride + 1) : 0xffffffffu;
+            uint32_t lo = __reduce_min_sync(0xffffffffu, d);
+            uint32_t hi = __reduce_max_sync(0xffffffffu, d == 0xffffffffu ? 0u : d);
+            if (lo == 0xffffffffu) lo = hi = total;  // every strand has finished
+            if (lo == tail && hi == front) __nanosleep(1000);
+            tail = lo;
+            front = hi;
         }
         for (uint32_t done = 0; done < batch;) {
             const uint32_t rows = min(32u, batch - done);
