@@ -554,3 +554,19 @@ def test_resync_energies_sets_the_tempering_cost(lib, port, gamma):
             st.run(3, 0)
             after = np.array([port.tempering_cost(omodel, s, gamma) for s in st.spins(0, st.n_chains)])
             np.testing.assert_allclose(st.running_energies(), after, rtol=REL_ENERGY, atol=1e-4)
+
+
+@pytest.mark.parametrize("kernel", LAYERED_KERNELS)
+def test_layered_families_keep_subnormal_field_parts(lib, port, kernel):
+    """A far and a band coupling in the subnormal range (3e-39, 7e-40): such a model is not
+    `reduction_safe` (a global f32 reduction flushes subnormals), so every family must apply its updates
+    as plain f32 additions.  The strand family pulls far updates into registers and needs no special case."""
+    positions, h, edges = ins.layered_spec(32, 4242)
+    edges = [e for e in edges if {e[0], e[1]} != {3, 20} and {e[0], e[1]} != {9, 10}]
+    edges += [(3, 20, float(np.float32(3e-39))), (9, 10, float(np.float32(7e-40)))]
+    csr = ins.build_layered_csr(positions, h, edges, 4, 0.9)
+    betas = ins.geometric_betas(0.3, 2.5, 6)
+    state, want = run_both(port, [csr], 6, betas, 60, 2, kernel=kernel, chunks=[25, 35])
+    assert state.info()["kernel"] == kernel
+    assert_batch_matches(state, want, REL_ENERGY)
+    state.close()
