@@ -11,17 +11,22 @@
 //   * space fields only ever receive updates from flips of their own layer, all issued by the one
 //     strand that owns the layer, in position order — the f32 sums round exactly as in the reference;
 //   * the tau field of these models takes the values {2J, +0, -2J} and is rebuilt from the two
-//     neighbouring spins (HostModel::layered_uniform), read from the neighbouring strands' spin bytes
-//     under the ordering above;
+//     neighbouring spins (HostModel::layered_uniform), read from the neighbouring strands' versioned
+//     spin words (DevBatch::spin_nbr) under the ordering above;
 //   * draw (sweep, l, p) of the chain's MT19937 stream is word (sweep*L + l)*P + p of a TAPE that a
 //     PRODUCER warp per tile generates in stream order (lane = chain, three coalesced row accesses per
 //     word: x[k] = f(x[k-624], x[k-623], x[k-227]), ref: proj/src/rng.cpp:22-25,89-96) into a ring in
 //     global memory; the strands temper and convert their own words.
 //
-// Nothing is staged on chip beyond registers, so a tile is not bound to an SM or to Tensor Memory:
-// strands and producers are independent warps of a persistent grid that meet through per-tile
-// progress counters in global memory (st.release.gpu / ld.acquire.gpu), a few thousand of them in
-// flight — enough to hide every latency, which the one-warp-per-tile kernels cannot.
+// A tile is not bound to an SM or to Tensor Memory: strands and producers are independent warps of a
+// persistent grid, a few thousand of them in flight, that meet through global memory only.  A release
+// store costs a device-wide fence (MEMBAR.ALL.GPU, ~3,500 cycles), so only the tape head (every 128
+// rows) and a strand's end of layer (where the running energy is handed on) are published that way.
+// Inside a layer a strand's progress counter is a fence-free hint, and what the next strand reads — the
+// chunk's spins — carries the chunk's sweep count in the same 16-bit word: the reader checks the
+// version instead of relying on an order between counter and data.  What a warp reads more than once
+// is staged in shared memory: the layer graph (per CTA), the cells of the layer being swept, and the
+// landing stages of the bulk copies that bring tape rows and field columns a chunk ahead.
 //
 // Per strand, fields move in chunks of 8 positions: the window of positions p-2..p+2 lives in
 // registers (band neighbours are predicated register adds, as in kernels_layered.cu); eight columns
@@ -36,8 +41,8 @@
 // order of subtractions from h[t] exactly.  Between sweeps the fields in memory therefore lack the far
 // updates of the latest sweep ("pending"); settle_fields_kernel applies them when anything else wants
 // the fields (Batch::settle).  All field traffic of a layer comes from one thread per chain, so
-// program order is the only ordering it needs.  HBM traffic per attempt: 4 B field in, 4 B out, 1/2 B
-// cells, plus the tape (4 B written, 4 B read).
+// program order is the only ordering it needs.  HBM traffic per attempt: 4 B field in, 4 B out, 3/4 B
+// cells and versioned spins, plus the tape (4 B written, 4 B read).
 #include "device_batch.hpp"
 #include "device_math.cuh"
 
@@ -422,9 +427,9 @@ constexpr uint32_t kWarpSmem = 2 * kStageBytes + 32;
 // Everything a chunk reads from global memory is requested one chunk ahead or more: the tape rows and
 // the eight field columns entering the window by bulk (TMA) copies of one elected lane into the warp's
 // landing stage (no registers held meanwhile; nobody but this strand writes those columns, and it last
-// did a sweep ago), the spin bytes of the two neighbouring layers by plain loads into a register each
-// (the layer below's only once its strand is known to have finished that chunk); the layer's cells
-// arrive by one bulk copy per layer.  So the loop-carried chain of the attempts is all a strand waits
+// did a sweep ago), the versioned spins of the two neighbouring layers by strong loads into a register
+// each (once the layer below's hint says it has finished that chunk; verified when used); the layer's
+// cells arrive by one bulk copy per layer.  So the loop-carried chain of the attempts is all a strand waits
 // for.
 template <int EXP, bool WAIT, bool STAGED>
 __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t P, uint32_t L, uint32_t tile, uint32_t j,
