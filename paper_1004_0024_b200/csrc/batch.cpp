@@ -614,7 +614,12 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         dev_.strand_graphs = strand_graphs_.as<DevStrandGraph>();
         // one model: its graph is staged in every CTA's shared memory, next to the strands' landing stages
         // and cell rows, when the launcher finds room (launch_sweep_strand)
-        dev_.strand_graph_smem = graphs.size() == 1 ? uint32_t(strand_graph_bytes(graphs[0].per_layer, graphs[0].n_edges)) : 0u;
+        // (several models: only when every CTA hosts warps of one tile — small batches, see launch_sweep_strand)
+        dev_.strand_graph_smem = 0;
+        for (const DevStrandGraph& g : graphs) {
+            dev_.strand_graph_smem = std::max(dev_.strand_graph_smem, uint32_t(strand_graph_bytes(g.per_layer, g.n_edges)));
+        }
+        dev_.strand_single_model = graphs.size() == 1 ? 1u : 0u;
         // How many layers of a tile are swept at once.  Every strand and producer of a round must be
         // resident, sm_count * warps of them; more strands hide more latency, fewer keep the tape ring
         // (S * per_layer rows per tile) small.  ISING_B200_STRANDS / ISING_B200_STRAND_WARPS override.

@@ -155,7 +155,8 @@ struct DevBatch {
     uint16_t* spin_nbr;
     uint32_t strand_epoch;  // sweeps done before this launch: the version every chunk carries at its start
     uint32_t* strand_flags; // per tile S + 1 progress counters (strand chunks done, tape head), one line each
-    uint32_t strand_graph_smem;  // bytes of model 0's graph staged in shared memory (0: tables read from global)
+    uint32_t strand_graph_smem;  // bytes of the largest layer graph as staged in shared memory
+    uint32_t strand_single_model;  // 1: every tile uses model 0
     // tempering
     const uint32_t* swap_seeds;  // per ladder
     uint32_t* swap_mt;           // [624][n_ladders]

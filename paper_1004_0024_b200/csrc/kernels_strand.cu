@@ -942,7 +942,8 @@ template <int EXP, bool WAIT, bool STAGED>
 __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(DevBatch b, uint32_t sweeps,
                                                                                  uint32_t tiles_per_round,
                                                                                  uint32_t strand_regions,
-                                                                                 uint32_t producer_slots, StrandWarpMap map) {
+                                                                                 uint32_t producer_slots, uint32_t tile_local,
+                                                                                 StrandWarpMap map) {
     extern __shared__ __align__(128) unsigned char strand_smem[];
     // `warp` is the LOGICAL warp index (see StrandWarpMap); kIdleWarp: a padding warp
     const uint32_t warp = map.logical[threadIdx.x >> 5], lane = threadIdx.x & 31u;
@@ -951,8 +952,11 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
     unsigned char* graph_smem = strand_smem + size_t(strand_regions) * region_bytes;
     unsigned char* producer_smem = graph_smem + ((STAGED ? b.strand_graph_smem : 0u) + 15u) / 16u * 16u;
     Tables<STAGED> staged{};
+    // STAGED with several models: the launcher has dealt the items so that every warp of this CTA works
+    // on tile blockIdx.x % tiles_per_round (tile_local; one round)
+    const uint32_t staged_model = STAGED && tile_local != 0u ? b.tile_model[blockIdx.x % tiles_per_round] : 0u;
     if constexpr (STAGED) {
-        const DevStrandGraph g0 = b.strand_graphs[0];
+        const DevStrandGraph g0 = b.strand_graphs[staged_model];
         const uint32_t P = g0.per_layer;
         uint4* pos = reinterpret_cast<uint4*>(graph_smem);
         uint4* band = pos + P;
@@ -992,7 +996,7 @@ __global__ void __launch_bounds__(kStrandMaxWarps * 32, 1) sweep_strand_kernel(D
             producer_run(b, tile, sweeps, lane, landing);
             continue;
         }
-        const DevStrandGraph& g = b.strand_graphs[STAGED ? 0u : b.tile_model[tile]];
+        const DevStrandGraph& g = b.strand_graphs[STAGED ? staged_model : b.tile_model[tile]];
         if constexpr (STAGED) {
             strand_run<EXP, WAIT, true>(b, staged, g.per_layer, g.layers, tile, role, sweeps, lane, warp_smem);
         } else {
@@ -1092,6 +1096,7 @@ constexpr size_t kStrandSmemLimit = 227 * 1024;
 struct StrandLaunch {
     dim3 grid, block;
     uint32_t round, regions, tiles_over_ctas;
+    bool tile_local;  // every CTA hosts warps of one tile only
     StrandWarpMap map;
 };
 
@@ -1142,7 +1147,7 @@ cudaError_t launch_strand_variant(const DevBatch& b, uint32_t sweeps, const Stra
     if (base + size_t(slots) * kProducerSmem > kStrandSmemLimit) slots = 0;
     const size_t total_smem = base + size_t(slots) * kProducerSmem;
     sweep_strand_kernel<EXP, WAIT, STAGED><<<geo.grid, geo.block, total_smem, stream>>>(b, sweeps, geo.round, geo.regions, slots,
-                                                                                        geo.map);
+                                                                                        geo.tile_local ? 1u : 0u, geo.map);
     return cudaGetLastError();
 }
 template <int EXP>
@@ -1152,7 +1157,7 @@ cudaError_t launch_strand_exp(const DevBatch& b, uint32_t sweeps, const StrandLa
     // in shared memory when the batch has one model and they fit.
     const bool wait = b.wait_counts != nullptr;
     const size_t staged_bytes = size_t(geo.regions) * (kWarpSmem + size_t(b.max_per_layer) * 8) + b.strand_graph_smem;
-    const bool staged = !wait && b.strand_graph_smem != 0u && staged_bytes <= kStrandSmemLimit;
+    const bool staged = !wait && (b.strand_single_model != 0u || geo.tile_local) && staged_bytes <= kStrandSmemLimit;
     if (wait) return launch_strand_variant<EXP, true, false>(b, sweeps, geo, stream);
     if (staged) return launch_strand_variant<EXP, false, true>(b, sweeps, geo, stream);
     return launch_strand_variant<EXP, false, false>(b, sweeps, geo, stream);
@@ -1177,9 +1182,16 @@ cudaError_t launch_sweep_strand(const DevBatch& b, uint32_t sweeps, int sm_count
         words_to_cells_kernel<<<unsigned((cells + 255) / 256), 256, 0, stream>>>(b);
     }
     const uint32_t items = tiles_per_round * per_tile;
-    const uint32_t ctas = min(uint32_t(sm_count), items);
+    uint32_t ctas = min(uint32_t(sm_count), items);
+    // Batches of several models with no more tiles than SMs, in one round: a whole number of CTAs per
+    // tile.  Items are dealt warp-major over the grid (item = warp * ctas + block, tile = item % tiles),
+    // so with ctas a multiple of the tile count every warp of a CTA works on tile block % tiles — and the
+    // CTA can stage that tile's graph and cells in shared memory like a single-model batch.
+    const bool tile_local = b.strand_single_model == 0u && rounds == 1 && b.n_tiles <= uint32_t(sm_count) && b.wait_counts == nullptr;
+    if (tile_local) ctas = min(uint32_t(sm_count) / b.n_tiles, per_tile) * b.n_tiles;
     warps_per_cta = (items + ctas - 1) / ctas;  // <= the caller's bound, since items <= capacity
     StrandLaunch geo;
+    geo.tile_local = tile_local;
     geo.grid = dim3(ctas);
     geo.round = tiles_per_round;
     geo.regions = min(warps_per_cta, (tiles_per_round * b.strands + ctas - 1) / ctas);  // warps that can be strands
