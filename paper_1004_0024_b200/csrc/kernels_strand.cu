@@ -20,7 +20,7 @@
 //
 // A tile is not bound to an SM or to Tensor Memory: strands and producers are independent warps of a
 // persistent grid, a few thousand of them in flight, that meet through global memory only.  A release
-// store costs a device-wide fence (MEMBAR.ALL.GPU, ~3,500 cycles), so only the tape head (every 128
+// store costs a device-wide fence (MEMBAR.ALL.GPU, ~3,500 cycles), so only the tape head (every 192
 // rows) and a strand's end of layer (where the running energy is handed on) are published that way.
 // Inside a layer a strand's progress counter is a fence-free hint, and what the next strand reads — the
 // chunk's spins — carries the chunk's sweep count in the same 16-bit word: the reader checks the
@@ -752,9 +752,10 @@ __device__ void strand_run(const DevBatch& b, const Tables<STAGED>& t, uint32_t 
 // 32 rows (about a third of the rate).
 constexpr uint32_t kProducerStage = 8192;
 // Rows between two publications of the head (each costs a device-scope fence, ~3,500 cycles, a third of
-// the producer's time at 64 rows — and the producer sets the pace of its tile); at most 192, see below.
+// the producer's time at 64 rows — and on small batches the producer sets the pace of its tile: c4 +5 % from
+// 128 to 192); at most 192, see below.
 #ifndef ISING_X_PRODUCER_BATCH
-#define ISING_X_PRODUCER_BATCH 128
+#define ISING_X_PRODUCER_BATCH 192
 #endif
 constexpr uint32_t kProducerBatch = ISING_X_PRODUCER_BATCH;
 // How far the head may run ahead of the most advanced strand's published need, in rows: 256 + 64 S.
