@@ -136,3 +136,20 @@ def test_instance_generators_have_the_advertised_shapes():
     assert space.min() >= 4 and space.max() <= 6 and len(edges) == 2 * 512 + 256
     betas = ins.geometric_betas(0.2, 5.0, 16)
     assert betas[0] == np.float32(0.2) and betas[-1] == np.float32(5.0) and (np.diff(betas) > 0).all()
+
+
+def test_committed_dram_traffic_belongs_to_the_committed_kernels():
+    """bench.py reports `roofline.traffic` from profiles/sweep_traffic.json only when the capture was taken
+    with the kernel sources in the tree: the c5 entry of the benchmark's kernel family must be current."""
+    import json
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    entry = json.load(open(os.path.join(root, "profiles", "sweep_traffic.json")))["c5:3"]
+    assert entry["kernel_source_hash"] == bench.kernel_source_hash()
+    traffic, source = bench.profiled_traffic("c5", 3, entry["attempts_in_profiled_launch"])
+    assert traffic == pytest.approx(entry["dram_bytes_read"] + entry["dram_bytes_write"], rel=1e-3) and "r02" in source
+    stale, why = bench.profiled_traffic("c5", 1, 1.0)
+    assert stale is None and "no ncu capture" in why
