@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <dlfcn.h>
 #include <cstring>
@@ -352,6 +354,7 @@ void Batch::release_cuda_objects() {
 void Batch::construct(const std::vector<const HostModel*>& models,
                       const std::vector<uint32_t>& model_of_ladder, const BatchConfig& cfg,
                       const int8_t* initial_spins) {
+    const auto t_begin = std::chrono::steady_clock::now();
     // ---- argument checks (ref: check_engine_model, sweep_state.cpp:108-158)
     if (models.empty()) throw Error("init_state: no model given");
     if (cfg.n_ladders == 0 || cfg.n_betas == 0) throw Error("init_state: batch needs at least one chain");
@@ -721,9 +724,16 @@ void Batch::construct(const std::vector<const HostModel*>& models,
                                    stream_),
                    "upload initial spins");
     }
+    const auto t_host = std::chrono::steady_clock::now();
     cuda_check(launch_init(dev_, initial_spins ? initial_dev.as<int8_t>() : nullptr, stream_), "init kernel");
     other_launches += 2;
     cuda_check(cudaStreamSynchronize(stream_), "init");
+    if (std::getenv("ISING_B200_TRACE") != nullptr) {  // where batch creation spends its time (profiles/init_time.py)
+        const auto t_done = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "ising_batch_create: host side (analysis, allocation, uploads) %.2f ms, init kernels %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(t_host - t_begin).count(),
+                     std::chrono::duration<double, std::milli>(t_done - t_host).count());
+    }
 
     // The MT19937 states (2,496 B per chain) are re-read and re-written every 624 attempts while
     // 8 B per attempt of field data stream past them.  Ask for them to persist in L2 so they stop
