@@ -570,3 +570,19 @@ def test_layered_families_keep_subnormal_field_parts(lib, port, kernel):
     assert state.info()["kernel"] == kernel
     assert_batch_matches(state, want, REL_ENERGY)
     state.close()
+
+
+def test_strand_family_many_tiles_of_alternating_models(lib, port):
+    """More tiles than SMs and two models alternating ladder by ladder (a tile never mixes models, so
+    every ladder is a tile of its own): the strand family then reads graph and cells from global memory
+    instead of staging them per CTA — the one launch variant the smaller multi-model tests do not reach."""
+    a = ins.build_layered_csr(*ins.layered_spec(16, 501), 4, 1.25)
+    b = ins.build_layered_csr(*chord_spec(16, 502, (3, 5, 7)), 4, 0.8)
+    ladders = 170
+    betas = ins.geometric_betas(0.3, 2.0, 3)
+    state, want = run_both(port, [a, b], ladders, betas, 24, 3, kernel=ib.KERNEL_STRAND,
+                           model_of_ladder=[k % 2 for k in range(ladders)], chunks=[10, 14])
+    info = state.info()
+    assert info["kernel"] == ib.KERNEL_STRAND and info["n_tiles"] == ladders
+    assert_batch_matches(state, want, REL_ENERGY)
+    state.close()
