@@ -586,3 +586,17 @@ def test_strand_family_many_tiles_of_alternating_models(lib, port):
     assert info["kernel"] == ib.KERNEL_STRAND and info["n_tiles"] == ladders
     assert_batch_matches(state, want, REL_ENERGY)
     state.close()
+
+
+def test_strand_family_more_tiles_than_one_round_holds(lib, port):
+    """1,600 tiles of one small model: with one strand and one producer per tile only 1,480 tiles are
+    resident at once on 148 SMs, so the launch sweeps them in two rounds of 800 (every warp of a round
+    must be resident: the rounds are sized by the launcher)."""
+    csr = ins.build_layered_csr(*ins.layered_spec(16, 733), 4, 1.0)
+    betas = ins.geometric_betas(0.4, 1.6, 4)
+    ladders = 1600 * 8  # 32 chains per tile
+    state, want = run_both(port, [csr], ladders, betas, 12, 4, kernel=ib.KERNEL_STRAND, chunks=[5, 7])
+    info = state.info()
+    assert info["n_tiles"] == 1600 and info["strands"] == 1
+    assert_batch_matches(state, want, REL_ENERGY)
+    state.close()
