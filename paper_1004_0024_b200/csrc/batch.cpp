@@ -446,6 +446,7 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         }
     }
 
+    const auto t_checked = std::chrono::steady_clock::now();
     // ---- device
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -661,6 +662,7 @@ void Batch::construct(const std::vector<const HostModel*>& models,
         dev_.strand_flags = strand_flags_.as<uint32_t>();
     }
 
+    const auto t_graphs = std::chrono::steady_clock::now();
     // ---- batch description
     dev_.n_spins = n;
     dev_.n_tiles = uint32_t(tile_first.size());
@@ -730,9 +732,10 @@ void Batch::construct(const std::vector<const HostModel*>& models,
     cuda_check(cudaStreamSynchronize(stream_), "init");
     if (std::getenv("ISING_B200_TRACE") != nullptr) {  // where batch creation spends its time (profiles/init_time.py)
         const auto t_done = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "ising_batch_create: host side (analysis, allocation, uploads) %.2f ms, init kernels %.2f ms\n",
-                     std::chrono::duration<double, std::milli>(t_host - t_begin).count(),
-                     std::chrono::duration<double, std::milli>(t_done - t_host).count());
+        const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "ising_batch_create: checks and tiling %.2f ms, model and graph uploads (+ family buffers) %.2f ms, "
+                             "state allocation and uploads %.2f ms, init kernels %.2f ms\n",
+                     ms(t_begin, t_checked), ms(t_checked, t_graphs), ms(t_graphs, t_host), ms(t_host, t_done));
     }
 
     // The MT19937 states (2,496 B per chain) are re-read and re-written every 624 attempts while
